@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the PLV / iPLV / ciPLV hot path (BASELINE.json metric:
+pair.samples/s for PLV+iPLV+ciPLV at 1/2/4/8 GPUs, % of tensor / HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl reference]
+
+A step = one pass of the hot path over one batch of the synthetic workload
+(SURVEY 8(d)): analytic/real input resident in HBM -> normalise (+Hilbert for
+real configs) -> upper-triangle Gram + fused PLV/iPLV/ciPLV epilogue, all
+three metrics written to HBM.  Default workload = config C5 (20k signals,
+BASELINE.json configs[4]): the config the metric's 1->8 GPU scaling target is
+quoted on; it fits one B200.  Multi-GPU (torchrun, one rank per GPU): input on
+rank 0, NCCL broadcast over NVLink inside the timed region, output tiles
+sharded across ranks (strong scaling, no gather).
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the reference's CPU
+algorithm (the NumPy restatement in oracle/, all host cores) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1710_08037_b200 import workloads as W  # noqa: E402
+
+METRIC = "pair·samples/s for PLV+iPLV+ciPLV at 1/2/4/8 GPU; % tensor/HBM roofline"
+UNIT = "pair·samples/s"
+FLOPS_PER_PAIR_SAMPLE = 8  # complex MAC
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["source"] = "measured (MEASURED_PEAKS.json)"
+    return p
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"ps_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU legs
+def cpu_sample_run(x, kind, n_sig, trial_reduce="mean", reps=1):
+    """Time the oracle (NumPy/OpenBLAS restatement of Appendix impl 3) on the
+    first n_sig signals of the workload; returns (pair.samples/s, seconds)."""
+    from oracle import plv_oracle as O
+
+    xs = np.ascontiguousarray(x[:n_sig])
+    N, T, R = xs.shape
+    O.plv_family(xs[: min(n_sig, 64)], input_kind=kind, trial_reduce=trial_reduce)  # warm-up
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.plv_family(xs, input_kind=kind, trial_reduce=trial_reduce)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return W.pair_samples(N, T, R) / best, best
+
+
+def cpu_baseline(x, kind, target_s=10.0, max_sig=None):
+    """Grow the signal sample until one oracle pass takes >= target_s / 4."""
+    N = x.shape[0]
+    n = min(N, 256)
+    while True:
+        rate, dt = cpu_sample_run(x, kind, n)
+        if dt >= target_s / 4 or n >= N or (max_sig and n >= max_sig):
+            break
+        n = min(N, int(n * max(1.5, min(4.0, (target_s / 4 / max(dt, 1e-3)) ** 0.5))))
+    return rate, dt, n
+
+
+def cores():
+    return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=sorted(W.CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="split", choices=["split", "fp64"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    N, T, R, B, dt, kind = W.CONFIGS[args.config]
+    work = W.pair_samples(N, T, R, B)
+    cfg = {"workload": f"{args.config}: {W.DESCRIPTIONS[args.config]}", "n_signals": N, "n_samples": T,
+           "n_trials": R, "n_bands": B, "input": dt, "input_kind": kind, "trial_reduce": "mean",
+           "precision": args.precision, "pair_samples_per_step": work,
+           "l2": "inputs larger than L2 (126 MB) every step",
+           "parallelism": f"output-tile shards x{world}" + (" + NCCL broadcast of the input" if world > 1 else "")}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores()))
+        x = W.generate(args.config)
+        if x.ndim == 4:
+            x = x[0]
+        for _ in range(max(0, args.warmup)):
+            cpu_sample_run(x, kind, min(N, 128))
+        n_s = None
+        rates = []
+        for _ in range(args.steps):
+            if n_s is None:
+                rate, dt_s, n_s = cpu_baseline(x, kind, target_s=8.0)
+            else:
+                rate, dt_s = cpu_sample_run(x, kind, n_s)
+            rates.append(rate)
+        val = float(np.median(rates))
+        sample = f"first {n_s} of {N} signals x {T} samples x {R} trials (band 0), full pipeline per step"
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": work / val * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded, SURVEY 8(d))", "config": cfg,
+                "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores(), "kind": "port", "sample": sample},
+                "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_08037_b200 import _native
+    from paper_1710_08037_b200 import connectivity as C
+    from paper_1710_08037_b200 import sharding
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # ---- workload: generated on the host (seeded), resident in HBM --------
+    x_host = W.generate(args.config)
+    if x_host.ndim == 3:
+        x_store = np.ascontiguousarray(np.transpose(x_host, (2, 0, 1)))        # [R, N, T]
+    else:
+        x_store = np.ascontiguousarray(np.transpose(x_host, (0, 3, 1, 2)))     # [B, R, N, T]
+    xd = torch.from_numpy(x_store).to(dev)
+    if world > 1 and rank != 0:
+        xd.zero_()
+    bands = x_host.ndim == 4
+    xv = xd.permute(1, 2, 0) if not bands else xd.permute(0, 2, 3, 1)
+    shard = (rank, world)
+    fp64 = args.precision == "fp64"
+    odt = torch.float64 if fp64 else torch.float32
+    outs = {m: torch.zeros((B, N, N), dtype=odt, device=dev) for m in ("plv", "iplv", "ciplv")}
+    bcast_t = torch.view_as_real(xd) if xd.is_complex() else xd
+
+    def step(timing=False):
+        if world > 1:
+            sharding.broadcast_input(bcast_t, src=0)
+        return C.plv_family(xv, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
+                            out=outs, timing=timing)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region ------------------------------------------------------
+    clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    clk.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    gram_ms, launches = [], 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        r = step(timing=True)
+        info = r["plv"].meta
+        gram_ms.append(info["ms_gram"])
+        launches += int(info["n_kernel_launches"])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_total = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        dist.barrier()
+    clocks = clk.stop()
+    ms_step = ms_total / args.steps
+    value = work / (ms_step / 1e3)
+
+    # ---- roofline of the dominant kernel (Gram + fused epilogue) ----------
+    pk = peaks()
+    my_tiles = sum(1 for t in range(_native.tile_count(N, args.precision)) if t % world == rank)
+    frac_tiles = my_tiles / max(1, _native.tile_count(N, args.precision))
+    gram_avg = float(np.mean(gram_ms)) if gram_ms else float("nan")
+    algo_flops = FLOPS_PER_PAIR_SAMPLE * work * frac_tiles
+    achieved = algo_flops / (gram_avg / 1e3) / 1e12
+    passes = 1 if fp64 else 3
+    peak = pk["bf16_tflops"] / passes if not fp64 else 40.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            if tj.get("config") == args.config and tj.get("precision") == args.precision:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "gram_split_kernel (tcgen05 fp16x3 upper-triangle Gram + fused PLV/iPLV/ciPLV)"
+                if not fp64 else "gram_f64_kernel (DMMA)",
+                "algorithmic_flops_per_launch": algo_flops, "gram_ms_per_launch": gram_avg,
+                "gram_share_of_step": gram_avg / ms_step,
+                "peak_basis": (f"bf16_tflops {pk['bf16_tflops']} ({pk['source']}, burst) / 3 fp16 passes of the "
+                               "hi/lo split = algorithmic ceiling of the split scheme") if not fp64 else
+                "FP64 DMMA datasheet ~40 TFLOP/s (unmeasured)",
+                "frac_of_bf16_peak": achieved / pk["bf16_tflops"]}
+
+    # ---- end to end through the public host API ----------------------------
+    e2e = None
+    if not args.no_e2e:
+        xin = torch.empty(x_store.shape, dtype=torch.from_numpy(x_store[:1]).dtype, pin_memory=True)
+        xin.numpy()[...] = x_store
+        xin_np = xin.numpy()
+        xin_view = np.transpose(xin_np, (1, 2, 0)) if not bands else np.transpose(xin_np, (0, 2, 3, 1))
+        hout = {m: torch.zeros((B, N, N), dtype=odt, pin_memory=True).numpy() for m in ("plv", "iplv", "ciplv")}
+        for _ in range(1):
+            C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard, out=hout)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard, out=hout)
+        dt_e = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([dt_e], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt_e = float(t.item())
+        e2e = {"value": work / dt_e, "unit": UNIT, "h2d_bytes_per_step": int(x_store.nbytes),
+               "d2h_bytes_per_step": int(sum(v.nbytes for v in hout.values())),
+               "ms_per_step": dt_e * 1e3, "api": "paper_1710_08037_b200.connectivity.plv_family(numpy pinned) "
+               "-> ps_plv_family_host (C ABI)"}
+
+    # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores()))
+        xs = x_host if x_host.ndim == 3 else x_host[0]
+        rate, dt_s, n_s = cpu_baseline(xs, kind, target_s=12.0)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores(), "kind": "port",
+               "sample": f"oracle/plv_oracle.py (NumPy + OpenBLAS, {cores()} threads) on the first {n_s} of "
+                         f"{N} signals x {T} samples x {R} trials{' (band 0)' if B > 1 else ''}: "
+                         f"{dt_s:.2f} s per pass"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None,
+                "dtype": "f16x3 split (fp32 accumulate, fp32 out)" if not fp64 else "f64",
+                "data": "synthetic (seeded numpy generator, SURVEY 8(d)); stands in for the paper's MEG data",
+                "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks,
+                "stages_ms": {"normalize": float(info["ms_normalize"]), "gram": gram_avg,
+                              "finish": float(info["ms_finish"])}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

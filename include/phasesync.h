@@ -1,0 +1,169 @@
+/*
+ * phasesync.h -- C ABI of libphasesync_cuda.so, the sm_100a PLV / iPLV / ciPLV
+ * hot path (arXiv 1710.08037 reformulation: Hilbert -> unit phasors ->
+ * Hermitian Gram Z Z^H -> fused PLV-family epilogue).
+ *
+ * The reference (/root/reference) defines this boundary only as SPEC text: the
+ * `bindings` module, SPEC.md:519-564 (ArrayView :524-527, py_analytic_signal
+ * :530-537, py_plv / py_iplv / py_ciplv :538-544, errors "mapped 1:1" :533,
+ * GIL released :554, no state :548).  Each entry point below names the
+ * reference operation it replaces.  No torch types cross this ABI: plain
+ * pointers, sizes and strides; device pointers unless stated otherwise.
+ *
+ * Errors: every function returns a ps_status; nothing throws or aborts across
+ * the ABI.  PS_E_SHAPE -> ShapeError (errors.py:32), PS_E_ALL_MASKED ->
+ * AllSamplesMaskedError (errors.py:12), PS_E_EMPTY_WINDOW ->
+ * EmptyEffectiveWindowError (errors.py:20); device/library failures map to
+ * RuntimeError subclasses.  ps_last_error() returns a thread-local message.
+ */
+#ifndef PHASESYNC_H_
+#define PHASESYNC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PS_ABI_VERSION 1
+
+typedef enum ps_status {
+  PS_OK = 0,
+  PS_E_SHAPE = 1,         /* ShapeError                 errors.py:32 */
+  PS_E_ALL_MASKED = 2,    /* AllSamplesMaskedError      errors.py:12 */
+  PS_E_EMPTY_WINDOW = 3,  /* EmptyEffectiveWindowError  errors.py:20 */
+  PS_E_INVALID = 4,       /* ValueError (bad argument combination)    */
+  PS_E_UNSUPPORTED = 5,   /* UnsupportedError (valid per SPEC, not built) */
+  PS_E_CUDA = 6,          /* CudaError                                */
+  PS_E_CUFFT = 7,         /* CudaError (cuFFT)                        */
+  PS_E_OOM = 8,           /* MemoryError                              */
+  PS_E_INTERNAL = 9       /* RuntimeError                             */
+} ps_status;
+
+typedef enum ps_dtype { PS_F32 = 0, PS_F64 = 1, PS_C64 = 2, PS_C128 = 3 } ps_dtype;
+
+/* What the input array holds. */
+typedef enum ps_input_kind {
+  PS_INPUT_REAL = 0,      /* RealEpochs: Hilbert + normalise + Gram        */
+  PS_INPUT_ANALYTIC = 1,  /* AnalyticEpochs: normalise + Gram              */
+  PS_INPUT_PHASOR = 2     /* PhasorEpochs: Gram (zeros are masked samples) */
+} ps_input_kind;
+
+typedef enum ps_precision {
+  PS_PREC_SPLIT_F16X3 = 0, /* tcgen05 kind::f16, hi/lo split, 3 products, fp32 out */
+  PS_PREC_FP64 = 1         /* DMMA f64 operands and accumulation, fp64 out       */
+} ps_precision;
+
+typedef enum ps_trial_reduce {
+  PS_TRIALS_MEAN = 0,  /* mean over trials of per-trial metrics (default) */
+  PS_TRIALS_NONE = 1,  /* one matrix per trial (PAPER.md:281-287 plv(:,:,t))        */
+  PS_TRIALS_POOL = 2   /* one Gram over all R*T observations                         */
+} ps_trial_reduce;
+
+enum {
+  PS_METRIC_PLV = 1,    /* (1/T)|z_i z_j^H|            Eq 7, */
+  PS_METRIC_IPLV = 2,   /* (1/T)|Im z_i z_j^H|         Eq 13 */
+  PS_METRIC_CIPLV = 4,  /* |Im|/sqrt(1-Re^2)           Eq 14 */
+  PS_METRIC_CRE = 8,    /* signed Re (1/T) z_i z_j^H (coherency real part)  */
+  PS_METRIC_CIM = 16    /* signed Im (1/T) z_i z_j^H (antisymmetric)        */
+};
+
+typedef struct ps_ctx ps_ctx;
+
+/* Input/output description for one call.  Shapes follow the reference
+ * ArrayView [n_signals x n_samples x n_trials] plus an optional
+ * leading band axis.  Strides are in ELEMENTS (complex elements for c64/c128)
+ * and may describe any layout; samples need not be contiguous (a
+ * non-unit sample stride costs one packing copy, reported in
+ * ps_plv_result.input_copied -- SPEC.md:526,551 copy-on-mismatch). */
+typedef struct ps_plv_args {
+  const void* input;           /* device pointer (host pointer for *_host entry) */
+  int32_t dtype;               /* ps_dtype */
+  int32_t input_kind;          /* ps_input_kind */
+  int64_t n_bands, n_signals, n_samples, n_trials;
+  int64_t stride_band, stride_signal, stride_sample, stride_trial;
+  double amp_floor;            /* SPEC.md:123 default 1e-6 */
+  uint32_t metrics;            /* PS_METRIC_* bitmask */
+  int32_t precision;           /* ps_precision */
+  int32_t trial_reduce;        /* ps_trial_reduce */
+  /* Outputs, one per requested metric: dense row-major [n_bands][n_signals]
+   * [n_signals] (MEAN/POOL) or [n_bands][n_trials][n_signals][n_signals]
+   * (NONE); float for SPLIT, double for FP64.  Symmetric (CIM: antisymmetric)
+   * with the SPEC diagonal rules applied. */
+  void* out_plv;
+  void* out_iplv;
+  void* out_ciplv;
+  void* out_cre;
+  void* out_cim;
+  /* Output-tile sharding across devices: this call computes
+   * only tiles t with t % shard_count == shard_index; other entries of the
+   * outputs are left untouched.  shard_count = 1 computes everything. */
+  int32_t shard_index;
+  int32_t shard_count;
+  void* stream;                /* cudaStream_t (NULL = legacy default stream) */
+} ps_plv_args;
+
+typedef struct ps_plv_result {
+  int64_t n_observations;      /* T used for normalisation (R*T for POOL) */
+  int64_t n_masked_samples;    /* total samples masked by the amplitude guard */
+  int64_t n_refined_pairs;     /* ill-conditioned ciPLV pairs recomputed in FP64 */
+  int32_t input_copied;        /* 1 if the input layout forced a packing copy */
+  int32_t n_kernel_launches;   /* kernels of this library launched by the call */
+  float ms_hilbert;            /* device time per stage (when timing enabled) */
+  float ms_normalize;
+  float ms_gram;
+  float ms_finish;
+} ps_plv_result;
+
+/* ABI version check (PS_ABI_VERSION). */
+int ps_abi_version(void);
+
+/* Thread-local description of the last error on this thread. */
+const char* ps_last_error(void);
+
+/* Context: owns cuFFT plans, workspace and per-device state for `device`.
+ * Results are never cached.  One context per thread, or
+ * external locking. */
+ps_status ps_ctx_create(int device, ps_ctx** out);
+ps_status ps_ctx_destroy(ps_ctx* ctx);
+/* Enable per-stage CUDA-event timing (fills ms_* in ps_plv_result). */
+ps_status ps_ctx_set_timing(ps_ctx* ctx, int enable);
+
+/* Replaces bindings.py_plv / py_iplv / py_ciplv and
+ * connectivity.plv_matrix / iplv / ciplv: all requested
+ * PLV-family metrics from ONE Gram per trial.  Device pointers; synchronises
+ * `stream` before returning so the status reflects device-side checks
+ * (AllSamplesMasked, EmptyEffectiveWindow).  result may be NULL. */
+ps_status ps_plv_family(ps_ctx* ctx, const ps_plv_args* args, ps_plv_result* result);
+
+/* Same contract with HOST input/output pointers (pinned memory recommended):
+ * host->device copy, compute, device->host copy, all inside the call.  This is
+ * the entry point a host binding (ctypes / cgo / JNI) uses for plain arrays. */
+ps_status ps_plv_family_host(ps_ctx* ctx, const ps_plv_args* args, ps_plv_result* result);
+
+/* Replaces signalprep.analytic_signal / bindings.py_analytic_signal
+ * (SPEC.md:76-84, :530-537): out = x + i H{x}, Re(out) == x bit-exactly.
+ * Input real (f32 or f64) with the strides of args; output interleaved
+ * complex (c64 for f32, c128 for f64), dense [n_bands][n_trials][n_signals]
+ * [n_samples].  Uses only: input, dtype, n_*, stride_*, stream. */
+ps_status ps_analytic_signal(ps_ctx* ctx, const ps_plv_args* args, void* out);
+
+/* Replaces signalprep.normalize_phasors: z = a/|a| with the
+ * amplitude-floor mask (masked samples exactly 0+0i).  Input complex (c64 /
+ * c128) or real (then the analytic signal is formed first); output complex of
+ * the input precision, dense [n_bands][n_trials][n_signals][n_samples];
+ * mask_out (optional, uint8, same dense layout) gets 1 where masked. */
+ps_status ps_normalize_phasors(ps_ctx* ctx, const ps_plv_args* args, void* out, uint8_t* mask_out);
+
+/* Host-only helpers (no GPU needed): the output-tile sharding rule of
+ * ps_plv_args.shard_index / shard_count.  ps_tile_count returns the number of
+ * upper-triangle output tiles for n_signals at `precision`; ps_pair_shard the
+ * shard that writes pair (i, j) (and its mirror) for shard_count shards. */
+int64_t ps_tile_count(int64_t n_signals, int32_t precision);
+int32_t ps_pair_shard(int64_t n_signals, int32_t precision, int32_t shard_count, int64_t i, int64_t j);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHASESYNC_H_ */

@@ -1,0 +1,343 @@
+"""CPU oracle for the PLV / iPLV / ciPLV hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module is the *checker*.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py`` (its ``cpu_baseline`` leg and ``--impl reference`` arm) may import
+it.  The product path (``paper_1710_08037_b200``) never calls into it; the
+product fails loudly when its CUDA library is missing.
+
+What it restates
+----------------
+The reference (``/root/reference``) ships no implementation code: its
+behavioural contract is ``SPEC.md`` + the paper's Eqs 1-16 + the three Matlab
+implementations in the paper's Appendix + ``pkg/src/phasesync/errors.py``.
+Each function below cites the SPEC / PAPER lines it follows.
+
+Third-party arithmetic the reference declares (``pkg/pyproject.toml:10-13``):
+numpy>=1.24 (complex matmul -> BLAS zgemm) and scipy>=1.10 (FFT).  Neither is
+vendored by the reference; this oracle uses the numpy/scipy installed here
+(numpy 2.3, scipy 1.18) and restates the published algorithms directly.
+
+Parity pinning
+--------------
+There are no reference tests, fixtures or golden vectors to pin against
+(``pkg/pyproject.toml:25`` names an absent ``tests/``).  The oracle is pinned
+against every closed-form known-answer example and invariant the SPEC states
+for this path (see ``tests/test_oracle_kats.py``) and against
+``scipy.signal.hilbert`` for the analytic signal.  Parity with an executable
+reference implementation is therefore "pinned to SPEC known answers", not to
+reference code ("Oracle").
+"""
+from __future__ import annotations
+
+import numpy as np
+
+try:  # threaded FFT for the CPU-baseline timing; numpy fallback is equivalent
+    import scipy.fft as _fft
+
+    def _rfft(x, axis):
+        return _fft.rfft(x, axis=axis, workers=-1)
+
+    def _irfft(X, n, axis):
+        return _fft.irfft(X, n=n, axis=axis, workers=-1)
+
+except Exception:  # pragma: no cover
+    def _rfft(x, axis):
+        return np.fft.rfft(x, axis=axis)
+
+    def _irfft(X, n, axis):
+        return np.fft.irfft(X, n=n, axis=axis)
+
+
+class OracleError(ValueError):
+    """Base for the oracle's own error signalling (mirrors errors.py names)."""
+
+
+class AllSamplesMaskedError(OracleError):
+    """errors.py:12 -- every sample of some signal/trial fell below the floor."""
+
+
+class EmptyEffectiveWindowError(OracleError):
+    """errors.py:20 -- all samples are masked for at least one signal pair."""
+
+
+CIPLV_SINGULAR_EPS = 1e-12
+DEFAULT_AMP_FLOOR = 1e-6
+ROW_BLOCK = 256
+
+
+# --------------------------------------------------------------------------
+# signalprep
+# --------------------------------------------------------------------------
+def hilbert_weights_half(n_samples: int) -> np.ndarray:
+    """Multiplier on the one-sided (rfft) spectrum that yields H{x}.
+
+    SPEC.md:79,124: DC and Nyquist kept at unit weight, strictly positive bins
+    doubled, strictly negative bins zeroed.  The analytic signal is then
+    a = x + i*H{x}, so H{x} = irfft(-i * sgn(k) * X_k): DC/Nyquist get 0,
+    strictly positive bins get -i (odd T has no Nyquist bin, matching
+    scipy.signal.hilbert's ``h[1:(N+1)//2] = 2``).
+    """
+    T = int(n_samples)
+    w = np.zeros(T // 2 + 1, dtype=np.complex128)
+    if T % 2 == 0:
+        w[1:T // 2] = -1j
+    else:
+        w[1:(T + 1) // 2] = -1j
+    return w
+
+
+def analytic_signal(x, axis: int = 1) -> np.ndarray:
+    """SPEC.md:76-84 (Eq 3): a = x + i*H{x}, Re(a) == x bit-exactly.
+
+    ``x`` is RealEpochs-shaped ``[n_signals, n_samples, n_trials]`` (or any
+    array with samples on ``axis``); computed in float64.  The
+    real part is copied from x -- only the imaginary part
+    comes from the inverse FFT.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape[axis] < 2:
+        raise ValueError("n_samples must be >= 2 (SPEC.md:31)")
+    T = x.shape[axis]
+    X = _rfft(x, axis)
+    shape = [1] * x.ndim
+    shape[axis] = T // 2 + 1
+    H = _irfft(X * hilbert_weights_half(T).reshape(shape), T, axis)
+    a = np.empty(x.shape, dtype=np.complex128)
+    a.real = x
+    a.imag = H
+    return a
+
+
+def normalize_phasors(a, amp_floor: float = DEFAULT_AMP_FLOOR, axis: int = 1):
+    """SPEC.md:85-93 (Eq 4): z = a/|a| with the amplitude guard.
+
+    Masked where |a| < amp_floor * median_row(|a|) (median per
+    signal/trial along the sample axis, numpy semantics: mean of the two middle
+    values for even T) or where |a| == 0.  Masked samples are
+    exactly 0+0i.  Raises AllSamplesMaskedError if a whole
+    signal/trial row is masked (errors.py:12).
+    Returns (z, mask).
+    """
+    a = np.asarray(a)
+    a = a.astype(np.complex128, copy=False)
+    amp = np.abs(a)
+    med = np.median(amp, axis=axis, keepdims=True)
+    mask = (amp < amp_floor * med) | (amp == 0.0)
+    if np.any(np.all(mask, axis=axis)):
+        raise AllSamplesMaskedError("an entire signal/trial is below the amplitude floor")
+    safe = np.where(mask, 1.0, amp)
+    z = np.where(mask, 0.0 + 0.0j, a / safe)
+    return z, mask
+
+
+def phasors_from_unit(z, axis: int = 1):
+    """PhasorEpochs given directly (plv_matrix input): mask = (z == 0)."""
+    z = np.asarray(z).astype(np.complex128, copy=False)
+    mask = (z == 0)
+    if np.any(np.all(mask, axis=axis)):
+        raise AllSamplesMaskedError("an entire signal/trial is masked")
+    return z, mask
+
+
+def instantaneous_phase(a) -> np.ndarray:
+    """angle in (-pi, pi]; phase of 0 is 0."""
+    ph = np.angle(np.asarray(a))
+    ph = np.where(ph == -np.pi, np.pi, ph)
+    return ph
+
+
+# --------------------------------------------------------------------------
+# connectivity
+# --------------------------------------------------------------------------
+def _gram_blocked(zt: np.ndarray) -> np.ndarray:
+    """G = Z Z^H for one trial [N, T] in row blocks of 256,
+    complex128 accumulation; PAPER.md:286 (impl 3)."""
+    N = zt.shape[0]
+    G = np.empty((N, N), dtype=np.complex128)
+    zh = zt.conj().T
+    for r0 in range(0, N, ROW_BLOCK):
+        G[r0:r0 + ROW_BLOCK] = zt[r0:r0 + ROW_BLOCK] @ zh
+    return G
+
+
+def _metrics_from_gram(G: np.ndarray, C: np.ndarray):
+    """Eq 7 / Eq 13 / Eq 14 epilogue with the SPEC's
+    design decisions: |Im| for iPLV, ciPLV singularity rule
+    (SPEC.md:259), per-pair effective T, diagonal rules
+    (SPEC.md:151,194)."""
+    if np.any(C <= 0):
+        raise EmptyEffectiveWindowError("all samples masked for some pair")
+    re = G.real / C
+    im = G.imag / C
+    plv = np.abs(G) / C
+    iplv = np.abs(im)
+    den = 1.0 - re * re
+    sing = np.abs(re) >= 1.0 - CIPLV_SINGULAR_EPS
+    ciplv = np.where(sing, 0.0, np.abs(im) / np.sqrt(np.where(sing, 1.0, den)))
+    n = G.shape[0]
+    d = np.arange(n)
+    plv[d, d] = 1.0
+    iplv[d, d] = 0.0
+    ciplv[d, d] = 0.0
+    return plv, iplv, ciplv
+
+
+def plv_family_from_phasors(z, mask, trial_reduce: str = "mean", raw: bool = False):
+    """All three metrics from one Gram per trial.
+
+    z, mask: [N, T, R].  trial_reduce:
+      'none' -> per-trial matrices [N, N, R] (the Appendix's plv(:,:,t));
+      'mean' -> mean over trials of the per-trial metrics [N, N] (default);
+      'pool' -> one Gram over all R*T observations [N, N].
+    Returns dict(plv=..., iplv=..., ciplv=..., n_observations=...).
+    With raw=True also returns the per-trial normalized complex Gram
+    ('cgram', [N, N, R]) used by the tests to separate Gram error from
+    epilogue conditioning.
+    """
+    z = np.asarray(z)
+    N, T, R = z.shape
+    any_mask = bool(np.any(mask))
+    if trial_reduce == "pool":
+        zz = np.transpose(z, (0, 2, 1)).reshape(N, R * T)
+        G = _gram_blocked(zz)
+        if any_mask:
+            u = (~np.transpose(mask, (0, 2, 1)).reshape(N, R * T)).astype(np.float64)
+            C = u @ u.T
+        else:
+            C = np.full((N, N), float(R * T))
+        p, i, c = _metrics_from_gram(G, C)
+        out = dict(plv=p, iplv=i, ciplv=c, n_observations=R * T)
+        if raw:
+            out["cgram"] = (G / C)[:, :, None]
+        return out
+    per = []
+    cg = []
+    for t in range(R):
+        zt = np.ascontiguousarray(z[:, :, t])
+        G = _gram_blocked(zt)
+        if any_mask:
+            u = (~mask[:, :, t]).astype(np.float64)
+            C = u @ u.T
+        else:
+            C = np.full((N, N), float(T))
+        per.append(_metrics_from_gram(G, C))
+        if raw:
+            cg.append(G / C)
+    if trial_reduce == "none":
+        out = dict(plv=np.stack([p[0] for p in per], axis=2),
+                   iplv=np.stack([p[1] for p in per], axis=2),
+                   ciplv=np.stack([p[2] for p in per], axis=2),
+                   n_observations=T)
+    elif trial_reduce == "mean":
+        out = dict(plv=np.mean([p[0] for p in per], axis=0),
+                   iplv=np.mean([p[1] for p in per], axis=0),
+                   ciplv=np.mean([p[2] for p in per], axis=0),
+                   n_observations=T)
+    else:
+        raise ValueError(f"unknown trial_reduce {trial_reduce!r}")
+    if raw:
+        out["cgram"] = np.stack(cg, axis=2)
+    return out
+
+
+def plv_family(x, input_kind: str = "real", amp_floor: float = DEFAULT_AMP_FLOOR,
+               trial_reduce: str = "mean", raw: bool = False):
+    """The whole hot path: [analytic ->] normalise -> Gram -> PLV/iPLV/ciPLV.
+
+    x: [N, T, R] (a 2-D [N, T] array is treated as one trial).
+    input_kind: 'real', 'analytic' or 'phasor'
+    (SPEC.md:186).
+    """
+    x = np.asarray(x)
+    if x.ndim == 2:
+        x = x[:, :, None]
+    if input_kind == "real":
+        z, mask = normalize_phasors(analytic_signal(x), amp_floor)
+    elif input_kind == "analytic":
+        z, mask = normalize_phasors(x, amp_floor)
+    elif input_kind == "phasor":
+        z, mask = phasors_from_unit(x)
+    else:
+        raise ValueError(f"unknown input_kind {input_kind!r}")
+    return plv_family_from_phasors(z, mask, trial_reduce, raw=raw)
+
+
+def plv_matrix(phasors, mode: str = "over_samples", trial_reduce: str = "mean"):
+    """(1/T)|z_i . z_j^H| via one complex product per trial
+    (mode 'over_samples', Eq 7) or per sample over trials (mode 'over_trials',
+    Eq 8 -> [N, N, T])."""
+    z, mask = phasors_from_unit(phasors)
+    if mode == "over_samples":
+        return plv_family_from_phasors(z, mask, trial_reduce)["plv"]
+    if mode == "over_trials":
+        return plv_over_trials(z, mask)
+    raise ValueError(mode)
+
+
+def plv_over_trials(z, mask):
+    """Eq 8: per sample t, Gram over trials.
+    Returns [N, N, T]."""
+    N, T, R = z.shape
+    out = np.empty((N, N, T))
+    u = (~mask).astype(np.float64)
+    for t in range(T):
+        zt = z[:, t, :]
+        G = zt @ zt.conj().T
+        C = u[:, t, :] @ u[:, t, :].T
+        if np.any(C <= 0):
+            raise EmptyEffectiveWindowError("all trials masked for some pair at a sample")
+        p = np.abs(G) / C
+        np.fill_diagonal(p, 1.0)
+        out[:, :, t] = p
+    return out
+
+
+# --------------------------------------------------------------------------
+# Phase-angle implementations: the
+# oracle's own oracle.  Small shapes only (pure-Python pair loop).
+# --------------------------------------------------------------------------
+def plv_reference(phases, mode: str = "over_samples") -> np.ndarray:
+    """Appendix impl 1: two nested loops over pairs.
+
+    phases: [N, T, R] in (-pi, pi].  Returns [N, N, R] (over_samples) with the
+    symmetric part and diagonal filled per ConnectivityMatrix
+    -- the Matlab code fills only c2 > c1.
+    """
+    ph = np.asarray(phases, dtype=np.float64)
+    N, T, R = ph.shape
+    if mode != "over_samples":
+        raise ValueError(mode)
+    plv = np.zeros((N, N, R))
+    for t in range(R):
+        for c1 in range(N):
+            plv[c1, c1, t] = 1.0
+            for c2 in range(c1 + 1, N):
+                d = ph[c1, :, t] - ph[c2, :, t]
+                v = abs(np.mean(np.exp(1j * d)))
+                plv[c1, c2, t] = v
+                plv[c2, c1, t] = v
+    return plv
+
+
+def plv_vectorized(phases, mode: str = "over_samples") -> np.ndarray:
+    """Appendix impl 2: all pairs at once, loop over samples."""
+    ph = np.asarray(phases, dtype=np.float64)
+    N, T, R = ph.shape
+    if mode != "over_samples":
+        raise ValueError(mode)
+    plv = np.zeros((N, N, R))
+    for t in range(R):
+        acc = np.zeros((N, N), dtype=np.complex128)
+        for s in range(T):
+            p = ph[:, s, t]
+            acc += np.exp(1j * (p[:, None] - p[None, :]))
+        plv[:, :, t] = np.abs(acc / T)
+        np.fill_diagonal(plv[:, :, t], 1.0)
+    return plv
+
+
+def make_surrogate(n_signals: int, n_samples: int, n_trials: int, seed: int) -> np.ndarray:
+    """seeded uniform phases -> unit phasors [N, T, R]."""
+    rng = np.random.default_rng(seed)
+    ph = rng.uniform(-np.pi, np.pi, size=(n_signals, n_samples, n_trials))
+    return np.exp(1j * ph)

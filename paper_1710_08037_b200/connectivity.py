@@ -1,0 +1,195 @@
+"""connectivity -- PLV / iPLV / ciPLV on the sm_100a path.
+
+Mirrors the reference module's operations and types:
+  plv_matrix(phasors, mode)  SPEC.md:186-194   Eq 7 / Appendix impl 3
+  iplv(phasors)              SPEC.md:195-203   Eq 13
+  ciplv(phasors)             SPEC.md:204-212   Eq 14
+  ConnectivityMatrix
+plus ``plv_family``, the fused entry point the B200 build is designed around:
+one call runs [Hilbert ->] normalise -> Gram -> all requested metrics from a
+single Gram per trial (north star (1)-(3)).
+
+Every call goes through libphasesync_cuda.so (``_native``); there is no CPU
+fallback.  numpy inputs take the host entry point (copies to/from the GPU
+inside the call, results returned as numpy); CUDA torch tensors take the
+device entry point on the current stream (results returned as torch tensors).
+The CPU phase-angle implementations of the reference (plv_reference /
+plv_vectorized) are test oracles and live in
+``oracle/plv_oracle.py``, not here.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Iterable
+
+import numpy as np
+
+from . import _native, errors
+from ._arrays import describe, dtype_code, is_torch
+
+METRIC_NAMES = {"plv": "PLV", "iplv": "iPLV", "ciplv": "ciPLV", "cre": "cRe", "cim": "cIm"}
+
+
+@dataclass
+class ConnectivityMatrix:
+    """SPEC.md:146-152.  ``values`` is [N, N] (one band, trial-reduced),
+    [B, N, N] (several bands) or [N, N, R] / [B, N, N, R] (trial_reduce='none',
+    the Appendix's ``plv(:,:,t)`` layout)."""
+
+    values: object
+    metric: str
+    n_observations: int
+    meta: dict = field(default_factory=dict)
+
+
+def _infer_kind(code: str, input_kind: str | None) -> str:
+    if input_kind is not None:
+        if input_kind not in _native.INPUT_KINDS:
+            raise ValueError(f"input_kind must be one of {sorted(_native.INPUT_KINDS)}")
+        return input_kind
+    return "real" if code in ("f32", "f64") else "analytic"
+
+
+def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("plv", "iplv", "ciplv"),
+               precision: str = "split", trial_reduce: str = "mean", amp_floor: float = 1e-6,
+               bands: bool = False, shard: tuple[int, int] = (0, 1), out: dict | None = None,
+               timing: bool = False) -> dict:
+    """All requested PLV-family metrics from one Gram per trial.
+
+    x: RealEpochs / AnalyticEpochs / PhasorEpochs data, shape [N, T], [N, T, R]
+       or with ``bands=True`` [B, N, T, R]; numpy (host) or CUDA torch tensor.
+    input_kind: 'real' (Hilbert first), 'analytic' (normalise first) or
+       'phasor' (unit phasors, zeros = masked); default from the dtype.
+    precision: 'split' (tcgen05 fp16x3, fp32 outputs, |err| <= 1e-5) or 'fp64'
+       (DMMA, fp64 outputs, |err| <= 1e-12).
+    trial_reduce: 'mean' (mean of per-trial metrics), 'none' (per trial), or
+       'pool' (one Gram over all R*T observations).  SURVEY D1.
+    shard: (index, count) output-tile sharding; entries owned by
+       other shards are left as allocated (zeros when ``out`` is None).
+    out: optional preallocated outputs {metric: array} (same kind as x).
+    Returns {metric: ConnectivityMatrix}.
+    """
+    if hasattr(x, "data") and not isinstance(x, np.ndarray) and not is_torch(x):
+        x = x.data  # RealEpochs / AnalyticEpochs / PhasorEpochs
+    metrics = tuple(metrics)
+    bad = [m for m in metrics if m not in _native.METRIC_BITS]
+    if bad or not metrics:
+        raise ValueError(f"unknown metrics {bad}; choose from {list(_native.METRIC_BITS)}")
+    if precision not in _native.PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(_native.PRECISIONS)}")
+    if trial_reduce not in _native.TRIAL_REDUCE:
+        raise ValueError(f"trial_reduce must be one of {sorted(_native.TRIAL_REDUCE)}")
+    d = describe(x, bands=bands)
+    kind = _infer_kind(d.dtype, input_kind)
+    B, N, T, R = d.dims
+    per_trial = trial_reduce == "none" and R > 1
+    slots = B * R if per_trial else B
+    fp64 = _native.PRECISIONS[precision] == 1
+    bits = 0
+    for m in metrics:
+        bits |= _native.METRIC_BITS[m]
+
+    a = _native.PlvArgs()
+    a.input = d.ptr
+    a.dtype = dtype_code(d.dtype)
+    a.input_kind = _native.INPUT_KINDS[kind]
+    a.n_bands, a.n_signals, a.n_samples, a.n_trials = B, N, T, R
+    a.stride_band, a.stride_signal, a.stride_sample, a.stride_trial = d.strides
+    a.amp_floor = float(amp_floor)
+    a.metrics = bits
+    a.precision = _native.PRECISIONS[precision]
+    a.trial_reduce = _native.TRIAL_REDUCE[trial_reduce]
+    a.shard_index, a.shard_count = int(shard[0]), int(shard[1])
+
+    outs = {}
+    if d.on_device:
+        import torch
+
+        tdt = torch.float64 if fp64 else torch.float32
+        dev = torch.device("cuda", d.device)
+        for m in metrics:
+            o = None if out is None else out.get(m)
+            if o is None:
+                o = (torch.zeros if shard[1] > 1 else torch.empty)((slots, N, N), dtype=tdt, device=dev)
+            elif o.dtype != tdt or not o.is_contiguous() or o.numel() != slots * N * N:
+                raise ValueError(f"out[{m!r}] must be a contiguous {tdt} tensor with {slots * N * N} elements")
+            outs[m] = o
+        with torch.cuda.device(dev):
+            a.stream = torch.cuda.current_stream(dev).cuda_stream
+            for m in metrics:
+                setattr(a, "out_" + m, outs[m].data_ptr())
+            ctx = _native.context(d.device)
+            ctx.set_timing(timing)
+            res = _native.PlvResult()
+            _native.check(_native.lib().ps_plv_family(ctx.handle, ctypes.byref(a), ctypes.byref(res)))
+    else:
+        ndt = np.float64 if fp64 else np.float32
+        for m in metrics:
+            o = None if out is None else out.get(m)
+            if o is None:
+                o = (np.zeros if shard[1] > 1 else np.empty)((slots, N, N), dtype=ndt)
+            elif o.dtype != ndt or not o.flags.c_contiguous or o.size != slots * N * N:
+                raise ValueError(f"out[{m!r}] must be a C-contiguous {ndt.__name__} array with {slots * N * N} "
+                                 "elements")
+            outs[m] = o
+            setattr(a, "out_" + m, o.ctypes.data)
+        a.stream = None
+        ctx = _native.context(0)
+        ctx.set_timing(timing)
+        res = _native.PlvResult()
+        _native.check(_native.lib().ps_plv_family_host(ctx.handle, ctypes.byref(a), ctypes.byref(res)))
+    info = res.as_dict()
+    info["input_copied"] = bool(info["input_copied"]) or d.copied
+    info["precision"] = precision
+    info["trial_reduce"] = trial_reduce
+    result = {}
+    for m in metrics:
+        v = outs[m]
+        if per_trial:
+            v = v.reshape(B, R, N, N)
+            v = v.permute(0, 2, 3, 1) if is_torch(v) else np.moveaxis(v, 1, 3)
+            if not bands:
+                v = v[0]
+        else:
+            v = v.reshape(B, N, N)
+            if not bands:
+                v = v[0]
+        result[m] = ConnectivityMatrix(values=v, metric=METRIC_NAMES[m],
+                                       n_observations=int(info["n_observations"]), meta=info)
+    return result
+
+
+def _phasor_input(phasors):
+    if hasattr(phasors, "data") and not isinstance(phasors, np.ndarray) and not is_torch(phasors):
+        return phasors.data
+    return phasors
+
+
+def plv_matrix(phasors, mode: str = "over_samples", *, trial_reduce: str = "mean",
+               precision: str = "split") -> ConnectivityMatrix:
+    """(1/T)|z_i z_j^H| for all pairs via one Gram per trial.
+
+    ``phasors``: PhasorEpochs (or its complex data) [N, T, R]; masked samples
+    are exactly 0 and drop out of both the product and the per-pair T
+    (SPEC.md:260).  Mode 'over_trials' (Eq 8, time-resolved PLV) is SURVEY
+    8(f) row 2 and not built yet.
+    """
+    if mode == "over_trials":
+        raise errors.UnsupportedError("mode='over_trials' (Eq 8) is not implemented by this build yet")
+    if mode != "over_samples":
+        raise ValueError("mode must be 'over_samples' or 'over_trials'")
+    return plv_family(_phasor_input(phasors), input_kind="phasor", metrics=("plv",), precision=precision,
+                      trial_reduce=trial_reduce)["plv"]
+
+
+def iplv(phasors, *, trial_reduce: str = "mean", precision: str = "split") -> ConnectivityMatrix:
+    """(1/T)|Im z_i z_j^H| (absolute value per SPEC.md:258)."""
+    return plv_family(_phasor_input(phasors), input_kind="phasor", metrics=("iplv",), precision=precision,
+                      trial_reduce=trial_reduce)["iplv"]
+
+
+def ciplv(phasors, *, trial_reduce: str = "mean", precision: str = "split") -> ConnectivityMatrix:
+    """|Im| / sqrt(1 - Re^2), 0 at the singularity."""
+    return plv_family(_phasor_input(phasors), input_kind="phasor", metrics=("ciplv",), precision=precision,
+                      trial_reduce=trial_reduce)["ciplv"]

@@ -1,0 +1,712 @@
+// Host side of libphasesync_cuda.so: the C ABI declared in include/phasesync.h.
+//
+// Owns per-context resources only (cuFFT plans, growable device workspace,
+// cached TMA descriptors and work-item tables); results are never cached
+// (SPEC.md:548).  Every entry point validates its arguments, launches the
+// sm_100a pipeline on the caller's stream, synchronises that stream and maps
+// device-side status flags to ps_status codes ("errors mapped 1:1").
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/phasesync.h"
+#include "ps_internal.h"
+
+using namespace ps;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+ps_status fail(ps_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define PS_CUDA(call)                                                                                   \
+  do {                                                                                                  \
+    cudaError_t e_ = (call);                                                                            \
+    if (e_ != cudaSuccess)                                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? PS_E_OOM : PS_E_CUDA,                               \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                                  \
+  } while (0)
+
+#define PS_CUFFT(call)                                                                                  \
+  do {                                                                                                  \
+    cufftResult r_ = (call);                                                                            \
+    if (r_ != CUFFT_SUCCESS) return fail(PS_E_CUFFT, std::string(#call) + ": cufft error " + std::to_string((int)r_)); \
+  } while (0)
+
+#define PS_TRY(expr)                 \
+  do {                               \
+    ps_status s_ = (expr);           \
+    if (s_ != PS_OK) return s_;      \
+  } while (0)
+
+struct Buf {
+  void* p = nullptr;
+  size_t n = 0;
+};
+
+using PlanKey = std::tuple<int, long long, long long, int, int>;  // T, batch, idist, double, dir
+
+struct TmapKey {
+  const void* base;
+  long long T, N, U, pitch;
+  bool operator<(const TmapKey& o) const {
+    return std::tie(base, T, N, U, pitch) < std::tie(o.base, o.T, o.N, o.U, o.pitch);
+  }
+};
+
+}  // namespace
+
+struct ps_ctx {
+  int device = 0;
+  int num_sms = 148;
+  bool timing = false;
+  std::mutex mu;
+  std::map<PlanKey, cufftHandle> plans;
+  Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout;
+  DevStatus* d_status = nullptr;
+  DevStatus* h_status = nullptr;  // pinned
+  std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
+  std::vector<Item> h_items;
+  Item* h_items_pinned = nullptr;
+  size_t h_items_cap = 0;
+  cudaEvent_t ev[8] = {};
+  int launches = 0;
+};
+
+namespace {
+
+ps_status ensure(Buf& b, size_t bytes) {
+  if (bytes <= b.n) return PS_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.n = 0;
+  size_t want = std::max(bytes, (size_t)256);
+  cudaError_t e = cudaMalloc(&b.p, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(PS_E_OOM, "cudaMalloc(" + std::to_string(want) + " bytes) failed: " + cudaGetErrorString(e));
+  }
+  b.n = want;
+  return PS_OK;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+long long round_up(long long a, long long b) { return (a + b - 1) / b * b; }
+
+struct Geometry {
+  long long B, N, T, R, rows;
+  bool cdouble;   // compute type of the Hilbert / normalise stage
+  bool split;     // split fp16 planes vs fp64 planes
+  bool complex_in;
+  int in_double;  // input scalar is double
+  long long pitch;
+  long long plane_stride;
+};
+
+ps_status validate(const ps_plv_args* a, Geometry& g) {
+  if (!a) return fail(PS_E_INVALID, "args is NULL");
+  if (!a->input) return fail(PS_E_INVALID, "input pointer is NULL");
+  if (a->n_bands < 1 || a->n_signals < 1 || a->n_trials < 1)
+    return fail(PS_E_SHAPE, "expected axes [n_signals x n_samples x n_trials] with n_signals >= 1, n_trials >= 1 "
+                            "(SPEC.md:31)");
+  if (a->n_samples < 2) return fail(PS_E_SHAPE, "n_samples must be >= 2 (SPEC.md:31)");
+  if (a->dtype < PS_F32 || a->dtype > PS_C128) return fail(PS_E_INVALID, "unknown dtype");
+  const bool cplx = a->dtype == PS_C64 || a->dtype == PS_C128;
+  if (a->input_kind == PS_INPUT_REAL && cplx)
+    return fail(PS_E_INVALID, "real input_kind requires a real dtype (f32/f64)");
+  if (a->input_kind != PS_INPUT_REAL && !cplx)
+    return fail(PS_E_INVALID, "analytic/phasor input_kind requires a complex dtype (c64/c128)");
+  if (a->input_kind < 0 || a->input_kind > 2) return fail(PS_E_INVALID, "unknown input_kind");
+  if (a->precision != PS_PREC_SPLIT_F16X3 && a->precision != PS_PREC_FP64)
+    return fail(PS_E_INVALID, "unknown precision");
+  if (a->trial_reduce < 0 || a->trial_reduce > 2) return fail(PS_E_INVALID, "unknown trial_reduce");
+  if (!(a->amp_floor >= 0.0)) return fail(PS_E_INVALID, "amp_floor must be >= 0");
+  if (a->n_signals > (1 << 30) || a->n_samples > (1LL << 31) - 1)
+    return fail(PS_E_SHAPE, "n_signals / n_samples exceed the supported range");
+  g.B = a->n_bands;
+  g.N = a->n_signals;
+  g.T = a->n_samples;
+  g.R = a->n_trials;
+  g.rows = g.B * g.R * g.N;
+  g.complex_in = cplx;
+  g.in_double = (a->dtype == PS_F64 || a->dtype == PS_C128) ? 1 : 0;
+  g.split = a->precision == PS_PREC_SPLIT_F16X3;
+  g.cdouble = g.in_double || !g.split;
+  g.pitch = g.split ? round_up(g.T, 8) : round_up(g.T, 16);
+  g.plane_stride = g.rows * g.pitch;
+  return PS_OK;
+}
+
+SrcDesc make_src(const ps_plv_args* a, const Geometry& g, const void* ptr) {
+  SrcDesc s;
+  s.ptr = ptr;
+  s.kind = a->input_kind;
+  s.is_double = g.in_double;
+  s.N = g.N;
+  s.R = g.R;
+  s.B = g.B;
+  s.T = g.T;
+  s.s_sig = a->stride_signal;
+  s.s_samp = a->stride_sample;
+  s.s_trial = a->stride_trial;
+  s.s_band = a->stride_band;
+  s.hbuf = nullptr;
+  s.h_row0 = 0;
+  return s;
+}
+
+// Rows directly consumable by a single batched cuFFT plan: sample stride 1,
+// dtype == compute type and row r at offset r * stride_signal.
+bool fft_direct(const ps_plv_args* a, const Geometry& g) {
+  if (a->stride_sample != 1) return false;
+  if ((bool)g.in_double != g.cdouble) return false;
+  const long long s = a->stride_signal;
+  if (s < g.T) return false;
+  if (g.R > 1 && a->stride_trial != g.N * s) return false;
+  if (g.B > 1 && a->stride_band != g.R * g.N * s) return false;
+  return true;
+}
+
+ps_status get_plan(ps_ctx* c, int T, long long batch, long long idist, bool dbl, int dir, cufftHandle* out) {
+  PlanKey k{T, batch, idist, dbl ? 1 : 0, dir};
+  auto it = c->plans.find(k);
+  if (it != c->plans.end()) {
+    *out = it->second;
+    return PS_OK;
+  }
+  cufftHandle h;
+  PS_CUFFT(cufftCreate(&h));
+  long long n[1] = {T};
+  long long nb = T / 2 + 1;
+  size_t ws = 0;
+  cufftResult r;
+  if (dir == 0) {  // R2C / D2Z: input real rows of distance idist, output half spectra
+    long long inembed[1] = {idist}, onembed[1] = {nb};
+    r = cufftMakePlanMany64(h, 1, n, inembed, 1, idist, onembed, 1, nb, dbl ? CUFFT_D2Z : CUFFT_R2C, batch, &ws);
+  } else {         // C2R / Z2D: half spectra -> dense real rows of length T
+    long long inembed[1] = {nb}, onembed[1] = {T};
+    r = cufftMakePlanMany64(h, 1, n, inembed, 1, nb, onembed, 1, T, dbl ? CUFFT_Z2D : CUFFT_C2R, batch, &ws);
+  }
+  if (r != CUFFT_SUCCESS) {
+    cufftDestroy(h);
+    return fail(PS_E_CUFFT, "cufftMakePlanMany64 failed: " + std::to_string((int)r));
+  }
+  c->plans[k] = h;
+  *out = h;
+  return PS_OK;
+}
+
+long long hilbert_chunk_rows(const Geometry& g) {
+  const long long target = 1LL << 27;  // samples per chunk (bounds spectrum + H workspace)
+  long long rc = target / g.T;
+  rc = std::max(1LL, std::min(rc, g.rows));
+  return rc;
+}
+
+// Hilbert stage for rows [row0, row0+nr): leaves H{x} (compute type) in c->hbuf.
+ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const SrcDesc& src, long long row0,
+                        long long nr, cudaStream_t st, bool* copied) {
+  const size_t es = g.cdouble ? 8 : 4;
+  const long long nb = g.T / 2 + 1;
+  PS_TRY(ensure(c->spec, (size_t)nr * nb * 2 * es));
+  PS_TRY(ensure(c->hbuf, (size_t)nr * g.T * es));
+  const void* in = nullptr;
+  long long idist = g.T;
+  if (fft_direct(a, g)) {
+    in = static_cast<const char*>(src.ptr) + (size_t)row0 * a->stride_signal * es;
+    idist = a->stride_signal;
+  } else {
+    PS_TRY(ensure(c->xw, (size_t)nr * g.T * es));
+    PS_CUDA(launch_pack_real(src, row0, nr, c->xw.p, g.cdouble ? 1 : 0, st));
+    c->launches++;
+    in = c->xw.p;
+    *copied = true;
+  }
+  cufftHandle fwd, inv;
+  PS_TRY(get_plan(c, (int)g.T, nr, idist, g.cdouble, 0, &fwd));
+  PS_TRY(get_plan(c, (int)g.T, nr, g.T, g.cdouble, 1, &inv));
+  PS_CUFFT(cufftSetStream(fwd, st));
+  PS_CUFFT(cufftSetStream(inv, st));
+  if (g.cdouble) {
+    PS_CUFFT(cufftExecD2Z(fwd, (cufftDoubleReal*)in, (cufftDoubleComplex*)c->spec.p));
+  } else {
+    PS_CUFFT(cufftExecR2C(fwd, (cufftReal*)in, (cufftComplex*)c->spec.p));
+  }
+  PS_CUDA(launch_hilbert_spectrum(c->spec.p, nr, (int)g.T, g.cdouble ? 1 : 0, st));
+  c->launches++;
+  if (g.cdouble) {
+    PS_CUFFT(cufftExecZ2D(inv, (cufftDoubleComplex*)c->spec.p, (cufftDoubleReal*)c->hbuf.p));
+  } else {
+    PS_CUFFT(cufftExecC2R(inv, (cufftComplex*)c->spec.p, (cufftReal*)c->hbuf.p));
+  }
+  return PS_OK;
+}
+
+ps_status reset_status(ps_ctx* c, cudaStream_t st) {
+  PS_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(DevStatus), st));
+  return PS_OK;
+}
+
+ps_status read_status(ps_ctx* c, cudaStream_t st) {
+  PS_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  PS_CUDA(cudaStreamSynchronize(st));
+  const int f = c->h_status->flags;
+  if (f & FLAG_TIMEOUT) return fail(PS_E_INTERNAL, "device pipeline timeout");
+  if (f & FLAG_NONFINITE) return fail(PS_E_INVALID, "input contains non-finite values (SPEC.md:32)");
+  if (f & FLAG_ALL_MASKED)
+    return fail(PS_E_ALL_MASKED, "every sample of some signal/trial fell below the amplitude floor");
+  if (f & FLAG_EMPTY_WINDOW) return fail(PS_E_EMPTY_WINDOW, "all samples are masked for at least one signal pair");
+  return PS_OK;
+}
+
+// Normalisation of all rows into `out` (fmt 0/1: planes, fmt 2: dense complex).
+ps_status prepare_phasors(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const void* in_ptr, void* out,
+                          int fmt, long long pitch, long long plane_stride, cudaStream_t st, bool* copied) {
+  PS_TRY(ensure(c->rowstat, (size_t)g.rows * 2 * sizeof(unsigned long long)));
+  PS_TRY(ensure(c->maskcount, (size_t)g.rows * sizeof(int)));
+  unsigned long long* rs = static_cast<unsigned long long*>(c->rowstat.p);
+  PS_CUDA(cudaMemsetAsync(rs, 0xFF, (size_t)g.rows * sizeof(unsigned long long), st));
+  PS_CUDA(cudaMemsetAsync(rs + g.rows, 0, (size_t)g.rows * sizeof(unsigned long long), st));
+  SrcDesc src = make_src(a, g, in_ptr);
+  const size_t ces = g.cdouble ? 8 : 4;
+  auto out_at = [&](long long row0) -> void* {
+    if (fmt != 2) return out;
+    return static_cast<char*>(out) + (size_t)row0 * g.T * 2 * ces;
+  };
+  if (a->input_kind == PS_INPUT_REAL) {
+    const long long rc = hilbert_chunk_rows(g);
+    for (long long row0 = 0; row0 < g.rows; row0 += rc) {
+      const long long nr = std::min(rc, g.rows - row0);
+      PS_TRY(hilbert_chunk(c, a, g, src, row0, nr, st, copied));
+      src.hbuf = c->hbuf.p;
+      src.h_row0 = row0;
+      PS_CUDA(launch_normalize_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs,
+                                   g.rows, c->d_status, st));
+      PS_CUDA(launch_fixup_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
+                               static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
+      c->launches += 2;
+    }
+  } else {
+    PS_CUDA(launch_normalize_fmt(src, 0, g.rows, out, fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
+                                 c->d_status, st));
+    PS_CUDA(launch_fixup_fmt(src, 0, g.rows, out, fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
+                             static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
+    c->launches += 2;
+  }
+  return PS_OK;
+}
+
+// Upper-triangle tile list (tiles that contain at least one pair i <= j).
+void build_tiles(long long N, int bm, int bn, std::vector<std::pair<int, int>>& tiles) {
+  tiles.clear();
+  const int nj = (int)((N + bn - 1) / bn), ni = (int)((N + bm - 1) / bm);
+  for (int J = 0; J < nj; ++J) {
+    const long long jmax = std::min<long long>((long long)J * bn + bn, N) - 1;
+    for (int I = 0; I < ni; ++I)
+      if ((long long)I * bm <= jmax) tiles.emplace_back(I, J);
+  }
+}
+
+int choose_groups(long long items_per_group, int R, int num_sms) {
+  // pick the number of trial groups that best fills whole waves of SMs
+  int best_g = 1;
+  double best_eff = -1.0;
+  for (int G = 1; G <= R; ++G) {
+    const int Rg = (R + G - 1) / G;
+    const int Ge = (R + Rg - 1) / Rg;
+    if (Ge != G) continue;
+    const long long items = items_per_group * G;
+    const long long waves = (items + num_sms - 1) / num_sms;
+    const double eff = (double)items * Rg / ((double)waves * num_sms * Rg);
+    // each item costs Rg trials; total time ~ waves * Rg
+    const double t = (double)waves * Rg;
+    const double score = 1.0 / t;  // higher is better
+    (void)eff;
+    if (score > best_eff * (1.0 + 1e-9)) {
+      best_eff = score;
+      best_g = G;
+    }
+  }
+  return best_g;
+}
+
+}  // namespace
+
+template <typename S>
+__global__ void mask_from_zero_kernel(const S* z, size_t n, uint8_t* m) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    m[e] = (z[2 * e] == S(0) && z[2 * e + 1] == S(0)) ? 1 : 0;
+}
+
+static cudaError_t ps_mask_from_zero(const void* z, int is_double, size_t n, uint8_t* m, cudaStream_t st) {
+  const int grid = (int)std::min<size_t>((n + 255) / 256, 148 * 16);
+  if (is_double) mask_from_zero_kernel<double><<<grid, 256, 0, st>>>((const double*)z, n, m);
+  else mask_from_zero_kernel<float><<<grid, 256, 0, st>>>((const float*)z, n, m);
+  return cudaGetLastError();
+}
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int ps_abi_version(void) { return PS_ABI_VERSION; }
+
+int64_t ps_tile_count(int64_t n_signals, int32_t precision) {
+  if (n_signals < 1) return 0;
+  std::vector<std::pair<int, int>> tiles;
+  const bool split = precision == PS_PREC_SPLIT_F16X3;
+  build_tiles(n_signals, split ? kSplitBM : kF64BM, split ? kSplitBN : kF64BN, tiles);
+  return (int64_t)tiles.size();
+}
+
+int32_t ps_pair_shard(int64_t n_signals, int32_t precision, int32_t shard_count, int64_t i, int64_t j) {
+  if (n_signals < 1 || i < 0 || j < 0 || i >= n_signals || j >= n_signals) return -1;
+  if (shard_count < 1) shard_count = 1;
+  if (i > j) std::swap(i, j);
+  const bool split = precision == PS_PREC_SPLIT_F16X3;
+  const int bm = split ? kSplitBM : kF64BM, bn = split ? kSplitBN : kF64BN;
+  const long long ni = (n_signals + bm - 1) / bm;
+  const long long I = i / bm, J = j / bn;
+  long long t = 0;
+  for (long long Jp = 0; Jp < J; ++Jp) {
+    const long long jmax = std::min<long long>(Jp * bn + bn, n_signals) - 1;
+    t += std::min<long long>(ni, jmax / bm + 1);
+  }
+  t += I;
+  return (int32_t)(t % shard_count);
+}
+
+const char* ps_last_error(void) { return g_last_error.c_str(); }
+
+ps_status ps_ctx_create(int device, ps_ctx** out) {
+  if (!out) return fail(PS_E_INVALID, "out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  PS_CUDA(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(PS_E_INVALID, "device index out of range");
+  PS_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  PS_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10) return fail(PS_E_UNSUPPORTED, std::string("sm_100a device required, found ") + prop.name);
+  ps_ctx* c = new ps_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  if (cudaMalloc(&c->d_status, sizeof(DevStatus)) != cudaSuccess ||
+      cudaMallocHost(&c->h_status, sizeof(DevStatus)) != cudaSuccess) {
+    delete c;
+    return fail(PS_E_OOM, "status allocation failed");
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  *out = c;
+  return PS_OK;
+}
+
+ps_status ps_ctx_destroy(ps_ctx* c) {
+  if (!c) return PS_OK;
+  cudaSetDevice(c->device);
+  for (auto& kv : c->plans) cufftDestroy(kv.second);
+  for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
+                 &c->hout})
+    if (b->p) cudaFree(b->p);
+  if (c->d_status) cudaFree(c->d_status);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  if (c->h_items_pinned) cudaFreeHost(c->h_items_pinned);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  delete c;
+  return PS_OK;
+}
+
+ps_status ps_ctx_set_timing(ps_ctx* c, int enable) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  c->timing = enable != 0;
+  return PS_OK;
+}
+
+ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  Geometry g;
+  PS_TRY(validate(a, g));
+  const uint32_t metrics = a->metrics;
+  if (metrics == 0) return fail(PS_E_INVALID, "no metric requested");
+  void* outs[5] = {a->out_plv, a->out_iplv, a->out_ciplv, a->out_cre, a->out_cim};
+  for (int m = 0; m < 5; ++m) {
+    const bool want = (metrics >> m) & 1u;
+    if (want && !outs[m]) return fail(PS_E_INVALID, "output pointer missing for a requested metric");
+    if (!want) outs[m] = nullptr;
+  }
+  const int shard_count = a->shard_count < 1 ? 1 : a->shard_count;
+  const int shard_index = a->shard_index;
+  if (shard_index < 0 || shard_index >= shard_count) return fail(PS_E_INVALID, "shard_index out of range");
+  if (g.rows > (long long)INT32_MAX || g.B * g.R > 65535) return fail(PS_E_SHAPE, "too many rows for one call");
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(a->stream);
+  c->launches = 0;
+  bool copied = false;
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[0], st));
+
+  // ---- phasor planes --------------------------------------------------------
+  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  PS_TRY(ensure(c->planes, plane_bytes));
+  PS_TRY(reset_status(c, st));
+  PS_TRY(prepare_phasors(c, a, g, a->input, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride, st, &copied));
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[1], st));
+
+  // ---- work items -----------------------------------------------------------
+  const int bm = g.split ? kSplitBM : kF64BM;
+  const int bn = g.split ? kSplitBN : kF64BN;
+  std::vector<std::pair<int, int>> tiles;
+  build_tiles(g.N, bm, bn, tiles);
+  std::vector<std::pair<int, int>> mine;
+  for (size_t t = 0; t < tiles.size(); ++t)
+    if ((int)(t % shard_count) == shard_index) mine.push_back(tiles[t]);
+  const bool pool = a->trial_reduce == PS_TRIALS_POOL;
+  int G = 1, slot_mode = 1, mean_div = 1;
+  if (pool || g.R == 1) {
+    G = 1;
+    slot_mode = 1;
+  } else if (a->trial_reduce == PS_TRIALS_NONE) {
+    G = (int)g.R;
+    slot_mode = 0;
+  } else {
+    G = shard_count > 1 ? 1 : choose_groups((long long)mine.size() * g.B, (int)g.R, c->num_sms);
+    slot_mode = G == 1 ? 1 : 2;
+    mean_div = G == 1 ? (int)g.R : 1;
+  }
+  const int Rg = (int)((g.R + G - 1) / G);
+  std::vector<Item>& items = c->h_items;
+  items.clear();
+  for (int b = 0; b < g.B; ++b)
+    for (int gi = 0; gi < G; ++gi)
+      for (auto& t : mine) items.push_back(Item{b, gi, t.first, t.second});
+  const size_t ibytes = std::max<size_t>(items.size(), 1) * sizeof(Item);
+  if (c->h_items_cap < ibytes) {
+    if (c->h_items_pinned) cudaFreeHost(c->h_items_pinned);
+    c->h_items_pinned = nullptr;
+    c->h_items_cap = 0;
+    PS_CUDA(cudaMallocHost(&c->h_items_pinned, ibytes));
+    c->h_items_cap = ibytes;
+  }
+  // the previous call synchronised its stream, so the pinned staging is free
+  if (!items.empty()) std::memcpy(c->h_items_pinned, items.data(), items.size() * sizeof(Item));
+  PS_TRY(ensure(c->items, ibytes));
+  if (!items.empty())
+    PS_CUDA(cudaMemcpyAsync(c->items.p, c->h_items_pinned, items.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
+
+  GramParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.N = (int)g.N;
+  p.T = (int)g.T;
+  p.R = (int)g.R;
+  p.B = (int)g.B;
+  p.Tp = (int)g.pitch;
+  p.rows = (int)g.rows;
+  p.Rg = Rg;
+  p.G = G;
+  p.pool = pool ? 1 : 0;
+  p.n_items = (int)items.size();
+  p.items = static_cast<const Item*>(c->items.p);
+  p.slot_mode = slot_mode;
+  p.mean_div = mean_div;
+  p.maskcount = static_cast<const int*>(c->maskcount.p);
+  p.planes = c->planes.p;
+  p.plane_stride = g.plane_stride;
+  p.status = c->d_status;
+  p.illcond_tol = 1e-6f;
+  const size_t oes = g.split ? 4 : 8;
+  const long long nn = g.N * g.N;
+  void* final_outs[5];
+  std::memcpy(final_outs, outs, sizeof(outs));
+  if (slot_mode == 2) {
+    // trial-group partial sums, reduced in a fixed order afterwards
+    const size_t per = (size_t)g.B * G * nn * oes;
+    PS_TRY(ensure(c->gws, per * 5));
+    for (int m = 0; m < 5; ++m) outs[m] = outs[m] ? static_cast<char*>(c->gws.p) + m * per : nullptr;
+  }
+  p.out_plv = outs[0];
+  p.out_iplv = outs[1];
+  p.out_ciplv = outs[2];
+  p.out_cre = outs[3];
+  p.out_cim = outs[4];
+  const int grid = (int)std::min<long long>((long long)items.size(), c->num_sms);
+  if (g.split) {
+    TmapKey key{c->planes.p, g.T, g.N, g.B * g.R, g.pitch};
+    auto it = c->tmaps.find(key);
+    if (it == c->tmaps.end()) {
+      auto enc = encode_fn();
+      if (!enc) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+      CUtensorMap ta, tb;
+      cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), 4};
+      cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 2, (cuuint64_t)(g.N * g.pitch * 2),
+                               (cuuint64_t)(g.plane_stride * 2)};
+      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)kSplitBM, 1, 4};
+      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)kSplitBN, 1, 4};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                     : kSplitBK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
+      CUresult r1 = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxA, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CUresult r2 = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxB, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+        return fail(PS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" +
+                                   std::to_string((int)r2));
+      if (c->tmaps.size() > 64) c->tmaps.clear();
+      it = c->tmaps.emplace(key, std::make_pair(ta, tb)).first;
+    }
+    PS_CUDA(launch_gram_split(&it->second.first, &it->second.second, p, grid, st));
+  } else {
+    PS_CUDA(launch_gram_f64(p, grid, st));
+  }
+  c->launches++;
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
+  if (slot_mode == 2) {
+    PS_CUDA(launch_group_reduce(c->gws.p, G, nn, 5, final_outs, g.B * nn, (int)g.R, g.split ? 0 : 1, st));
+    for (int m = 0; m < 5; ++m) c->launches += final_outs[m] ? 1 : 0;
+  }
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[3], st));
+  ps_status s = read_status(c, st);
+  if (res) {
+    std::memset(res, 0, sizeof(*res));
+    res->n_observations = pool ? g.T * g.R : g.T;
+    res->n_masked_samples = (int64_t)c->h_status->n_masked;
+    res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->input_copied = copied ? 1 : 0;
+    res->n_kernel_launches = c->launches;
+    if (c->timing) {
+      cudaEventElapsedTime(&res->ms_normalize, c->ev[0], c->ev[1]);
+      cudaEventElapsedTime(&res->ms_gram, c->ev[1], c->ev[2]);
+      cudaEventElapsedTime(&res->ms_finish, c->ev[2], c->ev[3]);
+    }
+  }
+  return s;
+}
+
+ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  Geometry g;
+  PS_TRY(validate(a, g));
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(a->stream);
+  // span of the (possibly strided) host input, in elements
+  const long long esz = (a->dtype == PS_F32) ? 4 : (a->dtype == PS_F64 || a->dtype == PS_C64) ? 8 : 16;
+  long long span = 1;
+  const long long dims[4] = {g.B, g.N, g.T, g.R};
+  const long long strides[4] = {a->stride_band, a->stride_signal, a->stride_sample, a->stride_trial};
+  for (int k = 0; k < 4; ++k) {
+    if (dims[k] > 1 && strides[k] < 0) return fail(PS_E_INVALID, "negative strides are not supported");
+    span += (dims[k] - 1) * strides[k];
+  }
+  PS_TRY(ensure(c->hin, (size_t)span * esz));
+  PS_CUDA(cudaMemcpyAsync(c->hin.p, a->input, (size_t)span * esz, cudaMemcpyHostToDevice, st));
+  const bool pool = a->trial_reduce == PS_TRIALS_POOL;
+  const long long slots = (a->trial_reduce == PS_TRIALS_NONE && !pool) ? g.B * g.R : g.B;
+  const size_t oes = g.split ? 4 : 8;
+  const size_t out_bytes = (size_t)slots * g.N * g.N * oes;
+  void* houts[5] = {a->out_plv, a->out_iplv, a->out_ciplv, a->out_cre, a->out_cim};
+  int nout = 0;
+  for (int m = 0; m < 5; ++m)
+    if (((a->metrics >> m) & 1u) && houts[m]) ++nout;
+  PS_TRY(ensure(c->hout, out_bytes * std::max(nout, 1)));
+  ps_plv_args d = *a;
+  d.input = c->hin.p;
+  void** douts[5] = {&d.out_plv, &d.out_iplv, &d.out_ciplv, &d.out_cre, &d.out_cim};
+  int k = 0;
+  for (int m = 0; m < 5; ++m) {
+    if (((a->metrics >> m) & 1u) && houts[m]) *douts[m] = static_cast<char*>(c->hout.p) + (size_t)(k++) * out_bytes;
+    else *douts[m] = nullptr;
+  }
+  ps_status s = ps_plv_family(c, &d, res);
+  if (s != PS_OK) return s;
+  k = 0;
+  for (int m = 0; m < 5; ++m)
+    if (((a->metrics >> m) & 1u) && houts[m])
+      PS_CUDA(cudaMemcpyAsync(houts[m], static_cast<char*>(c->hout.p) + (size_t)(k++) * out_bytes, out_bytes,
+                              cudaMemcpyDeviceToHost, st));
+  PS_CUDA(cudaStreamSynchronize(st));
+  return PS_OK;
+}
+
+ps_status ps_analytic_signal(ps_ctx* c, const ps_plv_args* a0, void* out) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  if (!out) return fail(PS_E_INVALID, "out is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  ps_plv_args a = *a0;
+  a.input_kind = PS_INPUT_REAL;
+  a.precision = PS_PREC_SPLIT_F16X3;  // compute type follows the input dtype
+  Geometry g;
+  PS_TRY(validate(&a, g));
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(a.stream);
+  SrcDesc src = make_src(&a, g, a.input);
+  bool copied = false;
+  PS_TRY(reset_status(c, st));
+  const long long rc = hilbert_chunk_rows(g);
+  const size_t es = g.cdouble ? 8 : 4;
+  for (long long row0 = 0; row0 < g.rows; row0 += rc) {
+    const long long nr = std::min(rc, g.rows - row0);
+    PS_TRY(hilbert_chunk(c, &a, g, src, row0, nr, st, &copied));
+    src.hbuf = c->hbuf.p;
+    src.h_row0 = row0;
+    PS_CUDA(launch_analytic_out(src, row0, nr, static_cast<char*>(out) + (size_t)row0 * g.T * 2 * es, st));
+  }
+  return read_status(c, st);
+}
+
+ps_status ps_normalize_phasors(ps_ctx* c, const ps_plv_args* a, void* out, uint8_t* mask_out) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  if (!out) return fail(PS_E_INVALID, "out is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  ps_plv_args aa = *a;
+  aa.precision = PS_PREC_SPLIT_F16X3;  // compute type follows the input dtype
+  Geometry g;
+  PS_TRY(validate(&aa, g));
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(aa.stream);
+  bool copied = false;
+  PS_TRY(reset_status(c, st));
+  PS_TRY(prepare_phasors(c, &aa, g, aa.input, out, 2, g.T, 0, st, &copied));
+  ps_status s = read_status(c, st);
+  if (s != PS_OK) return s;
+  if (mask_out) {
+    // masked samples are exactly 0+0i; unmasked unit phasors never are
+    const size_t n = (size_t)g.rows * g.T;
+    PS_CUDA(ps_mask_from_zero(out, g.cdouble ? 1 : 0, n, mask_out, st));
+    PS_CUDA(cudaStreamSynchronize(st));
+  }
+  return PS_OK;
+}
+
+}  // extern "C"
+

@@ -1,0 +1,156 @@
+// Fused PLV / iPLV / ciPLV epilogue shared by the two Gram kernels.
+//
+// Given one Gram entry G_ij = sum_t z_i(t) conj(z_j(t)) (Eq 7)
+// and the effective observation count T_ij, emit the requested
+// metrics straight from the accumulator registers -- the complex N x N Gram
+// never round-trips HBM (north star (3)).
+//   PLV   = |G|/T                          Eq 7
+//   iPLV  = |Im G|/T                       Eq 13  SPEC.md:198, abs per :258
+//   ciPLV = |Im|/sqrt(1 - Re^2)            Eq 14  SPEC.md:207, singular -> 0 :259
+// Diagonal: PLV = 1, iPLV = ciPLV = 0.
+#pragma once
+#include <cuda_fp16.h>
+#include "ps_internal.h"
+
+namespace ps {
+
+template <typename S>
+struct PairMetrics {
+  S plv, iplv, ciplv, cre, cim;
+};
+
+// SPLIT: fp32 path. 1 - Re^2 is formed as (1-|Re|)(1+|Re|) (exact for
+// |Re| >= 1/2), PLV and ciPLV are clamped to <= 1; the SPEC's
+// 1e-12 singularity threshold is below fp32 resolution, so "singular" means
+// 1 - |Re| rounds to <= 0.  FP64 path: the SPEC rule verbatim.
+template <typename S, bool SPLIT>
+__device__ __forceinline__ PairMetrics<S> pair_metrics(S gre, S gim, S inv_t) {
+  PairMetrics<S> m;
+  const S cre = gre * inv_t, cim = gim * inv_t;
+  const S are = fabs(cre), aim = fabs(cim);
+  S plv = sqrt(cre * cre + cim * cim);
+  S ci;
+  if (SPLIT) {
+    plv = plv > S(1) ? S(1) : plv;
+    const S d = (S(1) - are) * (S(1) + are);
+    ci = d > S(0) ? aim / sqrt(d) : S(0);
+    ci = ci > S(1) ? S(1) : ci;
+  } else {
+    ci = (are >= S(1) - S(1e-12)) ? S(0) : aim / sqrt(S(1) - cre * cre);
+  }
+  m.plv = plv;
+  m.iplv = aim;
+  m.ciplv = ci;
+  m.cre = cre;
+  m.cim = cim;
+  return m;
+}
+
+template <typename S>
+__device__ __forceinline__ PairMetrics<S> diag_metrics() {
+  PairMetrics<S> m;
+  m.plv = S(1);
+  m.iplv = S(0);
+  m.ciplv = S(0);
+  m.cre = S(1);
+  m.cim = S(0);
+  return m;
+}
+
+// Is sample t of row `row` masked?  Masked samples are exactly 0 in every
+// plane; an unmasked unit phasor has max(|re|,|im|) >= 1/sqrt(2), so its hi
+// parts can never both be zero.
+template <bool SPLIT>
+__device__ __forceinline__ bool sample_masked(const GramParams& p, long long row, long long t) {
+  const long long idx = row * p.Tp + t;
+  if (SPLIT) {
+    const __half* h = static_cast<const __half*>(p.planes);
+    return __half2float(h[idx]) == 0.0f && __half2float(h[2 * p.plane_stride + idx]) == 0.0f;
+  } else {
+    const double* d = static_cast<const double*>(p.planes);
+    return d[idx] == 0.0 && d[p.plane_stride + idx] == 0.0;
+  }
+}
+
+// Effective observation count of pair (i, j) over units [u0, u0 + nu)
+// (SPEC.md:260): samples unmasked in both signals.  Only called when the
+// fixup kernel reported masked samples.
+template <bool SPLIT>
+__device__ __noinline__ long long effective_T(const GramParams& p, int u0, int nu, int i, int j) {
+  long long tot = 0;
+  for (int u = u0; u < u0 + nu; ++u) {
+    const long long ri = (long long)u * p.N + i, rj = (long long)u * p.N + j;
+    const int mi = p.maskcount[ri], mj = p.maskcount[rj];
+    long long c = (long long)p.T - mi - mj;
+    if (mi > 0 && mj > 0) {
+      long long both = 0;
+      for (long long t = 0; t < p.T; ++t)
+        both += (sample_masked<SPLIT>(p, ri, t) && sample_masked<SPLIT>(p, rj, t)) ? 1 : 0;
+      c += both;
+    }
+    tot += c;
+  }
+  return tot;
+}
+
+// Accumulating store of one metric value into slot `base` at (i, j); the
+// mirror (j, i) is written at the last round of the slot (negated for the
+// antisymmetric signed imaginary part).
+template <typename S>
+__device__ __forceinline__ void emit(S* base, long long N, int i, int j, S v, bool first, bool last, int div,
+                                     bool anti) {
+  const long long idx = (long long)i * N + j;
+  S acc = first ? v : base[idx] + v;
+  if (last && div != 1) acc = acc / S(div);
+  base[idx] = acc;
+  if (last && i != j) base[(long long)j * N + i] = anti ? -acc : acc;
+}
+
+template <typename S>
+__device__ __forceinline__ void emit_all(const GramParams& p, long long slot, int i, int j,
+                                         const PairMetrics<S>& m, bool first, bool last) {
+  const long long off = slot * (long long)p.N * p.N;
+  const long long N = p.N;
+  if (p.out_plv) emit<S>(static_cast<S*>(p.out_plv) + off, N, i, j, m.plv, first, last, p.mean_div, false);
+  if (p.out_iplv) emit<S>(static_cast<S*>(p.out_iplv) + off, N, i, j, m.iplv, first, last, p.mean_div, false);
+  if (p.out_ciplv)
+    emit<S>(static_cast<S*>(p.out_ciplv) + off, N, i, j, m.ciplv, first, last, p.mean_div, false);
+  if (p.out_cre) emit<S>(static_cast<S*>(p.out_cre) + off, N, i, j, m.cre, first, last, p.mean_div, false);
+  if (p.out_cim) emit<S>(static_cast<S*>(p.out_cim) + off, N, i, j, m.cim, first, last, p.mean_div, true);
+}
+
+// Round bookkeeping common to both kernels: which slot a (item, trial) round
+// writes and whether it is the first / last contribution to that slot.
+struct RoundInfo {
+  long long slot;
+  bool first, last;
+  int u0, nu;  // units covered by the round's Gram
+};
+
+__device__ __forceinline__ RoundInfo round_info(const GramParams& p, const Item& w, int r, int r0, int r1) {
+  RoundInfo ri;
+  if (p.pool) {
+    ri.slot = w.b;
+    ri.first = ri.last = true;
+    ri.u0 = w.b * p.R;
+    ri.nu = p.R;
+    return ri;
+  }
+  ri.u0 = w.b * p.R + r;
+  ri.nu = 1;
+  if (p.slot_mode == 0) {
+    ri.slot = (long long)w.b * p.R + r;
+    ri.first = ri.last = true;
+  } else if (p.slot_mode == 1) {
+    ri.slot = w.b;
+    ri.first = (r == r0);
+    ri.last = (r == r1 - 1);
+  } else {
+    ri.slot = (long long)w.b * p.G + w.g;
+    ri.first = (r == r0);
+    ri.last = (r == r1 - 1);
+  }
+  return ri;
+}
+
+}  // namespace ps

@@ -1,0 +1,511 @@
+// Phasor preparation kernels: input packing for cuFFT, the one-sided Hilbert
+// spectral mask (K2), normalisation to unit phasors with split-plane output
+// (K4), the exact-median amplitude-floor fixup, and the trial-group reduce.
+//
+// Reference semantics: SPEC.md:76-93 (analytic_signal, normalize_phasors),
+// design decisions SPEC.md:120-125, per-pair effective T SPEC.md:260.
+// All of these are HBM-bound streaming kernels.
+#include <cuda_fp16.h>
+#include <cfloat>
+#include <cstdint>
+
+#include "ps_internal.h"
+
+namespace ps {
+
+namespace {
+
+constexpr int kNormThreads = 256;
+constexpr int kNormPerThread = 4;
+constexpr int kNormSamplesPerBlock = kNormThreads * kNormPerThread;
+
+// Output formats of the normalisation stage.
+enum OutFmt : int { OUT_SPLIT = 0, OUT_F64 = 1, OUT_COMPLEX = 2 };
+
+__device__ __forceinline__ long long row_offset(const SrcDesc& s, long long r) {
+  const long long n = r % s.N;
+  const long long u = r / s.N;
+  const long long t = u % s.R;
+  const long long b = u / s.R;
+  return b * s.s_band + t * s.s_trial + n * s.s_sig;
+}
+
+// Loads sample (r, t) of the source as a complex value in compute type S.
+template <typename IT, typename S, int KIND>
+__device__ __forceinline__ void load_a(const SrcDesc& s, long long roff, long long r, long long t, S& re,
+                                       S& im) {
+  if (KIND == 0) {
+    re = static_cast<S>(static_cast<const IT*>(s.ptr)[roff + t * s.s_samp]);
+    im = static_cast<const S*>(s.hbuf)[(r - s.h_row0) * s.T + t];
+  } else {
+    const IT* p = static_cast<const IT*>(s.ptr) + 2 * (roff + t * s.s_samp);
+    re = static_cast<S>(p[0]);
+    im = static_cast<S>(p[1]);
+  }
+}
+
+template <typename S>
+__device__ __forceinline__ S amp_of(S re, S im) {
+  return sqrt(re * re + im * im);
+}
+
+// Writes z = (zr, zi) at element (row r, sample t) in the requested format.
+template <typename S, int FMT>
+__device__ __forceinline__ void store_z(void* out, long long plane_stride, long long idx, S zr, S zi) {
+  if (FMT == OUT_SPLIT) {
+    __half* p = static_cast<__half*>(out);
+    const float fr = static_cast<float>(zr), fi = static_cast<float>(zi);
+    const __half rh = __float2half_rn(fr);
+    const __half ih = __float2half_rn(fi);
+    // residuals from the full-precision value (exact for S = float; for
+    // S = double the residual is rounded once to fp16)
+    const __half rl = __float2half_rn(static_cast<float>(zr - static_cast<S>(__half2float(rh))));
+    const __half il = __float2half_rn(static_cast<float>(zi - static_cast<S>(__half2float(ih))));
+    p[idx] = rh;
+    p[plane_stride + idx] = rl;
+    p[2 * plane_stride + idx] = ih;
+    p[3 * plane_stride + idx] = il;
+  } else if (FMT == OUT_F64) {
+    double* p = static_cast<double*>(out);
+    p[idx] = static_cast<double>(zr);
+    p[plane_stride + idx] = static_cast<double>(zi);
+  } else {
+    S* p = static_cast<S*>(out);
+    p[2 * idx] = zr;
+    p[2 * idx + 1] = zi;
+  }
+}
+
+template <typename S, int FMT>
+__device__ __forceinline__ void zero_z(void* out, long long plane_stride, long long idx) {
+  store_z<S, FMT>(out, plane_stride, idx, S(0), S(0));
+}
+
+__device__ __forceinline__ unsigned long long key_of(double a) {
+  return static_cast<unsigned long long>(__double_as_longlong(a));
+}
+__device__ __forceinline__ double val_of(unsigned long long k) {
+  return __longlong_as_double(static_cast<long long>(k));
+}
+
+// ---------------------------------------------------------------------------
+// K4: z = a/|a| (or z = a for phasor input), split/planes output, row min/max
+// of |a| for the amplitude-floor pre-check.  Each block handles 1024
+// consecutive samples of one row; loads are warp-coalesced along samples.
+// ---------------------------------------------------------------------------
+template <typename IT, typename S, int KIND, int FMT>
+__global__ void __launch_bounds__(kNormThreads) normalize_kernel(SrcDesc src, long long row0, int chunks,
+                                                                 void* out, int pitch, long long plane_stride,
+                                                                 unsigned long long* rowmin,
+                                                                 unsigned long long* rowmax, DevStatus* st) {
+  const long long rl = blockIdx.x / chunks;
+  const int ch = blockIdx.x % chunks;
+  const long long r = row0 + rl;
+  const long long roff = row_offset(src, r);
+  const long long T = src.T;
+  S amin = sizeof(S) == 4 ? S(FLT_MAX) : S(DBL_MAX);
+  S amax = S(0);
+  bool bad = false;
+  const long long obase = (FMT == OUT_COMPLEX ? (r - row0) : r) * pitch;
+#pragma unroll
+  for (int k = 0; k < kNormPerThread; ++k) {
+    const long long t = (long long)ch * kNormSamplesPerBlock + k * kNormThreads + threadIdx.x;
+    if (t < T) {
+      S re, im;
+      load_a<IT, S, KIND>(src, roff, r, t, re, im);
+      const S a = amp_of(re, im);
+      S zr = S(0), zi = S(0);
+      if (KIND == 2) {
+        zr = re;
+        zi = im;
+      } else if (a > S(0)) {
+        zr = re / a;
+        zi = im / a;
+      }
+      store_z<S, FMT>(out, plane_stride, obase + t, zr, zi);
+      if (!(a <= (sizeof(S) == 4 ? S(FLT_MAX) : S(DBL_MAX)))) bad = true;
+      amin = a < amin ? a : amin;
+      amax = a > amax ? a : amax;
+    } else if (t < pitch && FMT != OUT_COMPLEX) {
+      zero_z<S, FMT>(out, plane_stride, obase + t);  // zero the pitch padding
+    }
+  }
+  // block reduce min / max
+  __shared__ double smin[kNormThreads / 32], smax[kNormThreads / 32];
+  double dmin = static_cast<double>(amin), dmax = static_cast<double>(amax);
+  for (int o = 16; o > 0; o >>= 1) {
+    dmin = fmin(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  }
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    smin[w] = dmin;
+    smax[w] = dmax;
+  }
+  if (bad) atomicOr(&st->flags, FLAG_NONFINITE);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kNormThreads / 32; ++i) {
+      dmin = fmin(dmin, smin[i]);
+      dmax = fmax(dmax, smax[i]);
+    }
+    dmin = fmin(smin[0], dmin);
+    dmax = fmax(smax[0], dmax);
+    atomicMin(&rowmin[r], key_of(dmin));
+    atomicMax(&rowmax[r], key_of(dmax));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Exact amplitude-floor fixup.  For each row: if the cheap
+// bound min|a| >= floor * max|a| holds, no sample can fall below
+// floor * median and the row is untouched (the common case: Rayleigh
+// amplitudes never get near 1e-6 of the median).  Otherwise the exact median
+// (numpy semantics: mean of the two middle values) is found by a 64-bit radix
+// select over the order-preserving bit patterns of |a|, and samples with
+// |a| < floor*median or |a| == 0 are zeroed (masked).
+// ---------------------------------------------------------------------------
+constexpr int kFixThreads = 256;
+
+template <typename IT, typename S, int KIND>
+__device__ double row_amp(const SrcDesc& src, long long roff, long long r, long long t) {
+  S re, im;
+  load_a<IT, S, KIND>(src, roff, r, t, re, im);
+  return static_cast<double>(amp_of(re, im));
+}
+
+template <typename IT, typename S, int KIND, int FMT>
+__global__ void __launch_bounds__(kFixThreads) fixup_kernel(SrcDesc src, long long row0, long long nrows,
+                                                            void* out, int pitch, long long plane_stride,
+                                                            const unsigned long long* rowmin,
+                                                            const unsigned long long* rowmax, int* maskcount,
+                                                            double amp_floor, DevStatus* st) {
+  __shared__ unsigned int hist[256];
+  __shared__ unsigned long long sh_prefix;
+  __shared__ long long sh_k;
+  __shared__ unsigned long long red_u[kFixThreads / 32];
+  __shared__ long long red_c[kFixThreads / 32];
+  const long long T = src.T;
+  for (long long rl = blockIdx.x; rl < nrows; rl += gridDim.x) {
+    const long long r = row0 + rl;
+    const double amin = val_of(rowmin[r]);
+    const double amax = val_of(rowmax[r]);
+    const bool need = (amin == 0.0) || (amin < amp_floor * amax);
+    if (!need) {
+      if (threadIdx.x == 0) maskcount[r] = 0;
+      continue;
+    }
+    const long long roff = row_offset(src, r);
+    // ---- radix select of the k-th smallest key -------------------------
+    auto select_kth = [&](long long k) -> unsigned long long {
+      unsigned long long prefix = 0, hmask = 0;
+      for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+        __syncthreads();
+        for (long long t = threadIdx.x; t < T; t += blockDim.x) {
+          const unsigned long long key = key_of(row_amp<IT, S, KIND>(src, roff, r, t));
+          if ((key & hmask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFFu], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          long long cum = 0;
+          int sel = 255;
+          for (int d = 0; d < 256; ++d) {
+            if (cum + (long long)hist[d] > k) {
+              sel = d;
+              break;
+            }
+            cum += hist[d];
+          }
+          sh_k = k - cum;
+          sh_prefix = prefix | ((unsigned long long)sel << shift);
+        }
+        __syncthreads();
+        prefix = sh_prefix;
+        k = sh_k;
+        hmask |= 0xFFull << shift;
+        __syncthreads();
+      }
+      return prefix;
+    };
+    const long long k1 = (T % 2 == 0) ? (T / 2 - 1) : (T / 2);
+    const unsigned long long v1 = select_kth(k1);
+    unsigned long long v2 = v1;
+    if (T % 2 == 0) {
+      // count of keys <= v1 and the smallest key > v1
+      unsigned long long mgt = ~0ull;
+      long long cle = 0;
+      for (long long t = threadIdx.x; t < T; t += blockDim.x) {
+        const unsigned long long key = key_of(row_amp<IT, S, KIND>(src, roff, r, t));
+        if (key <= v1) ++cle;
+        else mgt = key < mgt ? key : mgt;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        cle += __shfl_xor_sync(0xffffffffu, cle, o);
+        const unsigned long long m2 = __shfl_xor_sync(0xffffffffu, mgt, o);
+        mgt = m2 < mgt ? m2 : mgt;
+      }
+      if ((threadIdx.x & 31) == 0) {
+        red_u[threadIdx.x >> 5] = mgt;
+        red_c[threadIdx.x >> 5] = cle;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int i = 1; i < kFixThreads / 32; ++i) {
+          cle += red_c[i];
+          mgt = red_u[i] < mgt ? red_u[i] : mgt;
+        }
+        red_c[0] = cle;
+        red_u[0] = mgt;
+      }
+      __syncthreads();
+      cle = red_c[0];
+      mgt = red_u[0];
+      v2 = (cle >= k1 + 2) ? v1 : mgt;
+      __syncthreads();
+    }
+    const double median = 0.5 * (val_of(v1) + val_of(v2));
+    const double thr = amp_floor * median;
+    // ---- masking pass ---------------------------------------------------
+    long long cnt = 0;
+    const long long obase = (FMT == OUT_COMPLEX ? rl : r) * pitch;
+    for (long long t = threadIdx.x; t < T; t += blockDim.x) {
+      const double a = row_amp<IT, S, KIND>(src, roff, r, t);
+      if (a < thr || a == 0.0) {
+        zero_z<S, FMT>(out, plane_stride, obase + t);
+        ++cnt;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) red_c[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < kFixThreads / 32; ++i) cnt += red_c[i];
+      maskcount[r] = static_cast<int>(cnt);
+      atomicAdd(&st->n_fix_rows, 1);
+      if (cnt > 0) {
+        atomicOr(&st->flags, FLAG_ANY_MASKED);
+        atomicAdd(&st->n_masked, static_cast<unsigned long long>(cnt));
+      }
+      if (cnt == T) atomicOr(&st->flags, FLAG_ALL_MASKED);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Pack rows of a real input into a dense [nrows][T] buffer of type OT (cuFFT
+// input when the caller's layout / dtype is not directly usable).
+// ---------------------------------------------------------------------------
+template <typename IT, typename OT>
+__global__ void pack_real_kernel(SrcDesc src, long long row0, long long nrows, OT* dst) {
+  const long long T = src.T;
+  const long long total = nrows * T;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long rl = e / T, t = e % T;
+    const long long roff = row_offset(src, row0 + rl);
+    dst[e] = static_cast<OT>(static_cast<const IT*>(src.ptr)[roff + t * src.s_samp]);
+  }
+}
+
+// K2: one-sided Hilbert multiplier on the half spectrum, scaled by 1/T so the
+// C2R output is H{x} directly: Y_k = -i X_k / T for strictly positive bins,
+// Y_0 = Y_{T/2} = 0.
+template <typename C>
+__global__ void hilbert_spectrum_kernel(C* spec, long long nrows, int T) {
+  const int nb = T / 2 + 1;
+  const long long total = nrows * nb;
+  using S = decltype(spec->x);
+  const S inv = S(1) / S(T);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int k = static_cast<int>(e % nb);
+    C v = spec[e];
+    C y;
+    if (k == 0 || (T % 2 == 0 && k == T / 2)) {
+      y.x = S(0);
+      y.y = S(0);
+    } else {
+      y.x = v.y * inv;
+      y.y = -v.x * inv;
+    }
+    spec[e] = y;
+  }
+}
+
+// analytic output: out[rl][t] = (x, H) -- Re taken from x unchanged.
+template <typename IT, typename S>
+__global__ void analytic_out_kernel(SrcDesc src, long long row0, long long nrows, S* out) {
+  const long long T = src.T;
+  const long long total = nrows * T;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long rl = e / T, t = e % T;
+    const long long r = row0 + rl;
+    const long long roff = row_offset(src, r);
+    S re, im;
+    load_a<IT, S, 0>(src, roff, r, t, re, im);
+    out[2 * e] = re;
+    out[2 * e + 1] = im;
+  }
+}
+
+// out_m[i] = sum_g ws_m[g][i] / R  (deterministic fixed-order trial-group sum)
+template <typename S>
+__global__ void group_reduce_kernel(const S* ws, int G, long long slot_elems, long long elems, int R,
+                                    S* out) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < elems;
+       e += (long long)gridDim.x * blockDim.x) {
+    // slot layout of ws: [band][G][N*N]; elems = B*N*N, slot_elems = N*N
+    const long long b = e / slot_elems, i = e % slot_elems;
+    const S* p = ws + (b * G) * slot_elems + i;
+    S acc = p[0];
+    for (int g = 1; g < G; ++g) acc += p[g * slot_elems];
+    out[e] = acc / S(R);
+  }
+}
+
+int grid_for(long long n, int threads) {
+  long long g = (n + threads - 1) / threads;
+  if (g > 148LL * 16) g = 148LL * 16;
+  if (g < 1) g = 1;
+  return static_cast<int>(g);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_pack_real(const SrcDesc& src, long long row0, long long nrows, void* dst, int dst_double,
+                             cudaStream_t st) {
+  const int g = grid_for(nrows * src.T, 256);
+  if (src.is_double) {
+    if (dst_double) pack_real_kernel<double, double><<<g, 256, 0, st>>>(src, row0, nrows, (double*)dst);
+    else return cudaErrorInvalidValue;
+  } else {
+    if (dst_double) pack_real_kernel<float, double><<<g, 256, 0, st>>>(src, row0, nrows, (double*)dst);
+    else pack_real_kernel<float, float><<<g, 256, 0, st>>>(src, row0, nrows, (float*)dst);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_double, cudaStream_t st) {
+  const int g = grid_for(nrows * (T / 2 + 1), 256);
+  if (is_double) hilbert_spectrum_kernel<double2><<<g, 256, 0, st>>>((double2*)spec, nrows, T);
+  else hilbert_spectrum_kernel<float2><<<g, 256, 0, st>>>((float2*)spec, nrows, T);
+  return cudaGetLastError();
+}
+
+// fmt: 0 split fp16 planes, 1 f64 planes, 2 complex interleaved (of compute type)
+#define PS_NORM_DISPATCH(KIND, FMT)                                                                    \
+  do {                                                                                               \
+    if (src.is_double)                                                                               \
+      normalize_kernel<double, double, KIND, FMT>                                                    \
+          <<<grid, kNormThreads, 0, st>>>(src, row0, chunks, out, pitch, plane_stride, rowmin, rowmax, \
+                                          status);                                                   \
+    else if (cdouble)                                                                                \
+      normalize_kernel<float, double, KIND, FMT>                                                     \
+          <<<grid, kNormThreads, 0, st>>>(src, row0, chunks, out, pitch, plane_stride, rowmin, rowmax, \
+                                          status);                                                   \
+    else                                                                                             \
+      normalize_kernel<float, float, KIND, FMT>                                                      \
+          <<<grid, kNormThreads, 0, st>>>(src, row0, chunks, out, pitch, plane_stride, rowmin, rowmax, \
+                                          status);                                                   \
+  } while (0)
+
+cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
+                                 int cdouble, int pitch, long long plane_stride, unsigned long long* rowstat,
+                                 long long rows_total, DevStatus* status, cudaStream_t st) {
+  const int chunks = static_cast<int>((src.T + kNormSamplesPerBlock - 1) / kNormSamplesPerBlock);
+  const long long nblk = nrows * chunks;
+  if (nblk <= 0) return cudaSuccess;
+  if (nblk > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const unsigned grid = static_cast<unsigned>(nblk);
+  unsigned long long* rowmin = rowstat;
+  unsigned long long* rowmax = rowstat + rows_total;
+  // real input with a float source but double compute keeps H in double
+  if (src.kind == 0) {
+    if (fmt == OUT_SPLIT) PS_NORM_DISPATCH(0, OUT_SPLIT);
+    else if (fmt == OUT_F64) PS_NORM_DISPATCH(0, OUT_F64);
+    else PS_NORM_DISPATCH(0, OUT_COMPLEX);
+  } else if (src.kind == 1) {
+    if (fmt == OUT_SPLIT) PS_NORM_DISPATCH(1, OUT_SPLIT);
+    else if (fmt == OUT_F64) PS_NORM_DISPATCH(1, OUT_F64);
+    else PS_NORM_DISPATCH(1, OUT_COMPLEX);
+  } else {
+    if (fmt == OUT_SPLIT) PS_NORM_DISPATCH(2, OUT_SPLIT);
+    else if (fmt == OUT_F64) PS_NORM_DISPATCH(2, OUT_F64);
+    else PS_NORM_DISPATCH(2, OUT_COMPLEX);
+  }
+  return cudaGetLastError();
+}
+#undef PS_NORM_DISPATCH
+
+#define PS_FIX_DISPATCH(KIND, FMT)                                                                    \
+  do {                                                                                              \
+    if (src.is_double)                                                                              \
+      fixup_kernel<double, double, KIND, FMT><<<grid, kFixThreads, 0, st>>>(                        \
+          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status); \
+    else if (cdouble)                                                                               \
+      fixup_kernel<float, double, KIND, FMT><<<grid, kFixThreads, 0, st>>>(                         \
+          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status); \
+    else                                                                                            \
+      fixup_kernel<float, float, KIND, FMT><<<grid, kFixThreads, 0, st>>>(                          \
+          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status); \
+  } while (0)
+
+cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
+                             int cdouble, int pitch, long long plane_stride, const unsigned long long* rowstat,
+                             long long rows_total, int* maskcount, double amp_floor, DevStatus* status,
+                             cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  const unsigned grid = static_cast<unsigned>(nrows < 148 * 8 ? nrows : 148 * 8);
+  const unsigned long long* rowmin = rowstat;
+  const unsigned long long* rowmax = rowstat + rows_total;
+  if (src.kind == 0) {
+    if (fmt == OUT_SPLIT) PS_FIX_DISPATCH(0, OUT_SPLIT);
+    else if (fmt == OUT_F64) PS_FIX_DISPATCH(0, OUT_F64);
+    else PS_FIX_DISPATCH(0, OUT_COMPLEX);
+  } else if (src.kind == 1) {
+    if (fmt == OUT_SPLIT) PS_FIX_DISPATCH(1, OUT_SPLIT);
+    else if (fmt == OUT_F64) PS_FIX_DISPATCH(1, OUT_F64);
+    else PS_FIX_DISPATCH(1, OUT_COMPLEX);
+  } else {
+    if (fmt == OUT_SPLIT) PS_FIX_DISPATCH(2, OUT_SPLIT);
+    else if (fmt == OUT_F64) PS_FIX_DISPATCH(2, OUT_F64);
+    else PS_FIX_DISPATCH(2, OUT_COMPLEX);
+  }
+  return cudaGetLastError();
+}
+#undef PS_FIX_DISPATCH
+
+cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nrows, void* out,
+                                cudaStream_t st) {
+  const int g = grid_for(nrows * src.T, 256);
+  // hbuf type decides the output precision: f64 input -> c128, else c64
+  if (src.is_double) analytic_out_kernel<double, double><<<g, 256, 0, st>>>(src, row0, nrows, (double*)out);
+  else analytic_out_kernel<float, float><<<g, 256, 0, st>>>(src, row0, nrows, (float*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs, void* const* outs,
+                                long long elems_per_out, int R, int is_double, cudaStream_t st) {
+  // ws holds n_outputs consecutive blocks of [B][G][slot_elems]
+  const int g = grid_for(elems_per_out, 256);
+  const long long ws_block = elems_per_out * G;
+  for (int m = 0; m < n_outputs; ++m) {
+    if (!outs[m]) continue;
+    if (is_double)
+      group_reduce_kernel<double><<<g, 256, 0, st>>>((const double*)ws + m * ws_block, G, slot_elems,
+                                                      elems_per_out, R, (double*)outs[m]);
+    else
+      group_reduce_kernel<float><<<g, 256, 0, st>>>((const float*)ws + m * ws_block, G, slot_elems,
+                                                     elems_per_out, R, (float*)outs[m]);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ps

@@ -1,0 +1,103 @@
+// Internal declarations shared by the host layer (capi.cu) and the kernels.
+// Data layout in HBM:
+//   rows      = n_bands * n_trials * n_signals; row r = (b*R + t)*N + n
+//   pitch     = Tp = roundup(T, 8) elements (16-byte TMA stride rule)
+//   split     : fp16 planes [4][rows][Tp] = {re_hi, re_lo, im_hi, im_lo}
+//   fp64      : f64 planes  [2][rows][Tp] = {re, im}
+//   rowstat   : per row {min |a|, max |a|} as order-preserving unsigned bits
+//   maskcount : per row number of masked samples (int32)
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ps {
+
+enum DevFlags : int {
+  FLAG_ALL_MASKED = 1,
+  FLAG_EMPTY_WINDOW = 2,
+  FLAG_NONFINITE = 4,
+  FLAG_TIMEOUT = 8,
+  FLAG_ANY_MASKED = 16,
+};
+
+// Device-visible status words (one small device allocation per context).
+struct DevStatus {
+  int flags;                 // DevFlags
+  int n_fix_rows;            // rows that needed the exact-median path
+  unsigned long long n_masked;
+  unsigned long long n_illcond;   // ciPLV pairs flagged ill-conditioned
+  int pad[10];
+};
+
+// Where the (possibly strided) source samples of row r live.
+struct SrcDesc {
+  const void* ptr;           // base pointer of the source (input or packed copy)
+  int kind;                  // 0 real, 1 complex (analytic), 2 complex (phasor)
+  int is_double;             // scalar type of the source
+  long long N, R, B, T;
+  long long s_sig, s_samp, s_trial, s_band;   // element strides
+  const void* hbuf;          // H{x} for real input: [rows_in_chunk][T] scalar
+  long long h_row0;          // first row held in hbuf
+};
+
+// One Gram work item: band b, trial group g (trials [g*Rg, min(R,(g+1)*Rg))),
+// row panel I (BM rows), column panel J (BN cols).
+struct Item { int b, g, I, J; };
+
+struct GramParams {
+  int N, T, R, B;
+  int Tp;
+  int rows;                  // B*R*N
+  int Rg;                    // trials per group
+  int G;                     // groups per band
+  int pool;                  // 1: K runs over all R*T observations
+  int n_items;
+  const Item* items;
+  // outputs (nullptr = not requested); element type float (split) / double (fp64)
+  // Each output is an array of [N][N] slots; the slot written by a round is
+  //   slot_mode 0: b*R + r     (per trial, PS_TRIALS_NONE)
+  //   slot_mode 1: b           (per band: MEAN with one group, or POOL)
+  //   slot_mode 2: b*G + g     (per trial group, reduced afterwards)
+  void* out_plv; void* out_iplv; void* out_ciplv; void* out_cre; void* out_cim;
+  int slot_mode;
+  int mean_div;                // divisor applied at the last round of a slot (1 = none)
+  // masks
+  const int* maskcount;        // [rows]
+  const void* planes;          // planes base (for masked-overlap scan)
+  long long plane_stride;      // elements between planes
+  DevStatus* status;
+  // timing / debug
+  float illcond_tol;           // flag ciPLV pairs whose predicted error > tol
+};
+
+// ---- launchers (return cudaError_t) --------------------------------------
+cudaError_t launch_pack_real(const SrcDesc& src, long long row0, long long nrows,
+                             void* dst, int dst_double, cudaStream_t st);
+cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_double,
+                                    cudaStream_t st);
+// fmt: 0 split fp16 planes, 1 f64 planes, 2 complex interleaved (compute type)
+// cdouble: compute in double although the source is float
+cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
+                                 int cdouble, int pitch, long long plane_stride, unsigned long long* rowstat,
+                                 long long rows_total, DevStatus* status, cudaStream_t st);
+cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
+                             int cdouble, int pitch, long long plane_stride, const unsigned long long* rowstat,
+                             long long rows_total, int* maskcount, double amp_floor, DevStatus* status,
+                             cudaStream_t st);
+cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nrows,
+                                void* out, cudaStream_t st);
+cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs,
+                                void* const* outs, long long elems_per_out, int R,
+                                int is_double, cudaStream_t st);
+cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p,
+                              int grid, cudaStream_t st);
+cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);
+
+// tile geometry of the two Gram kernels
+constexpr int kSplitBM = 128;
+constexpr int kSplitBN = 256;
+constexpr int kSplitBK = 32;
+constexpr int kF64BM = 64;
+constexpr int kF64BN = 64;
+
+}  // namespace ps

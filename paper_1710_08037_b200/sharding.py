@@ -1,0 +1,73 @@
+"""Multi-GPU output-tile sharding for the PLV family.
+
+One process per GPU (torchrun / torch.distributed over NCCL).  Each rank
+computes the upper-triangle output tiles t with t % world_size == rank
+(``ps_plv_args.shard_index/shard_count``) into zero-initialised outputs; every
+pair (i, j) and its mirror is written by exactly one tile, so the full matrix
+is the element-wise SUM of the shards -- a single NCCL reduce / all-reduce
+gathers it exactly (x + 0 == x), and only when the caller asks for it.
+
+When the input lives on one rank only ("input on GPU 0"),
+``broadcast_input`` ships it over NVLink before the compute; with per-rank
+pre-placed inputs (independent bands / trials) nothing crosses the link.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+
+SPLIT_TILE = (128, 256)
+FP64_TILE = (64, 64)
+
+
+def tiles(n_signals: int, precision: str = "split"):
+    """Upper-triangle tile list in the library's enumeration order
+    (capi.cu build_tiles): J-major, tiles holding at least one pair i <= j."""
+    bm, bn = SPLIT_TILE if _native.PRECISIONS[precision] == 0 else FP64_TILE
+    out = []
+    nj = -(-n_signals // bn)
+    ni = -(-n_signals // bm)
+    for J in range(nj):
+        jmax = min(J * bn + bn, n_signals) - 1
+        for I in range(ni):
+            if I * bm <= jmax:
+                out.append((I, J))
+    return out
+
+
+def owner_matrix(n_signals: int, precision: str, shard_count: int) -> np.ndarray:
+    """owner[i, j] = shard that writes (i, j) (symmetric)."""
+    bm, bn = SPLIT_TILE if _native.PRECISIONS[precision] == 0 else FP64_TILE
+    own = np.full((n_signals, n_signals), -1, dtype=np.int32)
+    for t, (I, J) in enumerate(tiles(n_signals, precision)):
+        i0, i1 = I * bm, min(I * bm + bm, n_signals)
+        j0, j1 = J * bn, min(J * bn + bn, n_signals)
+        blk = own[i0:i1, j0:j1]
+        ii, jj = np.meshgrid(np.arange(i0, i1), np.arange(j0, j1), indexing="ij")
+        sel = ii <= jj
+        blk[sel] = t % shard_count
+    iu = np.triu_indices(n_signals)
+    own.T[iu] = own[iu]
+    return own
+
+
+def broadcast_input(x, src: int = 0, group=None):
+    """Ship a device input from rank `src` to every rank (NCCL broadcast)."""
+    import torch.distributed as dist
+
+    dist.broadcast(x, src=src, group=group)
+    return x
+
+
+def gather(outputs: dict, dst: int | None = 0, group=None) -> dict:
+    """Assemble sharded outputs: reduce (dst given) or all-reduce (dst None)."""
+    import torch.distributed as dist
+
+    for v in outputs.values():
+        t = v.values if hasattr(v, "values") and not hasattr(v, "dtype") else v
+        if dst is None:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        else:
+            dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
+    return outputs

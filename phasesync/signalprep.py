@@ -1,0 +1,6 @@
+"""phasesync.signalprep -- reference import name (pkg/pyproject.toml:6) for paper_1710_08037_b200.signalprep."""
+from paper_1710_08037_b200.signalprep import *  # noqa: F401,F403
+from paper_1710_08037_b200 import signalprep as _impl
+
+__all__ = [n for n in dir(_impl) if not n.startswith("_")]
+globals().update({n: getattr(_impl, n) for n in __all__})

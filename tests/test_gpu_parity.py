@@ -1,0 +1,235 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Tolerances (north star): max-abs <= 1e-5 for the split-precision path,
+<= 1e-12 for the FP64 mode.  Full-size configs are checked through
+size-independent properties plus exact oracle recomputation on random signal
+subsets (a PLV-family entry depends only on its two rows).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import plv_oracle as O
+from paper_1710_08037_b200 import connectivity as C
+from paper_1710_08037_b200 import errors, signalprep
+from paper_1710_08037_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"split": 1e-5, "fp64": 1e-12}
+METRICS = ("plv", "iplv", "ciplv")
+
+
+def golden(name):
+    return np.load(os.path.join(G, name + ".npz"), allow_pickle=False)
+
+
+def maxerr(got, ref):
+    return float(np.max(np.abs(np.asarray(got, dtype=np.float64) - ref)))
+
+
+def check(res, ref, prec, label=""):
+    errs = {m: maxerr(res[m].values, ref[m]) for m in METRICS}
+    print(f"[parity] {label} {prec} " + " ".join(f"{m}={e:.3e}" for m, e in errs.items()))
+    for m, e in errs.items():
+        assert e <= TOL[prec], (label, prec, m, e)
+
+
+# ------------------------------------------------------------ golden configs
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+@pytest.mark.parametrize("name", ["c1_full", "c2_small", "c3_small", "c5_small"])
+def test_golden_configs(name, prec):
+    d = golden(name)
+    res = C.plv_family(d["x"], input_kind=str(d["input_kind"]), precision=prec,
+                       trial_reduce=str(d["trial_reduce"]))
+    check(res, {m: d[m] for m in METRICS}, prec, name)
+
+
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_golden_c4_bands(prec):
+    d = golden("c4_small")
+    res = C.plv_family(d["x"], input_kind="real", precision=prec, bands=True)
+    check(res, {m: d[m] for m in METRICS}, prec, "c4_small")
+
+
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_kat_offsets(prec):
+    d = golden("kat_offsets")
+    res = C.plv_family(d["z"], input_kind="phasor", precision=prec)
+    check(res, {m: d[m] for m in METRICS}, prec, "kat_offsets")
+    # zero-lag pairs hit the singularity rule exactly
+    assert float(res["ciplv"].values[0, 0]) == 0.0
+
+
+def test_kat_cancel():
+    d = golden("kat_cancel")
+    for prec in ("split", "fp64"):
+        v = C.plv_matrix(d["z"], precision=prec).values
+        assert abs(float(v[0, 1])) < TOL[prec]
+
+
+# ------------------------------------------------------------ API surfaces
+def test_host_and_device_paths_bit_identical():
+    import torch
+
+    x = W.c1()
+    h = C.plv_family(x, precision="split")
+    dv = C.plv_family(torch.from_numpy(x).cuda(), precision="split")
+    for m in METRICS:
+        assert np.array_equal(h[m].values, dv[m].values.cpu().numpy())
+
+
+def test_deterministic_repeat():
+    d = golden("c2_small")
+    a = C.plv_family(d["x"], precision="split")
+    b = C.plv_family(d["x"], precision="split")
+    for m in METRICS:
+        assert np.array_equal(a[m].values, b[m].values)
+
+
+@pytest.mark.parametrize("reduce_", ["none", "pool", "mean"])
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_trial_reduce_modes(reduce_, prec):
+    z = O.make_surrogate(70, 300, 5, seed=31)
+    z[::7] *= np.exp(1j * 0.4)  # some structure
+    ref = O.plv_family(z, input_kind="phasor", trial_reduce=reduce_)
+    res = C.plv_family(z, input_kind="phasor", precision=prec, trial_reduce=reduce_)
+    check(res, ref, prec, f"reduce={reduce_}")
+
+
+@pytest.mark.parametrize("N,T,R", [(1, 16, 1), (2, 2, 1), (3, 7, 2), (129, 1001, 1), (257, 2001, 3),
+                                   (300, 64, 1), (130, 8, 1)])
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_edge_shapes_real(N, T, R, prec):
+    rng = np.random.default_rng(N * 1000 + T)
+    x = rng.standard_normal((N, T, R))
+    ref = O.plv_family(x, input_kind="real")
+    res = C.plv_family(x, input_kind="real", precision=prec)
+    check(res, ref, prec, f"real N={N} T={T} R={R}")
+
+
+def test_float32_trial_fastest_layout_copies():
+    # reference layout [N, T, R] row-major: samples are strided -> packing copy
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((90, 1500, 3)).astype(np.float32)
+    ref = O.plv_family(x, input_kind="real")
+    res = C.plv_family(x, precision="split")
+    check(res, ref, "split", "f32 [N,T,R] contiguous")
+    assert res["plv"].meta["input_copied"]
+
+
+def test_signed_coherency_outputs():
+    z = O.make_surrogate(40, 500, 1, seed=8)
+    raw = O.plv_family(z, input_kind="phasor", raw=True)["cgram"][:, :, 0]
+    res = C.plv_family(z, input_kind="phasor", precision="fp64", metrics=("cre", "cim"))
+    re = raw.real.copy()
+    im = raw.imag.copy()
+    np.fill_diagonal(re, 1.0)
+    np.fill_diagonal(im, 0.0)
+    assert maxerr(res["cre"].values, re) < 1e-12
+    assert maxerr(res["cim"].values, im) < 1e-12
+
+
+# ------------------------------------------------------------ masks / errors
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_masked_samples_effective_T(prec):
+    rng = np.random.default_rng(3)
+    a = (rng.standard_normal((20, 400, 2)) + 1j * rng.standard_normal((20, 400, 2)))
+    a[2, 10:50, 0] = 0
+    a[5, 30:90, 0] = 0
+    a[5, :5, 1] = 1e-9  # below 1e-6 x median amplitude -> masked
+    ref = O.plv_family(a, input_kind="analytic")
+    res = C.plv_family(a, input_kind="analytic", precision=prec)
+    check(res, ref, prec, "masked")
+    assert res["plv"].meta["n_masked_samples"] == 40 + 60 + 5
+
+
+def test_all_masked_raises():
+    a = np.ones((4, 64, 1), np.complex128)
+    a[2] = 0
+    with pytest.raises(errors.AllSamplesMaskedError):
+        C.plv_family(a, input_kind="analytic")
+
+
+def test_empty_effective_window_raises():
+    z = O.make_surrogate(3, 8, 1, seed=5)
+    z[0, :4, 0] = 0
+    z[1, 4:, 0] = 0
+    with pytest.raises(errors.EmptyEffectiveWindowError):
+        C.plv_family(z, input_kind="phasor")
+
+
+def test_shape_error():
+    with pytest.raises(errors.ShapeError):
+        C.plv_family(np.zeros((4,)))
+    with pytest.raises(errors.ShapeError):
+        C.plv_family(np.zeros((4, 1, 1)))
+
+
+# ------------------------------------------------------------ signalprep
+@pytest.mark.parametrize("T", [2000, 2001, 4096])
+def test_analytic_signal_matches_oracle(T):
+    rng = np.random.default_rng(T)
+    x = rng.standard_normal((7, T, 2))
+    a = signalprep.analytic_signal(x).data
+    ref = O.analytic_signal(x)
+    assert np.array_equal(a.real, x)
+    assert np.max(np.abs(a.imag - ref.imag)) < 1e-12 * np.sqrt(T) * 10
+    x32 = x.astype(np.float32)
+    a32 = signalprep.analytic_signal(x32).data
+    assert a32.dtype == np.complex64 and np.array_equal(a32.real, x32)
+    assert np.max(np.abs(a32.imag - ref.imag)) < 1e-4
+
+
+def test_normalize_phasors_matches_oracle():
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((9, 300, 2)) + 1j * rng.standard_normal((9, 300, 2))
+    a[1, 4, 0] = 0
+    a[3, 7, 1] = 1e-12
+    p = signalprep.normalize_phasors(a)
+    z, m = O.normalize_phasors(a)
+    assert np.array_equal(np.asarray(p.mask), m)
+    assert np.max(np.abs(p.data - z)) < 1e-15
+
+
+# ------------------------------------------------------------ full-size configs
+def subset_check(x, res, idx, input_kind, prec, label, trial_reduce="mean"):
+    xs = x[idx]
+    ref = O.plv_family(xs, input_kind=input_kind, trial_reduce=trial_reduce)
+    sub = {m: np.asarray(res[m].values[np.ix_(idx, idx)], dtype=np.float64) for m in METRICS}
+    errs = {m: maxerr(sub[m], ref[m]) for m in METRICS}
+    print(f"[parity] {label} {prec} subset={len(idx)} " + " ".join(f"{m}={e:.3e}" for m, e in errs.items()))
+    return errs
+
+
+def props(res, N):
+    p = res["plv"].values
+    for m in METRICS:
+        v = res[m].values
+        assert float(v.max()) <= 1.0 + 1e-9 and float(v.min()) >= 0.0
+        # symmetric (each pair written once with its mirror)
+        k = np.random.default_rng(0).integers(0, N, size=(2000, 2))
+        vv = np.asarray(v)
+        assert np.array_equal(vv[k[:, 0], k[:, 1]], vv[k[:, 1], k[:, 0]])
+    dg = np.asarray(p)[np.arange(N), np.arange(N)]
+    assert np.all(dg == 1.0)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c5", "c2"])
+def test_full_size_configs_subset_parity(cfg):
+    import torch
+
+    N, T, R, B, dt, kind = W.CONFIGS[cfg]
+    x = W.generate(cfg)
+    xd = torch.from_numpy(np.ascontiguousarray(np.transpose(x, (2, 0, 1)))).cuda()  # [R, N, T]
+    xd = xd.permute(1, 2, 0)                                                         # [N, T, R] view
+    res = C.plv_family(xd, input_kind=kind, precision="split")
+    host = {m: res[m].values.cpu().numpy() for m in METRICS}
+    hres = {m: C.ConnectivityMatrix(values=host[m], metric=m, n_observations=T) for m in METRICS}
+    props(hres, N)
+    idx = np.sort(np.random.default_rng(1).choice(N, size=min(N, 160), replace=False))
+    errs = subset_check(x, hres, idx, kind, "split", f"{cfg}-full")
+    for m, e in errs.items():
+        assert e <= TOL["split"], (cfg, m, e)
