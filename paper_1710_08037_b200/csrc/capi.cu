@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -540,7 +541,15 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   p.planes = c->planes.p;
   p.plane_stride = g.plane_stride;
   p.status = c->d_status;
-  p.illcond_tol = 1e-6f;
+  p.illcond_tol = 2e-6f;
+  {
+    // TMEM accumulation chunk (drain period) in 32-sample K blocks; see gram_tc.cu
+    static const int kcb_env = [] {
+      const char* s = std::getenv("PS_KC_BLOCKS");
+      return s ? std::max(1, std::atoi(s)) : 4;
+    }();
+    p.kc_blocks = kcb_env;
+  }
   const size_t oes = g.split ? 4 : 8;
   const long long nn = g.N * g.N;
   void* final_outs[5];

@@ -61,33 +61,40 @@ __device__ __forceinline__ PairMetrics<S> diag_metrics() {
 // plane; an unmasked unit phasor has max(|re|,|im|) >= 1/sqrt(2), so its hi
 // parts can never both be zero.
 template <bool SPLIT>
-__device__ __forceinline__ bool sample_masked(const GramParams& p, long long row, long long t) {
-  const long long idx = row * p.Tp + t;
+__device__ __forceinline__ bool sample_masked(const void* planes, long long plane_stride, long long idx) {
   if (SPLIT) {
-    const __half* h = static_cast<const __half*>(p.planes);
-    return __half2float(h[idx]) == 0.0f && __half2float(h[2 * p.plane_stride + idx]) == 0.0f;
+    const __half* h = static_cast<const __half*>(planes);
+    return __half2float(h[idx]) == 0.0f && __half2float(h[2 * plane_stride + idx]) == 0.0f;
   } else {
-    const double* d = static_cast<const double*>(p.planes);
-    return d[idx] == 0.0 && d[p.plane_stride + idx] == 0.0;
+    const double* d = static_cast<const double*>(planes);
+    return d[idx] == 0.0 && d[plane_stride + idx] == 0.0;
   }
+}
+
+// Samples masked in both rows (only when both rows have masked samples).
+template <bool SPLIT>
+__device__ __noinline__ int masked_overlap(const void* planes, long long plane_stride, long long ri, long long rj,
+                                           int T, int Tp) {
+  int both = 0;
+  for (int t = 0; t < T; ++t)
+    both += (sample_masked<SPLIT>(planes, plane_stride, ri * Tp + t) &&
+             sample_masked<SPLIT>(planes, plane_stride, rj * Tp + t))
+                ? 1
+                : 0;
+  return both;
 }
 
 // Effective observation count of pair (i, j) over units [u0, u0 + nu)
 // (SPEC.md:260): samples unmasked in both signals.  Only called when the
 // fixup kernel reported masked samples.
 template <bool SPLIT>
-__device__ __noinline__ long long effective_T(const GramParams& p, int u0, int nu, int i, int j) {
+__device__ __forceinline__ long long effective_T(const GramParams& p, int u0, int nu, int i, int j) {
   long long tot = 0;
   for (int u = u0; u < u0 + nu; ++u) {
     const long long ri = (long long)u * p.N + i, rj = (long long)u * p.N + j;
     const int mi = p.maskcount[ri], mj = p.maskcount[rj];
     long long c = (long long)p.T - mi - mj;
-    if (mi > 0 && mj > 0) {
-      long long both = 0;
-      for (long long t = 0; t < p.T; ++t)
-        both += (sample_masked<SPLIT>(p, ri, t) && sample_masked<SPLIT>(p, rj, t)) ? 1 : 0;
-      c += both;
-    }
+    if (mi > 0 && mj > 0) c += masked_overlap<SPLIT>(p.planes, p.plane_stride, ri, rj, p.T, p.Tp);
     tot += c;
   }
   return tot;

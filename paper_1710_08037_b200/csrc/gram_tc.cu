@@ -5,18 +5,27 @@
 // (`ndat(:,:,t) * ndat(:,:,t)'`) and SPEC plv_matrix /
 // iplv / ciplv.  Z = Zr + i Zi is held as four fp16 planes
 // (hi/lo of Re and Im, z = hi + lo to ~2^-24).  Per K-step of 16 samples the
-// single MMA-issuing thread launches 12 UMMAs (M=128, N=256, K=16):
+// single MMA-issuing thread launches 12 UMMAs (M=128, N=128, K=16):
 //   Re += Rh.Rh' + Rh.Rl' + Rl.Rh' + Ih.Ih' + Ih.Il' + Il.Ih'
 //   Im += Ih.Rh' + Ih.Rl' + Il.Rh' - Rh.Ih' - Rh.Il' - Rl.Ih'
 // (negation through the instruction descriptor's negate-A bit; the lo*lo
-// terms, <= 2^-24, are dropped).  Re and Im accumulate in fp32 in TMEM
-// (2 x 256 columns = all 512).  Only tiles touching the upper triangle are
-// computed; each pair (i <= j) is emitted by exactly one tile.
+// terms, <= 2^-24, are dropped).
 //
-// Warp roles (192 threads, one CTA per SM, persistent over work items):
-//   warp 0      TMA producer (one elected lane)
+// Accumulation accuracy.  The tensor core's fp32 accumulate is biased
+// (measured on B200: relative error ~= n_accumulates * 2^-25, i.e. each
+// UMMA truncates the running sum): accumulating all of T in TMEM would cost
+// ~2.5e-5 at T = 2000 and ~8e-4 at T = 65536.  So the K loop is cut into
+// chunks of kc_blocks * 32 samples; each chunk accumulates from zero in one of
+// two TMEM buffers (ping-pong, 2 x (Re 128 + Im 128) = 512 columns) while the
+// epilogue warps drain the other buffer into fp32 register sums
+// (round-to-nearest).  With 128-sample chunks the bias is ~1.4e-6 relative.
+//
+// Warp roles (320 threads, one CTA per SM, persistent over work items):
+//   warp 0      TMA producer (one lane)
 //   warp 1      TMEM allocator + MMA issuer (one lane)
-//   warps 2..5  epilogue: tcgen05.ld -> metrics -> global stores
+//   warps 2..17 epilogue: warp w reads TMEM lane quadrant w%4, column quarter
+//               (w-2)/4; drains chunks into 32 Re + 32 Im register sums and,
+//               at the end of a round, emits PLV / iPLV / ciPLV.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
@@ -28,10 +37,10 @@
 namespace ps {
 namespace {
 
-constexpr int BM = kSplitBM;   // 128 rows of panel I  (UMMA M)
-constexpr int BN = kSplitBN;   // 256 rows of panel J  (UMMA N)
+constexpr int BM = kSplitBM;   // 128 rows of panel I  (UMMA M, TMEM lanes)
+constexpr int BN = kSplitBN;   // 128 rows of panel J  (UMMA N)
 constexpr int BK = kSplitBK;   // 32 samples per pipeline stage
-constexpr int STAGES = 2;
+constexpr int STAGES = 3;
 constexpr int A_PLANE = BM * BK * 2;
 constexpr int B_PLANE = BN * BK * 2;
 constexpr int A_BYTES = 4 * A_PLANE;
@@ -39,23 +48,94 @@ constexpr int B_BYTES = 4 * B_PLANE;
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t SWZ = (BK == 16) ? 6u : (BK == 32) ? 4u : 2u;  // 32B / 64B / 128B swizzle
 constexpr uint32_t SBO = 8u * BK * 2u;                             // bytes per 8-row core group
-constexpr int NTHREADS = 192;
+constexpr int NEPI_WARPS = 16;
+constexpr int NTHREADS = 64 + NEPI_WARPS * 32;
 constexpr uint32_t TMEM_COLS = 512;
+constexpr uint32_t BUF_COLS = 2 * BN;   // Re + Im of one accumulation buffer
+constexpr int HALF = BN / (NEPI_WARPS / 4);  // columns per epilogue warp
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 
-static_assert(2 * BN <= (int)TMEM_COLS, "Re + Im accumulators must fit TMEM");
+static_assert(2 * BUF_COLS <= TMEM_COLS, "two Re+Im buffers must fit TMEM");
 static_assert(BK % 16 == 0 && BK * 2 <= 128, "BK must be a multiple of 16 within one swizzle row");
+static_assert(HALF % 32 == 0, "epilogue loads 32 columns at a time");
 
-__global__ void __launch_bounds__(NTHREADS, 1)
+__device__ __forceinline__ void add_chunk(float (&s)[HALF], uint32_t taddr, bool assign) {
+  uint32_t v[16];
+#pragma unroll
+  for (int c = 0; c < HALF; c += 16) {
+    ptx::tmem_ld_32x32b_x16(taddr + c, v);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) s[c + k] = assign ? __uint_as_float(v[k]) : s[c + k] + __uint_as_float(v[k]);
+  }
+}
+
+__device__ __forceinline__ void store_sums(const float (&s)[HALF], uint32_t taddr) {
+#pragma unroll
+  for (int c = 0; c < HALF; c += 16) {
+    uint32_t v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(s[c + k]);
+    ptx::tmem_st_32x32b_x16(taddr + c, v);
+  }
+}
+
+// PLV-family epilogue of one finished round for this thread's row i and its
+// HALF-column slice; sums are read back 4 columns at a time from TMEM.
+__device__ __noinline__ void emit_round(const GramParams& p, const Item& w, int r, int r0, int r1, uint32_t ta,
+                                        int il, int h, bool any_masked) {
+  const RoundInfo ri = round_info(p, w, r, r0, r1);
+  const int i = w.I * BM + il;
+  const long long Tobs = (long long)p.T * ri.nu;
+  const float inv_t = 1.0f / static_cast<float>(Tobs);
+  unsigned illc = 0;
+#pragma unroll 1
+  for (int g = 0; g < HALF; g += 4) {
+    uint32_t vre[4], vim[4];
+    ptx::tmem_ld_32x32b_x4(ta + g, vre);
+    ptx::tmem_ld_32x32b_x4(ta + BN + g, vim);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int j = w.J * BN + h * HALF + g + e;
+      if (i >= p.N || j >= p.N || j < i) continue;
+      PairMetrics<float> m;
+      if (j == i) {
+        m = diag_metrics<float>();
+      } else {
+        float it_ = inv_t;
+        if (any_masked) {
+          const long long te = effective_T<true>(p, ri.u0, ri.nu, i, j);
+          if (te <= 0) {
+            atomicOr(&p.status->flags, FLAG_EMPTY_WINDOW);
+            it_ = 0.0f;
+          } else {
+            it_ = 1.0f / static_cast<float>(te);
+          }
+        }
+        m = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), it_);
+        const float are = fabsf(m.cre);
+        const float d = (1.0f - are) * (1.0f + are);
+        // predicted ciPLV error for a ~1e-6 error in Re / Im
+        if (d > 0.0f && 1e-6f * (fabsf(m.cim) * are / d + 1.0f) > p.illcond_tol * sqrtf(d)) ++illc;
+      }
+      emit_all<float>(p, ri.slot, i, j, m, ri.first, ri.last);
+    }
+  }
+  if (illc) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+}
+
+// 576 threads, one CTA per SM: 112 registers per thread is the whole file.
+__global__ void __maxnreg__(112)
     gram_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GramParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -66,8 +146,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(tfull, 1);
-    ptx::mbar_init(tempty, 128);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], NEPI_WARPS * 32);
+    }
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
@@ -82,6 +164,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tmem = *tslot;
 
   const int nk = (p.T + BK - 1) / BK;
+  const int kcb = p.kc_blocks;
+  const int nchunks = (nk + kcb - 1) / kcb;
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -113,37 +197,43 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_pos = ptx::make_idesc_f16(BM, BN, false);
       constexpr uint32_t idesc_neg = ptx::make_idesc_f16(BM, BN, true);
-      const uint32_t d_re = tmem;
-      const uint32_t d_im = tmem + BN;
       int stage = 0;
-      uint32_t phase = 0, acc_phase = 0;
+      uint32_t phase = 0;
+      uint32_t uses[2] = {0u, 0u};
+      int buf = 0;
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
         const Item w = p.items[it];
         const int r0 = p.pool ? 0 : w.g * p.Rg;
         const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
         for (int r = r0; r < r1; ++r) {
-          const bool start_acc = !p.pool || r == r0;
-          if (start_acc) {
-            ptx::mbar_wait(tempty, acc_phase ^ 1u, tflag);
-            ptx::tc_fence_after();
-          }
           for (int kb = 0; kb < nk; ++kb) {
+            const bool chunk_start = (kb % kcb) == 0;
+            const bool chunk_end = (kb % kcb) == kcb - 1 || kb == nk - 1;
+            if (chunk_start) {
+              ptx::mbar_wait(&tempty[buf], (uses[buf] & 1u) ^ 1u, tflag);
+              ptx::tc_fence_after();
+            }
+            const uint32_t d_re = tmem + (uint32_t)buf * BUF_COLS;
+            const uint32_t d_im = d_re + BN;
             ptx::mbar_wait(&full[stage], phase, tflag);
             ptx::tc_fence_after();
-            const uint32_t sa = ptx::smem_u32(smem + stage * STAGE_BYTES);
-            const uint32_t sb = sa + A_BYTES;
+            // descriptor of the stage's A tile; planes / K sub-steps are
+            // constant offsets added to the 14-bit start-address field
+            // (smem addresses < 256 KB never carry out of it)
+            const uint64_t dA = ptx::make_smem_desc(ptx::smem_u32(smem + stage * STAGE_BYTES), SBO, SWZ);
+            const uint64_t dB = dA + (uint64_t)(A_BYTES >> 4);
 #pragma unroll
             for (int ks = 0; ks < BK / 16; ++ks) {
-              const uint32_t ko = ks * 32;  // 16 fp16 = 32 bytes along K inside the swizzle row
-              const uint64_t aRh = ptx::make_smem_desc(sa + 0 * A_PLANE + ko, SBO, SWZ);
-              const uint64_t aRl = ptx::make_smem_desc(sa + 1 * A_PLANE + ko, SBO, SWZ);
-              const uint64_t aIh = ptx::make_smem_desc(sa + 2 * A_PLANE + ko, SBO, SWZ);
-              const uint64_t aIl = ptx::make_smem_desc(sa + 3 * A_PLANE + ko, SBO, SWZ);
-              const uint64_t bRh = ptx::make_smem_desc(sb + 0 * B_PLANE + ko, SBO, SWZ);
-              const uint64_t bRl = ptx::make_smem_desc(sb + 1 * B_PLANE + ko, SBO, SWZ);
-              const uint64_t bIh = ptx::make_smem_desc(sb + 2 * B_PLANE + ko, SBO, SWZ);
-              const uint64_t bIl = ptx::make_smem_desc(sb + 3 * B_PLANE + ko, SBO, SWZ);
-              const uint32_t acc0 = (start_acc && kb == 0 && ks == 0) ? 0u : 1u;
+              const uint64_t ko = (uint64_t)(ks * 32) >> 4;  // 16 fp16 = 32 bytes along K
+              const uint64_t aRh = dA + ko + 0 * (A_PLANE >> 4);
+              const uint64_t aRl = dA + ko + 1 * (A_PLANE >> 4);
+              const uint64_t aIh = dA + ko + 2 * (A_PLANE >> 4);
+              const uint64_t aIl = dA + ko + 3 * (A_PLANE >> 4);
+              const uint64_t bRh = dB + ko + 0 * (B_PLANE >> 4);
+              const uint64_t bRl = dB + ko + 1 * (B_PLANE >> 4);
+              const uint64_t bIh = dB + ko + 2 * (B_PLANE >> 4);
+              const uint64_t bIl = dB + ko + 3 * (B_PLANE >> 4);
+              const uint32_t acc0 = (chunk_start && ks == 0) ? 0u : 1u;
               // Re = Zr Zr' + Zi Zi'
               ptx::mma_f16_ss(d_re, aRh, bRh, idesc_pos, acc0);
               ptx::mma_f16_ss(d_re, aRh, bRl, idesc_pos, 1u);
@@ -164,74 +254,51 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               stage = 0;
               phase ^= 1u;
             }
-          }
-          const bool end_acc = !p.pool || r == r1 - 1;
-          if (end_acc) {
-            ptx::mma_commit(tfull);  // accumulators complete -> epilogue
-            acc_phase ^= 1u;
+            if (chunk_end) {
+              ptx::mma_commit(&tfull[buf]);  // chunk partial complete -> epilogue
+              uses[buf]++;
+              buf ^= 1;
+            }
           }
         }
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5) =====================
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    // ===================== epilogue (warps 2..17) =====================
+    const int q = warp & 3;           // TMEM lane quadrant this warp may access
+    const int h = (warp - 2) >> 2;    // column slice
     const int il = q * 32 + lane;
-    uint32_t acc_phase = 0;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint32_t uses[2] = {0u, 0u};
+    int buf = 0;
     const bool any_masked = (p.status->flags & FLAG_ANY_MASKED) != 0;
+    float sre[HALF], sim[HALF];
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
       const Item w = p.items[it];
       const int r0 = p.pool ? 0 : w.g * p.Rg;
       const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
       for (int r = r0; r < r1; ++r) {
-        if (p.pool && r != r1 - 1) continue;
-        const RoundInfo ri = round_info(p, w, r, r0, r1);
-        ptx::mbar_wait(tfull, acc_phase, tflag);
-        ptx::tc_fence_after();
-        const int i = w.I * BM + il;
-        const long long Tobs = (long long)p.T * ri.nu;
-        const float inv_t = 1.0f / static_cast<float>(Tobs);
-        unsigned illc = 0;
-        for (int c = 0; c < BN; c += 32) {
-          uint32_t vre[32], vim[32];
-          const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c;
-          ptx::tmem_ld_32x32b_x32(ta, vre);
-          ptx::tmem_ld_32x32b_x32(ta + BN, vim);
-          ptx::tmem_wait_ld();
-          if (i < p.N) {
-#pragma unroll
-            for (int k = 0; k < 32; ++k) {
-              const int j = w.J * BN + c + k;
-              if (j >= p.N || j < i) continue;
-              PairMetrics<float> m;
-              if (j == i) {
-                m = diag_metrics<float>();
-              } else {
-                float it_ = inv_t;
-                if (any_masked) {
-                  const long long te = effective_T<true>(p, ri.u0, ri.nu, i, j);
-                  if (te <= 0) {
-                    atomicOr(&p.status->flags, FLAG_EMPTY_WINDOW);
-                    it_ = 0.0f;
-                  } else {
-                    it_ = 1.0f / static_cast<float>(te);
-                  }
-                }
-                m = pair_metrics<float, true>(__uint_as_float(vre[k]), __uint_as_float(vim[k]), it_);
-                const float are = fabsf(m.cre);
-                const float d = (1.0f - are) * (1.0f + are);
-                // predicted ciPLV error from an fp32-accumulation error of
-                // ~4e-7 in Re: |Im| |Re| / d^1.5 * 4e-7
-                if (d > 0.0f && fabsf(m.cim) * are * 4e-7f > p.illcond_tol * d * sqrtf(d)) ++illc;
-              }
-              emit_all<float>(p, ri.slot, i, j, m, ri.first, ri.last);
-            }
+        for (int c = 0; c < nchunks; ++c) {
+          ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
+          ptx::tc_fence_after();
+          const uint32_t ta = tmem + lane_base + (uint32_t)buf * BUF_COLS + (uint32_t)(h * HALF);
+          const bool assign = (c == 0) && (!p.pool || r == r0);
+          add_chunk(sre, ta, assign);
+          add_chunk(sim, ta + BN, assign);
+          if (c == nchunks - 1 && (!p.pool || r == r1 - 1)) {
+            // Round complete: park the fp32 sums back in this (still owned)
+            // TMEM buffer and emit from there with a compact loop, so the
+            // 64 register sums are dead during the store-heavy epilogue.
+            store_sums(sre, ta);
+            store_sums(sim, ta + BN);
+            ptx::tmem_wait_st();
+            emit_round(p, w, r, r0, r1, ta, il, h, any_masked);
           }
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(&tempty[buf]);
+          uses[buf]++;
+          buf ^= 1;
         }
-        if (illc) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
-        ptx::tc_fence_before();
-        ptx::mbar_arrive(tempty);
-        acc_phase ^= 1u;
       }
     }
   }

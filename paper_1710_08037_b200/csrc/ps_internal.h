@@ -68,6 +68,7 @@ struct GramParams {
   DevStatus* status;
   // timing / debug
   float illcond_tol;           // flag ciPLV pairs whose predicted error > tol
+  int kc_blocks;               // split kernel: K blocks per TMEM accumulation chunk (drain period)
 };
 
 // ---- launchers (return cudaError_t) --------------------------------------
@@ -95,7 +96,7 @@ cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);
 
 // tile geometry of the two Gram kernels
 constexpr int kSplitBM = 128;
-constexpr int kSplitBN = 256;
+constexpr int kSplitBN = 128;
 constexpr int kSplitBK = 32;
 constexpr int kF64BM = 64;
 constexpr int kF64BN = 64;
