@@ -77,7 +77,7 @@ struct ps_ctx {
   bool timing = false;
   std::mutex mu;
   std::map<PlanKey, cufftHandle> plans;
-  Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout;
+  Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout, refine, refine_sorted;
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
   std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
@@ -434,7 +434,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   cudaSetDevice(c->device);
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
-                 &c->hout})
+                 &c->hout, &c->refine, &c->refine_sorted})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -542,6 +542,12 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   p.plane_stride = g.plane_stride;
   p.status = c->d_status;
   p.illcond_tol = 2e-6f;
+  if (g.split && outs[2]) {
+    const int cap = 1 << 22;  // queued ill-conditioned ciPLV (pair, round) entries
+    PS_TRY(ensure(c->refine, (size_t)cap * sizeof(RefineEntry)));
+    p.refine = static_cast<RefineEntry*>(c->refine.p);
+    p.refine_cap = cap;
+  }
   {
     // TMEM accumulation chunk (drain period) in 32-sample K blocks; see gram_tc.cu
     static const int kcb_env = [] {
@@ -604,8 +610,40 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
     PS_CUDA(launch_group_reduce(c->gws.p, G, nn, 5, final_outs, g.B * nn, (int)g.R, g.split ? 0 : 1, st));
     for (int m = 0; m < 5; ++m) c->launches += final_outs[m] ? 1 : 0;
   }
-  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[3], st));
   ps_status s = read_status(c, st);
+  // ---- exact FP64 refinement of ill-conditioned ciPLV pairs (split path) ----
+  const unsigned long long n_ref = c->h_status->n_illcond;
+  if (s == PS_OK && g.split && final_outs[2] && n_ref > 0) {
+    if (n_ref > (unsigned long long)p.refine_cap)
+      return fail(PS_E_INTERNAL, "ciPLV refinement queue overflow (" + std::to_string(n_ref) + " pairs)");
+    std::vector<RefineEntry> ent(n_ref);
+    PS_CUDA(cudaMemcpy(ent.data(), c->refine.p, n_ref * sizeof(RefineEntry), cudaMemcpyDeviceToHost));
+    if (slot_mode == 2)
+      for (auto& e : ent) e.slot /= G;  // workspace slot b*G+g -> final output slot b
+    std::sort(ent.begin(), ent.end(), [](const RefineEntry& x, const RefineEntry& y) {
+      return std::tie(x.slot, x.i, x.j, x.u0) < std::tie(y.slot, y.i, y.j, y.u0);
+    });
+    std::vector<int> groups;
+    for (size_t k = 0; k < ent.size(); ++k)
+      if (k == 0 || ent[k].slot != ent[k - 1].slot || ent[k].i != ent[k - 1].i || ent[k].j != ent[k - 1].j)
+        groups.push_back((int)k);
+    const int n_groups = (int)groups.size();
+    groups.push_back((int)ent.size());
+    PS_TRY(ensure(c->refine_sorted, ent.size() * sizeof(RefineEntry) + groups.size() * sizeof(int) + 64));
+    RefineEntry* d_ent = static_cast<RefineEntry*>(c->refine_sorted.p);
+    int* d_grp = reinterpret_cast<int*>(static_cast<char*>(c->refine_sorted.p) +
+                                        round_up((long long)(ent.size() * sizeof(RefineEntry)), 16));
+    PS_CUDA(cudaMemcpyAsync(d_ent, ent.data(), ent.size() * sizeof(RefineEntry), cudaMemcpyHostToDevice, st));
+    PS_CUDA(cudaMemcpyAsync(d_grp, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    GramParams pr = p;
+    pr.out_ciplv = final_outs[2];
+    const bool single_round = pool || g.R == 1 || slot_mode == 0;
+    PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, single_round ? 1 : 0, (int)g.R, st));
+    c->launches++;
+    PS_CUDA(cudaStreamSynchronize(st));
+  }
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[3], st));
+  if (c->timing) PS_CUDA(cudaEventSynchronize(c->ev[3]));
   if (res) {
     std::memset(res, 0, sizeof(*res));
     res->n_observations = pool ? g.T * g.R : g.T;

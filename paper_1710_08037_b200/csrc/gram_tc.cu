@@ -59,14 +59,14 @@ static_assert(2 * BUF_COLS <= TMEM_COLS, "two Re+Im buffers must fit TMEM");
 static_assert(BK % 16 == 0 && BK * 2 <= 128, "BK must be a multiple of 16 within one swizzle row");
 static_assert(HALF % 32 == 0, "epilogue loads 32 columns at a time");
 
-__device__ __forceinline__ void add_chunk(float (&s)[HALF], uint32_t taddr, bool assign) {
+__device__ __forceinline__ void add_chunk(float (&s)[HALF], uint32_t taddr) {
   uint32_t v[16];
 #pragma unroll
   for (int c = 0; c < HALF; c += 16) {
     ptx::tmem_ld_32x32b_x16(taddr + c, v);
     ptx::tmem_wait_ld();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) s[c + k] = assign ? __uint_as_float(v[k]) : s[c + k] + __uint_as_float(v[k]);
+    for (int k = 0; k < 16; ++k) s[c + k] += __uint_as_float(v[k]);
   }
 }
 
@@ -82,7 +82,7 @@ __device__ __forceinline__ void store_sums(const float (&s)[HALF], uint32_t tadd
 
 // PLV-family epilogue of one finished round for this thread's row i and its
 // HALF-column slice; sums are read back 4 columns at a time from TMEM.
-__device__ __noinline__ void emit_round(const GramParams& p, const Item& w, int r, int r0, int r1, uint32_t ta,
+__device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, int r, int r0, int r1, uint32_t ta,
                                         int il, int h, bool any_masked) {
   const RoundInfo ri = round_info(p, w, r, r0, r1);
   const int i = w.I * BM + il;
@@ -116,17 +116,34 @@ __device__ __noinline__ void emit_round(const GramParams& p, const Item& w, int 
         m = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), it_);
         const float are = fabsf(m.cre);
         const float d = (1.0f - are) * (1.0f + are);
-        // predicted ciPLV error for a ~1e-6 error in Re / Im
-        if (d > 0.0f && 1e-6f * (fabsf(m.cim) * are / d + 1.0f) > p.illcond_tol * sqrtf(d)) ++illc;
+        // predicted ciPLV error for a ~1e-6 error in Re / Im: queue the pair
+        // for exact FP64 recomputation (refine kernel) when it exceeds tol
+        if (d > 0.0f && 1e-6f * (fabsf(m.cim) * are / d + 1.0f) > p.illcond_tol * sqrtf(d)) {
+          ++illc;
+          if (p.refine) {
+            const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
+            if (k < (unsigned long long)p.refine_cap) {
+              RefineEntry e;
+              e.slot = (int)ri.slot;
+              e.i = i;
+              e.j = j;
+              e.u0 = ri.u0;
+              e.nu = ri.nu;
+              e.approx = m.ciplv;
+              p.refine[k] = e;
+            }
+          }
+        }
       }
       emit_all<float>(p, ri.slot, i, j, m, ri.first, ri.last);
     }
   }
-  if (illc) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+  if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
 }
 
-// 576 threads, one CTA per SM: 112 registers per thread is the whole file.
-__global__ void __maxnreg__(112)
+// 576 threads = 18 warps, one CTA per SM; with 5 warps on some SM sub-partition
+// the register budget is 16384 / (5 * 32) -> 96 per thread.
+__global__ void __launch_bounds__(NTHREADS, 1)
     gram_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GramParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -273,6 +290,8 @@ __global__ void __maxnreg__(112)
     int buf = 0;
     const bool any_masked = (p.status->flags & FLAG_ANY_MASKED) != 0;
     float sre[HALF], sim[HALF];
+#pragma unroll
+    for (int k = 0; k < HALF; ++k) sre[k] = sim[k] = 0.0f;
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
       const Item w = p.items[it];
       const int r0 = p.pool ? 0 : w.g * p.Rg;
@@ -282,9 +301,8 @@ __global__ void __maxnreg__(112)
           ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
           ptx::tc_fence_after();
           const uint32_t ta = tmem + lane_base + (uint32_t)buf * BUF_COLS + (uint32_t)(h * HALF);
-          const bool assign = (c == 0) && (!p.pool || r == r0);
-          add_chunk(sre, ta, assign);
-          add_chunk(sim, ta + BN, assign);
+          add_chunk(sre, ta);
+          add_chunk(sim, ta + BN);
           if (c == nchunks - 1 && (!p.pool || r == r1 - 1)) {
             // Round complete: park the fp32 sums back in this (still owned)
             // TMEM buffer and emit from there with a compact loop, so the
@@ -293,6 +311,8 @@ __global__ void __maxnreg__(112)
             store_sums(sim, ta + BN);
             ptx::tmem_wait_st();
             emit_round(p, w, r, r0, r1, ta, il, h, any_masked);
+#pragma unroll
+            for (int k = 0; k < HALF; ++k) sre[k] = sim[k] = 0.0f;  // sums dead across the emission
           }
           ptx::tc_fence_before();
           ptx::mbar_arrive(&tempty[buf]);

@@ -40,6 +40,15 @@ struct SrcDesc {
   long long h_row0;          // first row held in hbuf
 };
 
+// An ill-conditioned ciPLV value of the split path queued for exact FP64
+// recomputation (slot / pair / units of one epilogue round + the value the
+// epilogue emitted).  Sorted on the host before the refine kernel runs, so
+// corrections are applied in a fixed order (deterministic output).
+struct RefineEntry {
+  int slot, i, j, u0, nu;
+  float approx;
+};
+
 // One Gram work item: band b, trial group g (trials [g*Rg, min(R,(g+1)*Rg))),
 // row panel I (BM rows), column panel J (BN cols).
 struct Item { int b, g, I, J; };
@@ -68,6 +77,8 @@ struct GramParams {
   DevStatus* status;
   // timing / debug
   float illcond_tol;           // flag ciPLV pairs whose predicted error > tol
+  RefineEntry* refine;         // queue of flagged pairs (nullptr: count only)
+  int refine_cap;
   int kc_blocks;               // split kernel: K blocks per TMEM accumulation chunk (drain period)
 };
 
@@ -93,6 +104,12 @@ cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int
 cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p,
                               int grid, cudaStream_t st);
 cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);
+// Exact FP64 recomputation of queued ciPLV pairs.  groups[g]..groups[g+1]
+// index a run of entries (sorted by slot, i, j, u0) sharing one output
+// location; `overwrite` = the slot holds a single round (else the mean over
+// `div` rounds gets (exact - approx) / div added).
+cudaError_t launch_refine(const GramParams& p, const RefineEntry* entries, const int* groups, int n_groups,
+                          int overwrite, int div, cudaStream_t st);
 
 // tile geometry of the two Gram kernels
 constexpr int kSplitBM = 128;
