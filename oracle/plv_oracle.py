@@ -17,15 +17,14 @@ numpy>=1.24 (complex matmul -> BLAS zgemm) and scipy>=1.10 (FFT).  Neither is
 vendored by the reference; this oracle uses the numpy/scipy installed here
 (numpy 2.3, scipy 1.18) and restates the published algorithms directly.
 
-Parity pinning
---------------
+Parity pinning -- parity unpinned by reference tests
+----------------------------------------------------
 There are no reference tests, fixtures or golden vectors to pin against
-(``pkg/pyproject.toml:25`` names an absent ``tests/``).  The oracle is pinned
+(``pkg/pyproject.toml:25`` names an absent ``tests/``) and no reference code to
+run, so parity against reference *code* is unpinned.  The oracle is pinned
 against every closed-form known-answer example and invariant the SPEC states
 for this path (see ``tests/test_oracle_kats.py``) and against
-``scipy.signal.hilbert`` for the analytic signal.  Parity with an executable
-reference implementation is therefore "pinned to SPEC known answers", not to
-reference code ("Oracle").
+``scipy.signal.hilbert`` for the analytic signal.
 """
 from __future__ import annotations
 
