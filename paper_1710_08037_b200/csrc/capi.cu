@@ -489,6 +489,20 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   std::vector<std::pair<int, int>> mine;
   for (size_t t = 0; t < tiles.size(); ++t)
     if ((int)(t % shard_count) == shard_index) mine.push_back(tiles[t]);
+  // Execution order: 12 x 12 supertiles (J-major between supertiles).  The
+  // ~148 items in flight at any time then share ~24 row panels, so operand
+  // panels are re-read from L2 instead of DRAM.  (Ownership above keeps the
+  // canonical J-major enumeration of ps_pair_shard.)
+  {
+    static const int S = [] {
+      const char* s = std::getenv("PS_RASTER");
+      return s ? std::max(1, std::atoi(s)) : 12;
+    }();
+    std::stable_sort(mine.begin(), mine.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+      return std::make_tuple(a.second / S, a.first / S, a.second, a.first) <
+             std::make_tuple(b.second / S, b.first / S, b.second, b.first);
+    });
+  }
   const bool pool = a->trial_reduce == PS_TRIALS_POOL;
   int G = 1, slot_mode = 1, mean_div = 1;
   if (pool || g.R == 1) {

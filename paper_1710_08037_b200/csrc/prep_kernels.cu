@@ -157,6 +157,102 @@ __global__ void __launch_bounds__(kNormThreads) normalize_kernel(SrcDesc src, lo
 }
 
 // ---------------------------------------------------------------------------
+// K4 fast path: fp32 source (real + H, or interleaved complex64), samples
+// contiguous and 16-byte aligned rows, split fp16 planes.  Each thread moves
+// 2 x 4 samples with 16-byte loads and 8-byte plane stores (HBM-bound:
+// 16 B/sample algorithmic traffic).
+// ---------------------------------------------------------------------------
+constexpr int kVecPer = 2;                                     // 4-sample groups per thread
+constexpr int kVecSamplesPerBlock = kNormThreads * 4 * kVecPer;
+
+__device__ __forceinline__ uint32_t pack_half2(__half a, __half b) {
+  return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src, long long row0, int chunks,
+                                                                     __half* out, int pitch, long long ps,
+                                                                     unsigned long long* rowmin,
+                                                                     unsigned long long* rowmax, DevStatus* st) {
+  const long long rl = blockIdx.x / chunks;
+  const int ch = blockIdx.x % chunks;
+  const long long r = row0 + rl;
+  const long long roff = row_offset(src, r);
+  const long long T = src.T;
+  float amin = FLT_MAX, amax = 0.0f;
+  bool bad = false;
+  const long long obase = r * pitch;
+#pragma unroll
+  for (int g = 0; g < kVecPer; ++g) {
+    const long long t0 = (long long)ch * kVecSamplesPerBlock + ((long long)g * kNormThreads + threadIdx.x) * 4;
+    if (t0 < T) {
+      float re[4], im[4];
+      if (KIND == 0) {
+        const float4 x = *reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + roff + t0);
+        const float4 h = *reinterpret_cast<const float4*>(static_cast<const float*>(src.hbuf) +
+                                                          (r - src.h_row0) * T + t0);
+        re[0] = x.x; re[1] = x.y; re[2] = x.z; re[3] = x.w;
+        im[0] = h.x; im[1] = h.y; im[2] = h.z; im[3] = h.w;
+      } else {
+        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + 2 * (roff + t0));
+        const float4 a = p[0], b = p[1];
+        re[0] = a.x; im[0] = a.y; re[1] = a.z; im[1] = a.w;
+        re[2] = b.x; im[2] = b.y; re[3] = b.z; im[3] = b.w;
+      }
+      __half rh[4], rlo[4], ih[4], ilo[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float a = sqrtf(re[k] * re[k] + im[k] * im[k]);
+        float zr = 0.0f, zi = 0.0f;
+        if (KIND == 2) {
+          zr = re[k];
+          zi = im[k];
+        } else if (a > 0.0f) {
+          zr = re[k] / a;
+          zi = im[k] / a;
+        }
+        rh[k] = __float2half_rn(zr);
+        ih[k] = __float2half_rn(zi);
+        rlo[k] = __float2half_rn(zr - __half2float(rh[k]));
+        ilo[k] = __float2half_rn(zi - __half2float(ih[k]));
+        if (!(a <= FLT_MAX)) bad = true;
+        amin = fminf(amin, a);
+        amax = fmaxf(amax, a);
+      }
+      __half* o = out + obase + t0;
+      *reinterpret_cast<uint2*>(o) = make_uint2(pack_half2(rh[0], rh[1]), pack_half2(rh[2], rh[3]));
+      *reinterpret_cast<uint2*>(o + ps) = make_uint2(pack_half2(rlo[0], rlo[1]), pack_half2(rlo[2], rlo[3]));
+      *reinterpret_cast<uint2*>(o + 2 * ps) = make_uint2(pack_half2(ih[0], ih[1]), pack_half2(ih[2], ih[3]));
+      *reinterpret_cast<uint2*>(o + 3 * ps) = make_uint2(pack_half2(ilo[0], ilo[1]), pack_half2(ilo[2], ilo[3]));
+    } else if (t0 < pitch) {  // T % 4 == 0: the pitch pad is one 4-sample group
+      __half* o = out + obase + t0;
+      const uint2 z = make_uint2(0u, 0u);
+#pragma unroll
+      for (int pl = 0; pl < 4; ++pl) *reinterpret_cast<uint2*>(o + pl * ps) = z;
+    }
+  }
+  __shared__ float smin[kNormThreads / 32], smax[kNormThreads / 32];
+  for (int o = 16; o > 0; o >>= 1) {
+    amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+    amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    smin[threadIdx.x >> 5] = amin;
+    smax[threadIdx.x >> 5] = amax;
+  }
+  if (bad) atomicOr(&st->flags, FLAG_NONFINITE);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i < kNormThreads / 32; ++i) {
+      amin = fminf(amin, smin[i]);
+      amax = fmaxf(amax, smax[i]);
+    }
+    atomicMin(&rowmin[r], key_of((double)amin));
+    atomicMax(&rowmax[r], key_of((double)amax));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exact amplitude-floor fixup.  For each row: if the cheap
 // bound min|a| >= floor * max|a| holds, no sample can fall below
 // floor * median and the row is untouched (the common case: Rayleigh
@@ -419,6 +515,33 @@ cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_d
 cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
                                  int cdouble, int pitch, long long plane_stride, unsigned long long* rowstat,
                                  long long rows_total, DevStatus* status, cudaStream_t st) {
+  // vectorised fast path: fp32 source, split planes, contiguous 16B-aligned rows
+  {
+    const bool aligned_base = (reinterpret_cast<uintptr_t>(src.ptr) & 15u) == 0;
+    const long long q = src.kind == 0 ? 4 : 2;  // row offsets must be 16-byte multiples
+    const bool strides_ok = (src.s_sig % q == 0) && (src.R == 1 || src.s_trial % q == 0) &&
+                            (src.B == 1 || src.s_band % q == 0);
+    if (fmt == OUT_SPLIT && !cdouble && !src.is_double && src.s_samp == 1 && src.T % 4 == 0 && aligned_base &&
+        strides_ok) {
+      const int vchunks = static_cast<int>((src.T + kVecSamplesPerBlock - 1) / kVecSamplesPerBlock);
+      const long long vblk = nrows * vchunks;
+      if (vblk <= 0) return cudaSuccess;
+      if (vblk > 0x7fffffffLL) return cudaErrorInvalidValue;
+      __half* o = static_cast<__half*>(out);
+      unsigned long long* rmin = rowstat;
+      unsigned long long* rmax = rowstat + rows_total;
+      if (src.kind == 0)
+        normalize_vec_kernel<0><<<(unsigned)vblk, kNormThreads, 0, st>>>(src, row0, vchunks, o, pitch, plane_stride,
+                                                                         rmin, rmax, status);
+      else if (src.kind == 1)
+        normalize_vec_kernel<1><<<(unsigned)vblk, kNormThreads, 0, st>>>(src, row0, vchunks, o, pitch, plane_stride,
+                                                                         rmin, rmax, status);
+      else
+        normalize_vec_kernel<2><<<(unsigned)vblk, kNormThreads, 0, st>>>(src, row0, vchunks, o, pitch, plane_stride,
+                                                                         rmin, rmax, status);
+      return cudaGetLastError();
+    }
+  }
   const int chunks = static_cast<int>((src.T + kNormSamplesPerBlock - 1) / kNormSamplesPerBlock);
   const long long nblk = nrows * chunks;
   if (nblk <= 0) return cudaSuccess;
