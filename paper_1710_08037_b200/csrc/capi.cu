@@ -519,9 +519,19 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   const int Rg = (int)((g.R + G - 1) / G);
   std::vector<Item>& items = c->h_items;
   items.clear();
+  // Split path: ownership tiles are 256 x 128; the single-CTA variant runs
+  // each as two 128-row halves (halves wholly below the diagonal dropped).
+  const int exec_rows = g.split ? split_panel_rows() : kF64BM;
+  const int sub = g.split ? kSplitBM / exec_rows : 1;
   for (int b = 0; b < g.B; ++b)
     for (int gi = 0; gi < G; ++gi)
-      for (auto& t : mine) items.push_back(Item{b, gi, t.first, t.second});
+      for (auto& t : mine)
+        for (int hs = 0; hs < sub; ++hs) {
+          const int I = t.first * sub + hs;
+          const long long jmax = std::min<long long>((long long)t.second * bn + bn, g.N) - 1;
+          if ((long long)I * exec_rows > jmax || (long long)I * exec_rows >= g.N) continue;
+          items.push_back(Item{b, gi, I, t.second});
+        }
   const size_t ibytes = std::max<size_t>(items.size(), 1) * sizeof(Item);
   if (c->h_items_cap < ibytes) {
     if (c->h_items_pinned) cudaFreeHost(c->h_items_pinned);
@@ -585,7 +595,8 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   p.out_ciplv = outs[2];
   p.out_cre = outs[3];
   p.out_cim = outs[4];
-  const int grid = (int)std::min<long long>((long long)items.size(), c->num_sms);
+  const int cta_per_group = g.split ? split_cta_group() : 1;
+  const int grid = (int)std::min<long long>((long long)items.size(), c->num_sms / cta_per_group);
   if (g.split) {
     TmapKey key{c->planes.p, g.T, g.N, g.B * g.R, g.pitch};
     auto it = c->tmaps.find(key);
@@ -596,8 +607,8 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
       cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), 4};
       cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 2, (cuuint64_t)(g.N * g.pitch * 2),
                                (cuuint64_t)(g.plane_stride * 2)};
-      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)kSplitBM, 1, 4};
-      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)kSplitBN, 1, 4};
+      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, 4};  // 128 rows of the I panel per CTA
+      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)split_b_box_rows(), 1, 4};
       cuuint32_t estr[4] = {1, 1, 1, 1};
       const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
                                      : kSplitBK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B

@@ -5,30 +5,38 @@
 // (`ndat(:,:,t) * ndat(:,:,t)'`) and SPEC plv_matrix /
 // iplv / ciplv.  Z = Zr + i Zi is held as four fp16 planes
 // (hi/lo of Re and Im, z = hi + lo to ~2^-24).  Per K-step of 16 samples the
-// single MMA-issuing thread launches 12 UMMAs (M=128, N=128, K=16):
+// single MMA-issuing thread launches 12 UMMAs (K=16):
 //   Re += Rh.Rh' + Rh.Rl' + Rl.Rh' + Ih.Ih' + Ih.Il' + Il.Ih'
 //   Im += Ih.Rh' + Ih.Rl' + Il.Rh' - Rh.Ih' - Rh.Il' - Rl.Ih'
 // (negation through the instruction descriptor's negate-A bit; the lo*lo
 // terms, <= 2^-24, are dropped).
 //
-// Accumulation accuracy.  The tensor core's fp32 accumulate is biased
-// (measured on B200: relative error ~= n_accumulates * 2^-25, i.e. each
-// UMMA truncates the running sum): accumulating all of T in TMEM would cost
-// ~2.5e-5 at T = 2000 and ~8e-4 at T = 65536.  So the K loop is cut into
-// chunks of kc_blocks * 32 samples; each chunk accumulates from zero in one of
-// two TMEM buffers (ping-pong, 2 x (Re 128 + Im 128) = 512 columns) while the
-// epilogue warps drain the other buffer into fp32 register sums
-// (round-to-nearest).  With 128-sample chunks the bias is ~1.4e-6 relative.
+// Two variants share this file (template CG):
+//   CG = 2 (default): a CTA pair (cluster of 2, tcgen05 cta_group::2) owns a
+//     256 x 128 output tile; UMMA M = 256, N = 128.  Each CTA stages its own
+//     128 rows of the I panel and half (64 rows) of the J panel; the rank-0
+//     CTA issues the MMAs, both CTAs' TMEM hold their 128 rows.
+//   CG = 1: one CTA per 128-row half of the tile (UMMA M = 128, N = 128).
 //
-// Warp roles (320 threads, one CTA per SM, persistent over work items):
+// Accumulation accuracy.  The tensor core's fp32 accumulate is biased
+// (measured on B200: relative error ~= n_accumulates * 2^-25, i.e. each UMMA
+// truncates the running sum): accumulating all of T in TMEM would cost
+// ~2e-5 at T = 2000 and ~8e-5 at T = 16384.  So the K loop is cut into chunks
+// of kc_blocks * 32 samples; each chunk accumulates from zero in one of two
+// TMEM buffers (ping-pong, 2 x (Re 128 + Im 128) = 512 columns) while the
+// epilogue warps drain the other buffer into fp32 register sums
+// (round-to-nearest).  With 128-sample chunks the error is ~1e-6.
+//
+// Warp roles (576 threads per CTA, one CTA per SM, persistent over items):
 //   warp 0      TMA producer (one lane)
-//   warp 1      TMEM allocator + MMA issuer (one lane)
+//   warp 1      TMEM allocator + MMA issuer (one lane; rank 0 only for CG=2)
 //   warps 2..17 epilogue: warp w reads TMEM lane quadrant w%4, column quarter
 //               (w-2)/4; drains chunks into 32 Re + 32 Im register sums and,
 //               at the end of a round, emits PLV / iPLV / ciPLV.
 #include <cuda.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <cstdlib>
 
 #include "epilogue.cuh"
 #include "ps_internal.h"
@@ -37,27 +45,33 @@
 namespace ps {
 namespace {
 
-constexpr int BM = kSplitBM;   // 128 rows of panel I  (UMMA M, TMEM lanes)
-constexpr int BN = kSplitBN;   // 128 rows of panel J  (UMMA N)
+constexpr int BMC = 128;       // rows per CTA (TMEM lanes)
+constexpr int BN = kSplitBN;   // 128 columns (UMMA N)
 constexpr int BK = kSplitBK;   // 32 samples per pipeline stage
-constexpr int STAGES = 3;
-constexpr int A_PLANE = BM * BK * 2;
-constexpr int B_PLANE = BN * BK * 2;
-constexpr int A_BYTES = 4 * A_PLANE;
-constexpr int B_BYTES = 4 * B_PLANE;
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr uint32_t SWZ = (BK == 16) ? 6u : (BK == 32) ? 4u : 2u;  // 32B / 64B / 128B swizzle
 constexpr uint32_t SBO = 8u * BK * 2u;                             // bytes per 8-row core group
 constexpr int NEPI_WARPS = 16;
 constexpr int NTHREADS = 64 + NEPI_WARPS * 32;
 constexpr uint32_t TMEM_COLS = 512;
-constexpr uint32_t BUF_COLS = 2 * BN;   // Re + Im of one accumulation buffer
-constexpr int HALF = BN / (NEPI_WARPS / 4);  // columns per epilogue warp
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t BUF_COLS = 2 * BN;          // Re + Im of one accumulation buffer
+constexpr int HALF = BN / (NEPI_WARPS / 4);    // columns per epilogue warp
+
+template <int CG>
+struct Geo {
+  static constexpr int BNC = BN / CG;                    // J-panel rows staged per CTA
+  static constexpr int A_PLANE = BMC * BK * 2;
+  static constexpr int B_PLANE = BNC * BK * 2;
+  static constexpr int A_BYTES = 4 * A_PLANE;
+  static constexpr int B_BYTES = 4 * B_PLANE;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
+  static constexpr int STAGES = CG == 2 ? 4 : 3;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int UMMA_M = BMC * CG;
+};
 
 static_assert(2 * BUF_COLS <= TMEM_COLS, "two Re+Im buffers must fit TMEM");
 static_assert(BK % 16 == 0 && BK * 2 <= 128, "BK must be a multiple of 16 within one swizzle row");
-static_assert(HALF % 32 == 0, "epilogue loads 32 columns at a time");
+static_assert(HALF % 16 == 0, "epilogue loads 16 columns at a time");
 
 __device__ __forceinline__ void add_chunk(float (&s)[HALF], uint32_t taddr) {
   uint32_t v[16];
@@ -80,12 +94,11 @@ __device__ __forceinline__ void store_sums(const float (&s)[HALF], uint32_t tadd
   }
 }
 
-// PLV-family epilogue of one finished round for this thread's row i and its
+// PLV-family epilogue of one finished round for row i and this warp's
 // HALF-column slice; sums are read back 4 columns at a time from TMEM.
 __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, int r, int r0, int r1, uint32_t ta,
-                                        int il, int h, bool any_masked) {
+                                           int i, int h, bool any_masked) {
   const RoundInfo ri = round_info(p, w, r, r0, r1);
-  const int i = w.I * BM + il;
   const long long Tobs = (long long)p.T * ri.nu;
   const float inv_t = 1.0f / static_cast<float>(Tobs);
   unsigned illc = 0;
@@ -123,14 +136,14 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
           if (p.refine) {
             const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
             if (k < (unsigned long long)p.refine_cap) {
-              RefineEntry e;
-              e.slot = (int)ri.slot;
-              e.i = i;
-              e.j = j;
-              e.u0 = ri.u0;
-              e.nu = ri.nu;
-              e.approx = m.ciplv;
-              p.refine[k] = e;
+              RefineEntry en;
+              en.slot = (int)ri.slot;
+              en.i = i;
+              en.j = j;
+              en.u0 = ri.u0;
+              en.nu = ri.nu;
+              en.approx = m.ciplv;
+              p.refine[k] = en;
             }
           }
         }
@@ -143,40 +156,51 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
 
 // 576 threads = 18 warps, one CTA per SM; with 5 warps on some SM sub-partition
 // the register budget is 16384 / (5 * 32) -> 96 per thread.
+//
+// Items carry 256-row tiles (I indexes 256-row panels).  CG = 2: the pair
+// covers all 256 rows.  CG = 1: item.g's high bit is unused; instead the host
+// doubles the items and the low bit of I (after << 1) selects the half -- see
+// launch_gram_split: for CG = 1 the host passes 128-row panel indices.
+template <int CG>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gram_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const GramParams p) {
+  using G = Geo<CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;      // [2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE_BYTES);
+  uint64_t* empty = full + G::STAGES;
+  uint64_t* tfull = empty + G::STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;         // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
+  const int grp = CG == 2 ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ngrp = CG == 2 ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   int* tflag = &p.status->flags;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < G::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], NEPI_WARPS * 32);
+      ptx::mbar_init(&tempty[b], CG * NEPI_WARPS);  // one arrival per epilogue warp of the group
     }
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
   }
   if (warp == 1) {
-    ptx::tmem_alloc(tslot, TMEM_COLS);
-    ptx::tmem_relinquish();
+    ptx::tmem_alloc_cg<CG>(tslot, TMEM_COLS);
+    ptx::tmem_relinquish_cg<CG>();
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrive
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tslot;
 
@@ -185,23 +209,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int nchunks = (nk + kcb - 1) / kcb;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (every CTA) =====================
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      for (int it = grp; it < p.n_items; it += ngrp) {
         const Item w = p.items[it];
         const int r0 = p.pool ? 0 : w.g * p.Rg;
         const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
+        const int rowA = w.I * G::UMMA_M + (int)rank * BMC;
+        const int rowB = w.J * BN + (int)rank * G::BNC;
         for (int r = r0; r < r1; ++r) {
           const int u = w.b * p.R + r;
           for (int kb = 0; kb < nk; ++kb) {
             ptx::mbar_wait(&empty[stage], phase ^ 1u, tflag);
-            uint8_t* sa = smem + stage * STAGE_BYTES;
-            ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-            ptx::tma_load_4d(sa, &tmA, &full[stage], kb * BK, w.I * BM, u, 0);
-            ptx::tma_load_4d(sa + A_BYTES, &tmB, &full[stage], kb * BK, w.J * BN, u, 0);
-            if (++stage == STAGES) {
+            uint8_t* sa = smem + stage * G::STAGE_BYTES;
+            if (CG == 1) {
+              ptx::mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
+              ptx::tma_load_4d(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
+              ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
+            } else {
+              // rank 0's full barrier counts the bytes of both CTAs
+              if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE_BYTES);
+              ptx::tma_load_4d_cg2(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
+              ptx::tma_load_4d_cg2(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
+            }
+            if (++stage == G::STAGES) {
               stage = 0;
               phase ^= 1u;
             }
@@ -210,15 +243,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t idesc_pos = ptx::make_idesc_f16(BM, BN, false);
-      constexpr uint32_t idesc_neg = ptx::make_idesc_f16(BM, BN, true);
+    // ===================== MMA issuer (rank 0) =====================
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc_pos = ptx::make_idesc_f16(G::UMMA_M, BN, false);
+      constexpr uint32_t idesc_neg = ptx::make_idesc_f16(G::UMMA_M, BN, true);
       int stage = 0;
       uint32_t phase = 0;
       uint32_t uses[2] = {0u, 0u};
       int buf = 0;
-      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      for (int it = grp; it < p.n_items; it += ngrp) {
         const Item w = p.items[it];
         const int r0 = p.pool ? 0 : w.g * p.Rg;
         const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
@@ -237,42 +270,42 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // descriptor of the stage's A tile; planes / K sub-steps are
             // constant offsets added to the 14-bit start-address field
             // (smem addresses < 256 KB never carry out of it)
-            const uint64_t dA = ptx::make_smem_desc(ptx::smem_u32(smem + stage * STAGE_BYTES), SBO, SWZ);
-            const uint64_t dB = dA + (uint64_t)(A_BYTES >> 4);
+            const uint64_t dA = ptx::make_smem_desc(ptx::smem_u32(smem + stage * G::STAGE_BYTES), SBO, SWZ);
+            const uint64_t dB = dA + (uint64_t)(G::A_BYTES >> 4);
 #pragma unroll
             for (int ks = 0; ks < BK / 16; ++ks) {
               const uint64_t ko = (uint64_t)(ks * 32) >> 4;  // 16 fp16 = 32 bytes along K
-              const uint64_t aRh = dA + ko + 0 * (A_PLANE >> 4);
-              const uint64_t aRl = dA + ko + 1 * (A_PLANE >> 4);
-              const uint64_t aIh = dA + ko + 2 * (A_PLANE >> 4);
-              const uint64_t aIl = dA + ko + 3 * (A_PLANE >> 4);
-              const uint64_t bRh = dB + ko + 0 * (B_PLANE >> 4);
-              const uint64_t bRl = dB + ko + 1 * (B_PLANE >> 4);
-              const uint64_t bIh = dB + ko + 2 * (B_PLANE >> 4);
-              const uint64_t bIl = dB + ko + 3 * (B_PLANE >> 4);
+              const uint64_t aRh = dA + ko + 0 * (G::A_PLANE >> 4);
+              const uint64_t aRl = dA + ko + 1 * (G::A_PLANE >> 4);
+              const uint64_t aIh = dA + ko + 2 * (G::A_PLANE >> 4);
+              const uint64_t aIl = dA + ko + 3 * (G::A_PLANE >> 4);
+              const uint64_t bRh = dB + ko + 0 * (G::B_PLANE >> 4);
+              const uint64_t bRl = dB + ko + 1 * (G::B_PLANE >> 4);
+              const uint64_t bIh = dB + ko + 2 * (G::B_PLANE >> 4);
+              const uint64_t bIl = dB + ko + 3 * (G::B_PLANE >> 4);
               const uint32_t acc0 = (chunk_start && ks == 0) ? 0u : 1u;
               // Re = Zr Zr' + Zi Zi'
-              ptx::mma_f16_ss(d_re, aRh, bRh, idesc_pos, acc0);
-              ptx::mma_f16_ss(d_re, aRh, bRl, idesc_pos, 1u);
-              ptx::mma_f16_ss(d_re, aRl, bRh, idesc_pos, 1u);
-              ptx::mma_f16_ss(d_re, aIh, bIh, idesc_pos, 1u);
-              ptx::mma_f16_ss(d_re, aIh, bIl, idesc_pos, 1u);
-              ptx::mma_f16_ss(d_re, aIl, bIh, idesc_pos, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_re, aRh, bRh, idesc_pos, acc0);
+              ptx::mma_f16_ss_cg<CG>(d_re, aRh, bRl, idesc_pos, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_re, aRl, bRh, idesc_pos, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_re, aIh, bIh, idesc_pos, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_re, aIh, bIl, idesc_pos, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_re, aIl, bIh, idesc_pos, 1u);
               // Im = Zi Zr' - Zr Zi'
-              ptx::mma_f16_ss(d_im, aIh, bRh, idesc_pos, acc0);
-              ptx::mma_f16_ss(d_im, aIh, bRl, idesc_pos, 1u);
-              ptx::mma_f16_ss(d_im, aIl, bRh, idesc_pos, 1u);
-              ptx::mma_f16_ss(d_im, aRh, bIh, idesc_neg, 1u);
-              ptx::mma_f16_ss(d_im, aRh, bIl, idesc_neg, 1u);
-              ptx::mma_f16_ss(d_im, aRl, bIh, idesc_neg, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_im, aIh, bRh, idesc_pos, acc0);
+              ptx::mma_f16_ss_cg<CG>(d_im, aIh, bRl, idesc_pos, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_im, aIl, bRh, idesc_pos, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_im, aRh, bIh, idesc_neg, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_im, aRh, bIl, idesc_neg, 1u);
+              ptx::mma_f16_ss_cg<CG>(d_im, aRl, bIh, idesc_neg, 1u);
             }
-            ptx::mma_commit(&empty[stage]);  // smem slot free once these MMAs retire
-            if (++stage == STAGES) {
+            ptx::mma_commit_cg<CG>(&empty[stage]);  // the group's smem slots free once these retire
+            if (++stage == G::STAGES) {
               stage = 0;
               phase ^= 1u;
             }
             if (chunk_end) {
-              ptx::mma_commit(&tfull[buf]);  // chunk partial complete -> epilogue
+              ptx::mma_commit_cg<CG>(&tfull[buf]);  // chunk partial complete -> epilogues
               uses[buf]++;
               buf ^= 1;
             }
@@ -281,7 +314,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   } else {
-    // ===================== epilogue (warps 2..17) =====================
+    // ===================== epilogue (warps 2..17, every CTA) =====================
     const int q = warp & 3;           // TMEM lane quadrant this warp may access
     const int h = (warp - 2) >> 2;    // column slice
     const int il = q * 32 + lane;
@@ -292,10 +325,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float sre[HALF], sim[HALF];
 #pragma unroll
     for (int k = 0; k < HALF; ++k) sre[k] = sim[k] = 0.0f;
-    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+    for (int it = grp; it < p.n_items; it += ngrp) {
       const Item w = p.items[it];
       const int r0 = p.pool ? 0 : w.g * p.Rg;
       const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
+      const int i = w.I * G::UMMA_M + (int)rank * BMC + il;
       for (int r = r0; r < r1; ++r) {
         for (int c = 0; c < nchunks; ++c) {
           ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
@@ -310,12 +344,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             store_sums(sre, ta);
             store_sums(sim, ta + BN);
             ptx::tmem_wait_st();
-            emit_round(p, w, r, r0, r1, ta, il, h, any_masked);
+            emit_round(p, w, r, r0, r1, ta, i, h, any_masked);
 #pragma unroll
             for (int k = 0; k < HALF; ++k) sre[k] = sim[k] = 0.0f;  // sums dead across the emission
           }
           ptx::tc_fence_before();
-          ptx::mbar_arrive(&tempty[buf]);
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 2) ptx::mbar_arrive_rank0(&tempty[buf]);
+            else ptx::mbar_arrive(&tempty[buf]);
+          }
           uses[buf]++;
           buf ^= 1;
         }
@@ -323,24 +361,56 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   }
 
-  __syncthreads();
+  ptx::tc_fence_before();
+  if (CG == 2) ptx::cluster_sync();  // both CTAs done with TMEM and remote barriers
+  else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem, TMEM_COLS);
+    ptx::tmem_dealloc_cg<CG>(tmem, TMEM_COLS);
   }
+}
+
+template <int CG>
+cudaError_t launch_cg(const void* tmapA, const void* tmapB, const GramParams& p, int groups, cudaStream_t st) {
+  using G = Geo<CG>;
+  cudaError_t e =
+      cudaFuncSetAttribute(gram_split_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  if (p.n_items <= 0) return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(groups * CG);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = G::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gram_split_kernel<CG>, *static_cast<const CUtensorMap*>(tmapA),
+                            *static_cast<const CUtensorMap*>(tmapB), p);
 }
 
 }  // namespace
 
-cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p, int grid,
+int split_cta_group() {
+  static const int cg = [] {
+    const char* s = std::getenv("PS_CTA_GROUP");
+    return (s && std::atoi(s) == 1) ? 1 : 2;
+  }();
+  return cg;
+}
+
+int split_panel_rows() { return split_cta_group() * BMC; }
+
+int split_b_box_rows() { return BN / split_cta_group(); }
+
+cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p, int groups,
                               cudaStream_t st) {
-  cudaError_t e =
-      cudaFuncSetAttribute(gram_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  if (p.n_items <= 0) return cudaSuccess;
-  gram_split_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(*static_cast<const CUtensorMap*>(tmapA),
-                                                          *static_cast<const CUtensorMap*>(tmapB), p);
-  return cudaGetLastError();
+  return split_cta_group() == 2 ? launch_cg<2>(tmapA, tmapB, p, groups, st)
+                                : launch_cg<1>(tmapA, tmapB, p, groups, st);
 }
 
 }  // namespace ps

@@ -111,8 +111,14 @@ cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);
 cudaError_t launch_refine(const GramParams& p, const RefineEntry* entries, const int* groups, int n_groups,
                           int overwrite, int div, cudaStream_t st);
 
-// tile geometry of the two Gram kernels
-constexpr int kSplitBM = 128;
+// split Gram variant: 2 = CTA pair (cta_group::2, 256-row panels), 1 = single
+// CTA (128-row panels).  PS_CTA_GROUP=1 selects the latter.
+int split_cta_group();
+int split_panel_rows();   // rows of one execution panel (= UMMA M)
+int split_b_box_rows();   // J-panel rows staged per CTA
+
+// tile geometry of the two Gram kernels (ownership / sharding granularity)
+constexpr int kSplitBM = 256;
 constexpr int kSplitBN = 128;
 constexpr int kSplitBK = 32;
 constexpr int kF64BM = 64;

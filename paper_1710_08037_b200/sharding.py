@@ -17,7 +17,7 @@ import numpy as np
 
 from . import _native
 
-SPLIT_TILE = (128, 128)
+SPLIT_TILE = (256, 128)
 FP64_TILE = (64, 64)
 
 
