@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (rank 0) =====================
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // whole warp: uniform descriptors, one elected lane issues
       constexpr uint32_t idesc_pos = ptx::make_idesc_f16(G::UMMA_M, BN, false);
       constexpr uint32_t idesc_neg = ptx::make_idesc_f16(G::UMMA_M, BN, true);
       int stage = 0;
@@ -263,14 +263,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               ptx::mbar_wait(&tempty[buf], (uses[buf] & 1u) ^ 1u, tflag);
               ptx::tc_fence_after();
             }
-            const uint32_t d_re = tmem + (uint32_t)buf * BUF_COLS;
+            // __shfl_sync makes the operands provably warp-uniform, so ptxas
+            // keeps them in uniform registers for UTCHMMA
+            const uint32_t d_re = __shfl_sync(0xffffffffu, tmem + (uint32_t)buf * BUF_COLS, 0);
             const uint32_t d_im = d_re + BN;
             ptx::mbar_wait(&full[stage], phase, tflag);
             ptx::tc_fence_after();
             // descriptor of the stage's A tile; planes / K sub-steps are
             // constant offsets added to the 14-bit start-address field
             // (smem addresses < 256 KB never carry out of it)
-            const uint64_t dA = ptx::make_smem_desc(ptx::smem_u32(smem + stage * G::STAGE_BYTES), SBO, SWZ);
+            const uint32_t sa_u = __shfl_sync(0xffffffffu, ptx::smem_u32(smem + stage * G::STAGE_BYTES), 0);
+            const uint64_t dA = ptx::make_smem_desc(sa_u, SBO, SWZ);
             const uint64_t dB = dA + (uint64_t)(G::A_BYTES >> 4);
 #pragma unroll
             for (int ks = 0; ks < BK / 16; ++ks) {
@@ -285,27 +288,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const uint64_t bIl = dB + ko + 3 * (G::B_PLANE >> 4);
               const uint32_t acc0 = (chunk_start && ks == 0) ? 0u : 1u;
               // Re = Zr Zr' + Zi Zi'
-              ptx::mma_f16_ss_cg<CG>(d_re, aRh, bRh, idesc_pos, acc0);
-              ptx::mma_f16_ss_cg<CG>(d_re, aRh, bRl, idesc_pos, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_re, aRl, bRh, idesc_pos, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_re, aIh, bIh, idesc_pos, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_re, aIh, bIl, idesc_pos, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_re, aIl, bIh, idesc_pos, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRh, idesc_pos, acc0);
+              ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRl, idesc_pos, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_re, aRl, bRh, idesc_pos, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIh, idesc_pos, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIl, idesc_pos, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_re, aIl, bIh, idesc_pos, 1u);
               // Im = Zi Zr' - Zr Zi'
-              ptx::mma_f16_ss_cg<CG>(d_im, aIh, bRh, idesc_pos, acc0);
-              ptx::mma_f16_ss_cg<CG>(d_im, aIh, bRl, idesc_pos, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_im, aIl, bRh, idesc_pos, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_im, aRh, bIh, idesc_neg, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_im, aRh, bIl, idesc_neg, 1u);
-              ptx::mma_f16_ss_cg<CG>(d_im, aRl, bIh, idesc_neg, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRh, idesc_pos, acc0);
+              ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRl, idesc_pos, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_im, aIl, bRh, idesc_pos, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIh, idesc_neg, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIl, idesc_neg, 1u);
+              ptx::mma_f16_ss_warp<CG>(d_im, aRl, bIh, idesc_neg, 1u);
             }
-            ptx::mma_commit_cg<CG>(&empty[stage]);  // the group's smem slots free once these retire
+            ptx::mma_commit_warp<CG>(&empty[stage]);  // the group's smem slots free once these retire
             if (++stage == G::STAGES) {
               stage = 0;
               phase ^= 1u;
             }
             if (chunk_end) {
-              ptx::mma_commit_cg<CG>(&tfull[buf]);  // chunk partial complete -> epilogues
+              ptx::mma_commit_warp<CG>(&tfull[buf]);  // chunk partial complete -> epilogues
               uses[buf]++;
               buf ^= 1;
             }
