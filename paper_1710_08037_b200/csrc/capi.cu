@@ -86,6 +86,11 @@ struct ps_ctx {
   size_t h_items_cap = 0;
   cudaEvent_t ev[8] = {};
   int launches = 0;
+  // host (e2e) pipeline: copy-in / compute / refine / copy-out streams
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_ref = nullptr, s_out = nullptr;
+  std::vector<cudaEvent_t> evpool;
+  unsigned long long* h_cnt = nullptr;  // pinned per-stage refine-queue counters
+  int h_cnt_cap = 0;
 };
 
 namespace {
@@ -286,41 +291,52 @@ ps_status read_status(ps_ctx* c, cudaStream_t st) {
   return PS_OK;
 }
 
-// Normalisation of all rows into `out` (fmt 0/1: planes, fmt 2: dense complex).
-ps_status prepare_phasors(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const void* in_ptr, void* out,
-                          int fmt, long long pitch, long long plane_stride, cudaStream_t st, bool* copied) {
+// Per-call row state: amplitude min/max (order-preserving bits) and masked
+// counts.  Must run (stream-ordered) before any prepare_rows of the call.
+ps_status init_row_state(ps_ctx* c, const Geometry& g, cudaStream_t st) {
   PS_TRY(ensure(c->rowstat, (size_t)g.rows * 2 * sizeof(unsigned long long)));
   PS_TRY(ensure(c->maskcount, (size_t)g.rows * sizeof(int)));
   unsigned long long* rs = static_cast<unsigned long long*>(c->rowstat.p);
   PS_CUDA(cudaMemsetAsync(rs, 0xFF, (size_t)g.rows * sizeof(unsigned long long), st));
   PS_CUDA(cudaMemsetAsync(rs + g.rows, 0, (size_t)g.rows * sizeof(unsigned long long), st));
+  return PS_OK;
+}
+
+// Normalisation of rows [row_lo, row_hi) into `out` (fmt 0/1: planes, fmt 2:
+// dense complex rows relative to `out`).  Real input goes through the cuFFT
+// Hilbert stage in bounded row chunks first.
+ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const void* in_ptr, void* out, int fmt,
+                       long long pitch, long long plane_stride, long long row_lo, long long row_hi, cudaStream_t st,
+                       bool* copied) {
+  unsigned long long* rs = static_cast<unsigned long long*>(c->rowstat.p);
   SrcDesc src = make_src(a, g, in_ptr);
   const size_t ces = g.cdouble ? 8 : 4;
   auto out_at = [&](long long row0) -> void* {
     if (fmt != 2) return out;
     return static_cast<char*>(out) + (size_t)row0 * g.T * 2 * ces;
   };
-  if (a->input_kind == PS_INPUT_REAL) {
-    const long long rc = hilbert_chunk_rows(g);
-    for (long long row0 = 0; row0 < g.rows; row0 += rc) {
-      const long long nr = std::min(rc, g.rows - row0);
+  const long long rc = a->input_kind == PS_INPUT_REAL ? hilbert_chunk_rows(g) : (row_hi - row_lo);
+  for (long long row0 = row_lo; row0 < row_hi; row0 += rc) {
+    const long long nr = std::min(rc, row_hi - row0);
+    if (a->input_kind == PS_INPUT_REAL) {
       PS_TRY(hilbert_chunk(c, a, g, src, row0, nr, st, copied));
       src.hbuf = c->hbuf.p;
       src.h_row0 = row0;
-      PS_CUDA(launch_normalize_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs,
-                                   g.rows, c->d_status, st));
-      PS_CUDA(launch_fixup_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
-                               static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
-      c->launches += 2;
     }
-  } else {
-    PS_CUDA(launch_normalize_fmt(src, 0, g.rows, out, fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
+    PS_CUDA(launch_normalize_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
                                  c->d_status, st));
-    PS_CUDA(launch_fixup_fmt(src, 0, g.rows, out, fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
+    PS_CUDA(launch_fixup_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
                              static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
     c->launches += 2;
   }
   return PS_OK;
+}
+
+// Normalisation of all rows.
+ps_status prepare_phasors(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const void* in_ptr, void* out,
+                          int fmt, long long pitch, long long plane_stride, cudaStream_t st, bool* copied) {
+  PS_TRY(init_row_state(c, g, st));
+  return prepare_rows(c, a, g, in_ptr, out, fmt, pitch, plane_stride, 0, g.rows, st, copied);
 }
 
 // Upper-triangle tile list (tiles that contain at least one pair i <= j).
@@ -371,6 +387,399 @@ static cudaError_t ps_mask_from_zero(const void* z, int is_double, size_t n, uin
   else mask_from_zero_kernel<float><<<grid, 256, 0, st>>>((const float*)z, n, m);
   return cudaGetLastError();
 }
+
+namespace {
+
+// Everything one ps_plv_family call needs after validation: work items (by
+// stage), kernel parameters, TMA descriptors, output routing.
+struct Call {
+  Geometry g;
+  void* outs[5] = {};   // final device outputs (nullptr = metric not requested)
+  int shard_count = 1, shard_index = 0;
+  bool pool = false;
+  int G = 1, slot_mode = 1, mean_div = 1, Rg = 1;
+  std::vector<int> stage_off;  // item offsets of the stages (size n_stages + 1)
+  GramParams p;
+  const CUtensorMap* ta = nullptr;
+  const CUtensorMap* tb = nullptr;
+  long long nn = 0;
+  size_t oes = 4;
+  long long slots = 1;  // output slots per metric
+};
+
+int kc_blocks_default() {
+  // TMEM accumulation chunk (drain period) in 32-sample K blocks; see gram_tc.cu
+  static const int kcb = [] {
+    const char* s = std::getenv("PS_KC_BLOCKS");
+    return s ? std::max(1, std::atoi(s)) : 4;
+  }();
+  return kcb;
+}
+
+// Work items, grouped by stage: stage s holds the tiles whose column panel
+// starts in [cols[s], cols[s+1]) (one stage covering everything when `cols` is
+// empty).  Ownership (sharding) uses the canonical J-major tile enumeration
+// of ps_pair_shard; within a stage items run in 12 x 12 supertile raster order.
+ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<long long>& cols, bool force_g1,
+                    cudaStream_t st) {
+  const Geometry& g = k.g;
+  const int bm = g.split ? kSplitBM : kF64BM;
+  const int bn = g.split ? kSplitBN : kF64BN;
+  std::vector<std::pair<int, int>> tiles;
+  build_tiles(g.N, bm, bn, tiles);
+  std::vector<std::pair<int, int>> mine;
+  for (size_t t = 0; t < tiles.size(); ++t)
+    if ((int)(t % k.shard_count) == k.shard_index) mine.push_back(tiles[t]);
+  const int n_stages = cols.empty() ? 1 : (int)cols.size() - 1;
+  auto stage_of = [&](int J) -> int {
+    if (cols.empty()) return 0;
+    const long long j0 = (long long)J * bn;
+    int s = 0;
+    while (s + 1 < n_stages && j0 >= cols[s + 1]) ++s;
+    return s;
+  };
+  static const int S = [] {
+    const char* s = std::getenv("PS_RASTER");
+    return s ? std::max(1, std::atoi(s)) : 12;
+  }();
+  std::stable_sort(mine.begin(), mine.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+    return std::make_tuple(stage_of(x.second), x.second / S, x.first / S, x.second, x.first) <
+           std::make_tuple(stage_of(y.second), y.second / S, y.first / S, y.second, y.first);
+  });
+  k.pool = a->trial_reduce == PS_TRIALS_POOL;
+  if (k.pool || g.R == 1) {
+    k.G = 1;
+    k.slot_mode = 1;
+  } else if (a->trial_reduce == PS_TRIALS_NONE) {
+    k.G = (int)g.R;
+    k.slot_mode = 0;
+  } else {
+    k.G = (k.shard_count > 1 || force_g1) ? 1 : choose_groups((long long)mine.size() * g.B, (int)g.R, c->num_sms);
+    k.slot_mode = k.G == 1 ? 1 : 2;
+    k.mean_div = k.G == 1 ? (int)g.R : 1;
+  }
+  k.Rg = (int)((g.R + k.G - 1) / k.G);
+  k.slots = (a->trial_reduce == PS_TRIALS_NONE && !k.pool) ? g.B * g.R : g.B;
+  // Split path: ownership tiles are 256 x 128; the single-CTA variant runs
+  // each as two 128-row halves (halves wholly below the diagonal dropped).
+  const int exec_rows = g.split ? split_panel_rows() : kF64BM;
+  const int sub = g.split ? kSplitBM / exec_rows : 1;
+  std::vector<Item>& items = c->h_items;
+  items.clear();
+  k.stage_off.assign(1, 0);
+  size_t t0 = 0;
+  for (int s = 0; s < n_stages; ++s) {
+    size_t t1 = t0;
+    while (t1 < mine.size() && stage_of(mine[t1].second) == s) ++t1;
+    for (int b = 0; b < g.B; ++b)
+      for (int gi = 0; gi < k.G; ++gi)
+        for (size_t t = t0; t < t1; ++t)
+          for (int hs = 0; hs < sub; ++hs) {
+            const int I = mine[t].first * sub + hs;
+            const long long jmax = std::min<long long>((long long)mine[t].second * bn + bn, g.N) - 1;
+            if ((long long)I * exec_rows > jmax || (long long)I * exec_rows >= g.N) continue;
+            items.push_back(Item{b, gi, I, mine[t].second});
+          }
+    k.stage_off.push_back((int)items.size());
+    t0 = t1;
+  }
+  const size_t ibytes = std::max<size_t>(items.size(), 1) * sizeof(Item);
+  if (c->h_items_cap < ibytes) {
+    if (c->h_items_pinned) cudaFreeHost(c->h_items_pinned);
+    c->h_items_pinned = nullptr;
+    c->h_items_cap = 0;
+    PS_CUDA(cudaMallocHost(&c->h_items_pinned, ibytes));
+    c->h_items_cap = ibytes;
+  }
+  // calls are synchronous: the previous call finished with the pinned staging
+  if (!items.empty()) std::memcpy(c->h_items_pinned, items.data(), items.size() * sizeof(Item));
+  PS_TRY(ensure(c->items, ibytes));
+  if (!items.empty())
+    PS_CUDA(cudaMemcpyAsync(c->items.p, c->h_items_pinned, items.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
+
+  GramParams& p = k.p;
+  std::memset(&p, 0, sizeof(p));
+  p.N = (int)g.N;
+  p.T = (int)g.T;
+  p.R = (int)g.R;
+  p.B = (int)g.B;
+  p.Tp = (int)g.pitch;
+  p.rows = (int)g.rows;
+  p.Rg = k.Rg;
+  p.G = k.G;
+  p.pool = k.pool ? 1 : 0;
+  p.items = static_cast<const Item*>(c->items.p);
+  p.slot_mode = k.slot_mode;
+  p.mean_div = k.mean_div;
+  p.maskcount = static_cast<const int*>(c->maskcount.p);
+  p.planes = c->planes.p;
+  p.plane_stride = g.plane_stride;
+  p.status = c->d_status;
+  p.illcond_tol = 2e-6f;
+  p.kc_blocks = kc_blocks_default();
+  if (g.split && k.outs[2]) {
+    const int cap = 1 << 22;  // queued ill-conditioned ciPLV (pair, round) entries
+    PS_TRY(ensure(c->refine, (size_t)cap * sizeof(RefineEntry)));
+    p.refine = static_cast<RefineEntry*>(c->refine.p);
+    p.refine_cap = cap;
+  }
+  k.oes = g.split ? 4 : 8;
+  k.nn = g.N * g.N;
+  void* kouts[5];
+  std::memcpy(kouts, k.outs, sizeof(kouts));
+  if (k.slot_mode == 2) {
+    // trial-group partial sums, reduced in a fixed order afterwards
+    const size_t per = (size_t)g.B * k.G * k.nn * k.oes;
+    PS_TRY(ensure(c->gws, per * 5));
+    for (int m = 0; m < 5; ++m) kouts[m] = kouts[m] ? static_cast<char*>(c->gws.p) + m * per : nullptr;
+  }
+  p.out_plv = kouts[0];
+  p.out_iplv = kouts[1];
+  p.out_ciplv = kouts[2];
+  p.out_cre = kouts[3];
+  p.out_cim = kouts[4];
+  if (g.split) {
+    TmapKey key{c->planes.p, g.T, g.N, g.B * g.R, g.pitch};
+    auto it = c->tmaps.find(key);
+    if (it == c->tmaps.end()) {
+      auto enc = encode_fn();
+      if (!enc) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+      CUtensorMap ta, tb;
+      cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), 4};
+      cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 2, (cuuint64_t)(g.N * g.pitch * 2),
+                               (cuuint64_t)(g.plane_stride * 2)};
+      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, 4};  // 128 rows of the I panel per CTA
+      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)split_b_box_rows(), 1, 4};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                     : kSplitBK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
+      CUresult r1 = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxA, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CUresult r2 = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxB, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+        return fail(PS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" +
+                                   std::to_string((int)r2));
+      if (c->tmaps.size() > 64) c->tmaps.clear();
+      it = c->tmaps.emplace(key, std::make_pair(ta, tb)).first;
+    }
+    k.ta = &it->second.first;
+    k.tb = &it->second.second;
+  }
+  return PS_OK;
+}
+
+ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
+  GramParams p = k.p;
+  const int i0 = k.stage_off[s], i1 = k.stage_off[s + 1];
+  p.items = k.p.items + i0;
+  p.n_items = i1 - i0;
+  if (p.n_items <= 0) return PS_OK;
+  const int cta_per_group = k.g.split ? split_cta_group() : 1;
+  const int grid = std::min(p.n_items, c->num_sms / cta_per_group);
+  if (k.g.split) PS_CUDA(launch_gram_split(k.ta, k.tb, p, grid, st));
+  else PS_CUDA(launch_gram_f64(p, grid, st));
+  c->launches++;
+  return PS_OK;
+}
+
+// Exact FP64 refinement of queued ill-conditioned ciPLV entries [lo, hi):
+// copied to the host, sorted (deterministic application order), grouped by
+// output location and recomputed by refine_kernel on stream `st`.
+ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long long hi, cudaStream_t st) {
+  if (hi <= lo || !k.g.split || !k.outs[2]) return PS_OK;
+  if (hi > (unsigned long long)k.p.refine_cap)
+    return fail(PS_E_INTERNAL, "ciPLV refinement queue overflow (" + std::to_string(hi) + " pairs)");
+  std::vector<RefineEntry> ent(hi - lo);
+  PS_CUDA(cudaMemcpyAsync(ent.data(), static_cast<RefineEntry*>(c->refine.p) + lo, ent.size() * sizeof(RefineEntry),
+                          cudaMemcpyDeviceToHost, st));
+  PS_CUDA(cudaStreamSynchronize(st));
+  if (k.slot_mode == 2)
+    for (auto& e : ent) e.slot /= k.G;  // workspace slot b*G+g -> final output slot b
+  std::sort(ent.begin(), ent.end(), [](const RefineEntry& x, const RefineEntry& y) {
+    return std::tie(x.slot, x.i, x.j, x.u0) < std::tie(y.slot, y.i, y.j, y.u0);
+  });
+  std::vector<int> groups;
+  for (size_t q = 0; q < ent.size(); ++q)
+    if (q == 0 || ent[q].slot != ent[q - 1].slot || ent[q].i != ent[q - 1].i || ent[q].j != ent[q - 1].j)
+      groups.push_back((int)q);
+  const int n_groups = (int)groups.size();
+  groups.push_back((int)ent.size());
+  const size_t ebytes = (size_t)round_up((long long)(ent.size() * sizeof(RefineEntry)), 16);
+  PS_TRY(ensure(c->refine_sorted, ebytes + groups.size() * sizeof(int) + 64));
+  RefineEntry* d_ent = static_cast<RefineEntry*>(c->refine_sorted.p);
+  int* d_grp = reinterpret_cast<int*>(static_cast<char*>(c->refine_sorted.p) + ebytes);
+  PS_CUDA(cudaMemcpyAsync(d_ent, ent.data(), ent.size() * sizeof(RefineEntry), cudaMemcpyHostToDevice, st));
+  PS_CUDA(cudaMemcpyAsync(d_grp, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  GramParams pr = k.p;
+  pr.out_ciplv = k.outs[2];
+  const bool single_round = k.pool || k.g.R == 1 || k.slot_mode == 0;
+  PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, single_round ? 1 : 0, (int)k.g.R, st));
+  c->launches++;
+  // host vectors must outlive the async copies
+  PS_CUDA(cudaStreamSynchronize(st));
+  return PS_OK;
+}
+
+ps_status setup_outputs(const ps_plv_args* a, Call& k) {
+  if (a->metrics == 0) return fail(PS_E_INVALID, "no metric requested");
+  void* outs[5] = {a->out_plv, a->out_iplv, a->out_ciplv, a->out_cre, a->out_cim};
+  for (int m = 0; m < 5; ++m) {
+    const bool want = (a->metrics >> m) & 1u;
+    if (want && !outs[m]) return fail(PS_E_INVALID, "output pointer missing for a requested metric");
+    k.outs[m] = want ? outs[m] : nullptr;
+  }
+  k.shard_count = a->shard_count < 1 ? 1 : a->shard_count;
+  k.shard_index = a->shard_index;
+  if (k.shard_index < 0 || k.shard_index >= k.shard_count) return fail(PS_E_INVALID, "shard_index out of range");
+  if (k.g.rows > (long long)INT32_MAX || k.g.B * k.g.R > 65535) return fail(PS_E_SHAPE, "too many rows for one call");
+  return PS_OK;
+}
+
+cudaEvent_t pool_event(ps_ctx* c, size_t i) {
+  while (c->evpool.size() <= i) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    c->evpool.push_back(e);
+  }
+  return c->evpool[i];
+}
+
+ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
+  if (!c->s_in) {
+    PS_CUDA(cudaStreamCreateWithFlags(&c->s_in, cudaStreamNonBlocking));
+    PS_CUDA(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    PS_CUDA(cudaStreamCreateWithFlags(&c->s_ref, cudaStreamNonBlocking));
+    PS_CUDA(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
+  }
+  if (c->h_cnt_cap < n_stages) {
+    if (c->h_cnt) cudaFreeHost(c->h_cnt);
+    c->h_cnt = nullptr;
+    PS_CUDA(cudaMallocHost(&c->h_cnt, (size_t)n_stages * sizeof(unsigned long long)));
+    c->h_cnt_cap = n_stages;
+  }
+  return PS_OK;
+}
+
+// E2E host path, pipelined over column stages (the "growing square"):
+// stage s owns output columns [cols[s], cols[s+1]).  Its Gram tiles need
+// only signal rows < cols[s+1], and once they are done the output block
+// rows [0, cols[s+1]) x cols [cols[s], cols[s+1]) plus its mirror
+// rows [cols[s], cols[s+1]) x cols [0, cols[s]) is final.  So the H2D of
+// stage s+1's input rows, the Gram of stage s and the D2H of stage s-1's
+// output blocks run concurrently on separate streams.
+ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long span, long long esz,
+                         ps_plv_result* res) {
+  const Geometry& g = k.g;
+  const long long W = std::max<long long>(1024, round_up((g.N + 7) / 8, 256));
+  std::vector<long long> cols;
+  for (long long x = 0; x < g.N; x += W) cols.push_back(x);
+  cols.push_back(g.N);
+  const int S = (int)cols.size() - 1;
+  PS_TRY(ensure_pipeline(c, S));
+  cudaStream_t si = c->s_in, sc = c->s_comp, sr = c->s_ref, so = c->s_out;
+  c->launches = 0;
+  bool copied = false;
+  // device buffers: input span (same element layout as the host array), planes, outputs
+  PS_TRY(ensure(c->hin, (size_t)span * esz));
+  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  PS_TRY(ensure(c->planes, plane_bytes));
+  const size_t oes = g.split ? 4 : 8;
+  void* houts[5];
+  std::memcpy(houts, k.outs, sizeof(houts));
+  int nout = 0;
+  for (int m = 0; m < 5; ++m) nout += houts[m] ? 1 : 0;
+  const size_t out_bytes = (size_t)k.slots * g.N * g.N * oes;
+  PS_TRY(ensure(c->hout, out_bytes * std::max(nout, 1)));
+  {
+    int q = 0;
+    for (int m = 0; m < 5; ++m) k.outs[m] = houts[m] ? static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes : nullptr;
+  }
+  if (a->input_kind == PS_INPUT_REAL) {  // size the Hilbert workspace once (no realloc mid-pipeline)
+    const size_t es = g.cdouble ? 8 : 4;
+    const long long rc = std::min(hilbert_chunk_rows(g), g.rows);
+    PS_TRY(ensure(c->spec, (size_t)rc * (g.T / 2 + 1) * 2 * es));
+    PS_TRY(ensure(c->hbuf, (size_t)rc * g.T * es));
+    PS_TRY(ensure(c->xw, (size_t)rc * g.T * es));
+  }
+  PS_TRY(reset_status(c, si));
+  PS_TRY(init_row_state(c, g, si));
+  PS_TRY(plan_call(c, a, k, cols, /*force_g1=*/true, si));
+  ps_plv_args d = *a;
+  d.input = c->hin.p;
+  const long long U = g.B * g.R;
+  // ---- copy-in + normalise, per stage --------------------------------------
+  for (int s = 0; s < S; ++s) {
+    for (long long u = 0; u < U; ++u) {
+      const long long b = u / g.R, t = u % g.R;
+      const long long off = b * a->stride_band + t * a->stride_trial + cols[s] * a->stride_signal;
+      const long long len = (cols[s + 1] - 1 - cols[s]) * a->stride_signal + (g.T - 1) * a->stride_sample + 1;
+      PS_CUDA(cudaMemcpyAsync(static_cast<char*>(c->hin.p) + off * esz, static_cast<const char*>(a->input) + off * esz,
+                              (size_t)len * esz, cudaMemcpyHostToDevice, si));
+    }
+    for (long long u = 0; u < U; ++u)
+      PS_TRY(prepare_rows(c, &d, g, c->hin.p, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride,
+                          u * g.N + cols[s], u * g.N + cols[s + 1], si, &copied));
+    PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), si));
+  }
+  // ---- Gram per stage ------------------------------------------------------
+  for (int s = 0; s < S; ++s) {
+    PS_CUDA(cudaStreamWaitEvent(sc, pool_event(c, 3 * s), 0));
+    PS_TRY(launch_stage(c, k, s, sc));
+    PS_CUDA(cudaMemcpyAsync(&c->h_cnt[s], &c->d_status->n_illcond, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            sc));
+    PS_CUDA(cudaEventRecord(pool_event(c, 3 * s + 1), sc));
+  }
+  // ---- refine + copy-out per stage ------------------------------------------
+  unsigned long long prev = 0;
+  for (int s = 0; s < S; ++s) {
+    cudaEvent_t ready = pool_event(c, 3 * s + 1);
+    PS_CUDA(cudaEventSynchronize(ready));
+    const unsigned long long n = c->h_cnt[s];
+    if (n > prev && k.outs[2] && g.split) {
+      PS_CUDA(cudaStreamWaitEvent(sr, ready, 0));
+      PS_TRY(refine_range(c, k, prev, n, sr));
+      ready = pool_event(c, 3 * s + 2);
+      PS_CUDA(cudaEventRecord(ready, sr));
+    }
+    prev = n;
+    PS_CUDA(cudaStreamWaitEvent(so, ready, 0));
+    const long long c0 = cols[s], c1 = cols[s + 1];
+    for (int m = 0; m < 5; ++m) {
+      if (!houts[m]) continue;
+      for (long long sl = 0; sl < k.slots; ++sl) {
+        const size_t base = (size_t)sl * g.N * g.N * oes;
+        char* hdst = static_cast<char*>(houts[m]) + base;
+        const char* dsrc = static_cast<const char*>(k.outs[m]) + base;
+        const size_t pitch = (size_t)g.N * oes;
+        // rows [0, c1) x cols [c0, c1)
+        PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * oes, pitch, dsrc + (size_t)c0 * oes, pitch,
+                                  (size_t)(c1 - c0) * oes, (size_t)c1, cudaMemcpyDeviceToHost, so));
+        // rows [c0, c1) x cols [0, c0)
+        if (c0 > 0)
+          PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * pitch, pitch, dsrc + (size_t)c0 * pitch, pitch,
+                                    (size_t)c0 * oes, (size_t)(c1 - c0), cudaMemcpyDeviceToHost, so));
+      }
+    }
+  }
+  PS_CUDA(cudaStreamSynchronize(so));
+  ps_status st = read_status(c, so);
+  if (res) {
+    std::memset(res, 0, sizeof(*res));
+    res->n_observations = k.pool ? g.T * g.R : g.T;
+    res->n_masked_samples = (int64_t)c->h_status->n_masked;
+    res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->input_copied = copied ? 1 : 0;
+    res->n_kernel_launches = c->launches;
+  }
+  std::memcpy(k.outs, houts, sizeof(houts));
+  return st;
+}
+
+}  // namespace
 
 // ============================================================================
 // C ABI
@@ -441,6 +850,10 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   if (c->h_items_pinned) cudaFreeHost(c->h_items_pinned);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->evpool) cudaEventDestroy(e);
+  for (cudaStream_t s : {c->s_in, c->s_comp, c->s_ref, c->s_out})
+    if (s) cudaStreamDestroy(s);
+  if (c->h_cnt) cudaFreeHost(c->h_cnt);
   delete c;
   return PS_OK;
 }
@@ -454,224 +867,37 @@ ps_status ps_ctx_set_timing(ps_ctx* c, int enable) {
 ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   std::lock_guard<std::mutex> lock(c->mu);
-  Geometry g;
-  PS_TRY(validate(a, g));
-  const uint32_t metrics = a->metrics;
-  if (metrics == 0) return fail(PS_E_INVALID, "no metric requested");
-  void* outs[5] = {a->out_plv, a->out_iplv, a->out_ciplv, a->out_cre, a->out_cim};
-  for (int m = 0; m < 5; ++m) {
-    const bool want = (metrics >> m) & 1u;
-    if (want && !outs[m]) return fail(PS_E_INVALID, "output pointer missing for a requested metric");
-    if (!want) outs[m] = nullptr;
-  }
-  const int shard_count = a->shard_count < 1 ? 1 : a->shard_count;
-  const int shard_index = a->shard_index;
-  if (shard_index < 0 || shard_index >= shard_count) return fail(PS_E_INVALID, "shard_index out of range");
-  if (g.rows > (long long)INT32_MAX || g.B * g.R > 65535) return fail(PS_E_SHAPE, "too many rows for one call");
+  Call k;
+  PS_TRY(validate(a, k.g));
+  PS_TRY(setup_outputs(a, k));
+  const Geometry& g = k.g;
   PS_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(a->stream);
   c->launches = 0;
   bool copied = false;
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[0], st));
-
   // ---- phasor planes --------------------------------------------------------
   const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
   PS_TRY(ensure(c->planes, plane_bytes));
   PS_TRY(reset_status(c, st));
   PS_TRY(prepare_phasors(c, a, g, a->input, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride, st, &copied));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[1], st));
-
-  // ---- work items -----------------------------------------------------------
-  const int bm = g.split ? kSplitBM : kF64BM;
-  const int bn = g.split ? kSplitBN : kF64BN;
-  std::vector<std::pair<int, int>> tiles;
-  build_tiles(g.N, bm, bn, tiles);
-  std::vector<std::pair<int, int>> mine;
-  for (size_t t = 0; t < tiles.size(); ++t)
-    if ((int)(t % shard_count) == shard_index) mine.push_back(tiles[t]);
-  // Execution order: 12 x 12 supertiles (J-major between supertiles).  The
-  // ~148 items in flight at any time then share ~24 row panels, so operand
-  // panels are re-read from L2 instead of DRAM.  (Ownership above keeps the
-  // canonical J-major enumeration of ps_pair_shard.)
-  {
-    static const int S = [] {
-      const char* s = std::getenv("PS_RASTER");
-      return s ? std::max(1, std::atoi(s)) : 12;
-    }();
-    std::stable_sort(mine.begin(), mine.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
-      return std::make_tuple(a.second / S, a.first / S, a.second, a.first) <
-             std::make_tuple(b.second / S, b.first / S, b.second, b.first);
-    });
-  }
-  const bool pool = a->trial_reduce == PS_TRIALS_POOL;
-  int G = 1, slot_mode = 1, mean_div = 1;
-  if (pool || g.R == 1) {
-    G = 1;
-    slot_mode = 1;
-  } else if (a->trial_reduce == PS_TRIALS_NONE) {
-    G = (int)g.R;
-    slot_mode = 0;
-  } else {
-    G = shard_count > 1 ? 1 : choose_groups((long long)mine.size() * g.B, (int)g.R, c->num_sms);
-    slot_mode = G == 1 ? 1 : 2;
-    mean_div = G == 1 ? (int)g.R : 1;
-  }
-  const int Rg = (int)((g.R + G - 1) / G);
-  std::vector<Item>& items = c->h_items;
-  items.clear();
-  // Split path: ownership tiles are 256 x 128; the single-CTA variant runs
-  // each as two 128-row halves (halves wholly below the diagonal dropped).
-  const int exec_rows = g.split ? split_panel_rows() : kF64BM;
-  const int sub = g.split ? kSplitBM / exec_rows : 1;
-  for (int b = 0; b < g.B; ++b)
-    for (int gi = 0; gi < G; ++gi)
-      for (auto& t : mine)
-        for (int hs = 0; hs < sub; ++hs) {
-          const int I = t.first * sub + hs;
-          const long long jmax = std::min<long long>((long long)t.second * bn + bn, g.N) - 1;
-          if ((long long)I * exec_rows > jmax || (long long)I * exec_rows >= g.N) continue;
-          items.push_back(Item{b, gi, I, t.second});
-        }
-  const size_t ibytes = std::max<size_t>(items.size(), 1) * sizeof(Item);
-  if (c->h_items_cap < ibytes) {
-    if (c->h_items_pinned) cudaFreeHost(c->h_items_pinned);
-    c->h_items_pinned = nullptr;
-    c->h_items_cap = 0;
-    PS_CUDA(cudaMallocHost(&c->h_items_pinned, ibytes));
-    c->h_items_cap = ibytes;
-  }
-  // the previous call synchronised its stream, so the pinned staging is free
-  if (!items.empty()) std::memcpy(c->h_items_pinned, items.data(), items.size() * sizeof(Item));
-  PS_TRY(ensure(c->items, ibytes));
-  if (!items.empty())
-    PS_CUDA(cudaMemcpyAsync(c->items.p, c->h_items_pinned, items.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
-
-  GramParams p;
-  std::memset(&p, 0, sizeof(p));
-  p.N = (int)g.N;
-  p.T = (int)g.T;
-  p.R = (int)g.R;
-  p.B = (int)g.B;
-  p.Tp = (int)g.pitch;
-  p.rows = (int)g.rows;
-  p.Rg = Rg;
-  p.G = G;
-  p.pool = pool ? 1 : 0;
-  p.n_items = (int)items.size();
-  p.items = static_cast<const Item*>(c->items.p);
-  p.slot_mode = slot_mode;
-  p.mean_div = mean_div;
-  p.maskcount = static_cast<const int*>(c->maskcount.p);
-  p.planes = c->planes.p;
-  p.plane_stride = g.plane_stride;
-  p.status = c->d_status;
-  p.illcond_tol = 2e-6f;
-  if (g.split && outs[2]) {
-    const int cap = 1 << 22;  // queued ill-conditioned ciPLV (pair, round) entries
-    PS_TRY(ensure(c->refine, (size_t)cap * sizeof(RefineEntry)));
-    p.refine = static_cast<RefineEntry*>(c->refine.p);
-    p.refine_cap = cap;
-  }
-  {
-    // TMEM accumulation chunk (drain period) in 32-sample K blocks; see gram_tc.cu
-    static const int kcb_env = [] {
-      const char* s = std::getenv("PS_KC_BLOCKS");
-      return s ? std::max(1, std::atoi(s)) : 4;
-    }();
-    p.kc_blocks = kcb_env;
-  }
-  const size_t oes = g.split ? 4 : 8;
-  const long long nn = g.N * g.N;
-  void* final_outs[5];
-  std::memcpy(final_outs, outs, sizeof(outs));
-  if (slot_mode == 2) {
-    // trial-group partial sums, reduced in a fixed order afterwards
-    const size_t per = (size_t)g.B * G * nn * oes;
-    PS_TRY(ensure(c->gws, per * 5));
-    for (int m = 0; m < 5; ++m) outs[m] = outs[m] ? static_cast<char*>(c->gws.p) + m * per : nullptr;
-  }
-  p.out_plv = outs[0];
-  p.out_iplv = outs[1];
-  p.out_ciplv = outs[2];
-  p.out_cre = outs[3];
-  p.out_cim = outs[4];
-  const int cta_per_group = g.split ? split_cta_group() : 1;
-  const int grid = (int)std::min<long long>((long long)items.size(), c->num_sms / cta_per_group);
-  if (g.split) {
-    TmapKey key{c->planes.p, g.T, g.N, g.B * g.R, g.pitch};
-    auto it = c->tmaps.find(key);
-    if (it == c->tmaps.end()) {
-      auto enc = encode_fn();
-      if (!enc) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-      CUtensorMap ta, tb;
-      cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), 4};
-      cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 2, (cuuint64_t)(g.N * g.pitch * 2),
-                               (cuuint64_t)(g.plane_stride * 2)};
-      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, 4};  // 128 rows of the I panel per CTA
-      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)split_b_box_rows(), 1, 4};
-      cuuint32_t estr[4] = {1, 1, 1, 1};
-      const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
-                                     : kSplitBK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                      : CU_TENSOR_MAP_SWIZZLE_128B;
-      CUresult r1 = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxA, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      CUresult r2 = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxB, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
-        return fail(PS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" +
-                                   std::to_string((int)r2));
-      if (c->tmaps.size() > 64) c->tmaps.clear();
-      it = c->tmaps.emplace(key, std::make_pair(ta, tb)).first;
-    }
-    PS_CUDA(launch_gram_split(&it->second.first, &it->second.second, p, grid, st));
-  } else {
-    PS_CUDA(launch_gram_f64(p, grid, st));
-  }
-  c->launches++;
+  // ---- Gram + fused epilogue ------------------------------------------------
+  PS_TRY(plan_call(c, a, k, {}, /*force_g1=*/false, st));
+  PS_TRY(launch_stage(c, k, 0, st));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
-  if (slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, G, nn, 5, final_outs, g.B * nn, (int)g.R, g.split ? 0 : 1, st));
-    for (int m = 0; m < 5; ++m) c->launches += final_outs[m] ? 1 : 0;
+  if (k.slot_mode == 2) {
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, (int)g.R, g.split ? 0 : 1, st));
+    for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
   ps_status s = read_status(c, st);
   // ---- exact FP64 refinement of ill-conditioned ciPLV pairs (split path) ----
-  const unsigned long long n_ref = c->h_status->n_illcond;
-  if (s == PS_OK && g.split && final_outs[2] && n_ref > 0) {
-    if (n_ref > (unsigned long long)p.refine_cap)
-      return fail(PS_E_INTERNAL, "ciPLV refinement queue overflow (" + std::to_string(n_ref) + " pairs)");
-    std::vector<RefineEntry> ent(n_ref);
-    PS_CUDA(cudaMemcpy(ent.data(), c->refine.p, n_ref * sizeof(RefineEntry), cudaMemcpyDeviceToHost));
-    if (slot_mode == 2)
-      for (auto& e : ent) e.slot /= G;  // workspace slot b*G+g -> final output slot b
-    std::sort(ent.begin(), ent.end(), [](const RefineEntry& x, const RefineEntry& y) {
-      return std::tie(x.slot, x.i, x.j, x.u0) < std::tie(y.slot, y.i, y.j, y.u0);
-    });
-    std::vector<int> groups;
-    for (size_t k = 0; k < ent.size(); ++k)
-      if (k == 0 || ent[k].slot != ent[k - 1].slot || ent[k].i != ent[k - 1].i || ent[k].j != ent[k - 1].j)
-        groups.push_back((int)k);
-    const int n_groups = (int)groups.size();
-    groups.push_back((int)ent.size());
-    PS_TRY(ensure(c->refine_sorted, ent.size() * sizeof(RefineEntry) + groups.size() * sizeof(int) + 64));
-    RefineEntry* d_ent = static_cast<RefineEntry*>(c->refine_sorted.p);
-    int* d_grp = reinterpret_cast<int*>(static_cast<char*>(c->refine_sorted.p) +
-                                        round_up((long long)(ent.size() * sizeof(RefineEntry)), 16));
-    PS_CUDA(cudaMemcpyAsync(d_ent, ent.data(), ent.size() * sizeof(RefineEntry), cudaMemcpyHostToDevice, st));
-    PS_CUDA(cudaMemcpyAsync(d_grp, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-    GramParams pr = p;
-    pr.out_ciplv = final_outs[2];
-    const bool single_round = pool || g.R == 1 || slot_mode == 0;
-    PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, single_round ? 1 : 0, (int)g.R, st));
-    c->launches++;
-    PS_CUDA(cudaStreamSynchronize(st));
-  }
+  if (s == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[3], st));
   if (c->timing) PS_CUDA(cudaEventSynchronize(c->ev[3]));
   if (res) {
     std::memset(res, 0, sizeof(*res));
-    res->n_observations = pool ? g.T * g.R : g.T;
+    res->n_observations = k.pool ? g.T * g.R : g.T;
     res->n_masked_samples = (int64_t)c->h_status->n_masked;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
@@ -687,19 +913,32 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
 
 ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
-  Geometry g;
-  PS_TRY(validate(a, g));
+  Call k;
+  PS_TRY(validate(a, k.g));
+  PS_TRY(setup_outputs(a, k));
+  const Geometry& g = k.g;
   PS_CUDA(cudaSetDevice(c->device));
-  cudaStream_t st = static_cast<cudaStream_t>(a->stream);
   // span of the (possibly strided) host input, in elements
   const long long esz = (a->dtype == PS_F32) ? 4 : (a->dtype == PS_F64 || a->dtype == PS_C64) ? 8 : 16;
   long long span = 1;
   const long long dims[4] = {g.B, g.N, g.T, g.R};
   const long long strides[4] = {a->stride_band, a->stride_signal, a->stride_sample, a->stride_trial};
-  for (int k = 0; k < 4; ++k) {
-    if (dims[k] > 1 && strides[k] < 0) return fail(PS_E_INVALID, "negative strides are not supported");
-    span += (dims[k] - 1) * strides[k];
+  for (int q = 0; q < 4; ++q) {
+    if (dims[q] > 1 && strides[q] < 0) return fail(PS_E_INVALID, "negative strides are not supported");
+    span += (dims[q] - 1) * strides[q];
   }
+  // Pipelined (copy-in / compute / copy-out overlapped) when the signal rows
+  // of each unit are contiguous spans and there are enough tiles to fill the
+  // GPU with one trial group.
+  static const bool no_pipe = std::getenv("PS_NO_PIPELINE") != nullptr;
+  const long long ntiles = ps_tile_count(g.N, a->precision);
+  const bool pipelinable = !no_pipe && k.shard_count == 1 && a->stride_sample == 1 && a->stride_signal >= g.T &&
+                           g.N >= 2048 && ntiles * g.B >= c->num_sms;
+  if (pipelinable) {
+    std::lock_guard<std::mutex> lock(c->mu);
+    return host_pipelined(c, a, k, span, esz, res);
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(a->stream);
   PS_TRY(ensure(c->hin, (size_t)span * esz));
   PS_CUDA(cudaMemcpyAsync(c->hin.p, a->input, (size_t)span * esz, cudaMemcpyHostToDevice, st));
   const bool pool = a->trial_reduce == PS_TRIALS_POOL;
@@ -714,17 +953,17 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
   ps_plv_args d = *a;
   d.input = c->hin.p;
   void** douts[5] = {&d.out_plv, &d.out_iplv, &d.out_ciplv, &d.out_cre, &d.out_cim};
-  int k = 0;
+  int q = 0;
   for (int m = 0; m < 5; ++m) {
-    if (((a->metrics >> m) & 1u) && houts[m]) *douts[m] = static_cast<char*>(c->hout.p) + (size_t)(k++) * out_bytes;
+    if (((a->metrics >> m) & 1u) && houts[m]) *douts[m] = static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes;
     else *douts[m] = nullptr;
   }
   ps_status s = ps_plv_family(c, &d, res);
   if (s != PS_OK) return s;
-  k = 0;
+  q = 0;
   for (int m = 0; m < 5; ++m)
     if (((a->metrics >> m) & 1u) && houts[m])
-      PS_CUDA(cudaMemcpyAsync(houts[m], static_cast<char*>(c->hout.p) + (size_t)(k++) * out_bytes, out_bytes,
+      PS_CUDA(cudaMemcpyAsync(houts[m], static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes, out_bytes,
                               cudaMemcpyDeviceToHost, st));
   PS_CUDA(cudaStreamSynchronize(st));
   return PS_OK;

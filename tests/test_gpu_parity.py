@@ -81,6 +81,30 @@ def test_host_and_device_paths_bit_identical():
         assert np.array_equal(h[m].values, dv[m].values.cpu().numpy())
 
 
+@pytest.mark.parametrize("kind", ["analytic", "real"])
+def test_pipelined_host_path_matches_device_path(kind):
+    # N >= 2048 with enough tiles takes the staged copy-in / Gram / copy-out
+    # pipeline of ps_plv_family_host; it must equal the device path bit-exactly
+    import torch
+
+    rng = np.random.default_rng(11)
+    N, T = 3000, 256
+    if kind == "analytic":
+        x = (rng.standard_normal((N, T)) + 1j * rng.standard_normal((N, T))).astype(np.complex64)
+    else:
+        x = rng.standard_normal((N, T)).astype(np.float32)
+    x[5, :7] = 0  # masked samples on the pipelined path too
+    h = C.plv_family(x, input_kind=kind, precision="split")
+    d = C.plv_family(torch.from_numpy(x).cuda(), input_kind=kind, precision="split")
+    for m in METRICS:
+        assert np.array_equal(h[m].values, d[m].values.cpu().numpy()), m
+    idx = np.sort(rng.choice(N, size=120, replace=False))
+    idx[0] = 5
+    ref = O.plv_family(x[idx][:, :, None], input_kind=kind)
+    for m in METRICS:
+        assert maxerr(h[m].values[np.ix_(idx, idx)], ref[m]) <= TOL["split"], m
+
+
 def test_deterministic_repeat():
     d = golden("c2_small")
     a = C.plv_family(d["x"], precision="split")
