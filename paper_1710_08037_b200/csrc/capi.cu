@@ -515,7 +515,7 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   p.planes = c->planes.p;
   p.plane_stride = g.plane_stride;
   p.status = c->d_status;
-  p.illcond_tol = 2e-6f;
+  p.illcond_tol = 4e-6f;  // 2.5x margin below the 1e-5 split-path tolerance
   p.kc_blocks = kc_blocks_default();
   if (g.split && k.outs[2]) {
     const int cap = 1 << 22;  // queued ill-conditioned ciPLV (pair, round) entries
@@ -609,16 +609,19 @@ ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long 
   const int n_groups = (int)groups.size();
   groups.push_back((int)ent.size());
   const size_t ebytes = (size_t)round_up((long long)(ent.size() * sizeof(RefineEntry)), 16);
-  PS_TRY(ensure(c->refine_sorted, ebytes + groups.size() * sizeof(int) + 64));
+  const size_t xbytes = ent.size() * sizeof(double);
+  PS_TRY(ensure(c->refine_sorted, ebytes + xbytes + groups.size() * sizeof(int) + 64));
   RefineEntry* d_ent = static_cast<RefineEntry*>(c->refine_sorted.p);
-  int* d_grp = reinterpret_cast<int*>(static_cast<char*>(c->refine_sorted.p) + ebytes);
+  double* d_exact = reinterpret_cast<double*>(static_cast<char*>(c->refine_sorted.p) + ebytes);
+  int* d_grp = reinterpret_cast<int*>(static_cast<char*>(c->refine_sorted.p) + ebytes + xbytes);
   PS_CUDA(cudaMemcpyAsync(d_ent, ent.data(), ent.size() * sizeof(RefineEntry), cudaMemcpyHostToDevice, st));
   PS_CUDA(cudaMemcpyAsync(d_grp, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   GramParams pr = k.p;
   pr.out_ciplv = k.outs[2];
   const bool single_round = k.pool || k.g.R == 1 || k.slot_mode == 0;
-  PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, single_round ? 1 : 0, (int)k.g.R, st));
-  c->launches++;
+  PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, (int)ent.size(), d_exact, single_round ? 1 : 0, (int)k.g.R,
+                        st));
+  c->launches += 2;
   // host vectors must outlive the async copies
   PS_CUDA(cudaStreamSynchronize(st));
   return PS_OK;

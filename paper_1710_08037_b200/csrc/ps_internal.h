@@ -109,7 +109,7 @@ cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);
 // location; `overwrite` = the slot holds a single round (else the mean over
 // `div` rounds gets (exact - approx) / div added).
 cudaError_t launch_refine(const GramParams& p, const RefineEntry* entries, const int* groups, int n_groups,
-                          int overwrite, int div, cudaStream_t st);
+                          int n_entries, double* exact, int overwrite, int div, cudaStream_t st);
 
 // split Gram variant: 2 = CTA pair (cta_group::2, 256-row panels), 1 = single
 // CTA (128-row panels).  PS_CTA_GROUP=1 selects the latter.
