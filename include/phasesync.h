@@ -137,6 +137,18 @@ ps_status ps_ctx_set_timing(ps_ctx* ctx, int enable);
  * (AllSamplesMasked, EmptyEffectiveWindow).  result may be NULL. */
 ps_status ps_plv_family(ps_ctx* ctx, const ps_plv_args* args, ps_plv_result* result);
 
+/* Device path with a staged input (multi-GPU input distribution):
+ * the signal rows [stage_cols[s], stage_cols[s+1]) of every (band, trial)
+ * unit become valid on the device once ready_events[s] (a cudaEvent_t, NULL =
+ * already valid) completes -- e.g. after an NCCL broadcast of that chunk from
+ * the rank holding the input.  Normalisation of a chunk and the Gram tiles
+ * whose columns fall in stage s start as soon as their rows have arrived, so
+ * the transfer of later chunks overlaps compute ("growing square").
+ * stage_cols: n_stages + 1 increasing signal indices, 0 ... n_signals, interior
+ * ones multiples of 256.  Trial means use one trial group per band. */
+ps_status ps_plv_family_staged(ps_ctx* ctx, const ps_plv_args* args, ps_plv_result* result, int32_t n_stages,
+                               const int64_t* stage_cols, void* const* ready_events);
+
 /* Same contract with HOST input/output pointers (pinned memory recommended):
  * host->device copy, compute, device->host copy, all inside the call.  This is
  * the entry point a host binding (ctypes / cgo / JNI) uses for plain arrays. */

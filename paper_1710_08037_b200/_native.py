@@ -99,6 +99,8 @@ _SIGNATURES = {
     "ps_ctx_set_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
     "ps_plv_family": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult)], ctypes.c_int),
     "ps_plv_family_host": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult)], ctypes.c_int),
+    "ps_plv_family_staged": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult), ctypes.c_int32,
+                              ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "ps_analytic_signal": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p], ctypes.c_int),
     "ps_normalize_phasors": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p, ctypes.c_void_p],
                              ctypes.c_int),

@@ -54,7 +54,7 @@ def _infer_kind(code: str, input_kind: str | None) -> str:
 def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("plv", "iplv", "ciplv"),
                precision: str = "split", trial_reduce: str = "mean", amp_floor: float = 1e-6,
                bands: bool = False, shard: tuple[int, int] = (0, 1), out: dict | None = None,
-               timing: bool = False) -> dict:
+               timing: bool = False, stages=None) -> dict:
     """All requested PLV-family metrics from one Gram per trial.
 
     x: RealEpochs / AnalyticEpochs / PhasorEpochs data, shape [N, T], [N, T, R]
@@ -68,6 +68,9 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     shard: (index, count) output-tile sharding; entries owned by
        other shards are left as allocated (zeros when ``out`` is None).
     out: optional preallocated outputs {metric: array} (same kind as x).
+    stages: (stage_cols, ready_events) for a CUDA input that arrives in row
+       chunks (ps_plv_family_staged): rows [cols[s], cols[s+1]) of every unit
+       are valid once torch.cuda.Event ready_events[s] completes.
     Returns {metric: ConnectivityMatrix}.
     """
     if hasattr(x, "data") and not isinstance(x, np.ndarray) and not is_torch(x):
@@ -122,7 +125,15 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
             ctx = _native.context(d.device)
             ctx.set_timing(timing)
             res = _native.PlvResult()
-            _native.check(_native.lib().ps_plv_family(ctx.handle, ctypes.byref(a), ctypes.byref(res)))
+            if stages is None:
+                _native.check(_native.lib().ps_plv_family(ctx.handle, ctypes.byref(a), ctypes.byref(res)))
+            else:
+                cols, events = stages
+                n = len(cols) - 1
+                ccols = (ctypes.c_int64 * (n + 1))(*[int(v) for v in cols])
+                cevs = (ctypes.c_void_p * n)(*[(e.cuda_event if e is not None else None) for e in events])
+                _native.check(_native.lib().ps_plv_family_staged(ctx.handle, ctypes.byref(a), ctypes.byref(res), n,
+                                                                 ccols, cevs))
     else:
         ndt = np.float64 if fp64 else np.float32
         for m in metrics:

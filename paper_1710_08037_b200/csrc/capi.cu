@@ -454,7 +454,11 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     k.G = (int)g.R;
     k.slot_mode = 0;
   } else {
-    k.G = (k.shard_count > 1 || force_g1) ? 1 : choose_groups((long long)mine.size() * g.B, (int)g.R, c->num_sms);
+    // concurrent work slots = CTA groups (pairs for the cta_group::2 kernel);
+    // items per group = tiles in 128-row halves for the single-CTA variant
+    const int slots = c->num_sms / (g.split ? split_cta_group() : 1);
+    const long long per_group = (long long)mine.size() * g.B * (g.split ? kSplitBM / split_panel_rows() : 1);
+    k.G = (k.shard_count > 1 || force_g1) ? 1 : choose_groups(per_group, (int)g.R, slots);
     k.slot_mode = k.G == 1 ? 1 : 2;
     k.mean_div = k.G == 1 ? (int)g.R : 1;
   }
@@ -910,6 +914,67 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
       cudaEventElapsedTime(&res->ms_gram, c->ev[1], c->ev[2]);
       cudaEventElapsedTime(&res->ms_finish, c->ev[2], c->ev[3]);
     }
+  }
+  return s;
+}
+
+ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, int32_t n_stages,
+                               const int64_t* stage_cols, void* const* ready_events) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  Call k;
+  PS_TRY(validate(a, k.g));
+  PS_TRY(setup_outputs(a, k));
+  const Geometry& g = k.g;
+  if (n_stages < 1 || !stage_cols) return fail(PS_E_INVALID, "n_stages must be >= 1 with stage_cols");
+  std::vector<long long> cols(stage_cols, stage_cols + n_stages + 1);
+  if (cols.front() != 0 || cols.back() != g.N) return fail(PS_E_INVALID, "stage_cols must run from 0 to n_signals");
+  for (int s = 0; s < n_stages; ++s) {
+    if (cols[s + 1] <= cols[s]) return fail(PS_E_INVALID, "stage_cols must increase");
+    if (s > 0 && cols[s] % kSplitBM != 0) return fail(PS_E_INVALID, "interior stage_cols must be multiples of 256");
+  }
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(a->stream);
+  PS_TRY(ensure_pipeline(c, n_stages));
+  c->launches = 0;
+  bool copied = false;
+  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  PS_TRY(ensure(c->planes, plane_bytes));
+  if (a->input_kind == PS_INPUT_REAL) {  // size the Hilbert workspace once (no realloc mid-stage)
+    const size_t es = g.cdouble ? 8 : 4;
+    const long long rc = std::min(hilbert_chunk_rows(g), g.rows);
+    PS_TRY(ensure(c->spec, (size_t)rc * (g.T / 2 + 1) * 2 * es));
+    PS_TRY(ensure(c->hbuf, (size_t)rc * g.T * es));
+    PS_TRY(ensure(c->xw, (size_t)rc * g.T * es));
+  }
+  PS_TRY(reset_status(c, st));
+  PS_TRY(init_row_state(c, g, st));
+  PS_TRY(plan_call(c, a, k, cols, /*force_g1=*/true, st));
+  const long long U = g.B * g.R;
+  for (int s = 0; s < n_stages; ++s) {
+    if (ready_events && ready_events[s])
+      PS_CUDA(cudaStreamWaitEvent(st, static_cast<cudaEvent_t>(ready_events[s]), 0));
+    for (long long u = 0; u < U; ++u)
+      PS_TRY(prepare_rows(c, a, g, a->input, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride,
+                          u * g.N + cols[s], u * g.N + cols[s + 1], st, &copied));
+    PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), st));
+  }
+  for (int s = 0; s < n_stages; ++s) {
+    PS_CUDA(cudaStreamWaitEvent(c->s_comp, pool_event(c, 3 * s), 0));
+    PS_TRY(launch_stage(c, k, s, c->s_comp));
+  }
+  cudaEvent_t done = pool_event(c, 3 * n_stages);
+  PS_CUDA(cudaEventRecord(done, c->s_comp));
+  PS_CUDA(cudaStreamWaitEvent(st, done, 0));
+  ps_status s = read_status(c, st);
+  if (s == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+  if (res) {
+    std::memset(res, 0, sizeof(*res));
+    res->n_observations = k.pool ? g.T * g.R : g.T;
+    res->n_masked_samples = (int64_t)c->h_status->n_masked;
+    res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->input_copied = copied ? 1 : 0;
+    res->n_kernel_launches = c->launches;
   }
   return s;
 }

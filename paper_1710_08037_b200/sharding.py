@@ -60,6 +60,36 @@ def broadcast_input(x, src: int = 0, group=None):
     return x
 
 
+def stage_cols(n_signals: int, n_stages: int = 8, min_width: int = 1024) -> list:
+    """Stage boundaries for the staged ("growing square") schedule: interior
+    boundaries are multiples of 256 (the split tile height)."""
+    per_stage = -(-n_signals // n_stages)                 # ceil(N / n_stages)
+    width = max(min_width, -(-per_stage // 256) * 256)    # rounded up to 256
+    cols = list(range(0, n_signals, width)) + [n_signals]
+    return cols
+
+
+def broadcast_input_staged(rows_view, cols, src: int = 0, group=None, stream=None):
+    """Chunked NCCL broadcast of a device input whose signal rows lie along
+    dim 0 (`rows_view[c0:c1]` must be contiguous, e.g. a single-trial
+    [N, T] / [N, T, 2] tensor).  Returns one torch.cuda.Event per chunk,
+    recorded on `stream` after that chunk's broadcast; feed them with `cols`
+    to connectivity.plv_family(stages=(cols, events)) so each rank starts
+    normalising / computing a chunk as soon as it has arrived."""
+    import torch
+    import torch.distributed as dist
+
+    stream = stream or torch.cuda.Stream()
+    events = []
+    with torch.cuda.stream(stream):
+        for c0, c1 in zip(cols[:-1], cols[1:]):
+            dist.broadcast(rows_view[c0:c1], src=src, group=group)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            events.append(ev)
+    return events
+
+
 def gather(outputs: dict, dst: int | None = 0, group=None) -> dict:
     """Assemble sharded outputs: reduce (dst given) or all-reduce (dst None)."""
     import torch.distributed as dist
