@@ -459,6 +459,11 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     const int slots = c->num_sms / (g.split ? split_cta_group() : 1);
     const long long per_group = (long long)mine.size() * g.B * (g.split ? kSplitBM / split_panel_rows() : 1);
     k.G = (k.shard_count > 1 || force_g1) ? 1 : choose_groups(per_group, (int)g.R, slots);
+    static const int g_env = [] {
+      const char* s = std::getenv("PS_GROUPS");  // experiment override
+      return s ? std::atoi(s) : 0;
+    }();
+    if (g_env > 0 && k.shard_count == 1 && !force_g1) k.G = std::min<int>(g_env, (int)g.R);
     k.slot_mode = k.G == 1 ? 1 : 2;
     k.mean_div = k.G == 1 ? (int)g.R : 1;
   }

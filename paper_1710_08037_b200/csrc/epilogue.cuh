@@ -33,7 +33,7 @@ __device__ __forceinline__ PairMetrics<S> pair_metrics(S gre, S gim, S inv_t) {
   if (SPLIT) {
     plv = plv > S(1) ? S(1) : plv;
     const S d = (S(1) - are) * (S(1) + are);
-    ci = d > S(0) ? aim / sqrt(d) : S(0);
+    ci = d > S(0) ? aim * rsqrtf(d) : S(0);  // MUFU.RSQ: ~2 ulp, far below the 1e-5 budget
     ci = ci > S(1) ? S(1) : ci;
   } else {
     ci = (are >= S(1) - S(1e-12)) ? S(0) : aim / sqrt(S(1) - cre * cre);
@@ -124,6 +124,48 @@ __device__ __forceinline__ void emit_all(const GramParams& p, long long slot, in
     emit<S>(static_cast<S*>(p.out_ciplv) + off, N, i, j, m.ciplv, first, last, p.mean_div, false);
   if (p.out_cre) emit<S>(static_cast<S*>(p.out_cre) + off, N, i, j, m.cre, first, last, p.mean_div, false);
   if (p.out_cim) emit<S>(static_cast<S*>(p.out_cim) + off, N, i, j, m.cim, first, last, p.mean_div, true);
+}
+
+// Four consecutive columns j0..j0+3 of row i, all strictly above the diagonal
+// and inside the matrix (caller checks; needs N % 4 == 0 for 16-byte rows):
+// one 16-byte read-modify-write per metric for the direct part, all reads
+// issued before any write so their latencies overlap; mirror writes are
+// coalesced across the warp's lanes (consecutive i).
+__device__ __forceinline__ void emit4_all(const GramParams& p, long long slot, int i, int j0,
+                                          const PairMetrics<float> (&m)[4], bool first, bool last) {
+  const long long N = p.N;
+  const long long off = slot * N * N;
+  float* outs[5] = {static_cast<float*>(p.out_plv), static_cast<float*>(p.out_iplv),
+                    static_cast<float*>(p.out_ciplv), static_cast<float*>(p.out_cre),
+                    static_cast<float*>(p.out_cim)};
+  float4 prev[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    prev[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (outs[q] && !first) prev[q] = *reinterpret_cast<const float4*>(outs[q] + off + (long long)i * N + j0);
+  }
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    if (!outs[q]) continue;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      v[e] = q == 0 ? m[e].plv : q == 1 ? m[e].iplv : q == 2 ? m[e].ciplv : q == 3 ? m[e].cre : m[e].cim;
+    float4 a = make_float4(prev[q].x + v[0], prev[q].y + v[1], prev[q].z + v[2], prev[q].w + v[3]);
+    if (last && p.mean_div != 1) {
+      const float d = (float)p.mean_div;
+      a = make_float4(a.x / d, a.y / d, a.z / d, a.w / d);
+    }
+    float* base = outs[q] + off;
+    *reinterpret_cast<float4*>(base + (long long)i * N + j0) = a;
+    if (last) {
+      const float s = q == 4 ? -1.f : 1.f;
+      base[(long long)(j0 + 0) * N + i] = s * a.x;
+      base[(long long)(j0 + 1) * N + i] = s * a.y;
+      base[(long long)(j0 + 2) * N + i] = s * a.z;
+      base[(long long)(j0 + 3) * N + i] = s * a.w;
+    }
+  }
 }
 
 // Round bookkeeping common to both kernels: which slot a (item, trial) round

@@ -108,11 +108,15 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
     ptx::tmem_ld_32x32b_x4(ta + g, vre);
     ptx::tmem_ld_32x32b_x4(ta + BN + g, vim);
     ptx::tmem_wait_ld();
+    const int j0 = w.J * BN + h * HALF + g;
+    // all four pairs strictly upper and inside: compute, then 16-byte RMW
+    const bool vec = (p.N & 3) == 0 && i < p.N && j0 > i && j0 + 3 < p.N;
+    PairMetrics<float> m4[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int j = w.J * BN + h * HALF + g + e;
+      const int j = j0 + e;
       if (i >= p.N || j >= p.N || j < i) continue;
-      PairMetrics<float> m;
+      PairMetrics<float>& m = m4[e];
       if (j == i) {
         m = diag_metrics<float>();
       } else {
@@ -148,8 +152,9 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
           }
         }
       }
-      emit_all<float>(p, ri.slot, i, j, m, ri.first, ri.last);
+      if (!vec) emit_all<float>(p, ri.slot, i, j, m, ri.first, ri.last);
     }
+    if (vec) emit4_all(p, ri.slot, i, j0, m4, ri.first, ri.last);
   }
   if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
 }
