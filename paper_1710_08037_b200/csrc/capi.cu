@@ -350,23 +350,26 @@ void build_tiles(long long N, int bm, int bn, std::vector<std::pair<int, int>>& 
   }
 }
 
-int choose_groups(long long items_per_group, int R, int num_sms) {
-  // pick the number of trial groups that best fills whole waves of SMs
-  int best_g = 1;
-  double best_eff = -1.0;
-  for (int G = 1; G <= R; ++G) {
-    const int Rg = (R + G - 1) / G;
-    const int Ge = (R + Rg - 1) / Rg;
-    if (Ge != G) continue;
+int choose_groups(long long items_per_group, int R, int num_slots, size_t ws_bytes_per_group, size_t ws_budget) {
+  // Trial groups: items = tiles x bands x G, each running Rg = ceil(R / G)
+  // trials back to back.  Time ~ waves(items) x Rg.  Rounds after the first
+  // of a group read-modify-write the partial sums (measured ~25% slower per
+  // round on C4), so among near-optimal choices prefer the most groups whose
+  // partial-sum workspace fits the budget.
+  auto cost = [&](int G, int Rg) {
     const long long items = items_per_group * G;
-    const long long waves = (items + num_sms - 1) / num_sms;
-    const double eff = (double)items * Rg / ((double)waves * num_sms * Rg);
-    // each item costs Rg trials; total time ~ waves * Rg
-    const double t = (double)waves * Rg;
-    const double score = 1.0 / t;  // higher is better
-    (void)eff;
-    if (score > best_eff * (1.0 + 1e-9)) {
-      best_eff = score;
+    const long long waves = (items + num_slots - 1) / num_slots;
+    return (double)waves * (1.0 + 1.25 * (Rg - 1));  // first round of an item 1, RMW rounds 1.25
+  };
+  int best_g = 1;
+  double best = cost(1, R);
+  for (int G = 2; G <= R; ++G) {
+    const int Rg = (R + G - 1) / G;
+    if ((R + Rg - 1) / Rg != G) continue;
+    if ((size_t)G * ws_bytes_per_group > ws_budget) break;
+    const double c = cost(G, Rg);
+    if (c <= best * 1.02) {
+      best = std::min(best, c);
       best_g = G;
     }
   }
@@ -458,7 +461,11 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     // items per group = tiles in 128-row halves for the single-CTA variant
     const int slots = c->num_sms / (g.split ? split_cta_group() : 1);
     const long long per_group = (long long)mine.size() * g.B * (g.split ? kSplitBM / split_panel_rows() : 1);
-    k.G = (k.shard_count > 1 || force_g1) ? 1 : choose_groups(per_group, (int)g.R, slots);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const size_t ws_per_group = (size_t)g.B * g.N * g.N * (g.split ? 4 : 8) * 5;  // worst case: 5 metrics
+    const size_t ws_budget = std::min<size_t>(free_b / 4, (size_t)24 << 30);
+    k.G = (k.shard_count > 1 || force_g1) ? 1 : choose_groups(per_group, (int)g.R, slots, ws_per_group, ws_budget);
     static const int g_env = [] {
       const char* s = std::getenv("PS_GROUPS");  // experiment override
       return s ? std::atoi(s) : 0;
