@@ -693,7 +693,11 @@ ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
 ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long span, long long esz,
                          ps_plv_result* res) {
   const Geometry& g = k.g;
-  const long long W = std::max<long long>(1024, round_up((g.N + 7) / 8, 256));
+  static const long long w_env = [] {
+    const char* s = std::getenv("PS_STAGE_W");  // experiment override (signals per stage)
+    return s ? std::atoll(s) : 0LL;
+  }();
+  const long long W = w_env > 0 ? round_up(w_env, 256) : std::max<long long>(1024, round_up((g.N + 7) / 8, 256));
   std::vector<long long> cols;
   for (long long x = 0; x < g.N; x += W) cols.push_back(x);
   cols.push_back(g.N);
