@@ -289,3 +289,25 @@ def test_full_size_configs_subset_parity(cfg):
     errs = subset_check(x, hres, idx, kind, "split", f"{cfg}-full")
     for m, e in errs.items():
         assert e <= TOL["split"], (cfg, m, e)
+
+
+# ------------------------------------------------------------ CLI (acceptance #9)
+def test_cli_matches_library_bit_exactly(tmp_path):
+    from paper_1710_08037_b200 import bindings, cli
+
+    rng = np.random.default_rng(20)
+    x = rng.standard_normal((20, 700, 2))
+    x[7] = x[3]  # duplicated channel: PLV 1, ciPLV 0
+    cli.write_bundle(tmp_path / "in", x, axes=["signal", "sample", "trial"])
+    for metric in ("plv", "iplv", "ciplv"):
+        out = tmp_path / metric
+        assert cli.entrypoint(["connectivity", str(tmp_path / "in"), "--metric", metric, "-o", str(out)]) == 0
+        got, hdr = cli.read_bundle(out)
+        lib = bindings.py_plv(x) if metric == "plv" else (
+            bindings.py_iplv(x) if metric == "iplv" else bindings.py_ciplv(x))
+        assert np.array_equal(got, np.asarray(lib, dtype=np.float64)), metric
+        assert (out.with_suffix(".csv")).exists() and (out.with_suffix(".manifest.json")).exists()
+        if metric == "plv":
+            assert abs(got[3, 7] - 1.0) < 1e-5
+        if metric == "ciplv":
+            assert got[3, 7] == 0.0
