@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 1
+#define PS_ABI_VERSION 2
 
 typedef enum ps_status {
   PS_OK = 0,
@@ -102,7 +102,15 @@ typedef struct ps_plv_args {
   int32_t shard_index;
   int32_t shard_count;
   void* stream;                /* cudaStream_t (NULL = legacy default stream) */
+  /* PS_MODE_OVER_SAMPLES (Eq 7, default) or PS_MODE_OVER_TRIALS (Eq 8,
+   * time-resolved: one matrix per sample from the Gram over trials, SPEC.md:
+   * 153-157,173,186-189).  Over trials, outputs are [n_bands][n_samples][N][N]
+   * and trial_reduce is ignored. */
+  int32_t mode;
+  int32_t reserved0;
 } ps_plv_args;
+
+enum { PS_MODE_OVER_SAMPLES = 0, PS_MODE_OVER_TRIALS = 1 };
 
 typedef struct ps_plv_result {
   int64_t n_observations;      /* T used for normalisation (R*T for POOL) */

@@ -275,20 +275,28 @@ def plv_matrix(phasors, mode: str = "over_samples", trial_reduce: str = "mean"):
 
 def plv_over_trials(z, mask):
     """Eq 8: per sample t, Gram over trials.
-    Returns [N, N, T]."""
+    Returns PLV [N, N, T]."""
+    return plv_family_over_trials(z, mask)["plv"]
+
+
+def plv_family_over_trials(z, mask):
+    """Time-resolved PLV / iPLV / ciPLV (Eq 8 with the Eq 13/14 epilogues; the
+    trial-axis variant SPEC.md:277 makes available): per sample t the Gram is
+    taken over trials and the per-pair count is the number of trials unmasked
+    in both signals.  Returns dict of [N, N, T] arrays."""
+    z = np.asarray(z)
     N, T, R = z.shape
-    out = np.empty((N, N, T))
+    outs = {k: np.empty((N, N, T)) for k in ("plv", "iplv", "ciplv")}
     u = (~mask).astype(np.float64)
     for t in range(T):
         zt = z[:, t, :]
         G = zt @ zt.conj().T
         C = u[:, t, :] @ u[:, t, :].T
-        if np.any(C <= 0):
-            raise EmptyEffectiveWindowError("all trials masked for some pair at a sample")
-        p = np.abs(G) / C
-        np.fill_diagonal(p, 1.0)
-        out[:, :, t] = p
-    return out
+        p, i, c = _metrics_from_gram(G, C)
+        outs["plv"][:, :, t] = p
+        outs["iplv"][:, :, t] = i
+        outs["ciplv"][:, :, t] = c
+    return outs
 
 
 # --------------------------------------------------------------------------

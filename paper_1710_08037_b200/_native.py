@@ -17,7 +17,7 @@ from pathlib import Path
 from . import errors
 
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 # ps_status -> exception class (include/phasesync.h)
 PS_OK = 0
@@ -68,6 +68,8 @@ class PlvArgs(ctypes.Structure):
         ("shard_index", ctypes.c_int32),
         ("shard_count", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
+        ("mode", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
     ]
 
 

@@ -54,7 +54,7 @@ def _infer_kind(code: str, input_kind: str | None) -> str:
 def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("plv", "iplv", "ciplv"),
                precision: str = "split", trial_reduce: str = "mean", amp_floor: float = 1e-6,
                bands: bool = False, shard: tuple[int, int] = (0, 1), out: dict | None = None,
-               timing: bool = False, stages=None) -> dict:
+               timing: bool = False, stages=None, mode: str = "over_samples") -> dict:
     """All requested PLV-family metrics from one Gram per trial.
 
     x: RealEpochs / AnalyticEpochs / PhasorEpochs data, shape [N, T], [N, T, R]
@@ -71,8 +71,14 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     stages: (stage_cols, ready_events) for a CUDA input that arrives in row
        chunks (ps_plv_family_staged): rows [cols[s], cols[s+1]) of every unit
        are valid once torch.cuda.Event ready_events[s] completes.
+    mode: 'over_samples' (Eq 7, default) or 'over_trials' (Eq 8: time-resolved,
+       one matrix per sample from the Gram over trials; values [N, N, T],
+       trial_reduce ignored).
     Returns {metric: ConnectivityMatrix}.
     """
+    if mode not in ("over_samples", "over_trials"):
+        raise ValueError("mode must be 'over_samples' or 'over_trials'")
+    over_trials = mode == "over_trials"
     if hasattr(x, "data") and not isinstance(x, np.ndarray) and not is_torch(x):
         x = x.data  # RealEpochs / AnalyticEpochs / PhasorEpochs
     metrics = tuple(metrics)
@@ -86,8 +92,8 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     d = describe(x, bands=bands)
     kind = _infer_kind(d.dtype, input_kind)
     B, N, T, R = d.dims
-    per_trial = trial_reduce == "none" and R > 1
-    slots = B * R if per_trial else B
+    per_trial = trial_reduce == "none" and R > 1 and not over_trials
+    slots = B * T if over_trials else (B * R if per_trial else B)
     fp64 = _native.PRECISIONS[precision] == 1
     bits = 0
     for m in metrics:
@@ -104,6 +110,7 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     a.precision = _native.PRECISIONS[precision]
     a.trial_reduce = _native.TRIAL_REDUCE[trial_reduce]
     a.shard_index, a.shard_count = int(shard[0]), int(shard[1])
+    a.mode = 1 if over_trials else 0
 
     outs = {}
     if d.on_device:
@@ -157,7 +164,12 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     result = {}
     for m in metrics:
         v = outs[m]
-        if per_trial:
+        if over_trials:  # TimeResolvedPLV layout [N, N, T]
+            v = v.reshape(B, T, N, N)
+            v = v.permute(0, 2, 3, 1) if is_torch(v) else np.moveaxis(v, 1, 3)
+            if not bands:
+                v = v[0]
+        elif per_trial:
             v = v.reshape(B, R, N, N)
             v = v.permute(0, 2, 3, 1) if is_torch(v) else np.moveaxis(v, 1, 3)
             if not bands:
@@ -183,15 +195,14 @@ def plv_matrix(phasors, mode: str = "over_samples", *, trial_reduce: str = "mean
 
     ``phasors``: PhasorEpochs (or its complex data) [N, T, R]; masked samples
     are exactly 0 and drop out of both the product and the per-pair T
-    (SPEC.md:260).  Mode 'over_trials' (Eq 8, time-resolved PLV) is SURVEY
-    8(f) row 2 and not built yet.
+    (SPEC.md:260).  Mode 'over_trials' (Eq 8): time-resolved PLV,
+    one matrix per sample from the Gram over trials -> values [N, N, T]
+    (TimeResolvedPLV, SPEC.md:153-157).
     """
-    if mode == "over_trials":
-        raise errors.UnsupportedError("mode='over_trials' (Eq 8) is not implemented by this build yet")
-    if mode != "over_samples":
+    if mode not in ("over_samples", "over_trials"):
         raise ValueError("mode must be 'over_samples' or 'over_trials'")
     return plv_family(_phasor_input(phasors), input_kind="phasor", metrics=("plv",), precision=precision,
-                      trial_reduce=trial_reduce)["plv"]
+                      trial_reduce=trial_reduce, mode=mode)["plv"]
 
 
 def iplv(phasors, *, trial_reduce: str = "mean", precision: str = "split") -> ConnectivityMatrix:

@@ -77,7 +77,7 @@ struct ps_ctx {
   bool timing = false;
   std::mutex mu;
   std::map<PlanKey, cufftHandle> plans;
-  Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout, refine, refine_sorted;
+  Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout, refine, refine_sorted, planes_t, maskcount_t;
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
   std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
@@ -152,6 +152,7 @@ ps_status validate(const ps_plv_args* a, Geometry& g) {
   if (a->precision != PS_PREC_SPLIT_F16X3 && a->precision != PS_PREC_FP64)
     return fail(PS_E_INVALID, "unknown precision");
   if (a->trial_reduce < 0 || a->trial_reduce > 2) return fail(PS_E_INVALID, "unknown trial_reduce");
+  if (a->mode != PS_MODE_OVER_SAMPLES && a->mode != PS_MODE_OVER_TRIALS) return fail(PS_E_INVALID, "unknown mode");
   if (!(a->amp_floor >= 0.0)) return fail(PS_E_INVALID, "amp_floor must be >= 0");
   if (a->n_signals > (1 << 30) || a->n_samples > (1LL << 31) - 1)
     return fail(PS_E_SHAPE, "n_signals / n_samples exceed the supported range");
@@ -866,7 +867,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   cudaSetDevice(c->device);
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
-                 &c->hout, &c->refine, &c->refine_sorted})
+                 &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -904,9 +905,29 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   PS_TRY(ensure(c->planes, plane_bytes));
   PS_TRY(reset_status(c, st));
   PS_TRY(prepare_phasors(c, a, g, a->input, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride, st, &copied));
+  // ---- time-resolved mode (Eq 8): Gram over trials, one matrix per sample ----
+  ps_plv_args at = *a;
+  if (a->mode == PS_MODE_OVER_TRIALS) {
+    if (g.R < 2) return fail(PS_E_SHAPE, "mode over_trials needs n_trials >= 2 (Eq 8: PLV across trials)");
+    at.n_samples = g.R;  // K axis = trials
+    at.n_trials = g.T;   // one unit (output slot) per sample
+    at.trial_reduce = PS_TRIALS_NONE;
+    Geometry gt;
+    PS_TRY(validate(&at, gt));
+    const size_t tb = gt.split ? (size_t)4 * gt.plane_stride * 2 : (size_t)2 * gt.plane_stride * 8;
+    PS_TRY(ensure(c->planes_t, tb));
+    PS_TRY(ensure(c->maskcount_t, (size_t)gt.rows * sizeof(int)));
+    PS_CUDA(launch_transpose_trials(c->planes.p, g.plane_stride, (int)g.pitch, c->planes_t.p, gt.plane_stride,
+                                    (int)gt.pitch, (int)g.B, (int)g.R, (int)g.N, (int)g.T, g.split ? 1 : 0,
+                                    static_cast<int*>(c->maskcount_t.p), st));
+    c->launches++;
+    std::swap(c->planes, c->planes_t);  // the Gram below reads the trial-keyed planes / masks
+    std::swap(c->maskcount, c->maskcount_t);
+    k.g = gt;
+  }
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[1], st));
   // ---- Gram + fused epilogue ------------------------------------------------
-  PS_TRY(plan_call(c, a, k, {}, /*force_g1=*/false, st));
+  PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
   PS_TRY(launch_stage(c, k, 0, st));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
   if (k.slot_mode == 2) {
@@ -943,6 +964,7 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
   PS_TRY(setup_outputs(a, k));
   const Geometry& g = k.g;
   if (n_stages < 1 || !stage_cols) return fail(PS_E_INVALID, "n_stages must be >= 1 with stage_cols");
+  if (a->mode != PS_MODE_OVER_SAMPLES) return fail(PS_E_UNSUPPORTED, "staged input supports mode over_samples only");
   std::vector<long long> cols(stage_cols, stage_cols + n_stages + 1);
   if (cols.front() != 0 || cols.back() != g.N) return fail(PS_E_INVALID, "stage_cols must run from 0 to n_signals");
   for (int s = 0; s < n_stages; ++s) {
@@ -1016,7 +1038,8 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
   // GPU with one trial group.
   static const bool no_pipe = std::getenv("PS_NO_PIPELINE") != nullptr;
   const long long ntiles = ps_tile_count(g.N, a->precision);
-  const bool pipelinable = !no_pipe && k.shard_count == 1 && a->stride_sample == 1 && a->stride_signal >= g.T &&
+  const bool pipelinable = !no_pipe && a->mode == PS_MODE_OVER_SAMPLES && k.shard_count == 1 &&
+                           a->stride_sample == 1 && a->stride_signal >= g.T &&
                            g.N >= 2048 && ntiles * g.B >= c->num_sms;
   if (pipelinable) {
     std::lock_guard<std::mutex> lock(c->mu);
@@ -1026,7 +1049,9 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
   PS_TRY(ensure(c->hin, (size_t)span * esz));
   PS_CUDA(cudaMemcpyAsync(c->hin.p, a->input, (size_t)span * esz, cudaMemcpyHostToDevice, st));
   const bool pool = a->trial_reduce == PS_TRIALS_POOL;
-  const long long slots = (a->trial_reduce == PS_TRIALS_NONE && !pool) ? g.B * g.R : g.B;
+  const long long slots = a->mode == PS_MODE_OVER_TRIALS ? g.B * g.T
+                          : (a->trial_reduce == PS_TRIALS_NONE && !pool) ? g.B * g.R
+                                                                       : g.B;
   const size_t oes = g.split ? 4 : 8;
   const size_t out_bytes = (size_t)slots * g.N * g.N * oes;
   void* houts[5] = {a->out_plv, a->out_iplv, a->out_ciplv, a->out_cre, a->out_cim};

@@ -471,6 +471,42 @@ __global__ void group_reduce_kernel(const S* ws, int G, long long slot_elems, lo
   }
 }
 
+// Time-resolved mode (Eq 8): re-key the phasor planes so the
+// Gram's K axis runs over trials.  src [P][B*R][N][Tp] -> dst [P][B*T][N][Rp]
+// (P = 4 fp16 planes or 2 f64 planes), trial padding zeroed; maskcount_dst
+// [(b*T + t)*N + n] = number of masked trials (masked samples are exactly 0 in
+// every plane).  One thread per (b, n, t); reads are coalesced along t.
+template <typename E, int P>
+__global__ void transpose_trials_kernel(const E* __restrict__ src, long long sps, int Tp, E* __restrict__ dst,
+                                        long long dps, int Rp, int B, int R, int N, int T,
+                                        int* __restrict__ maskcount_dst) {
+  const long long total = (long long)B * N * T;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(e % T);
+    const long long bn = e / T;
+    const int n = (int)(bn % N);
+    const int b = (int)(bn / N);
+    const long long drow = ((long long)(b * T + t) * N + n) * Rp;
+    int masked = 0;
+    for (int r = 0; r < R; ++r) {
+      const long long sidx = ((long long)(b * R + r) * N + n) * Tp + t;
+      bool zero = true;
+#pragma unroll
+      for (int pl = 0; pl < P; ++pl) {
+        const E v = src[pl * sps + sidx];
+        dst[pl * dps + drow + r] = v;
+        zero = zero && (static_cast<float>(v) == 0.0f);
+      }
+      masked += zero ? 1 : 0;
+    }
+    for (int r = R; r < Rp; ++r)
+#pragma unroll
+      for (int pl = 0; pl < P; ++pl) dst[pl * dps + drow + r] = E(0.0f);
+    maskcount_dst[(long long)(b * T + t) * N + n] = masked;
+  }
+}
+
 int grid_for(long long n, int threads) {
   long long g = (n + threads - 1) / threads;
   if (g > 148LL * 16) g = 148LL * 16;
@@ -619,6 +655,20 @@ cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nr
   // hbuf type decides the output precision: f64 input -> c128, else c64
   if (src.is_double) analytic_out_kernel<double, double><<<g, 256, 0, st>>>(src, row0, nrows, (double*)out);
   else analytic_out_kernel<float, float><<<g, 256, 0, st>>>(src, row0, nrows, (float*)out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void* dst, long long dps, int Rp, int B,
+                                    int R, int N, int T, int split, int* maskcount_dst, cudaStream_t st) {
+  const int g = grid_for((long long)B * N * T, 256);
+  if (split)
+    transpose_trials_kernel<__half, 4><<<g, 256, 0, st>>>(static_cast<const __half*>(src), sps, Tp,
+                                                          static_cast<__half*>(dst), dps, Rp, B, R, N, T,
+                                                          maskcount_dst);
+  else
+    transpose_trials_kernel<double, 2><<<g, 256, 0, st>>>(static_cast<const double*>(src), sps, Tp,
+                                                          static_cast<double*>(dst), dps, Rp, B, R, N, T,
+                                                          maskcount_dst);
   return cudaGetLastError();
 }
 

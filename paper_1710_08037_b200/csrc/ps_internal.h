@@ -98,6 +98,9 @@ cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows
                              cudaStream_t st);
 cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nrows,
                                 void* out, cudaStream_t st);
+// Eq 8 (over trials): planes [P][B*R][N][Tp] -> [P][B*T][N][Rp] + masked-trial counts
+cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void* dst, long long dps, int Rp, int B,
+                                    int R, int N, int T, int split, int* maskcount_dst, cudaStream_t st);
 cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs,
                                 void* const* outs, long long elems_per_out, int R,
                                 int is_double, cudaStream_t st);

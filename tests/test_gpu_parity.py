@@ -137,6 +137,23 @@ def test_staged_input_matches_device_path():
         assert torch.equal(parts[0][m].values + parts[1][m].values, ref[m].values), m
 
 
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_over_trials_time_resolved(prec):
+    # Eq 8 / SPEC.md:153-157: one N x N matrix per sample, Gram over trials
+    rng = np.random.default_rng(21)
+    N, T, R = 150, 40, 37
+    a = rng.standard_normal((N, T, R)) + 1j * rng.standard_normal((N, T, R))
+    a[::9] *= np.exp(1j * rng.uniform(0, np.pi, (1, T, 1)))  # sample-dependent structure
+    a[4, 3, :5] = 0            # masked trials at one sample
+    z, mask = O.normalize_phasors(a)
+    ref = O.plv_family_over_trials(z, mask)
+    res = C.plv_family(a, input_kind="analytic", precision=prec, mode="over_trials")
+    assert res["plv"].values.shape == (N, N, T) and res["plv"].n_observations == R
+    check(res, ref, prec, "over_trials")
+    v = C.plv_matrix(z, mode="over_trials", precision=prec).values
+    assert maxerr(v, ref["plv"]) <= TOL[prec]
+
+
 def test_deterministic_repeat():
     d = golden("c2_small")
     a = C.plv_family(d["x"], precision="split")

@@ -237,6 +237,20 @@ def test_von_mises_monotone():
     assert all(b > a + 3 * 0.01 for a, b in zip(vals, vals[1:]))
 
 
+def test_over_trials_mode():
+    # Eq 8: PLV_ij(t) = |mean over trials of exp(i (phi_i(t,n) - phi_j(t,n)))|
+    z = O.make_surrogate(5, 12, 9, seed=4)
+    ph = np.angle(z)
+    got = O.plv_matrix(z, mode="over_trials")
+    for t in range(12):
+        for a in range(5):
+            for b in range(5):
+                ref = 1.0 if a == b else abs(np.mean(np.exp(1j * (ph[a, t] - ph[b, t]))))
+                assert abs(got[a, b, t] - ref) < 1e-12
+    fam = O.plv_family_over_trials(*O.phasors_from_unit(z))
+    assert np.all(fam["iplv"] <= fam["plv"] + 1e-12)
+
+
 def test_trial_reduce_modes():
     z = O.make_surrogate(6, 64, 3, seed=21)
     none = O.plv_family(z, input_kind="phasor", trial_reduce="none")
