@@ -81,12 +81,19 @@ __global__ void refine_apply_kernel(const GramParams p, const RefineEntry* __res
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= n_groups || !p.out_ciplv) return;
   const int k0 = groups[g], k1 = groups[g + 1];
-  double corr = 0.0;
-  for (int k = k0; k < k1; ++k) corr += exact[k] - (double)e[k].approx;
+  double corr = 0.0, sum = 0.0;
+  for (int k = k0; k < k1; ++k) {
+    corr += exact[k] - (double)e[k].approx;
+    sum += exact[k];
+  }
   const RefineEntry& e0 = e[k0];
   float* o = static_cast<float*>(p.out_ciplv) + (long long)e0.slot * p.N * p.N;
   const long long a = (long long)e0.i * p.N + e0.j, b = (long long)e0.j * p.N + e0.i;
-  const float v = overwrite ? (float)exact[k1 - 1] : (float)((double)o[a] + corr / (double)div);
+  // every round of the slot refined: take the exact mean outright (keeps
+  // exact zeros of the singularity rule exact); otherwise correct the mean
+  const float v = overwrite ? (float)exact[k1 - 1]
+                  : (k1 - k0 == div) ? (float)(sum / (double)div)
+                                     : (float)((double)o[a] + corr / (double)div);
   o[a] = v;
   o[b] = v;
 }
