@@ -275,6 +275,15 @@ ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cons
   return PS_OK;
 }
 
+// PS_HILBERT=cufft forces the cuFFT chain where the fused kernel applies
+bool hilbert_fused_enabled() {
+  static const bool on = [] {
+    const char* s = std::getenv("PS_HILBERT");
+    return !(s && std::string(s) == "cufft");
+  }();
+  return on;
+}
+
 ps_status reset_status(ps_ctx* c, cudaStream_t st) {
   PS_CUDA(cudaMemsetAsync(c->d_status, 0, sizeof(DevStatus), st));
   return PS_OK;
@@ -317,8 +326,23 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
     return static_cast<char*>(out) + (size_t)row0 * g.T * 2 * ces;
   };
   const long long rc = a->input_kind == PS_INPUT_REAL ? hilbert_chunk_rows(g) : (row_hi - row_lo);
+  const bool fused = a->input_kind == PS_INPUT_REAL && hilbert_fused_enabled() &&
+                     hilbert_fused_supported(src, fmt, g.cdouble ? 1 : 0, (int)pitch);
   for (long long row0 = row_lo; row0 < row_hi; row0 += rc) {
     const long long nr = std::min(rc, row_hi - row0);
+    if (fused) {
+      // one kernel: FFT -> multiplier -> IFFT -> normalise; H is kept (in
+      // hbuf) only for rows the exact-median fixup will inspect
+      PS_TRY(ensure(c->hbuf, (size_t)nr * g.T * sizeof(float)));
+      src.hbuf = c->hbuf.p;
+      src.h_row0 = row0;
+      PS_CUDA(launch_hilbert_fused(src, row0, nr, out, (int)pitch, plane_stride, rs, g.rows, a->amp_floor,
+                                   c->d_status, st));
+      PS_CUDA(launch_fixup_fmt(src, row0, nr, out, fmt, 0, (int)pitch, plane_stride, rs, g.rows,
+                               static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
+      c->launches += 2;
+      continue;
+    }
     if (a->input_kind == PS_INPUT_REAL) {
       PS_TRY(hilbert_chunk(c, a, g, src, row0, nr, st, copied));
       src.hbuf = c->hbuf.p;

@@ -259,6 +259,303 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
 }
 
 // ---------------------------------------------------------------------------
+// Fused Hilbert + normalise for real fp32 rows of length T = 4096 (the
+// short-T, many-trial regime of config C4): one CTA per pair of rows, the two
+// rows packed as x_a + i x_b into one complex FFT (the Hilbert multiplier
+// -i sgn(k) is real-linear, so IFFT(h . FFT(x_a + i x_b)) = H{x_a} + i H{x_b}).
+// Radix-16 Stockham FFT in shared memory (3 passes each way, 256 threads x
+// 16 values), the multiplier fused into the first inverse pass, and the
+// normalisation / fp16 hi-lo split / row min-max fused into the epilogue.
+// HBM traffic 12 B/sample (x in, planes out) versus ~40 B/sample for the
+// cuFFT R2C -> K2 -> C2R -> K4 chain.  H is written to `hbuf` only for rows
+// whose amplitude pre-check fails, so the exact-median fixup can run as usual.
+// ---------------------------------------------------------------------------
+constexpr int kFftT = 4096;
+constexpr int kFftThreads = 256;  // kFftT / 16
+__host__ __device__ constexpr int kFftPad(int i) { return i + (i >> 4); }  // breaks the stride-16 bank pattern
+// twiddle tables per pass, laid out [r][k] (lanes read consecutive k):
+//   pass NS=16 : W_256^(k r),  k < 16,  r = 1..15
+//   pass NS=256: W_4096^(k r), k < 256, r = 1..15
+constexpr int kTw16 = 0;
+constexpr int kTw256 = 15 * 16;
+constexpr int kTwCount = kTw256 + 15 * 256;
+constexpr int kFftSmemBytes = (kFftPad(kFftT) + kTwCount) * 8;
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+template <bool INV>
+__device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
+  const float2 s0 = cadd(a0, a2), d0 = csub(a0, a2), s1 = cadd(a1, a3), d1 = csub(a1, a3);
+  const float2 t = INV ? make_float2(-d1.y, d1.x) : make_float2(d1.y, -d1.x);  // d1 * (+-i)
+  a0 = cadd(s0, s1);
+  a2 = csub(s0, s1);
+  a1 = cadd(d0, t);
+  a3 = csub(d0, t);
+}
+
+// W16^m (forward sign) for compile-time m in [0, 9]
+__device__ __forceinline__ float2 w16(int m) {
+  const float c1 = 0.92387953251128674f, s1 = 0.38268343236508977f, c2 = 0.70710678118654752f;
+  switch (m) {
+    case 1: return make_float2(c1, -s1);
+    case 2: return make_float2(c2, -c2);
+    case 3: return make_float2(s1, -c1);
+    case 4: return make_float2(0.f, -1.f);
+    case 6: return make_float2(-c2, -c2);
+    case 9: return make_float2(-c1, s1);
+    default: return make_float2(1.f, 0.f);
+  }
+}
+
+// Position of output k of dft16 in v[]: the result is left transposed
+// (X[k1 + 4 k2] in v[4 k1 + k2]) and consumers index through this map.
+__host__ __device__ constexpr int d16(int k) { return 4 * (k & 3) + (k >> 2); }
+
+// In-register 16-point DFT (4 x 4 decomposition), sign per INV; output k in v[d16(k)].
+template <bool INV>
+__device__ __forceinline__ void dft16(float2 (&v)[16]) {
+  // n = 4 n1 + n2 ; first 4-point DFTs over n1
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
+  // v[4 k1 + n2] = A[n2][k1]; twiddle W16^(n2 k1)
+#pragma unroll
+  for (int k1 = 1; k1 < 4; ++k1)
+#pragma unroll
+    for (int n2 = 1; n2 < 4; ++n2) {
+      float2 tw = w16(n2 * k1);
+      if (INV) tw.y = -tw.y;
+      v[4 * k1 + n2] = cmul(v[4 * k1 + n2], tw);
+    }
+  // second 4-point DFTs over n2 -> X[k1 + 4 k2] lands in v[4 k1 + k2]
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(v[4 * k1 + 0], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+}
+
+// One radix-16 Stockham pass for sub-transform size NS (1, 16, 256): the
+// thread's v[] holds x[j + 256 r] in natural order; twiddle, DFT16, and (if
+// STORE) scatter to buf.  Without STORE the result stays in v[d16(r)].
+template <bool INV, int NS, bool STORE>
+__device__ __forceinline__ void stockham_pass(float2 (&v)[16], float2* buf, const float2* tw) {
+  const int j = threadIdx.x;
+  const int k = j % NS;
+  if (NS > 1) {
+    const float2* t = tw + (NS == 16 ? kTw16 : kTw256) + k;
+#pragma unroll
+    for (int r = 1; r < 16; ++r) {
+      float2 w = t[(r - 1) * NS];
+      if (INV) w.y = -w.y;
+      v[r] = cmul(v[r], w);
+    }
+  }
+  dft16<INV>(v);
+  if (STORE) {
+    const int idx = (j / NS) * NS * 16 + k;
+    __syncthreads();  // every thread has read its inputs of this pass
+#pragma unroll
+    for (int r = 0; r < 16; ++r) buf[kFftPad(idx + r * NS)] = v[d16(r)];
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ void load16(float2 (&v)[16], const float2* buf) {
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = buf[kFftPad(threadIdx.x + r * kFftThreads)];
+}
+
+__global__ void __launch_bounds__(kFftThreads, 2) hilbert_fused4096_kernel(
+    SrcDesc src, long long row0, long long nrows, __half* out, int pitch, long long ps, unsigned long long* rowmin,
+    unsigned long long* rowmax, float* hbuf, double amp_floor, DevStatus* st) {
+  extern __shared__ float2 fsm[];
+  float2* buf = fsm;
+  float2* tw = fsm + kFftPad(kFftT);
+  for (int m = threadIdx.x; m < kTwCount; m += kFftThreads) {
+    int ns, kk, r;
+    if (m < kTw256) {
+      ns = 16;
+      r = 1 + m / 16;
+      kk = m % 16;
+    } else {
+      ns = 256;
+      r = 1 + (m - kTw256) / 256;
+      kk = (m - kTw256) % 256;
+    }
+    const int n = 16 * ns;  // sub-transform length after the pass
+    float s, c;
+    sincospif(-2.0f * (float)((kk * r) % n) / (float)n, &s, &c);
+    tw[m] = make_float2(c, s);
+  }
+  __shared__ float red[4][kFftThreads / 32];
+  __syncthreads();
+  const long long npairs = (nrows + 1) / 2;
+  for (long long pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
+    const long long ra = row0 + 2 * pr, rb = ra + 1;
+    const bool hasb = 2 * pr + 1 < nrows;
+    const long long oa = row_offset(src, ra), ob = hasb ? row_offset(src, rb) : 0;
+    const float* x = static_cast<const float*>(src.ptr);  // s_samp == 1 (hilbert_fused_supported)
+    const float* xpa = x + oa + threadIdx.x;
+    const float* xpb = x + ob + threadIdx.x;
+    float2 v[16];
+    float ma = 0.f, mb = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      v[q] = make_float2(__ldg(xpa + q * kFftThreads), hasb ? __ldg(xpb + q * kFftThreads) : 0.0f);
+      ma = fmaxf(ma, fabsf(v[q].x));
+      mb = fmaxf(mb, fabsf(v[q].y));
+    }
+    // Scale each row by a power of two to max |x| in [1, 2) before packing:
+    // the FFT's rounding error scales with the larger row of the pair, so
+    // rows of very different magnitude would otherwise leak error into the
+    // smaller one.  Exact (power of two) and z = a / |a| is scale-free.
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
+      mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      red[0][threadIdx.x >> 5] = ma;
+      red[1][threadIdx.x >> 5] = mb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kFftThreads / 32; ++w) {
+      ma = fmaxf(ma, red[0][w]);
+      mb = fmaxf(mb, red[1][w]);
+    }
+    int ea = 0, eb = 0;
+    if (ma > 0.f && ma <= FLT_MAX) frexpf(ma, &ea);
+    if (mb > 0.f && mb <= FLT_MAX) frexpf(mb, &eb);
+    const float sa = ldexpf(1.0f, min(126, max(-126, 1 - ea)));
+    const float sb = ldexpf(1.0f, min(126, max(-126, 1 - eb)));
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      v[q].x *= sa;
+      v[q].y *= sb;
+    }
+    // forward FFT
+    stockham_pass<false, 1, true>(v, buf, tw);
+    load16(v, buf);
+    stockham_pass<false, 16, true>(v, buf, tw);
+    load16(v, buf);
+    stockham_pass<false, 256, true>(v, buf, tw);
+    // Hilbert multiplier on the natural-order spectrum, folded into the load:
+    // -i for 0 < k < T/2, +i for T/2 < k < T, 0 at DC and Nyquist; 1/T scale
+    const float inv_t = 1.0f / (float)kFftT;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int kk = threadIdx.x + r * kFftThreads;
+      const float2 z = buf[kFftPad(kk)];
+      float2 y;
+      if (kk == 0 || kk == kFftT / 2) y = make_float2(0.f, 0.f);
+      else if (kk < kFftT / 2) y = make_float2(z.y * inv_t, -z.x * inv_t);   // -i z
+      else y = make_float2(-z.y * inv_t, z.x * inv_t);                        // +i z
+      v[r] = y;
+    }
+    // inverse FFT; the last pass leaves H_a + i H_b at t = j + 256 r in v[d16(r)]
+    stockham_pass<true, 1, true>(v, buf, tw);
+    load16(v, buf);
+    stockham_pass<true, 16, true>(v, buf, tw);
+    load16(v, buf);
+    stockham_pass<true, 256, true>(v, buf, tw);
+    // normalise both rows from (x, H in smem): 4 consecutive samples per
+    // thread and step (16-byte x loads, 8-byte plane stores), row min / max
+    float amin_a = FLT_MAX, amax_a = 0.f, amin_b = FLT_MAX, amax_b = 0.f;
+    bool bad = false;
+#pragma unroll 1
+    for (int g = 0; g < kFftT / (4 * kFftThreads); ++g) {
+      const int t0 = 4 * (threadIdx.x + g * kFftThreads);
+      float2 h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = buf[kFftPad(t0 + k)];
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        if (s == 1 && !hasb) continue;
+        const float4 x4 = *reinterpret_cast<const float4*>(x + (s == 0 ? oa : ob) + t0);
+        const float sc = s == 0 ? sa : sb;
+        const float re[4] = {x4.x * sc, x4.y * sc, x4.z * sc, x4.w * sc};
+        __half rh[4], rlo[4], ih[4], ilo[4];
+        float lo = FLT_MAX, hi = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float im = s == 0 ? h[k].x : h[k].y;
+          const float a2 = re[k] * re[k] + im * im;
+          const float inv = a2 > 0.0f ? rsqrtf(a2) : 0.0f;
+          const float a = a2 * inv;
+          const float zr = re[k] * inv, zi = im * inv;
+          rh[k] = __float2half_rn(zr);
+          ih[k] = __float2half_rn(zi);
+          rlo[k] = __float2half_rn(zr - __half2float(rh[k]));
+          ilo[k] = __float2half_rn(zi - __half2float(ih[k]));
+          if (!(a <= FLT_MAX)) bad = true;
+          lo = fminf(lo, a);
+          hi = fmaxf(hi, a);
+        }
+        __half* o = out + (s == 0 ? ra : rb) * pitch + t0;
+        *reinterpret_cast<uint2*>(o) = make_uint2(pack_half2(rh[0], rh[1]), pack_half2(rh[2], rh[3]));
+        *reinterpret_cast<uint2*>(o + ps) = make_uint2(pack_half2(rlo[0], rlo[1]), pack_half2(rlo[2], rlo[3]));
+        *reinterpret_cast<uint2*>(o + 2 * ps) = make_uint2(pack_half2(ih[0], ih[1]), pack_half2(ih[2], ih[3]));
+        *reinterpret_cast<uint2*>(o + 3 * ps) = make_uint2(pack_half2(ilo[0], ilo[1]), pack_half2(ilo[2], ilo[3]));
+        if (s == 0) {
+          amin_a = fminf(amin_a, lo);
+          amax_a = fmaxf(amax_a, hi);
+        } else {
+          amin_b = fminf(amin_b, lo);
+          amax_b = fmaxf(amax_b, hi);
+        }
+      }
+    }
+    if (bad) atomicOr(&st->flags, FLAG_NONFINITE);
+    // block min / max of both rows (the CTA owns them: plain stores)
+    float vals[4] = {amin_a, amax_a, amin_b, amax_b};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      vals[0] = fminf(vals[0], __shfl_xor_sync(0xffffffffu, vals[0], o));
+      vals[1] = fmaxf(vals[1], __shfl_xor_sync(0xffffffffu, vals[1], o));
+      vals[2] = fminf(vals[2], __shfl_xor_sync(0xffffffffu, vals[2], o));
+      vals[3] = fmaxf(vals[3], __shfl_xor_sync(0xffffffffu, vals[3], o));
+    }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) red[q][threadIdx.x >> 5] = vals[q];
+    __syncthreads();
+    __shared__ int need_flags[2];
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < kFftThreads / 32; ++w) {
+        vals[0] = fminf(vals[0], red[0][w]);
+        vals[1] = fmaxf(vals[1], red[1][w]);
+        vals[2] = fminf(vals[2], red[2][w]);
+        vals[3] = fmaxf(vals[3], red[3][w]);
+      }
+      // back to input units (exact: powers of two); the fixup decides on
+      // the min / max ratio, which the scaling leaves unchanged
+      rowmin[ra] = key_of((double)vals[0] / sa);
+      rowmax[ra] = key_of((double)vals[1] / sa);
+      need_flags[0] = (vals[0] == 0.0f) || ((double)vals[0] < amp_floor * (double)vals[1] * (1.0 + 1e-5));
+      need_flags[1] = 0;
+      if (hasb) {
+        rowmin[rb] = key_of((double)vals[2] / sb);
+        rowmax[rb] = key_of((double)vals[3] / sb);
+        need_flags[1] = (vals[2] == 0.0f) || ((double)vals[2] < amp_floor * (double)vals[3] * (1.0 + 1e-5));
+      }
+    }
+    __syncthreads();
+    // rare: keep H (input units) of a row the exact-median fixup will inspect
+    if (need_flags[0] || need_flags[1]) {
+      const float ua = 1.0f / sa, ub = 1.0f / sb;
+      for (int t = threadIdx.x; t < kFftT; t += kFftThreads) {
+        const float2 hv = buf[kFftPad(t)];
+        if (need_flags[0]) hbuf[(ra - src.h_row0) * src.T + t] = hv.x * ua;
+        if (need_flags[1]) hbuf[(rb - src.h_row0) * src.T + t] = hv.y * ub;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exact amplitude-floor fixup.  For each row: if the cheap
 // bound min|a| >= floor * max|a| holds, no sample can fall below
 // floor * median and the row is untouched (the common case: Rayleigh
@@ -539,8 +836,40 @@ cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_d
   return cudaGetLastError();
 }
 
+bool hilbert_fused_supported(const SrcDesc& src, int fmt, int cdouble, int pitch) {
+  const bool aligned = (reinterpret_cast<uintptr_t>(src.ptr) & 15u) == 0 && src.s_samp == 1 && src.s_sig % 4 == 0 &&
+                       (src.R == 1 || src.s_trial % 4 == 0) && (src.B == 1 || src.s_band % 4 == 0);
+  return src.kind == 0 && !src.is_double && !cdouble && fmt == OUT_SPLIT && src.T == kFftT && pitch == kFftT &&
+         aligned;
+}
+
+cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long nrows, void* out, int pitch,
+                                 long long plane_stride, unsigned long long* rowstat, long long rows_total,
+                                 double amp_floor, DevStatus* status, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  static int per_sm = 0, n_sms = 0;
+  if (per_sm == 0) {
+    cudaError_t e = cudaFuncSetAttribute(hilbert_fused4096_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         kFftSmemBytes);
+    if (e != cudaSuccess) return e;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hilbert_fused4096_kernel, kFftThreads, kFftSmemBytes);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  const long long npairs = (nrows + 1) / 2;
+  const long long cap = (long long)per_sm * n_sms;
+  const unsigned grid = (unsigned)(npairs < cap ? npairs : cap);
+  hilbert_fused4096_kernel<<<grid, kFftThreads, kFftSmemBytes, st>>>(
+      src, row0, nrows, static_cast<__half*>(out), pitch, plane_stride, rowstat, rowstat + rows_total,
+      static_cast<float*>(const_cast<void*>(src.hbuf)), amp_floor, status);
+  return cudaGetLastError();
+}
+
 // fmt: 0 split fp16 planes, 1 f64 planes, 2 complex interleaved (of compute type)
-#define PS_NORM_DISPATCH(KIND, FMT)                                                                    \
+#define PS_NORM_DISPATCH(KIND, FMT)                                                                  \
   do {                                                                                               \
     if (src.is_double)                                                                               \
       normalize_kernel<double, double, KIND, FMT>                                                    \

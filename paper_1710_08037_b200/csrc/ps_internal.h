@@ -96,6 +96,12 @@ cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows
                              int cdouble, int pitch, long long plane_stride, const unsigned long long* rowstat,
                              long long rows_total, int* maskcount, double amp_floor, DevStatus* status,
                              cudaStream_t st);
+// Fused Hilbert + normalise (real fp32 rows, T = 4096, split planes): writes
+// planes and row min/max; H lands in src.hbuf only for rows the fixup inspects.
+bool hilbert_fused_supported(const SrcDesc& src, int fmt, int cdouble, int pitch);
+cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long nrows, void* out, int pitch,
+                                 long long plane_stride, unsigned long long* rowstat, long long rows_total,
+                                 double amp_floor, DevStatus* status, cudaStream_t st);
 cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nrows,
                                 void* out, cudaStream_t st);
 // Eq 8 (over trials): planes [P][B*R][N][Tp] -> [P][B*T][N][Rp] + masked-trial counts

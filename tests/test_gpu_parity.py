@@ -183,6 +183,44 @@ def test_edge_shapes_real(N, T, R, prec):
     check(res, ref, prec, f"real N={N} T={T} R={R}")
 
 
+# ---------------------------------------- fused Hilbert kernel (fp32, T = 4096)
+def test_fused_hilbert_t4096_bands():
+    # odd N * R: the last row of the chunk has no partner in its FFT pair
+    x = W.c4(n_signals=37, n_samples=4096, n_trials=3, n_latent=4)
+    assert x.dtype == np.float32 and x.strides[2] == 4
+    per = [O.plv_family(x[b].astype(np.float64), input_kind="real") for b in range(x.shape[0])]
+    ref = {m: np.stack([p[m] for p in per]) for m in METRICS}
+    res = C.plv_family(x, input_kind="real", precision="split", bands=True)
+    check(res, ref, "split", "fused hilbert c4-like")
+    assert not res["plv"].meta["input_copied"]
+
+
+def test_fused_hilbert_mixed_row_scales():
+    # rows sharing one packed FFT differ by 1e10 in amplitude
+    rng = np.random.default_rng(41)
+    x = rng.standard_normal((9, 4096, 1)).astype(np.float32)
+    x = np.ascontiguousarray(x[:, :, 0])[:, :, None]
+    x[0] *= 1e6
+    x[1] *= 1e-4
+    x[4] *= 3e-30
+    ref = O.plv_family(x.astype(np.float64), input_kind="real")
+    res = C.plv_family(x, input_kind="real", precision="split")
+    check(res, ref, "split", "fused hilbert mixed scales")
+
+
+def test_fused_hilbert_amplitude_floor_fixup():
+    rng = np.random.default_rng(42)
+    x = rng.standard_normal((6, 4096)).astype(np.float32)
+    x[1, 1000:1400] = 0.0
+    x[4, 100:130] = 0.0
+    x = x[:, :, None]
+    ref = O.plv_family(x.astype(np.float64), input_kind="real", amp_floor=0.05)
+    res = C.plv_family(x, input_kind="real", precision="split", amp_floor=0.05)
+    check(res, ref, "split", "fused hilbert floor")
+    m = O.normalize_phasors(O.analytic_signal(x.astype(np.float64), axis=1), amp_floor=0.05)[1]
+    assert res["plv"].meta["n_masked_samples"] == int(m.sum())
+
+
 def test_float32_trial_fastest_layout_copies():
     # reference layout [N, T, R] row-major: samples are strided -> packing copy
     rng = np.random.default_rng(5)
