@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 2
+#define PS_ABI_VERSION 3
 
 typedef enum ps_status {
   PS_OK = 0,
@@ -38,7 +38,8 @@ typedef enum ps_status {
   PS_E_CUDA = 6,          /* CudaError                                */
   PS_E_CUFFT = 7,         /* CudaError (cuFFT)                        */
   PS_E_OOM = 8,           /* MemoryError                              */
-  PS_E_INTERNAL = 9       /* RuntimeError                             */
+  PS_E_INTERNAL = 9,      /* RuntimeError                             */
+  PS_E_SIGNAL_TOO_SHORT = 10 /* SignalTooShortError (n_samples <= order + 1) */
 } ps_status;
 
 typedef enum ps_dtype { PS_F32 = 0, PS_F64 = 1, PS_C64 = 2, PS_C128 = 3 } ps_dtype;
@@ -70,6 +71,18 @@ enum {
 };
 
 typedef struct ps_ctx ps_ctx;
+
+/* Band-pass front end for real input (decisions :121-122):
+ * reflection padding of pad_samples per side, zero-phase two-pass FIR (forward,
+ * reverse, forward, reverse; zero initial state), analytic signal of the padded
+ * record, then trim ("prior to the removal of the padding").
+ * taps: HOST pointer to n_taps = order + 1 coefficients (design_bandpass_fir).
+ * Requires n_samples > n_taps (SignalTooShort) and pad_samples < n_samples. */
+typedef struct ps_fir {
+  const double* taps;
+  int64_t n_taps;
+  int64_t pad_samples;
+} ps_fir;
 
 /* Input/output description for one call.  Shapes follow the reference
  * ArrayView [n_signals x n_samples x n_trials] plus an optional
@@ -108,6 +121,9 @@ typedef struct ps_plv_args {
    * and trial_reduce is ignored. */
   int32_t mode;
   int32_t reserved0;
+  /* Optional band-pass front end (real input only; NULL = input is already
+   * band-limited, the configs' case). */
+  const ps_fir* fir;
 } ps_plv_args;
 
 enum { PS_MODE_OVER_SAMPLES = 0, PS_MODE_OVER_TRIALS = 1 };
@@ -168,6 +184,12 @@ ps_status ps_plv_family_host(ps_ctx* ctx, const ps_plv_args* args, ps_plv_result
  * complex (c64 for f32, c128 for f64), dense [n_bands][n_trials][n_signals]
  * [n_samples].  Uses only: input, dtype, n_*, stride_*, stream. */
 ps_status ps_analytic_signal(ps_ctx* ctx, const ps_plv_args* args, void* out);
+
+/* Replaces signalprep.filter_two_pass: zero-phase two-pass
+ * FIR of real input with reflection padding, trimmed back to the input shape.
+ * Uses args->fir (required) and the input fields of args; output real of the
+ * input precision, dense [n_bands][n_trials][n_signals][n_samples]. */
+ps_status ps_filter_two_pass(ps_ctx* ctx, const ps_plv_args* args, void* out);
 
 /* Replaces signalprep.normalize_phasors: z = a/|a| with the
  * amplitude-floor mask (masked samples exactly 0+0i).  Input complex (c64 /

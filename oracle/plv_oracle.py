@@ -129,6 +129,99 @@ def normalize_phasors(a, amp_floor: float = DEFAULT_AMP_FLOOR, axis: int = 1):
     return z, mask
 
 
+# --------------------------------------------------------------------------
+# band-pass front end (design decisions :121-122)
+# --------------------------------------------------------------------------
+class InvalidBandError(OracleError):
+    """errors.py InvalidBandError -- low >= high or edges outside (0, pi)."""
+
+
+class SignalTooShortError(OracleError):
+    """errors.py SignalTooShortError -- n_samples <= order + 1."""
+
+
+def design_bandpass_fir(low: float, high: float, order: int) -> np.ndarray:
+    """SPEC.md:58-66 design_bandpass_fir, with the SPEC's design decision
+    (SPEC.md:121): windowed sinc with a Hamming window, order + 1 taps,
+    linear phase (symmetric).  Band edges in radians per sample.  The SPEC
+    asks for pass-band gain within +-1 dB of unity at the band centre; this
+    restatement scales the taps so the gain there is exactly 1 (the one
+    free normalisation choice; DESIGN.md section 8(f) #1).
+    """
+    if not (0.0 < low < high < np.pi):
+        raise InvalidBandError("band edges must satisfy 0 < low < high < pi")
+    if order <= 0 or order % 2:
+        raise ValueError("order must be a positive even integer")
+    M = int(order)
+    m = np.arange(M + 1, dtype=np.float64) - M / 2.0
+    h = np.empty(M + 1)
+    nz = m != 0
+    h[nz] = (np.sin(high * m[nz]) - np.sin(low * m[nz])) / (np.pi * m[nz])
+    h[~nz] = (high - low) / np.pi
+    h *= 0.54 - 0.46 * np.cos(2.0 * np.pi * np.arange(M + 1) / M)
+    wc = 0.5 * (low + high)
+    g = abs(np.sum(h * np.exp(-1j * wc * np.arange(M + 1))))
+    return h / g
+
+
+def reflect_pad(x, pad: int, axis: int = 1) -> np.ndarray:
+    """reflection padding of `pad` samples on each side
+    (numpy 'reflect': the edge sample is not repeated).  pad < n_samples."""
+    x = np.asarray(x, dtype=np.float64)
+    if pad >= x.shape[axis]:
+        raise SignalTooShortError("reflection padding needs pad < n_samples")
+    widths = [(0, 0)] * x.ndim
+    widths[axis] = (pad, pad)
+    return np.pad(x, widths, mode="reflect")
+
+
+def _fir_causal(x, taps, axis):
+    """Causal FIR with zero initial state: y[n] = sum_k h[k] x[n-k], len(y) = len(x)."""
+    xm = np.moveaxis(x, axis, -1)
+    L = xm.shape[-1]
+    flat = xm.reshape(-1, L)
+    out = np.empty_like(flat)
+    for r in range(flat.shape[0]):
+        out[r] = np.convolve(flat[r], taps)[:L]
+    return np.moveaxis(out.reshape(xm.shape), -1, axis)
+
+
+def two_pass_padded(x, taps, pad: int, axis: int = 1) -> np.ndarray:
+    """SPEC.md:67-75 filter_two_pass on the reflection-padded record, padding
+    kept: forward pass, reverse, second pass, reverse (zero phase, |H|^2)."""
+    taps = np.asarray(taps, dtype=np.float64)
+    T = np.asarray(x).shape[axis]
+    if T <= taps.size:  # n_samples <= order + 1
+        raise SignalTooShortError("n_samples must exceed order + 1")
+    xp = reflect_pad(x, pad, axis)
+    y = _fir_causal(xp, taps, axis)
+    y = np.flip(_fir_causal(np.flip(y, axis), taps, axis), axis)
+    return y
+
+
+def _trim(y, pad, T, axis):
+    sl = [slice(None)] * y.ndim
+    sl[axis] = slice(pad, pad + T)
+    return y[tuple(sl)]
+
+
+def filter_two_pass(x, taps, pad: int, axis: int = 1) -> np.ndarray:
+    """zero-phase two-pass FIR with reflection padding
+    (SPEC.md:122), output trimmed back to the input's shape."""
+    T = np.asarray(x).shape[axis]
+    return np.ascontiguousarray(_trim(two_pass_padded(x, taps, pad, axis), pad, T, axis))
+
+
+def bandpass_analytic(x, taps, pad: int, axis: int = 1) -> np.ndarray:
+    """The real-input front end of cmd_connectivity: band-pass
+    (two-pass, reflection padded) -> analytic signal of the PADDED record ->
+    trim ("the analytical signal was calculated prior to the removal of the
+    padding", SPEC.md:77,122)."""
+    T = np.asarray(x).shape[axis]
+    a = analytic_signal(two_pass_padded(x, taps, pad, axis), axis)
+    return np.ascontiguousarray(_trim(a, pad, T, axis))
+
+
 def phasors_from_unit(z, axis: int = 1):
     """PhasorEpochs given directly (plv_matrix input): mask = (z == 0)."""
     z = np.asarray(z).astype(np.complex128, copy=False)
@@ -240,17 +333,21 @@ def plv_family_from_phasors(z, mask, trial_reduce: str = "mean", raw: bool = Fal
 
 
 def plv_family(x, input_kind: str = "real", amp_floor: float = DEFAULT_AMP_FLOOR,
-               trial_reduce: str = "mean", raw: bool = False):
-    """The whole hot path: [analytic ->] normalise -> Gram -> PLV/iPLV/ciPLV.
+               trial_reduce: str = "mean", raw: bool = False, fir=None):
+    """The whole hot path: [band-pass ->] [analytic ->] normalise -> Gram ->
+    PLV/iPLV/ciPLV.
 
     x: [N, T, R] (a 2-D [N, T] array is treated as one trial).
     input_kind: 'real' (SPEC.md:76), 'analytic' (SPEC.md:85) or 'phasor'
-    (SPEC.md:186).
+    (SPEC.md:186).  fir: optional (taps, pad_samples) for real input -> the
+    band-pass front end bandpass_analytic.
     """
     x = np.asarray(x)
     if x.ndim == 2:
         x = x[:, :, None]
-    if input_kind == "real":
+    if input_kind == "real" and fir is not None:
+        z, mask = normalize_phasors(bandpass_analytic(x, fir[0], int(fir[1])), amp_floor)
+    elif input_kind == "real":
         z, mask = normalize_phasors(analytic_signal(x), amp_floor)
     elif input_kind == "analytic":
         z, mask = normalize_phasors(x, amp_floor)

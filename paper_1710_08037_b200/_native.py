@@ -17,7 +17,7 @@ from pathlib import Path
 from . import errors
 
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # ps_status -> exception class (include/phasesync.h)
 PS_OK = 0
@@ -31,6 +31,7 @@ STATUS_EXC = {
     7: errors.CudaError,
     8: MemoryError,
     9: RuntimeError,
+    10: errors.SignalTooShortError,
 }
 
 DTYPES = {"f32": 0, "f64": 1, "c64": 2, "c128": 3}
@@ -39,6 +40,16 @@ PRECISIONS = {"split": 0, "f16x3": 0, "fp64": 1}
 TRIAL_REDUCE = {"mean": 0, "none": 1, "pool": 2}
 METRIC_BITS = {"plv": 1, "iplv": 2, "ciplv": 4, "cre": 8, "cim": 16}
 METRIC_ORDER = ("plv", "iplv", "ciplv", "cre", "cim")
+
+
+class Fir(ctypes.Structure):
+    """Mirror of ps_fir (band-pass front end; taps is a HOST pointer)."""
+
+    _fields_ = [
+        ("taps", ctypes.POINTER(ctypes.c_double)),
+        ("n_taps", ctypes.c_int64),
+        ("pad_samples", ctypes.c_int64),
+    ]
 
 
 class PlvArgs(ctypes.Structure):
@@ -70,6 +81,7 @@ class PlvArgs(ctypes.Structure):
         ("stream", ctypes.c_void_p),
         ("mode", ctypes.c_int32),
         ("reserved0", ctypes.c_int32),
+        ("fir", ctypes.POINTER(Fir)),
     ]
 
 
@@ -104,6 +116,7 @@ _SIGNATURES = {
     "ps_plv_family_staged": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult), ctypes.c_int32,
                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "ps_analytic_signal": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p], ctypes.c_int),
+    "ps_filter_two_pass": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p], ctypes.c_int),
     "ps_normalize_phasors": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p, ctypes.c_void_p],
                              ctypes.c_int),
     "ps_pair_shard": ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64],

@@ -54,7 +54,8 @@ def _infer_kind(code: str, input_kind: str | None) -> str:
 def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("plv", "iplv", "ciplv"),
                precision: str = "split", trial_reduce: str = "mean", amp_floor: float = 1e-6,
                bands: bool = False, shard: tuple[int, int] = (0, 1), out: dict | None = None,
-               timing: bool = False, stages=None, mode: str = "over_samples") -> dict:
+               timing: bool = False, stages=None, mode: str = "over_samples", fir=None,
+               pad_samples: int = 0) -> dict:
     """All requested PLV-family metrics from one Gram per trial.
 
     x: RealEpochs / AnalyticEpochs / PhasorEpochs data, shape [N, T], [N, T, R]
@@ -74,6 +75,11 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     mode: 'over_samples' (Eq 7, default) or 'over_trials' (Eq 8: time-resolved,
        one matrix per sample from the Gram over trials; values [N, N, T],
        trial_reduce ignored).
+    fir, pad_samples: optional band-pass front end for real input (a
+       signalprep.FirFilter or taps): two-pass zero-phase FIR on the record
+       reflection-padded by pad_samples, analytic signal before the trim
+       (SURVEY 3.2, 8(f) #1), fused into the Hilbert
+       stage of the same call.
     Returns {metric: ConnectivityMatrix}.
     """
     if mode not in ("over_samples", "over_trials"):
@@ -111,6 +117,12 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     a.trial_reduce = _native.TRIAL_REDUCE[trial_reduce]
     a.shard_index, a.shard_count = int(shard[0]), int(shard[1])
     a.mode = 1 if over_trials else 0
+    fir_keep = None
+    if fir is not None:
+        from .signalprep import fir_struct
+
+        fs, fir_keep = fir_struct(fir, pad_samples)
+        a.fir = ctypes.pointer(fs)
 
     outs = {}
     if d.on_device:

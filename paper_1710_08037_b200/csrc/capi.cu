@@ -78,6 +78,7 @@ struct ps_ctx {
   std::mutex mu;
   std::map<PlanKey, cufftHandle> plans;
   Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout, refine, refine_sorted, planes_t, maskcount_t;
+  Buf fir_taps, fir_spec;  // band-pass front end: padded taps, filter spectrum (double)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
   std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
@@ -156,6 +157,17 @@ ps_status validate(const ps_plv_args* a, Geometry& g) {
   if (!(a->amp_floor >= 0.0)) return fail(PS_E_INVALID, "amp_floor must be >= 0");
   if (a->n_signals > (1 << 30) || a->n_samples > (1LL << 31) - 1)
     return fail(PS_E_SHAPE, "n_signals / n_samples exceed the supported range");
+  if (a->fir) {
+    if (a->input_kind != PS_INPUT_REAL) return fail(PS_E_INVALID, "the band-pass front end applies to real input");
+    if (!a->fir->taps || a->fir->n_taps < 1) return fail(PS_E_INVALID, "fir: taps missing");
+    if (a->fir->pad_samples < 0) return fail(PS_E_INVALID, "fir: pad_samples must be >= 0");
+    if (a->n_samples <= a->fir->n_taps)
+      return fail(PS_E_SIGNAL_TOO_SHORT, "n_samples must exceed order + 1 (SPEC.md:69)");
+    if (a->fir->pad_samples >= a->n_samples)
+      return fail(PS_E_SIGNAL_TOO_SHORT, "reflection padding needs pad_samples < n_samples (SPEC.md:122)");
+    if (a->n_samples + 2 * a->fir->pad_samples + a->fir->n_taps > (1LL << 30))
+      return fail(PS_E_SHAPE, "padded record length exceeds the supported range");
+  }
   g.B = a->n_bands;
   g.N = a->n_signals;
   g.T = a->n_samples;
@@ -185,6 +197,7 @@ SrcDesc make_src(const ps_plv_args* a, const Geometry& g, const void* ptr) {
   s.s_band = a->stride_band;
   s.hbuf = nullptr;
   s.h_row0 = 0;
+  s.h_ld = g.T;
   return s;
 }
 
@@ -275,6 +288,129 @@ ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cons
   return PS_OK;
 }
 
+// ---- band-pass front end (DESIGN.md 8(f) #1) -------
+// Record of length L = T + 2 pad (reflection padded), filtered by the two-pass
+// FIR evaluated spectrally on Lf >= L + n_taps - 1 (no wrap-around), then the
+// analytic signal of the padded record (length-L Hilbert), trimmed to T.
+struct FirGeom {
+  long long P = 0, L = 0, Lf = 0, nt = 0;
+};
+
+long long next_fast_len(long long n) {  // smallest 2^a 3^b 5^c 7^d >= n
+  for (long long m = std::max(n, 1LL);; ++m) {
+    long long r = m;
+    for (long long f : {2LL, 3LL, 5LL, 7LL})
+      while (r % f == 0) r /= f;
+    if (r == 1) return m;
+  }
+}
+
+FirGeom fir_geom(const ps_plv_args* a, const Geometry& g) {
+  FirGeom f;
+  f.P = a->fir->pad_samples;
+  f.nt = a->fir->n_taps;
+  f.L = g.T + 2 * f.P;
+  f.Lf = next_fast_len(f.L + f.nt - 1);
+  return f;
+}
+
+long long prep_chunk_rows(const ps_plv_args* a, const Geometry& g) {
+  if (a->fir) {
+    const long long rc = (1LL << 27) / fir_geom(a, g).Lf;
+    return std::max(1LL, std::min(rc, g.rows));
+  }
+  return hilbert_chunk_rows(g);
+}
+
+// Call-scope preparation of the real-input stage: size the workspace once
+// for the largest chunk (no reallocation between pipelined stages) and, with
+// a band-pass front end, the filter spectrum Hf = FFT_Lf(taps) in double.
+ps_status prep_begin(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cudaStream_t st) {
+  if (a->input_kind != PS_INPUT_REAL) return PS_OK;
+  const size_t es = g.cdouble ? 8 : 4;
+  const long long rc = std::min(prep_chunk_rows(a, g), g.rows);
+  if (!a->fir) {
+    PS_TRY(ensure(c->spec, (size_t)rc * (g.T / 2 + 1) * 2 * es));
+    PS_TRY(ensure(c->hbuf, (size_t)rc * g.T * es));
+    PS_TRY(ensure(c->xw, (size_t)rc * g.T * es));
+    return PS_OK;
+  }
+  const FirGeom f = fir_geom(a, g);
+  PS_TRY(ensure(c->xw, (size_t)rc * f.Lf * es));
+  PS_TRY(ensure(c->spec, (size_t)rc * (f.Lf / 2 + 1) * 2 * es));
+  PS_TRY(ensure(c->hbuf, (size_t)rc * f.L * es));
+  PS_TRY(ensure(c->fir_taps, (size_t)f.Lf * sizeof(double)));
+  PS_TRY(ensure(c->fir_spec, (size_t)(f.Lf / 2 + 1) * 2 * sizeof(double)));
+  PS_CUDA(cudaMemsetAsync(c->fir_taps.p, 0, (size_t)f.Lf * sizeof(double), st));
+  PS_CUDA(cudaMemcpyAsync(c->fir_taps.p, a->fir->taps, (size_t)f.nt * sizeof(double), cudaMemcpyHostToDevice, st));
+  cufftHandle h;
+  PS_TRY(get_plan(c, (int)f.Lf, 1, f.Lf, true, 0, &h));
+  PS_CUFFT(cufftSetStream(h, st));
+  PS_CUFFT(cufftExecD2Z(h, (cufftDoubleReal*)c->fir_taps.p, (cufftDoubleComplex*)c->fir_spec.p));
+  return PS_OK;
+}
+
+// Band-pass stage for rows [row0, row0+nr): c->xw rows (stride Lf) hold the
+// filtered padded record; with `hilbert`, c->hbuf rows (stride L) hold its
+// Hilbert transform.  *fs describes the trimmed (x_f, H) pair for the
+// normalisation kernels (row r -> xw[(r - row0) * Lf + P + t]).
+ps_status bandpass_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const SrcDesc& src, long long row0,
+                         long long nr, bool hilbert, cudaStream_t st, SrcDesc* fs) {
+  const FirGeom f = fir_geom(a, g);
+  const size_t es = g.cdouble ? 8 : 4;
+  const int dbl = g.cdouble ? 1 : 0;
+  const long long nbf = f.Lf / 2 + 1;
+  PS_CUDA(launch_reflect_pad(src, row0, nr, f.P, f.L, f.Lf, c->xw.p, dbl, st));
+  cufftHandle fwd, inv;
+  PS_TRY(get_plan(c, (int)f.Lf, nr, f.Lf, g.cdouble, 0, &fwd));
+  PS_TRY(get_plan(c, (int)f.Lf, nr, f.Lf, g.cdouble, 1, &inv));
+  PS_CUFFT(cufftSetStream(fwd, st));
+  PS_CUFFT(cufftSetStream(inv, st));
+  auto r2c = [&](cufftHandle h, void* in) -> cufftResult {
+    return dbl ? cufftExecD2Z(h, (cufftDoubleReal*)in, (cufftDoubleComplex*)c->spec.p)
+               : cufftExecR2C(h, (cufftReal*)in, (cufftComplex*)c->spec.p);
+  };
+  auto c2r = [&](cufftHandle h, void* out) -> cufftResult {
+    return dbl ? cufftExecZ2D(h, (cufftDoubleComplex*)c->spec.p, (cufftDoubleReal*)out)
+               : cufftExecC2R(h, (cufftComplex*)c->spec.p, (cufftReal*)out);
+  };
+  const double inv_lf = 1.0 / (double)f.Lf;
+  // pass 1: y1 = h * xp, truncated to L samples (zero initial state)
+  PS_CUFFT(r2c(fwd, c->xw.p));
+  PS_CUDA(launch_spectrum_mul(c->spec.p, nr, nbf, c->fir_spec.p, 0, inv_lf, dbl, st));
+  PS_CUFFT(c2r(inv, c->xw.p));
+  PS_CUDA(launch_zero_tail(c->xw.p, nr, f.L, f.Lf, dbl, st));
+  // pass 2 on the reversed record == correlation with h: spectrum * conj(Hf)
+  PS_CUFFT(r2c(fwd, c->xw.p));
+  PS_CUDA(launch_spectrum_mul(c->spec.p, nr, nbf, c->fir_spec.p, 1, inv_lf, dbl, st));
+  PS_CUFFT(c2r(inv, c->xw.p));
+  c->launches += 5;
+  if (hilbert) {  // analytic signal of the padded record (length L), before the trim
+    cufftHandle fl, il;
+    PS_TRY(get_plan(c, (int)f.L, nr, f.Lf, g.cdouble, 0, &fl));
+    PS_TRY(get_plan(c, (int)f.L, nr, f.L, g.cdouble, 1, &il));
+    PS_CUFFT(cufftSetStream(fl, st));
+    PS_CUFFT(cufftSetStream(il, st));
+    PS_CUFFT(r2c(fl, c->xw.p));
+    PS_CUDA(launch_hilbert_spectrum(c->spec.p, nr, (int)f.L, dbl, st));
+    PS_CUFFT(c2r(il, c->hbuf.p));
+    c->launches++;
+  }
+  SrcDesc s = src;
+  s.ptr = static_cast<const char*>(c->xw.p) + (f.P - row0 * f.Lf) * (long long)es;
+  s.kind = 0;
+  s.is_double = dbl;
+  s.s_sig = f.Lf;
+  s.s_samp = 1;
+  s.s_trial = g.N * f.Lf;
+  s.s_band = g.R * g.N * f.Lf;
+  s.hbuf = static_cast<const char*>(c->hbuf.p) + f.P * (long long)es;
+  s.h_row0 = row0;
+  s.h_ld = f.L;
+  *fs = s;
+  return PS_OK;
+}
+
 // PS_HILBERT=cufft forces the cuFFT chain where the fused kernel applies
 bool hilbert_fused_enabled() {
   static const bool on = [] {
@@ -325,11 +461,22 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
     if (fmt != 2) return out;
     return static_cast<char*>(out) + (size_t)row0 * g.T * 2 * ces;
   };
-  const long long rc = a->input_kind == PS_INPUT_REAL ? hilbert_chunk_rows(g) : (row_hi - row_lo);
-  const bool fused = a->input_kind == PS_INPUT_REAL && hilbert_fused_enabled() &&
+  const long long rc = a->input_kind == PS_INPUT_REAL ? prep_chunk_rows(a, g) : (row_hi - row_lo);
+  const bool bandpass = a->input_kind == PS_INPUT_REAL && a->fir;
+  const bool fused = a->input_kind == PS_INPUT_REAL && !bandpass && hilbert_fused_enabled() &&
                      hilbert_fused_supported(src, fmt, g.cdouble ? 1 : 0, (int)pitch);
   for (long long row0 = row_lo; row0 < row_hi; row0 += rc) {
     const long long nr = std::min(rc, row_hi - row0);
+    if (bandpass) {  // Hf was computed by prep_begin for this call
+      SrcDesc fs;
+      PS_TRY(bandpass_chunk(c, a, g, src, row0, nr, true, st, &fs));
+      PS_CUDA(launch_normalize_fmt(fs, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
+                                   c->d_status, st));
+      PS_CUDA(launch_fixup_fmt(fs, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
+                               static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
+      c->launches += 2;
+      continue;
+    }
     if (fused) {
       // one kernel: FFT -> multiplier -> IFFT -> normalise; H is kept (in
       // hbuf) only for rows the exact-median fixup will inspect
@@ -361,6 +508,7 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
 ps_status prepare_phasors(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const void* in_ptr, void* out,
                           int fmt, long long pitch, long long plane_stride, cudaStream_t st, bool* copied) {
   PS_TRY(init_row_state(c, g, st));
+  PS_TRY(prep_begin(c, a, g, st));
   return prepare_rows(c, a, g, in_ptr, out, fmt, pitch, plane_stride, 0, g.rows, st, copied);
 }
 
@@ -746,13 +894,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     int q = 0;
     for (int m = 0; m < 5; ++m) k.outs[m] = houts[m] ? static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes : nullptr;
   }
-  if (a->input_kind == PS_INPUT_REAL) {  // size the Hilbert workspace once (no realloc mid-pipeline)
-    const size_t es = g.cdouble ? 8 : 4;
-    const long long rc = std::min(hilbert_chunk_rows(g), g.rows);
-    PS_TRY(ensure(c->spec, (size_t)rc * (g.T / 2 + 1) * 2 * es));
-    PS_TRY(ensure(c->hbuf, (size_t)rc * g.T * es));
-    PS_TRY(ensure(c->xw, (size_t)rc * g.T * es));
-  }
+  PS_TRY(prep_begin(c, a, g, si));  // Hilbert workspace sized once (no realloc mid-pipeline)
   PS_TRY(reset_status(c, si));
   PS_TRY(init_row_state(c, g, si));
   PS_TRY(plan_call(c, a, k, cols, /*force_g1=*/true, si));
@@ -891,7 +1033,8 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   cudaSetDevice(c->device);
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
-                 &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t})
+                 &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
+                 &c->fir_spec})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1002,13 +1145,7 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
   bool copied = false;
   const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
   PS_TRY(ensure(c->planes, plane_bytes));
-  if (a->input_kind == PS_INPUT_REAL) {  // size the Hilbert workspace once (no realloc mid-stage)
-    const size_t es = g.cdouble ? 8 : 4;
-    const long long rc = std::min(hilbert_chunk_rows(g), g.rows);
-    PS_TRY(ensure(c->spec, (size_t)rc * (g.T / 2 + 1) * 2 * es));
-    PS_TRY(ensure(c->hbuf, (size_t)rc * g.T * es));
-    PS_TRY(ensure(c->xw, (size_t)rc * g.T * es));
-  }
+  PS_TRY(prep_begin(c, a, g, st));  // Hilbert workspace sized once (no realloc mid-stage)
   PS_TRY(reset_status(c, st));
   PS_TRY(init_row_state(c, g, st));
   PS_TRY(plan_call(c, a, k, cols, /*force_g1=*/true, st));
@@ -1116,16 +1253,50 @@ ps_status ps_analytic_signal(ps_ctx* c, const ps_plv_args* a0, void* out) {
   SrcDesc src = make_src(&a, g, a.input);
   bool copied = false;
   PS_TRY(reset_status(c, st));
-  const long long rc = hilbert_chunk_rows(g);
+  PS_TRY(prep_begin(c, &a, g, st));
+  const long long rc = prep_chunk_rows(&a, g);
   const size_t es = g.cdouble ? 8 : 4;
   for (long long row0 = 0; row0 < g.rows; row0 += rc) {
     const long long nr = std::min(rc, g.rows - row0);
-    PS_TRY(hilbert_chunk(c, &a, g, src, row0, nr, st, &copied));
-    src.hbuf = c->hbuf.p;
-    src.h_row0 = row0;
-    PS_CUDA(launch_analytic_out(src, row0, nr, static_cast<char*>(out) + (size_t)row0 * g.T * 2 * es, st));
+    SrcDesc s = src;
+    if (a.fir) {
+      PS_TRY(bandpass_chunk(c, &a, g, src, row0, nr, true, st, &s));
+    } else {
+      PS_TRY(hilbert_chunk(c, &a, g, src, row0, nr, st, &copied));
+      s.hbuf = c->hbuf.p;
+      s.h_row0 = row0;
+    }
+    PS_CUDA(launch_analytic_out(s, row0, nr, static_cast<char*>(out) + (size_t)row0 * g.T * 2 * es, st));
   }
   return read_status(c, st);
+}
+
+ps_status ps_filter_two_pass(ps_ctx* c, const ps_plv_args* a0, void* out) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  if (!out) return fail(PS_E_INVALID, "out is NULL");
+  if (!a0 || !a0->fir) return fail(PS_E_INVALID, "args->fir is required");
+  std::lock_guard<std::mutex> lock(c->mu);
+  ps_plv_args a = *a0;
+  a.input_kind = PS_INPUT_REAL;
+  a.precision = PS_PREC_SPLIT_F16X3;  // compute type follows the input dtype
+  Geometry g;
+  PS_TRY(validate(&a, g));
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(a.stream);
+  const SrcDesc src = make_src(&a, g, a.input);
+  PS_TRY(prep_begin(c, &a, g, st));
+  const FirGeom f = fir_geom(&a, g);
+  const long long rc = prep_chunk_rows(&a, g);
+  const size_t es = g.cdouble ? 8 : 4;
+  for (long long row0 = 0; row0 < g.rows; row0 += rc) {
+    const long long nr = std::min(rc, g.rows - row0);
+    SrcDesc s;
+    PS_TRY(bandpass_chunk(c, &a, g, src, row0, nr, false, st, &s));
+    PS_CUDA(launch_trim_rows(c->xw.p, nr, f.Lf, f.P, g.T, static_cast<char*>(out) + (size_t)row0 * g.T * es,
+                             g.cdouble ? 1 : 0, st));
+  }
+  PS_CUDA(cudaStreamSynchronize(st));
+  return PS_OK;
 }
 
 ps_status ps_normalize_phasors(ps_ctx* c, const ps_plv_args* a, void* out, uint8_t* mask_out) {

@@ -36,7 +36,7 @@ __device__ __forceinline__ void load_a(const SrcDesc& s, long long roff, long lo
                                        S& im) {
   if (KIND == 0) {
     re = static_cast<S>(static_cast<const IT*>(s.ptr)[roff + t * s.s_samp]);
-    im = static_cast<const S*>(s.hbuf)[(r - s.h_row0) * s.T + t];
+    im = static_cast<const S*>(s.hbuf)[(r - s.h_row0) * s.h_ld + t];
   } else {
     const IT* p = static_cast<const IT*>(s.ptr) + 2 * (roff + t * s.s_samp);
     re = static_cast<S>(p[0]);
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
       if (KIND == 0) {
         const float4 x = *reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + roff + t0);
         const float4 h = *reinterpret_cast<const float4*>(static_cast<const float*>(src.hbuf) +
-                                                          (r - src.h_row0) * T + t0);
+                                                          (r - src.h_row0) * src.h_ld + t0);
         re[0] = x.x; re[1] = x.y; re[2] = x.z; re[3] = x.w;
         im[0] = h.x; im[1] = h.y; im[2] = h.z; im[3] = h.w;
       } else {
@@ -547,8 +547,8 @@ __global__ void __launch_bounds__(kFftThreads, 2) hilbert_fused4096_kernel(
       const float ua = 1.0f / sa, ub = 1.0f / sb;
       for (int t = threadIdx.x; t < kFftT; t += kFftThreads) {
         const float2 hv = buf[kFftPad(t)];
-        if (need_flags[0]) hbuf[(ra - src.h_row0) * src.T + t] = hv.x * ua;
-        if (need_flags[1]) hbuf[(rb - src.h_row0) * src.T + t] = hv.y * ub;
+        if (need_flags[0]) hbuf[(ra - src.h_row0) * src.h_ld + t] = hv.x * ua;
+        if (need_flags[1]) hbuf[(rb - src.h_row0) * src.h_ld + t] = hv.y * ub;
       }
     }
     __syncthreads();
@@ -811,7 +811,111 @@ int grid_for(long long n, int threads) {
   return static_cast<int>(g);
 }
 
+// ---------------------------------------------------------------------------
+// Band-pass front end (DESIGN.md section 8(f) #1).
+// The two-pass zero-phase FIR is evaluated spectrally on FFT length Lf >=
+// L + n_taps - 1 (L = T + 2 pad): linear convolution without wrap-around,
+// the first pass truncated to L samples exactly as the time-domain filter
+// with zero initial state leaves it.
+// ---------------------------------------------------------------------------
+// xp[rl][i] = reflect-padded x (numpy 'reflect') for i < L, 0 for L <= i < Lf
+template <typename IT, typename S>
+__global__ void reflect_pad_kernel(SrcDesc src, long long row0, long long nrows, long long pad, long long L,
+                                   long long Lf, S* xp) {
+  const long long total = nrows * Lf;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long rl = e / Lf, i = e % Lf;
+    S v = S(0);
+    if (i < L) {
+      long long j = i - pad;
+      if (j < 0) j = -j;
+      if (j >= src.T) j = 2 * (src.T - 1) - j;
+      const long long roff = row_offset(src, row0 + rl);
+      v = static_cast<S>(static_cast<const IT*>(src.ptr)[roff + j * src.s_samp]);
+    }
+    xp[e] = v;
+  }
+}
+
+// spec[rl][k] *= (conj ? conj(Hf[k]) : Hf[k]) * scale
+template <typename C>
+__global__ void spectrum_mul_kernel(C* spec, long long nrows, long long nb, const double2* Hf, int conj,
+                                    double scale) {
+  using S = decltype(spec->x);
+  const long long total = nrows * nb;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double2 h = Hf[e % nb];
+    const S hr = static_cast<S>(h.x * scale), hi = static_cast<S>((conj ? -h.y : h.y) * scale);
+    const C v = spec[e];
+    C y;
+    y.x = v.x * hr - v.y * hi;
+    y.y = v.x * hi + v.y * hr;
+    spec[e] = y;
+  }
+}
+
+// y[rl][i] = 0 for L <= i < Lf (first-pass truncation)
+template <typename S>
+__global__ void zero_tail_kernel(S* y, long long nrows, long long L, long long Lf) {
+  const long long w = Lf - L;
+  const long long total = nrows * w;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    y[(e / w) * Lf + L + e % w] = S(0);
+}
+
+// out[rl][t] = y[rl][pad + t] (dense trimmed rows)
+template <typename S>
+__global__ void trim_rows_kernel(const S* y, long long nrows, long long ld, long long pad, long long T, S* out) {
+  const long long total = nrows * T;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    out[e] = y[(e / T) * ld + pad + e % T];
+}
+
 }  // namespace
+
+cudaError_t launch_reflect_pad(const SrcDesc& src, long long row0, long long nrows, long long pad, long long L,
+                               long long Lf, void* xp, int dst_double, cudaStream_t st) {
+  const int g = grid_for(nrows * Lf, 256);
+  if (src.is_double) {
+    if (!dst_double) return cudaErrorInvalidValue;
+    reflect_pad_kernel<double, double><<<g, 256, 0, st>>>(src, row0, nrows, pad, L, Lf, (double*)xp);
+  } else if (dst_double) {
+    reflect_pad_kernel<float, double><<<g, 256, 0, st>>>(src, row0, nrows, pad, L, Lf, (double*)xp);
+  } else {
+    reflect_pad_kernel<float, float><<<g, 256, 0, st>>>(src, row0, nrows, pad, L, Lf, (float*)xp);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_spectrum_mul(void* spec, long long nrows, long long nb, const void* Hf, int conj, double scale,
+                                int is_double, cudaStream_t st) {
+  const int g = grid_for(nrows * nb, 256);
+  if (is_double)
+    spectrum_mul_kernel<double2><<<g, 256, 0, st>>>((double2*)spec, nrows, nb, (const double2*)Hf, conj, scale);
+  else
+    spectrum_mul_kernel<float2><<<g, 256, 0, st>>>((float2*)spec, nrows, nb, (const double2*)Hf, conj, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_tail(void* y, long long nrows, long long L, long long Lf, int is_double, cudaStream_t st) {
+  if (Lf <= L) return cudaSuccess;
+  const int g = grid_for(nrows * (Lf - L), 256);
+  if (is_double) zero_tail_kernel<double><<<g, 256, 0, st>>>((double*)y, nrows, L, Lf);
+  else zero_tail_kernel<float><<<g, 256, 0, st>>>((float*)y, nrows, L, Lf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trim_rows(const void* y, long long nrows, long long ld, long long pad, long long T, void* out,
+                             int is_double, cudaStream_t st) {
+  const int g = grid_for(nrows * T, 256);
+  if (is_double) trim_rows_kernel<double><<<g, 256, 0, st>>>((const double*)y, nrows, ld, pad, T, (double*)out);
+  else trim_rows_kernel<float><<<g, 256, 0, st>>>((const float*)y, nrows, ld, pad, T, (float*)out);
+  return cudaGetLastError();
+}
 
 // ---------------------------------------------------------------------------
 // launchers
@@ -890,7 +994,9 @@ cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long n
                                  long long rows_total, DevStatus* status, cudaStream_t st) {
   // vectorised fast path: fp32 source, split planes, contiguous 16B-aligned rows
   {
-    const bool aligned_base = (reinterpret_cast<uintptr_t>(src.ptr) & 15u) == 0;
+    const bool aligned_base = (reinterpret_cast<uintptr_t>(src.ptr) & 15u) == 0 &&
+                              (src.kind != 0 || ((reinterpret_cast<uintptr_t>(src.hbuf) & 15u) == 0 &&
+                                                 src.h_ld % 4 == 0));
     const long long q = src.kind == 0 ? 4 : 2;  // row offsets must be 16-byte multiples
     const bool strides_ok = (src.s_sig % q == 0) && (src.R == 1 || src.s_trial % q == 0) &&
                             (src.B == 1 || src.s_band % q == 0);

@@ -38,6 +38,7 @@ struct SrcDesc {
   long long s_sig, s_samp, s_trial, s_band;   // element strides
   const void* hbuf;          // H{x} for real input: [rows_in_chunk][T] scalar
   long long h_row0;          // first row held in hbuf
+  long long h_ld;            // hbuf row stride (elements; T unless band-pass padded)
 };
 
 // An ill-conditioned ciPLV value of the split path queued for exact FP64
@@ -102,6 +103,14 @@ bool hilbert_fused_supported(const SrcDesc& src, int fmt, int cdouble, int pitch
 cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long nrows, void* out, int pitch,
                                  long long plane_stride, unsigned long long* rowstat, long long rows_total,
                                  double amp_floor, DevStatus* status, cudaStream_t st);
+// Band-pass front end (two-pass FIR evaluated spectrally on length Lf)
+cudaError_t launch_reflect_pad(const SrcDesc& src, long long row0, long long nrows, long long pad, long long L,
+                               long long Lf, void* xp, int dst_double, cudaStream_t st);
+cudaError_t launch_spectrum_mul(void* spec, long long nrows, long long nb, const void* Hf, int conj, double scale,
+                                int is_double, cudaStream_t st);
+cudaError_t launch_zero_tail(void* y, long long nrows, long long L, long long Lf, int is_double, cudaStream_t st);
+cudaError_t launch_trim_rows(const void* y, long long nrows, long long ld, long long pad, long long T, void* out,
+                             int is_double, cudaStream_t st);
 cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nrows,
                                 void* out, cudaStream_t st);
 // Eq 8 (over trials): planes [P][B*R][N][Tp] -> [P][B*T][N][Rp] + masked-trial counts

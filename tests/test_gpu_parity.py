@@ -183,6 +183,76 @@ def test_edge_shapes_real(N, T, R, prec):
     check(res, ref, prec, f"real N={N} T={T} R={R}")
 
 
+# ------------------------------------ band-pass front end
+def _fir(order=300, lo=0.1, hi=0.2):
+    return signalprep.design_bandpass_fir((lo * np.pi, hi * np.pi), order)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_filter_two_pass_matches_oracle(dt):
+    rng = np.random.default_rng(31)
+    x = rng.standard_normal((5, 1500, 2)).astype(dt)
+    f = _fir()
+    y = signalprep.filter_two_pass(x, f, 400)
+    ref = O.filter_two_pass(x.astype(np.float64), f.taps, 400)
+    assert y.dtype == dt and y.shape == x.shape
+    e = maxerr(y, ref) / np.max(np.abs(ref))
+    print(f"[parity] filter_two_pass {np.dtype(dt).name} rel={e:.3e}")
+    assert e <= (1e-12 if dt is np.float64 else 2e-6)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_bandpass_analytic_matches_oracle(dt):
+    rng = np.random.default_rng(32)
+    x = rng.standard_normal((4, 2001, 3)).astype(dt)
+    f = _fir(order=200)
+    a = signalprep.analytic_signal(x, fir=f, pad_samples=333).data
+    ref = O.bandpass_analytic(x.astype(np.float64), f.taps, 333)
+    e = float(np.max(np.abs(a.astype(np.complex128) - ref)) / np.max(np.abs(ref)))
+    print(f"[parity] bandpass analytic {np.dtype(dt).name} rel={e:.3e}")
+    assert e <= (1e-12 if dt is np.float64 else 2e-6)
+    # Re(a) is the filtered record
+    assert maxerr(a.real, O.filter_two_pass(x.astype(np.float64), f.taps, 333)) <= (
+        1e-12 if dt is np.float64 else 2e-6) * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_plv_family_with_bandpass_front_end(prec):
+    import torch
+
+    x = W.c4(n_signals=24, n_samples=3000, n_trials=3, n_latent=3, bands=((8.0, 12.0),))[0]
+    x = x.astype(np.float64) if prec == "fp64" else x
+    f = _fir(order=400, lo=0.014, hi=0.026)  # ~7-13 Hz at 1 kHz
+    ref = O.plv_family(x.astype(np.float64), input_kind="real", fir=(f.taps, 500))
+    res = C.plv_family(x, input_kind="real", precision=prec, fir=f, pad_samples=500)
+    check(res, ref, prec, "bandpass host")
+    dev = C.plv_family(torch.from_numpy(np.ascontiguousarray(x)).cuda(), input_kind="real", precision=prec,
+                       fir=f, pad_samples=500)
+    for m in METRICS:
+        assert maxerr(dev[m].values.cpu().numpy(), ref[m]) <= TOL[prec], m
+
+
+def test_bandpass_pipelined_host_path_and_errors():
+    import torch
+
+    rng = np.random.default_rng(33)
+    N, T = 2600, 600
+    x = rng.standard_normal((N, T)).astype(np.float32)
+    f = _fir(order=100, lo=0.2, hi=0.3)
+    h = C.plv_family(x, input_kind="real", fir=f, pad_samples=150)
+    d = C.plv_family(torch.from_numpy(x).cuda(), input_kind="real", fir=f, pad_samples=150)
+    for m in METRICS:
+        assert np.array_equal(h[m].values, d[m].values.cpu().numpy()), m
+    idx = np.sort(rng.choice(N, size=64, replace=False))
+    ref = O.plv_family(x[idx][:, :, None], input_kind="real", fir=(f.taps, 150))
+    for m in METRICS:
+        assert maxerr(h[m].values[np.ix_(idx, idx)], ref[m]) <= TOL["split"], m
+    with pytest.raises(errors.SignalTooShortError):
+        C.plv_family(x[:4, :101], input_kind="real", fir=f, pad_samples=10)
+    with pytest.raises(errors.SignalTooShortError):
+        signalprep.filter_two_pass(x[:4], f, 600)
+
+
 # ---------------------------------------- fused Hilbert kernel (fp32, T = 4096)
 def test_fused_hilbert_t4096_bands():
     # odd N * R: the last row of the chunk has no partner in its FFT pair

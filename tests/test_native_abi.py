@@ -29,9 +29,33 @@ def test_library_exports_header_symbols():
 
 
 def test_struct_layout_matches_header():
-    # ps_plv_args: 8 + 2*4 + 8*8 + 8 + 3*4 (+4 pad) + 5*8 + 2*4 + 8
-    assert ctypes.sizeof(_native.PlvArgs) == 8 + 8 + 64 + 8 + 16 + 40 + 8 + 8 + 8
+    # ps_plv_args: 8 + 2*4 + 8*8 + 8 + 3*4 (+4 pad) + 5*8 + 2*4 + 8 + 2*4 + 8 (fir)
+    assert ctypes.sizeof(_native.PlvArgs) == 8 + 8 + 64 + 8 + 16 + 40 + 8 + 8 + 8 + 8
+    assert _native.PlvArgs.fir.offset == ctypes.sizeof(_native.PlvArgs) - 8
     assert ctypes.sizeof(_native.PlvResult) == 3 * 8 + 2 * 4 + 4 * 4
+    assert ctypes.sizeof(_native.Fir) == 24
+
+
+def test_fir_design_host_matches_oracle_and_validates():
+    import warnings
+
+    import numpy as np
+
+    from oracle import plv_oracle as O
+    from paper_1710_08037_b200 import signalprep as S
+
+    f = S.design_bandpass_fir((0.57 * np.pi, 0.6 * np.pi), 2000)
+    assert f.order == 2000 and f.taps.shape == (2001,)
+    assert np.array_equal(f.taps, O.design_bandpass_fir(0.57 * np.pi, 0.6 * np.pi, 2000))
+    with pytest.raises(errors.InvalidBandError):
+        S.design_bandpass_fir((0.6, 0.5), 100)
+    with pytest.raises(errors.InvalidBandError):
+        S.design_bandpass_fir((0.5, 4.0), 100)
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        S.design_bandpass_fir((0.25 * np.pi, 0.75 * np.pi), 10)
+    assert any(issubclass(x.category, errors.OrderTooSmallWarning) for x in w)
+    assert _native.STATUS_EXC[10] is errors.SignalTooShortError
 
 
 def test_ctx_create_fails_cleanly_without_gpu():

@@ -262,3 +262,95 @@ def test_trial_reduce_modes():
     p = np.abs(g)
     np.fill_diagonal(p, 1)
     assert np.allclose(pool["plv"], p, atol=1e-14)
+
+
+# ----------------------------------------- band-pass front end
+def _dtft(h, w):
+    return np.sum(h * np.exp(-1j * w * np.arange(h.size)))
+
+
+def test_fir_design_kats():
+    # [0.570pi, 0.600pi], order 2000 -> |H(0.585pi)| within +-1 dB
+    h = O.design_bandpass_fir(0.570 * np.pi, 0.600 * np.pi, 2000)
+    assert h.size == 2001
+    assert abs(20 * np.log10(abs(_dtft(h, 0.585 * np.pi)))) < 1.0
+    assert np.max(np.abs(h - h[::-1])) < 1e-16  # linear phase (to rounding)
+    # [0.25pi, 0.75pi], order 10 -> centre response ~ 1
+    h10 = O.design_bandpass_fir(0.25 * np.pi, 0.75 * np.pi, 10)
+    assert abs(abs(_dtft(h10, 0.5 * np.pi)) - 1.0) < 1e-12
+    # low >= high -> InvalidBand
+    with pytest.raises(O.InvalidBandError):
+        O.design_bandpass_fir(0.6 * np.pi, 0.5 * np.pi, 100)
+    with pytest.raises(O.InvalidBandError):
+        O.design_bandpass_fir(0.5, 3.5, 100)
+
+
+def test_fir_design_pinned_to_scipy_firwin():
+    # the SPEC's design decision (windowed sinc, Hamming) is
+    # scipy.signal.firwin(..., window='hamming', scale=True): pin the restatement
+    for lo, hi, order in [(0.57, 0.6, 2000), (0.25, 0.75, 10), (0.016, 0.024, 800)]:
+        h = O.design_bandpass_fir(lo * np.pi, hi * np.pi, order)
+        ref = scipy.signal.firwin(order + 1, [lo, hi], pass_zero=False, window="hamming", scale=True)
+        assert np.max(np.abs(h - ref)) < 1e-14
+
+
+def test_two_pass_matches_lfilter_definition():
+    # forward, reverse, forward, reverse with zero initial state
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((3, 700, 2))
+    h = O.design_bandpass_fir(0.2 * np.pi, 0.4 * np.pi, 60)
+    pad = 100
+    xp = np.pad(x, ((0, 0), (pad, pad), (0, 0)), mode="reflect")
+    y = scipy.signal.lfilter(h, [1.0], xp, axis=1)
+    y = scipy.signal.lfilter(h, [1.0], y[:, ::-1], axis=1)[:, ::-1]
+    assert np.max(np.abs(O.two_pass_padded(x, h, pad) - y)) < 1e-13
+    assert np.max(np.abs(O.filter_two_pass(x, h, pad) - y[:, pad:pad + 700])) < 1e-13
+
+
+def test_two_pass_zero_phase_and_attenuation():
+    h = O.design_bandpass_fir(0.2 * np.pi, 0.3 * np.pi, 200)
+    T, pad = 4000, 1000
+    t = np.arange(T)
+    # band-centre sinusoid -> zero phase shift (xcorr peak at lag 0)
+    x = np.cos(0.25 * np.pi * t)
+    y = O.filter_two_pass(x[None, :, None], h, pad)[0, :, 0]
+    mid = slice(500, T - 500)
+    lags = np.arange(-5, 6)
+    xc = [np.dot(x[mid], np.roll(y, k)[mid]) for k in lags]
+    assert lags[int(np.argmax(xc))] == 0
+    # single-pass -10 dB -> two-pass -20 dB +- 1 dB
+    w = np.linspace(0.05 * np.pi, 0.2 * np.pi, 20000)
+    mag = 20 * np.log10(np.abs(np.exp(-1j * np.outer(w, np.arange(h.size))) @ h))
+    w10 = w[np.argmin(np.abs(mag + 10.0))]
+    s = np.cos(w10 * t)
+    ys = O.filter_two_pass(s[None, :, None], h, pad)[0, :, 0]
+    gain = 20 * np.log10(np.std(ys[mid]) / np.std(s[mid]))
+    assert abs(gain + 20.0) < 1.0
+
+
+def test_two_pass_white_noise_band_limited():
+    # power outside [low - tw, high + tw] < 1% of total
+    rng = np.random.default_rng(12)
+    lo, hi, order = 0.2 * np.pi, 0.3 * np.pi, 400
+    h = O.design_bandpass_fir(lo, hi, order)
+    x = rng.standard_normal((1, 20000, 1))
+    y = O.filter_two_pass(x, h, 2000)[0, :, 0]
+    f, p = scipy.signal.periodogram(y)
+    w = 2 * np.pi * f
+    tw = 3.3 * 2 * np.pi / order  # Hamming transition width
+    out = (w < lo - tw) | (w > hi + tw)
+    assert p[out].sum() < 0.01 * p.sum()
+
+
+def test_two_pass_too_short_and_bandpass_analytic_trim():
+    h = O.design_bandpass_fir(0.2 * np.pi, 0.4 * np.pi, 60)
+    with pytest.raises(O.SignalTooShortError):
+        O.filter_two_pass(np.zeros((1, 61, 1)), h, 10)
+    rng = np.random.default_rng(13)
+    x = rng.standard_normal((2, 500, 1))
+    a = O.bandpass_analytic(x, h, 120)
+    assert a.shape == x.shape
+    # Re is the filtered record bit-exactly; H comes from the padded record
+    assert np.array_equal(a.real, O.filter_two_pass(x, h, 120))
+    full = O.analytic_signal(O.two_pass_padded(x, h, 120))
+    assert np.array_equal(a, full[:, 120:620])
