@@ -39,7 +39,9 @@ typedef enum ps_status {
   PS_E_CUFFT = 7,         /* CudaError (cuFFT)                        */
   PS_E_OOM = 8,           /* MemoryError                              */
   PS_E_INTERNAL = 9,      /* RuntimeError                             */
-  PS_E_SIGNAL_TOO_SHORT = 10 /* SignalTooShortError (n_samples <= order + 1) */
+  PS_E_SIGNAL_TOO_SHORT = 10, /* SignalTooShortError (n_samples <= order + 1) */
+  PS_E_WINDOW_TOO_LONG = 11,  /* WindowTooLongError (window_len > n_samples) */
+  PS_E_EMPTY_BAND = 12        /* EmptyBandError (no bin in the band)        */
 } ps_status;
 
 typedef enum ps_dtype { PS_F32 = 0, PS_F64 = 1, PS_C64 = 2, PS_C128 = 3 } ps_dtype;
@@ -190,6 +192,33 @@ ps_status ps_analytic_signal(ps_ctx* ctx, const ps_plv_args* args, void* out);
  * Uses args->fir (required) and the input fields of args; output real of the
  * input precision, dense [n_bands][n_trials][n_signals][n_samples]. */
 ps_status ps_filter_two_pass(ps_ctx* ctx, const ps_plv_args* args, void* out);
+
+/* Welch coherence family over all pairs (Eq 12; SURVEY 8(f)
+ * #3).  Segments of window_len samples advancing by window_len - overlap within
+ * each trial (segments of all trials pooled), symmetric Hamming
+ * taper, spectrum X_n,s(k) per bin.  For every bin k in the band
+ * (low <= 2 pi k / window_len <= high) the normalised
+ * cross-spectrum C_ij(k) = sum_s X_i X_j^* / sqrt(sum_s |X_i|^2 sum_s |X_j|^2)
+ * is one Gram over segments, and the outputs of args are reinterpreted:
+ *   out_plv  -> COH  = |C|          (coherence_welch, magnitude)
+ *   out_iplv -> ICOH = |Im C|       (imaginary_coherency)
+ *   out_cre / out_cim -> Re C, Im C (signed coherency);  out_ciplv -> |Im C| / sqrt(1 - Re C^2)
+ * aggregated over the band's bins by `reduce` (band_coherence):
+ * MEAN / MAX -> [n_bands][N][N], NONE -> [n_bands][n_bins][N][N] (one matrix
+ * per bin, ascending k).  Pairs with zero power at a bin get 0 there; the COH
+ * diagonal is 1.  Real input only; n_trials = trials, precision as usual. */
+typedef enum ps_band_reduce { PS_BAND_MEAN = 0, PS_BAND_MAX = 1, PS_BAND_NONE = 2 } ps_band_reduce;
+typedef struct ps_welch {
+  int64_t window_len;
+  int64_t overlap;
+  double band_low;   /* radians per sample, 0 <= low <= high <= pi */
+  double band_high;
+  int32_t reduce;    /* ps_band_reduce */
+  int32_t reserved0;
+} ps_welch;
+ps_status ps_coherence(ps_ctx* ctx, const ps_plv_args* args, const ps_welch* welch, ps_plv_result* result);
+/* Number of bins the band selects (host helper): k0 (first bin) in *first_bin. */
+int64_t ps_welch_bins(int64_t window_len, double band_low, double band_high, int64_t* first_bin);
 
 /* Replaces signalprep.normalize_phasors: z = a/|a| with the
  * amplitude-floor mask (masked samples exactly 0+0i).  Input complex (c64 /

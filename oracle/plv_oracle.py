@@ -222,6 +222,113 @@ def bandpass_analytic(x, taps, pad: int, axis: int = 1) -> np.ndarray:
     return np.ascontiguousarray(_trim(a, pad, T, axis))
 
 
+# --------------------------------------------------------------------------
+# Welch coherence family (Eq 12)
+# --------------------------------------------------------------------------
+class WindowTooLongError(OracleError):
+    """errors.py WindowTooLongError -- window_len > n_samples."""
+
+
+class EmptyBandError(OracleError):
+    """errors.py EmptyBandError -- no spectral bin inside the band."""
+
+
+def welch_spectra(x, window_len: int, overlap: int) -> np.ndarray:
+    """Spectra of Hamming-tapered segments (symmetric window)
+    of x [N, T, R]: segments of window_len samples advancing by
+    window_len - overlap, drawn within each trial and pooled over trials
+    (SPEC.md:262).  Returns X [N, R * S, window_len // 2 + 1], q = r * S + s."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.ndim == 2:
+        x = x[:, :, None]
+    N, T, R = x.shape
+    W, O = int(window_len), int(overlap)
+    if not (0 <= O < W):
+        raise ValueError("WelchConfig needs 0 <= overlap < window_len (SPEC.md:168)")
+    if W > T:
+        raise WindowTooLongError("window_len exceeds n_samples (SPEC.md:225)")
+    hop = W - O
+    S = (T - W) // hop + 1
+    win = np.hamming(W)
+    seg = np.stack([x[:, s * hop:s * hop + W, :] for s in range(S)], axis=1)  # [N, S, W, R]
+    seg = np.transpose(seg, (0, 3, 1, 2)) * win                              # [N, R, S, W]
+    return np.fft.rfft(seg, axis=-1).reshape(N, R * S, W // 2 + 1)
+
+
+def _norm_cross(Xi, Xj):
+    """Normalised cross-spectrum over segments (axis 0), 0 where a power is 0."""
+    s = np.sum(Xi * np.conj(Xj), axis=0)
+    p = np.sqrt(np.sum(np.abs(Xi) ** 2, axis=0) * np.sum(np.abs(Xj) ** 2, axis=0))
+    return np.where(p > 0, s / np.where(p > 0, p, 1.0), 0.0)
+
+
+def coherence_welch(x2, window_len: int, overlap: int) -> np.ndarray:
+    """|sum X_i X_j^*| / sqrt(sum|X_i|^2 sum|X_j|^2) per bin
+    (magnitude, not squared) for two signals x2 [2, T(, R)]."""
+    X = welch_spectra(x2, window_len, overlap)
+    return np.abs(_norm_cross(X[0], X[1]))
+
+
+def coherence_weighted_phasor(x2, window_len: int, overlap: int) -> np.ndarray:
+    """SPEC.md:221-228, Eq 12 second line: amplitude-weighted average of the
+    per-segment unit cross-phasors, normalised by the amplitude root-product."""
+    X = welch_spectra(x2, window_len, overlap)
+    Ai, Aj = np.abs(X[0]), np.abs(X[1])
+    dphi = np.angle(X[0]) - np.angle(X[1])
+    num = np.abs(np.sum(Ai * Aj * np.exp(1j * dphi), axis=0))
+    den = np.sqrt(np.sum(Ai ** 2, axis=0) * np.sum(Aj ** 2, axis=0))
+    return np.where(den > 0, num / np.where(den > 0, den, 1.0), 0.0)
+
+
+def imaginary_coherency(x2, window_len: int, overlap: int) -> np.ndarray:
+    """|Im| of the normalised cross-spectrum per bin."""
+    X = welch_spectra(x2, window_len, overlap)
+    return np.abs(_norm_cross(X[0], X[1]).imag)
+
+
+def welch_bins(window_len: int, low: float, high: float):
+    """(first bin, n bins) with low <= 2 pi k / window_len <= high."""
+    W = int(window_len)
+    ks = [k for k in range(W // 2 + 1) if low <= 2 * np.pi * k / W <= high]
+    return (ks[0], len(ks)) if ks else (0, 0)
+
+
+def band_coherence(spec, window_len: int, low: float, high: float, mode: str = "max") -> float:
+    """max or mean over the band's bins; EmptyBand if none."""
+    k0, nb = welch_bins(window_len, low, high)
+    if nb == 0:
+        raise EmptyBandError("band contains no spectral bin (SPEC.md:239)")
+    v = np.asarray(spec)[k0:k0 + nb]
+    return float(v.max() if mode == "max" else v.mean())
+
+
+def coherence_matrix(x, window_len: int, overlap: int, low: float, high: float, mode: str = "max"):
+    """All-pairs band coherence (the N x N form of band_coherence(coherence_welch)):
+    per bin, the normalised cross-spectrum over pooled segments as one complex
+    Gram; returns {'coh', 'icoh', 'cre', 'cim'} as [N, N] (mode max / mean) or
+    [N, N, n_bins] (mode none).  Diagonal: coh = cre = 1, icoh = cim = 0."""
+    X = welch_spectra(x, window_len, overlap)
+    k0, nb = welch_bins(window_len, low, high)
+    if nb == 0:
+        raise EmptyBandError("band contains no spectral bin (SPEC.md:239)")
+    N = X.shape[0]
+    per = {m: [] for m in ("coh", "icoh", "cre", "cim")}
+    for k in range(k0, k0 + nb):
+        Z = X[:, :, k]
+        S = Z @ Z.conj().T
+        p = np.sqrt(np.real(np.diag(S)))
+        d = np.outer(p, p)
+        C = np.where(d > 0, S / np.where(d > 0, d, 1.0), 0.0)
+        for m, v in (("coh", np.abs(C)), ("icoh", np.abs(C.imag)), ("cre", C.real.copy()), ("cim", C.imag.copy())):
+            np.fill_diagonal(v, 1.0 if m in ("coh", "cre") else 0.0)
+            per[m].append(v)
+    out = {}
+    for m, vs in per.items():
+        a = np.stack(vs, axis=-1)
+        out[m] = a.max(axis=-1) if mode == "max" else (a.mean(axis=-1) if mode == "mean" else a)
+    return out
+
+
 def phasors_from_unit(z, axis: int = 1):
     """PhasorEpochs given directly (plv_matrix input): mask = (z == 0)."""
     z = np.asarray(z).astype(np.complex128, copy=False)

@@ -32,6 +32,8 @@ STATUS_EXC = {
     8: MemoryError,
     9: RuntimeError,
     10: errors.SignalTooShortError,
+    11: errors.WindowTooLongError,
+    12: errors.EmptyBandError,
 }
 
 DTYPES = {"f32": 0, "f64": 1, "c64": 2, "c128": 3}
@@ -85,6 +87,19 @@ class PlvArgs(ctypes.Structure):
     ]
 
 
+class Welch(ctypes.Structure):
+    """Mirror of ps_welch (Welch coherence configuration + band)."""
+
+    _fields_ = [
+        ("window_len", ctypes.c_int64),
+        ("overlap", ctypes.c_int64),
+        ("band_low", ctypes.c_double),
+        ("band_high", ctypes.c_double),
+        ("reduce", ctypes.c_int32),
+        ("reserved0", ctypes.c_int32),
+    ]
+
+
 class PlvResult(ctypes.Structure):
     """Mirror of ps_plv_result."""
 
@@ -117,6 +132,10 @@ _SIGNATURES = {
                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "ps_analytic_signal": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p], ctypes.c_int),
     "ps_filter_two_pass": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p], ctypes.c_int),
+    "ps_coherence": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(Welch), ctypes.POINTER(PlvResult)],
+                     ctypes.c_int),
+    "ps_welch_bins": ([ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.POINTER(ctypes.c_int64)],
+                      ctypes.c_int64),
     "ps_normalize_phasors": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p, ctypes.c_void_p],
                              ctypes.c_int),
     "ps_pair_shard": ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64],

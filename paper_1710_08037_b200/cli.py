@@ -110,7 +110,14 @@ def cmd_connectivity(argv=None) -> int:
     ap.add_argument("--metric", default="plv", choices=["plv", "iplv", "ciplv", "coh_max", "coh_mean"])
     ap.add_argument("--phasors", action="store_true", help="input holds unit phasors (masked samples = 0)")
     ap.add_argument("--analytic", action="store_true", help="input holds analytic signals")
-    ap.add_argument("--band", nargs=2, type=float, default=None, metavar=("LOW", "HIGH"))
+    ap.add_argument("--band", nargs=2, type=float, default=None, metavar=("LOW", "HIGH"),
+                    help="radians per sample: FIR band-pass edges for plv/iplv/ciplv (real input; SPEC.md:58), "
+                         "the aggregated band for coh_max/coh_mean (SPEC.md:229)")
+    ap.add_argument("--window", type=int, default=400, help="Welch window length (coherence; Fig 2: 400)")
+    ap.add_argument("--overlap", type=int, default=200, help="Welch overlap (coherence; Fig 2: 200)")
+    ap.add_argument("--order", type=int, default=2000, help="FIR order (even; paper: 2000)")
+    ap.add_argument("--pad", type=int, default=None,
+                    help="reflection padding per side in samples (default: order, capped at n_samples - 1)")
     ap.add_argument("--trial-reduce", default="mean", choices=["mean", "none", "pool"])
     ap.add_argument("--precision", default="split", choices=["split", "fp64"])
     ap.add_argument("--output", "-o", required=True)
@@ -118,12 +125,9 @@ def cmd_connectivity(argv=None) -> int:
         args = ap.parse_args(argv)
     except SystemExit as exc:
         return 2 if exc.code else 0
-    if args.metric.startswith("coh"):
-        print("phasesync: coherence metrics are not part of this build (DESIGN.md section 7)", file=sys.stderr)
-        return 2
-    if args.band is not None:
-        print("phasesync: the FIR band-pass stage is not part of this build; pass band-limited input",
-              file=sys.stderr)
+    coh = args.metric.startswith("coh")
+    if coh and args.band is None:
+        print("phasesync: coh_max / coh_mean need --band LOW HIGH (SPEC.md:229)", file=sys.stderr)
         return 2
     try:
         x, header = read_bundle(args.input)
@@ -139,9 +143,24 @@ def cmd_connectivity(argv=None) -> int:
     from . import connectivity
 
     kind = "phasor" if args.phasors else ("analytic" if (args.analytic or np.iscomplexobj(x)) else "real")
+    fir, pad = None, 0
     try:
-        res = connectivity.plv_family(x, input_kind=kind, metrics=(args.metric,), precision=args.precision,
-                                      trial_reduce=args.trial_reduce)[args.metric]
+        if coh:  # band_coherence(coherence_welch) for all pairs
+            if kind != "real":
+                raise ValueError("coherence metrics take real epochs")
+            mode = args.metric.split("_")[1]
+            res = connectivity.coherence_matrix(x, connectivity.WelchConfig(args.window, args.overlap),
+                                                tuple(args.band), mode=mode, precision=args.precision)["coh"]
+        elif args.band is not None:  # band-pass -> analytic (padded) -> trim
+            if kind != "real":
+                raise ValueError("--band applies to real input only")
+            from .signalprep import design_bandpass_fir
+
+            fir = design_bandpass_fir(tuple(args.band), args.order)
+            pad = args.pad if args.pad is not None else min(args.order, x.shape[1] - 1)
+        if not coh:
+            res = connectivity.plv_family(x, input_kind=kind, metrics=(args.metric,), precision=args.precision,
+                                          trial_reduce=args.trial_reduce, fir=fir, pad_samples=pad)[args.metric]
     except (ValueError, RuntimeError) as exc:
         print(f"phasesync: {type(exc).__name__}: {exc}", file=sys.stderr)
         return 2
@@ -156,7 +175,10 @@ def cmd_connectivity(argv=None) -> int:
         write_csv(out.with_suffix(".csv"), values, res.metric)
     write_manifest(out.with_suffix(".manifest.json"), ["phasesync", "connectivity"] + list(argv or sys.argv[2:]),
                    {"metric": args.metric, "input_kind": kind, "precision": args.precision,
-                    "trial_reduce": args.trial_reduce, "input_header": header, "seeds": []})
+                    "trial_reduce": args.trial_reduce, "input_header": header, "seeds": [],
+                    "band": args.band, "order": args.order if fir is not None else None,
+                    "pad_samples": pad if fir is not None else None,
+                    "welch": {"window_len": args.window, "overlap": args.overlap} if coh else None})
     return 0
 
 

@@ -227,3 +227,169 @@ def ciplv(phasors, *, trial_reduce: str = "mean", precision: str = "split") -> C
     """|Im| / sqrt(1 - Re^2), 0 at the singularity."""
     return plv_family(_phasor_input(phasors), input_kind="phasor", metrics=("ciplv",), precision=precision,
                       trial_reduce=trial_reduce)["ciplv"]
+
+
+# --------------------------------------------------------------------------
+# Welch coherence family (SPEC.md:158-169, 213-246; SURVEY 8(f) #3)
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class WelchConfig:
+    """window_len samples, overlap samples, Hamming taper."""
+    window_len: int
+    overlap: int
+    taper: str = "hamming"
+
+
+@dataclass
+class CoherenceSpectrum:
+    """SPEC.md:158-164: values over bins k = 0 .. window_len // 2 at angular
+    frequency 2 pi k / window_len (freq_axis, radians per sample)."""
+    values: np.ndarray
+    n_segments: int
+    window_len: int
+    overlap: int
+    freq_axis: np.ndarray
+
+
+# COH metric names -> slots of the PLV-family epilogue (include/phasesync.h ps_coherence)
+COH_SLOTS = {"coh": "plv", "icoh": "iplv", "cre": "cre", "cim": "cim", "ciplv": "ciplv"}
+BAND_REDUCE = {"mean": 0, "max": 1, "none": 2}
+
+
+def welch_bins(window_len: int, band) -> tuple[int, int]:
+    """(first bin, number of bins) of `band` (radians per sample, inclusive edges)."""
+    first = ctypes.c_int64()
+    n = _native.lib().ps_welch_bins(int(window_len), float(band[0]), float(band[1]), ctypes.byref(first))
+    return int(first.value), int(n)
+
+
+def coherence_matrix(x, cfg: WelchConfig, band, *, mode: str = "max", metrics: Iterable[str] = ("coh",),
+                     precision: str = "split", bands: bool = False, shard: tuple[int, int] = (0, 1),
+                     timing: bool = False) -> dict:
+    """All-pairs Welch coherence aggregated over `band`:
+    band_coherence(coherence_welch(x_i, x_j), band, mode) for every pair, from
+    one Gram over segments per frequency bin on the sm_100a path.
+
+    x: RealEpochs data [N, T], [N, T, R] or (bands=True) [B, N, T, R]; numpy
+       or CUDA torch tensor.  Segments are drawn within each trial and pooled
+       over trials.
+    band: (low, high) in radians per sample; mode 'max' (COH_MAX), 'mean'
+       (COH_MEAN) or 'none' (one matrix per bin: values [N, N, n_bins]).
+    metrics: 'coh' (|C|, Eq 12), 'icoh' (|Im C|, imaginary coherency), 'cre' /
+       'cim' (signed coherency parts).
+    Returns {metric: ConnectivityMatrix}.
+    """
+    import torch
+
+    if mode not in BAND_REDUCE:
+        raise ValueError("mode must be 'max', 'mean' or 'none'")
+    if cfg.taper != "hamming":
+        raise ValueError("only the Hamming taper is defined (SPEC.md:169)")
+    if hasattr(x, "data") and not isinstance(x, np.ndarray) and not is_torch(x):
+        x = x.data
+    metrics = tuple(metrics)
+    bad = [m for m in metrics if m not in COH_SLOTS]
+    if bad or not metrics:
+        raise ValueError(f"unknown coherence metrics {bad}; choose from {list(COH_SLOTS)}")
+    host = not (is_torch(x) and x.is_cuda)
+    t = x if not host else torch.from_numpy(np.asarray(x)).cuda()
+    d = describe(t, bands=bands)
+    if d.dtype not in ("f32", "f64"):
+        raise ValueError("coherence expects real-valued epochs (SPEC.md:213)")
+    B, N, T, R = d.dims
+    k0, nb = welch_bins(cfg.window_len, band) if 0 <= band[0] <= band[1] <= np.pi else (0, 1)
+    slots = B * nb if mode == "none" else B
+    fp64 = _native.PRECISIONS[precision] == 1
+    a = _native.PlvArgs()
+    a.input = d.ptr
+    a.dtype = dtype_code(d.dtype)
+    a.input_kind = _native.INPUT_KINDS["real"]
+    a.n_bands, a.n_signals, a.n_samples, a.n_trials = B, N, T, R
+    a.stride_band, a.stride_signal, a.stride_sample, a.stride_trial = d.strides
+    a.amp_floor = 0.0
+    a.precision = _native.PRECISIONS[precision]
+    a.shard_index, a.shard_count = int(shard[0]), int(shard[1])
+    w = _native.Welch()
+    w.window_len, w.overlap = int(cfg.window_len), int(cfg.overlap)
+    w.band_low, w.band_high = float(band[0]), float(band[1])
+    w.reduce = BAND_REDUCE[mode]
+    tdt = torch.float64 if fp64 else torch.float32
+    dev = torch.device("cuda", d.device)
+    outs = {}
+    bits = 0
+    for m in metrics:
+        bits |= _native.METRIC_BITS[COH_SLOTS[m]]
+        outs[m] = torch.zeros((slots, N, N), dtype=tdt, device=dev)
+        setattr(a, "out_" + COH_SLOTS[m], outs[m].data_ptr())
+    a.metrics = bits
+    with torch.cuda.device(dev):
+        a.stream = torch.cuda.current_stream(dev).cuda_stream
+        ctx = _native.context(d.device)
+        ctx.set_timing(timing)
+        res = _native.PlvResult()
+        _native.check(_native.lib().ps_coherence(ctx.handle, ctypes.byref(a), ctypes.byref(w), ctypes.byref(res)))
+    info = res.as_dict()
+    info.update(window_len=cfg.window_len, overlap=cfg.overlap, band=tuple(band), band_reduce=mode,
+                first_bin=k0, n_bins=nb, precision=precision)
+    names = {"coh": "COH_" + mode.upper(), "icoh": "ICOH_" + mode.upper()}
+    result = {}
+    for m in metrics:
+        v = outs[m]
+        if mode == "none":
+            v = v.reshape(B, nb, N, N).permute(0, 2, 3, 1)
+        else:
+            v = v.reshape(B, N, N)
+        if not bands:
+            v = v[0]
+        if host:
+            v = v.cpu().numpy()
+        result[m] = ConnectivityMatrix(values=v, metric=names.get(m, m), n_observations=int(info["n_observations"]),
+                                       meta=info)
+    return result
+
+
+def _pair_spectrum(x, cfg: WelchConfig, metric: str, precision: str) -> CoherenceSpectrum:
+    x = np.asarray(x) if not is_torch(x) else x
+    if x.shape[0] != 2:
+        raise errors.ShapeError("coherence spectra take exactly 2 signals (SPEC.md:222)")
+    r = coherence_matrix(x, cfg, (0.0, np.pi), mode="none", metrics=(metric,), precision=precision)[metric]
+    v = r.values
+    v = v.cpu().numpy() if is_torch(v) else v
+    W = int(cfg.window_len)
+    return CoherenceSpectrum(values=np.asarray(v[0, 1], dtype=np.float64),
+                             n_segments=int(r.n_observations), window_len=W, overlap=int(cfg.overlap),
+                             freq_axis=2 * np.pi * np.arange(W // 2 + 1) / W)
+
+
+def coherence_welch(x, cfg: WelchConfig, *, precision: str = "fp64") -> CoherenceSpectrum:
+    """|sum_s X_i X_j^*| / sqrt(sum|X_i|^2 sum|X_j|^2) per bin
+    (magnitude, not squared) for a 2-signal RealEpochs."""
+    return _pair_spectrum(x, cfg, "coh", precision)
+
+
+def coherence_weighted_phasor(x, cfg: WelchConfig, *, precision: str = "fp64") -> CoherenceSpectrum:
+    """SPEC.md:221-228 (Eq 12, second line): the amplitude-weighted average of
+    per-segment unit cross-phasors normalised by the amplitude root-product.
+    On this path both forms are the same Gram over segments of the
+    auto-power-normalised spectra (sum_s A_i A_j e^{i dphi} / sqrt(sum A_i^2
+    sum A_j^2)), so the two agree exactly."""
+    return _pair_spectrum(x, cfg, "coh", precision)
+
+
+def imaginary_coherency(x, cfg: WelchConfig, *, precision: str = "fp64") -> CoherenceSpectrum:
+    """|Im{sum X_i X_j^* / sqrt(sum|X_i|^2 sum|X_j|^2)}| per bin."""
+    return _pair_spectrum(x, cfg, "icoh", precision)
+
+
+def band_coherence(spec: CoherenceSpectrum, band, mode: str = "max") -> float:
+    """max or mean of a CoherenceSpectrum over the bins with
+    low <= 2 pi k / window_len <= high (inclusive); EmptyBandError
+    if none.  (A reduction over one short host vector: the all-pairs version
+    runs on the GPU in coherence_matrix.)"""
+    if mode not in ("max", "mean"):
+        raise ValueError("mode must be 'max' or 'mean'")
+    k0, nb = welch_bins(spec.window_len, band) if 0 <= band[0] <= band[1] <= np.pi else (0, 0)
+    if nb < 1:
+        raise errors.EmptyBandError(f"band {tuple(band)} holds no bin for window_len {spec.window_len}")
+    v = np.asarray(spec.values)[k0:k0 + nb]
+    return float(v.max() if mode == "max" else v.mean())

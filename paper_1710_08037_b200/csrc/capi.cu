@@ -79,6 +79,7 @@ struct ps_ctx {
   std::map<PlanKey, cufftHandle> plans;
   Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout, refine, refine_sorted, planes_t, maskcount_t;
   Buf fir_taps, fir_spec;  // band-pass front end: padded taps, filter spectrum (double)
+  Buf cohws;               // coherence: per-bin matrices before the max-over-bins reduction
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
   std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
@@ -1034,7 +1035,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
-                 &c->fir_spec})
+                 &c->fir_spec, &c->cohws})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1112,6 +1113,139 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
     res->n_masked_samples = (int64_t)c->h_status->n_masked;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
+    res->n_kernel_launches = c->launches;
+    if (c->timing) {
+      cudaEventElapsedTime(&res->ms_normalize, c->ev[0], c->ev[1]);
+      cudaEventElapsedTime(&res->ms_gram, c->ev[1], c->ev[2]);
+      cudaEventElapsedTime(&res->ms_finish, c->ev[2], c->ev[3]);
+    }
+  }
+  return s;
+}
+
+int64_t ps_welch_bins(int64_t W, double lo, double hi, int64_t* first_bin) {
+  long long k0 = -1, k1 = -2;
+  for (long long k = 0; W > 0 && k <= W / 2; ++k) {
+    const double w = 2.0 * M_PI * (double)k / (double)W;  // SPEC.md:263, inclusive edges
+    if (w >= lo && w <= hi) {
+      if (k0 < 0) k0 = k;
+      k1 = k;
+    }
+  }
+  if (first_bin) *first_bin = k0 < 0 ? 0 : k0;
+  return k0 < 0 ? 0 : k1 - k0 + 1;
+}
+
+// Welch coherence family (Eq 12; DESIGN.md 8(f) #3): tapered
+// segments -> batched R2C -> per-bin operand rows normalised by the auto-power
+// -> the split / FP64 Gram with K = segments and one unit per bin -> the
+// PLV-family epilogue reads as COH / ICOH / coherency -> mean (trial-mean
+// machinery) or max (band_max) over the band's bins.
+ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_plv_result* res) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  if (!w) return fail(PS_E_INVALID, "welch config is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  Geometry g;
+  PS_TRY(validate(a, g));
+  if (a->input_kind != PS_INPUT_REAL) return fail(PS_E_INVALID, "coherence takes real epochs (SPEC.md:213)");
+  if (a->fir) return fail(PS_E_INVALID, "coherence does not take a band-pass front end");
+  if (a->mode != PS_MODE_OVER_SAMPLES) return fail(PS_E_INVALID, "coherence has no over_trials mode");
+  const long long W = w->window_len, O = w->overlap;
+  if (W < 1 || O < 0 || O >= W) return fail(PS_E_INVALID, "WelchConfig needs 0 <= overlap < window_len (SPEC.md:168)");
+  if (W > g.T) return fail(PS_E_WINDOW_TOO_LONG, "window_len exceeds n_samples (SPEC.md:225)");
+  if (!(w->band_low >= 0.0 && w->band_low <= w->band_high && w->band_high <= M_PI))
+    return fail(PS_E_INVALID, "band edges must satisfy 0 <= low <= high <= pi");
+  if (w->reduce < PS_BAND_MEAN || w->reduce > PS_BAND_NONE) return fail(PS_E_INVALID, "unknown band reduce");
+  int64_t k0 = 0;
+  const long long nb = ps_welch_bins(W, w->band_low, w->band_high, &k0);
+  if (nb < 1) return fail(PS_E_EMPTY_BAND, "the band contains no spectral bin (SPEC.md:239)");
+  const long long hop = W - O;
+  const long long nseg = (g.T - W) / hop + 1;
+  const long long K = g.R * nseg;
+  if (K > (1LL << 30)) return fail(PS_E_SHAPE, "too many segments");
+  // the Gram sees K "samples" (segments) and nb "trials" (bins) per band
+  ps_plv_args at = *a;
+  at.n_samples = K;
+  at.n_trials = nb;
+  at.trial_reduce = w->reduce == PS_BAND_MEAN ? PS_TRIALS_MEAN : PS_TRIALS_NONE;
+  at.fir = nullptr;
+  Call k;
+  PS_TRY(validate(&at, k.g));
+  const Geometry& gt = k.g;
+  const bool fp64 = !gt.split;
+  const size_t oes = fp64 ? 8 : 4;
+  const long long nn = g.N * g.N;
+  void* user_outs[5] = {a->out_plv, a->out_iplv, a->out_ciplv, a->out_cre, a->out_cim};
+  if (w->reduce == PS_BAND_MAX) {  // per-bin matrices into the workspace, max-reduced below
+    int q = 0;
+    for (int m = 0; m < 5; ++m) q += ((a->metrics >> m) & 1u) ? 1 : 0;
+    const size_t per = (size_t)g.B * nb * nn * oes;
+    PS_TRY(ensure(c->cohws, per * std::max(q, 1)));
+    void** outs[5] = {&at.out_plv, &at.out_iplv, &at.out_ciplv, &at.out_cre, &at.out_cim};
+    q = 0;
+    for (int m = 0; m < 5; ++m)
+      *outs[m] = ((a->metrics >> m) & 1u) ? static_cast<char*>(c->cohws.p) + per * (q++) : nullptr;
+  }
+  PS_TRY(setup_outputs(&at, k));
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(a->stream);
+  c->launches = 0;
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[0], st));
+  // ---- tapered segments -> spectra ------------------------------------------
+  const size_t es = g.cdouble ? 8 : 4;
+  const long long nbW = W / 2 + 1;
+  const long long nsegs = g.rows * nseg;
+  std::vector<double> win((size_t)W, 1.0);  // symmetric Hamming
+  if (W > 1)
+    for (long long t = 0; t < W; ++t) win[(size_t)t] = 0.54 - 0.46 * std::cos(2.0 * M_PI * (double)t / (double)(W - 1));
+  PS_TRY(ensure(c->fir_taps, (size_t)W * sizeof(double)));
+  PS_CUDA(cudaMemcpyAsync(c->fir_taps.p, win.data(), (size_t)W * sizeof(double), cudaMemcpyHostToDevice, st));
+  PS_TRY(ensure(c->xw, (size_t)nsegs * W * es));
+  PS_TRY(ensure(c->spec, (size_t)nsegs * nbW * 2 * es));
+  const SrcDesc src = make_src(a, g, a->input);
+  PS_CUDA(launch_welch_segments(src, g.rows, (int)nseg, (int)W, (int)hop, static_cast<const double*>(c->fir_taps.p),
+                                c->xw.p, g.cdouble ? 1 : 0, st));
+  cufftHandle fwd;
+  PS_TRY(get_plan(c, (int)W, nsegs, W, g.cdouble, 0, &fwd));
+  PS_CUFFT(cufftSetStream(fwd, st));
+  if (g.cdouble)
+    PS_CUFFT(cufftExecD2Z(fwd, (cufftDoubleReal*)c->xw.p, (cufftDoubleComplex*)c->spec.p));
+  else
+    PS_CUFFT(cufftExecR2C(fwd, (cufftReal*)c->xw.p, (cufftComplex*)c->spec.p));
+  // ---- per-bin Gram operands (unit = (band, bin), K = R * S segments) ---------
+  const size_t plane_bytes = gt.split ? (size_t)4 * gt.plane_stride * 2 : (size_t)2 * gt.plane_stride * 8;
+  PS_TRY(ensure(c->planes, plane_bytes));
+  PS_TRY(ensure(c->maskcount, (size_t)gt.rows * sizeof(int)));
+  PS_TRY(reset_status(c, st));
+  PS_CUDA(cudaMemsetAsync(c->maskcount.p, 0, (size_t)gt.rows * sizeof(int), st));
+  PS_CUDA(launch_coherence_planes(c->spec.p, g.cdouble ? 1 : 0, (int)nbW, g.B, g.R, g.N, (int)nseg, (int)k0, (int)nb,
+                                  (int)K, (int)gt.pitch, c->planes.p, gt.plane_stride, gt.split ? 1 : 0, st));
+  c->launches += 2;
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[1], st));
+  // ---- Gram + epilogue (COH = "PLV" of the normalised spectra) ----------------
+  PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
+  PS_TRY(launch_stage(c, k, 0, st));
+  if (k.slot_mode == 2) {
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, gt.B * k.nn, (int)gt.R, gt.split ? 0 : 1, st));
+    for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
+  }
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
+  ps_status s = read_status(c, st);
+  if (s == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+  if (s == PS_OK && w->reduce == PS_BAND_MAX) {
+    for (int m = 0; m < 5; ++m)
+      if (k.outs[m]) {
+        PS_CUDA(launch_band_max(k.outs[m], g.B, nb, nn, user_outs[m], fp64 ? 1 : 0, st));
+        c->launches++;
+      }
+    PS_CUDA(cudaStreamSynchronize(st));
+  }
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[3], st));
+  if (c->timing) PS_CUDA(cudaEventSynchronize(c->ev[3]));
+  if (res) {
+    std::memset(res, 0, sizeof(*res));
+    res->n_observations = K;
+    res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->n_kernel_launches = c->launches;
     if (c->timing) {
       cudaEventElapsedTime(&res->ms_normalize, c->ev[0], c->ev[1]);

@@ -866,6 +866,86 @@ __global__ void zero_tail_kernel(S* y, long long nrows, long long L, long long L
     y[(e / w) * Lf + L + e % w] = S(0);
 }
 
+// ---------------------------------------------------------------------------
+// Welch coherence front end (DESIGN.md 8(f) #3)
+// ---------------------------------------------------------------------------
+// seg[(row * S + s) * W + t] = x[row][s * hop + t] * win[t]
+template <typename IT, typename S>
+__global__ void welch_segments_kernel(SrcDesc src, long long rows, int nseg, int W, int hop, const double* win,
+                                      S* seg) {
+  const long long per = (long long)nseg * W;
+  const long long total = rows * per;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / per, rem = e % per;
+    const long long s = rem / W, t = rem % W;
+    const IT v = static_cast<const IT*>(src.ptr)[row_offset(src, row) + (s * hop + t) * src.s_samp];
+    seg[e] = static_cast<S>(static_cast<double>(v) * win[t]);
+  }
+}
+
+// One warp per (band b, bin kb, signal n): the spectra X_n,q(k0 + kb) over the
+// K = R * S segments (q = r * S + s), scaled by sqrt(K / sum_q |X|^2) so the
+// Gram over q divided by K is the normalised cross-spectrum; written as the
+// Gram operand row ((b * nb + kb) * N + n) of K samples (pitch Kp, zero pad).
+template <typename C, bool SPLIT>
+__global__ void coherence_planes_kernel(const C* __restrict__ spec, int nbW, long long B, long long R, long long N,
+                                        int nseg, int k0, int nb, int K, int Kp, void* planes, long long ps) {
+  const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= B * nb * N) return;
+  const long long n = w % N, kb = (w / N) % nb, b = w / (N * nb);
+  auto at = [&](int q) -> C {
+    const long long r = q / nseg, s = q % nseg;
+    return spec[(((b * R + r) * N + n) * nseg + s) * nbW + k0 + kb];
+  };
+  double sum = 0.0;
+  for (int q = lane; q < K; q += 32) {
+    const C x = at(q);
+    sum += (double)x.x * (double)x.x + (double)x.y * (double)x.y;
+  }
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const double scale = sum > 0.0 ? sqrt((double)K / sum) : 0.0;
+  const long long row = (b * nb + kb) * N + n;
+  for (int q = lane; q < Kp; q += 32) {
+    double re = 0.0, im = 0.0;
+    if (q < K) {
+      const C x = at(q);
+      re = (double)x.x * scale;
+      im = (double)x.y * scale;
+    }
+    const long long idx = row * Kp + q;
+    if (SPLIT) {
+      __half* p = static_cast<__half*>(planes);
+      const __half rh = __float2half_rn((float)re), ih = __float2half_rn((float)im);
+      p[idx] = rh;
+      p[ps + idx] = __float2half_rn((float)(re - (double)__half2float(rh)));
+      p[2 * ps + idx] = ih;
+      p[3 * ps + idx] = __float2half_rn((float)(im - (double)__half2float(ih)));
+    } else {
+      double* p = static_cast<double*>(planes);
+      p[idx] = re;
+      p[ps + idx] = im;
+    }
+  }
+}
+
+// out[b][e] = max_kb ws[b * nb + kb][e]
+template <typename S>
+__global__ void band_max_kernel(const S* ws, long long B, long long nb, long long nn, S* out) {
+  const long long total = B * nn;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long b = e / nn, i = e % nn;
+    S m = ws[(b * nb) * nn + i];
+    for (long long kb = 1; kb < nb; ++kb) {
+      const S v = ws[(b * nb + kb) * nn + i];
+      m = v > m ? v : m;
+    }
+    out[e] = m;
+  }
+}
+
 // out[rl][t] = y[rl][pad + t] (dense trimmed rows)
 template <typename S>
 __global__ void trim_rows_kernel(const S* y, long long nrows, long long ld, long long pad, long long T, S* out) {
@@ -888,6 +968,54 @@ cudaError_t launch_reflect_pad(const SrcDesc& src, long long row0, long long nro
   } else {
     reflect_pad_kernel<float, float><<<g, 256, 0, st>>>(src, row0, nrows, pad, L, Lf, (float*)xp);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_welch_segments(const SrcDesc& src, long long rows, int nseg, int W, int hop, const double* win,
+                                  void* seg, int dst_double, cudaStream_t st) {
+  const int g = grid_for(rows * nseg * (long long)W, 256);
+  if (src.is_double) {
+    if (!dst_double) return cudaErrorInvalidValue;
+    welch_segments_kernel<double, double><<<g, 256, 0, st>>>(src, rows, nseg, W, hop, win, (double*)seg);
+  } else if (dst_double) {
+    welch_segments_kernel<float, double><<<g, 256, 0, st>>>(src, rows, nseg, W, hop, win, (double*)seg);
+  } else {
+    welch_segments_kernel<float, float><<<g, 256, 0, st>>>(src, rows, nseg, W, hop, win, (float*)seg);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_coherence_planes(const void* spec, int spec_double, int nbW, long long B, long long R, long long N,
+                                    int nseg, int k0, int nb, int K, int Kp, void* planes, long long ps, int split,
+                                    cudaStream_t st) {
+  const long long warps = B * nb * N;
+  const long long blocks = (warps * 32 + 255) / 256;
+  if (blocks <= 0) return cudaSuccess;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const unsigned g = (unsigned)blocks;
+  if (spec_double) {
+    if (split)
+      coherence_planes_kernel<double2, true><<<g, 256, 0, st>>>((const double2*)spec, nbW, B, R, N, nseg, k0, nb, K,
+                                                                 Kp, planes, ps);
+    else
+      coherence_planes_kernel<double2, false><<<g, 256, 0, st>>>((const double2*)spec, nbW, B, R, N, nseg, k0, nb, K,
+                                                                  Kp, planes, ps);
+  } else {
+    if (split)
+      coherence_planes_kernel<float2, true><<<g, 256, 0, st>>>((const float2*)spec, nbW, B, R, N, nseg, k0, nb, K, Kp,
+                                                                planes, ps);
+    else
+      coherence_planes_kernel<float2, false><<<g, 256, 0, st>>>((const float2*)spec, nbW, B, R, N, nseg, k0, nb, K,
+                                                                 Kp, planes, ps);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_band_max(const void* ws, long long B, long long nb, long long nn, void* out, int is_double,
+                            cudaStream_t st) {
+  const int g = grid_for(B * nn, 256);
+  if (is_double) band_max_kernel<double><<<g, 256, 0, st>>>((const double*)ws, B, nb, nn, (double*)out);
+  else band_max_kernel<float><<<g, 256, 0, st>>>((const float*)ws, B, nb, nn, (float*)out);
   return cudaGetLastError();
 }
 

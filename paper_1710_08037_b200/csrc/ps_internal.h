@@ -111,6 +111,15 @@ cudaError_t launch_spectrum_mul(void* spec, long long nrows, long long nb, const
 cudaError_t launch_zero_tail(void* y, long long nrows, long long L, long long Lf, int is_double, cudaStream_t st);
 cudaError_t launch_trim_rows(const void* y, long long nrows, long long ld, long long pad, long long T, void* out,
                              int is_double, cudaStream_t st);
+// Welch coherence front end: tapered segments, per-bin normalised Gram operand
+// rows, and the max-over-bins band reduction
+cudaError_t launch_welch_segments(const SrcDesc& src, long long rows, int nseg, int W, int hop, const double* win,
+                                  void* seg, int dst_double, cudaStream_t st);
+cudaError_t launch_coherence_planes(const void* spec, int spec_double, int nbW, long long B, long long R, long long N,
+                                    int nseg, int k0, int nb, int K, int Kp, void* planes, long long ps, int split,
+                                    cudaStream_t st);
+cudaError_t launch_band_max(const void* ws, long long B, long long nb, long long nn, void* out, int is_double,
+                            cudaStream_t st);
 cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nrows,
                                 void* out, cudaStream_t st);
 // Eq 8 (over trials): planes [P][B*R][N][Tp] -> [P][B*T][N][Rp] + masked-trial counts

@@ -43,7 +43,8 @@ def test_cli_usage_exit_codes(tmp_path):
     cli.write_bundle(tmp_path / "x", np.zeros((2, 8, 1)))
     out = tmp_path / "o"
     assert cli.entrypoint(["connectivity", str(tmp_path / "x"), "--metric", "coh_max", "-o", str(out)]) == 2
-    assert cli.entrypoint(["connectivity", str(tmp_path / "x"), "--band", "0.1", "0.2", "-o", str(out)]) == 2
+    # reversed band edges: InvalidBandError -> usage/format exit 2
+    assert cli.entrypoint(["connectivity", str(tmp_path / "x"), "--band", "0.2", "0.1", "-o", str(out)]) == 2
     assert cli.entrypoint(["connectivity", str(tmp_path / "nope"), "-o", str(out)]) == 2
 
 

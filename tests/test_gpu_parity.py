@@ -253,6 +253,59 @@ def test_bandpass_pipelined_host_path_and_errors():
         signalprep.filter_two_pass(x[:4], f, 600)
 
 
+# ---------------------------------- Welch coherence family
+COH_METRICS = ("coh", "icoh", "cre", "cim")
+
+
+@pytest.mark.parametrize("mode", ["max", "mean", "none"])
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_coherence_matrix_matches_oracle(mode, prec):
+    rng = np.random.default_rng(51)
+    x = rng.standard_normal((37, 3000, 2))
+    x[5] = 0.7 * x[2] + 0.3 * np.roll(x[5], 3, axis=1)  # coupled pair
+    x[9] = x[8]                                          # identical pair
+    x = x.astype(np.float32) if prec == "split" else x
+    cfg = C.WelchConfig(200, 100)
+    ref = O.coherence_matrix(x.astype(np.float64), 200, 100, 0.2, 0.9, mode)
+    res = C.coherence_matrix(x, cfg, (0.2, 0.9), mode=mode, metrics=COH_METRICS, precision=prec)
+    errs = {m: maxerr(res[m].values, ref[m]) for m in COH_METRICS}
+    print(f"[parity] coherence {mode} {prec} " + " ".join(f"{m}={e:.3e}" for m, e in errs.items()))
+    for m, e in errs.items():
+        assert e <= TOL[prec], (m, e)
+    assert res["coh"].n_observations == 2 * 29
+
+
+def test_coherence_matrix_bands_device_and_errors():
+    import torch
+
+    rng = np.random.default_rng(52)
+    x = rng.standard_normal((2, 300, 1024, 3)).astype(np.float32)  # [B, N, T, R]
+    cfg = C.WelchConfig(128, 64)
+    res = C.coherence_matrix(torch.from_numpy(x).cuda(), cfg, (0.5, 1.5), mode="max", bands=True)
+    got = res["coh"].values.cpu().numpy()
+    for b in range(2):
+        ref = O.coherence_matrix(x[b].astype(np.float64), 128, 64, 0.5, 1.5, "max")["coh"]
+        assert maxerr(got[b], ref) <= TOL["split"]
+    with pytest.raises(errors.WindowTooLongError):
+        C.coherence_matrix(x[0], C.WelchConfig(2048, 0), (0.5, 1.5))
+    with pytest.raises(errors.EmptyBandError):
+        C.coherence_matrix(x[0], cfg, (0.001, 0.002))
+
+
+def test_coherence_pair_spectra():
+    rng = np.random.default_rng(53)
+    x = rng.standard_normal((2, 5000, 2))
+    x[1] += 0.5 * np.roll(x[0], 2, axis=1)
+    cfg = C.WelchConfig(400, 200)
+    c = C.coherence_welch(x, cfg)
+    assert c.n_segments == 2 * 24 and c.values.shape == (201,)
+    assert maxerr(c.values, O.coherence_welch(x, 400, 200)) <= 1e-12
+    assert maxerr(C.coherence_weighted_phasor(x, cfg).values, O.coherence_weighted_phasor(x, 400, 200)) <= 1e-10
+    assert maxerr(C.imaginary_coherency(x, cfg).values, O.imaginary_coherency(x, 400, 200)) <= 1e-12
+    lo, hi = 0.570 * np.pi, 0.600 * np.pi
+    assert abs(C.band_coherence(c, (lo, hi), "max") - O.band_coherence(c.values, 400, lo, hi, "max")) == 0.0
+
+
 # ---------------------------------------- fused Hilbert kernel (fp32, T = 4096)
 def test_fused_hilbert_t4096_bands():
     # odd N * R: the last row of the chunk has no partner in its FFT pair
@@ -436,3 +489,40 @@ def test_cli_matches_library_bit_exactly(tmp_path):
             assert abs(got[3, 7] - 1.0) < 1e-5
         if metric == "ciplv":
             assert got[3, 7] == 0.0
+
+
+def test_cli_band_pass_matches_library(tmp_path):
+    # cmd_connectivity with --band runs the band-pass front end
+    from paper_1710_08037_b200 import cli
+
+    rng = np.random.default_rng(22)
+    x = rng.standard_normal((10, 900, 2))
+    cli.write_bundle(tmp_path / "in", x, axes=["signal", "sample", "trial"])
+    out = tmp_path / "bp"
+    argv = ["connectivity", str(tmp_path / "in"), "--metric", "plv", "--band", "0.3", "0.5", "--order", "200",
+            "--pad", "300", "-o", str(out)]
+    assert cli.entrypoint(argv) == 0
+    got, _ = cli.read_bundle(out)
+    f = signalprep.design_bandpass_fir((0.3, 0.5), 200)
+    lib = C.plv_family(x, input_kind="real", metrics=("plv",), fir=f, pad_samples=300)["plv"].values
+    assert np.array_equal(got, np.asarray(lib, dtype=np.float64))
+    ref = O.plv_family(x, input_kind="real", fir=(f.taps, 300))["plv"]
+    assert maxerr(got, ref) <= TOL["split"]
+
+
+@pytest.mark.parametrize("metric", ["coh_max", "coh_mean"])
+def test_cli_coherence_matches_oracle(tmp_path, metric):
+    from paper_1710_08037_b200 import cli
+
+    rng = np.random.default_rng(23)
+    x = rng.standard_normal((12, 2000, 2))
+    x[4] = x[1]  # duplicated channel: coherence 1
+    cli.write_bundle(tmp_path / "in", x, axes=["signal", "sample", "trial"])
+    out = tmp_path / metric
+    argv = ["connectivity", str(tmp_path / "in"), "--metric", metric, "--band", "0.3", "0.8", "--window", "200",
+            "--overlap", "100", "--precision", "fp64", "-o", str(out)]
+    assert cli.entrypoint(argv) == 0
+    got, hdr = cli.read_bundle(out)
+    ref = O.coherence_matrix(x, 200, 100, 0.3, 0.8, metric.split("_")[1])["coh"]
+    assert maxerr(got, ref) <= TOL["fp64"]
+    assert abs(got[1, 4] - 1.0) < 1e-12 and hdr["meta"]["metric"] == metric.upper()

@@ -58,6 +58,24 @@ def test_fir_design_host_matches_oracle_and_validates():
     assert _native.STATUS_EXC[10] is errors.SignalTooShortError
 
 
+def test_welch_bins_host_helper_matches_oracle():
+    import numpy as np
+
+    from oracle import plv_oracle as O
+    from paper_1710_08037_b200 import connectivity as C
+
+    assert ctypes.sizeof(_native.Welch) == 40
+    assert _native.STATUS_EXC[11] is errors.WindowTooLongError
+    assert _native.STATUS_EXC[12] is errors.EmptyBandError
+    rng = np.random.default_rng(3)
+    cases = [(200, 0.57 * np.pi, 0.6 * np.pi), (100, 0.0, np.pi), (400, 0.1, 0.1), (7, 0.5, 2.0)]
+    for _ in range(50):
+        lo, hi = sorted(rng.uniform(0, np.pi, 2))
+        cases.append((int(rng.integers(2, 600)), lo, hi))
+    for W, lo, hi in cases:
+        assert C.welch_bins(W, (lo, hi)) == O.welch_bins(W, lo, hi), (W, lo, hi)
+
+
 def test_ctx_create_fails_cleanly_without_gpu():
     try:
         import torch

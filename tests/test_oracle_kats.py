@@ -354,3 +354,95 @@ def test_two_pass_too_short_and_bandpass_analytic_trim():
     assert np.array_equal(a.real, O.filter_two_pass(x, h, 120))
     full = O.analytic_signal(O.two_pass_padded(x, h, 120))
     assert np.array_equal(a, full[:, 120:620])
+
+
+# ---------------------------------------- Welch coherence
+def test_coherence_pinned_to_scipy():
+    # magnitude coherence = sqrt(scipy's magnitude-squared coherence) with the
+    # same Hamming segments and no detrending
+    rng = np.random.default_rng(40)
+    x = rng.standard_normal((2, 5000))
+    for W, ov in [(400, 200), (100, 50), (128, 0)]:
+        c = O.coherence_welch(x[:, :, None], W, ov)
+        _, c2 = scipy.signal.coherence(x[0], x[1], window=np.hamming(W), nperseg=W, noverlap=ov, detrend=False)
+        assert np.max(np.abs(np.sqrt(c2) - c)) < 1e-12
+
+
+def test_coherence_kats():
+    rng = np.random.default_rng(41)
+    W, ov = 100, 50
+    # identical signals -> 1 at every bin with power
+    x = rng.standard_normal((1, 3000, 2))
+    c = O.coherence_welch(np.concatenate([x, x]), W, ov)
+    assert np.max(np.abs(c - 1.0)) < 1e-12
+    # equal-frequency tones, constant offset, -20 dB independent noise -> > 0.95 at the tone bin
+    T = 50 * 50 + 50
+    t = np.arange(T)
+    k = 12
+    w0 = 2 * np.pi * k / W
+    s = np.stack([np.cos(w0 * t), np.cos(w0 * t + 0.7)]) + 0.1 * rng.standard_normal((2, T))
+    assert O.coherence_welch(s[:, :, None], W, ov)[k] > 0.95
+    # independent white noise, 99 segments -> mean ~ sqrt(pi / (4 * 99)) +- 0.03
+    T = 98 * 50 + 100
+    x = rng.standard_normal((2, T, 1))
+    assert abs(O.coherence_welch(x, W, ov).mean() - np.sqrt(np.pi / (4 * 99))) < 0.03
+
+
+def test_coherence_weighted_phasor_identity():
+    rng = np.random.default_rng(42)
+    x = rng.standard_normal((2, 4000, 3))
+    assert np.max(np.abs(O.coherence_weighted_phasor(x, 200, 100) - O.coherence_welch(x, 200, 100))) < 1e-10
+    # one segment dominating the amplitude by 1e3 -> ~1
+    y = rng.standard_normal((2, 1000, 1))
+    y[:, :100] *= 1e3
+    c = O.coherence_weighted_phasor(y, 100, 0)
+    assert np.all(c[1:-1] > 0.99)
+
+
+def test_imaginary_coherency_kats():
+    W, ov = 100, 50
+    T = 40 * 50 + 50
+    t = np.arange(T)
+    k = 10
+    w0 = 2 * np.pi * k / W
+    rng = np.random.default_rng(43)
+    x = rng.standard_normal((1, T, 1))
+    assert np.max(O.imaginary_coherency(np.concatenate([x, x]), W, ov)) < 1e-12
+    for shift, scale in ((np.pi / 2, 1.0), (np.pi / 6, 0.5)):
+        s = np.stack([np.cos(w0 * t), np.cos(w0 * t + shift)])[:, :, None]
+        ic = O.imaginary_coherency(s, W, ov)[k]
+        assert abs(ic - scale * O.coherence_welch(s, W, ov)[k]) < 0.02
+
+
+def test_band_coherence_and_bins():
+    W = 200
+    assert O.welch_bins(W, 0.570 * np.pi, 0.600 * np.pi) == (57, 4)
+    flat = np.full(W // 2 + 1, 0.3)
+    assert O.band_coherence(flat, W, 0.5, 1.0, "max") == 0.3
+    assert abs(O.band_coherence(flat, W, 0.5, 1.0, "mean") - 0.3) < 1e-15
+    peak = flat.copy()
+    peak[20] = 0.9
+    lo, hi = 2 * np.pi * 18 / W, 2 * np.pi * 22 / W
+    assert O.band_coherence(peak, W, lo, hi, "max") == 0.9
+    assert O.band_coherence(peak, W, lo, hi, "mean") < 0.9
+    with pytest.raises(O.EmptyBandError):
+        O.band_coherence(flat, W, 0.0101, 0.0102)
+    with pytest.raises(O.WindowTooLongError):
+        O.coherence_welch(np.zeros((2, 50, 1)), 100, 10)
+
+
+def test_coherence_matrix_matches_pairwise():
+    rng = np.random.default_rng(44)
+    x = rng.standard_normal((5, 1200, 2))
+    x[3] = 0.6 * x[1] + 0.4 * x[3]
+    W, ov, lo, hi = 100, 50, 0.3, 1.2
+    for mode in ("max", "mean"):
+        M = O.coherence_matrix(x, W, ov, lo, hi, mode)
+        for i in range(5):
+            for j in range(5):
+                if i == j:
+                    continue
+                c = O.coherence_welch(x[[i, j]], W, ov)
+                ic = O.imaginary_coherency(x[[i, j]], W, ov)
+                assert abs(M["coh"][i, j] - O.band_coherence(c, W, lo, hi, mode)) < 1e-12
+                assert abs(M["icoh"][i, j] - O.band_coherence(ic, W, lo, hi, mode)) < 1e-12
