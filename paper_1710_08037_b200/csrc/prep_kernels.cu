@@ -326,9 +326,22 @@ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
   for (int k1 = 1; k1 < 4; ++k1)
 #pragma unroll
     for (int n2 = 1; n2 < 4; ++n2) {
-      float2 tw = w16(n2 * k1);
-      if (INV) tw.y = -tw.y;
-      v[4 * k1 + n2] = cmul(v[4 * k1 + n2], tw);
+      const int m = n2 * k1;
+      float2& x = v[4 * k1 + n2];
+      const float c2 = 0.70710678118654752f;
+      // W16^m with the trivial factors spelled out (the compiler may not fold
+      // multiplications by 0 / +-1 under IEEE semantics)
+      if (m == 4) {
+        x = INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
+      } else if (m == 2) {
+        x = INV ? make_float2((x.x - x.y) * c2, (x.x + x.y) * c2) : make_float2((x.x + x.y) * c2, (x.y - x.x) * c2);
+      } else if (m == 6) {
+        x = INV ? make_float2(-(x.x + x.y) * c2, (x.x - x.y) * c2) : make_float2((x.y - x.x) * c2, -(x.x + x.y) * c2);
+      } else {
+        float2 tw = w16(m);
+        if (INV) tw.y = -tw.y;
+        x = cmul(x, tw);
+      }
     }
   // second 4-point DFTs over n2 -> X[k1 + 4 k2] lands in v[4 k1 + k2]
 #pragma unroll
