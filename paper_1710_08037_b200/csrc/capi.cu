@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -857,6 +858,32 @@ ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
   return PS_OK;
 }
 
+// PS_PIPE_TRACE=1: per-stage event timeline of the pipelined host path on stderr
+struct PipeTrace {
+  cudaEvent_t t0 = nullptr;
+  std::vector<std::tuple<cudaEvent_t, const char*, int>> ev;
+  explicit PipeTrace(cudaStream_t st) {
+    cudaEventCreate(&t0);
+    cudaEventRecord(t0, st);
+  }
+  void rec(cudaStream_t st, const char* what, int s) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.emplace_back(e, what, s);
+  }
+  void dump() {
+    for (auto& x : ev) {
+      cudaEventSynchronize(std::get<0>(x));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t0, std::get<0>(x));
+      std::fprintf(stderr, "[pipe] %-6s stage %2d  %8.2f ms\n", std::get<1>(x), std::get<2>(x), ms);
+      cudaEventDestroy(std::get<0>(x));
+    }
+    cudaEventDestroy(t0);
+  }
+};
+
 // E2E host path, pipelined over column stages (the "growing square"):
 // stage s owns output columns [cols[s], cols[s+1]).  Its Gram tiles need
 // only signal rows < cols[s+1], and once they are done the output block
@@ -902,6 +929,9 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   ps_plv_args d = *a;
   d.input = c->hin.p;
   const long long U = g.B * g.R;
+  static const bool want_trace = std::getenv("PS_PIPE_TRACE") != nullptr;
+  std::unique_ptr<PipeTrace> trace_holder(want_trace ? new PipeTrace(si) : nullptr);
+  PipeTrace* trace = trace_holder.get();
   // ---- copy-in + normalise, per stage --------------------------------------
   for (int s = 0; s < S; ++s) {
     for (long long u = 0; u < U; ++u) {
@@ -911,15 +941,18 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
       PS_CUDA(cudaMemcpyAsync(static_cast<char*>(c->hin.p) + off * esz, static_cast<const char*>(a->input) + off * esz,
                               (size_t)len * esz, cudaMemcpyHostToDevice, si));
     }
+    if (trace) trace->rec(si, "h2d", s);
     for (long long u = 0; u < U; ++u)
       PS_TRY(prepare_rows(c, &d, g, c->hin.p, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride,
                           u * g.N + cols[s], u * g.N + cols[s + 1], si, &copied));
+    if (trace) trace->rec(si, "norm", s);
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), si));
   }
   // ---- Gram per stage ------------------------------------------------------
   for (int s = 0; s < S; ++s) {
     PS_CUDA(cudaStreamWaitEvent(sc, pool_event(c, 3 * s), 0));
     PS_TRY(launch_stage(c, k, s, sc));
+    if (trace) trace->rec(sc, "gram", s);
     PS_CUDA(cudaMemcpyAsync(&c->h_cnt[s], &c->d_status->n_illcond, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                             sc));
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s + 1), sc));
@@ -955,8 +988,11 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
                                     (size_t)c0 * oes, (size_t)(c1 - c0), cudaMemcpyDeviceToHost, so));
       }
     }
+    if (trace && s + 1 < S) trace->rec(so, "d2h", s);
   }
+  if (trace) trace->rec(so, "d2h", S - 1);
   PS_CUDA(cudaStreamSynchronize(so));
+  if (trace) trace->dump();
   ps_status st = read_status(c, so);
   if (res) {
     std::memset(res, 0, sizeof(*res));
