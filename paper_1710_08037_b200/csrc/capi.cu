@@ -92,7 +92,8 @@ struct ps_ctx {
   // host (e2e) pipeline: copy-in / compute / refine / copy-out streams
   cudaStream_t s_in = nullptr, s_comp = nullptr, s_ref = nullptr, s_out = nullptr;
   std::vector<cudaEvent_t> evpool;
-  unsigned long long* h_cnt = nullptr;  // pinned per-stage refine-queue counters
+  unsigned long long* h_cnt = nullptr;  // mapped pinned per-stage refine-queue counters
+  unsigned long long* d_cnt = nullptr;  // device alias of h_cnt
   int h_cnt_cap = 0;
 };
 
@@ -852,7 +853,9 @@ ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
   if (c->h_cnt_cap < n_stages) {
     if (c->h_cnt) cudaFreeHost(c->h_cnt);
     c->h_cnt = nullptr;
-    PS_CUDA(cudaMallocHost(&c->h_cnt, (size_t)n_stages * sizeof(unsigned long long)));
+    PS_CUDA(cudaHostAlloc(&c->h_cnt, (size_t)n_stages * sizeof(unsigned long long),
+                          cudaHostAllocMapped | cudaHostAllocPortable));
+    PS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_cnt), c->h_cnt, 0));
     c->h_cnt_cap = n_stages;
   }
   return PS_OK;
@@ -898,9 +901,19 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     const char* s = std::getenv("PS_STAGE_W");  // experiment override (signals per stage)
     return s ? std::atoll(s) : 0LL;
   }();
-  const long long W = w_env > 0 ? round_up(w_env, 256) : std::max<long long>(1024, round_up((g.N + 7) / 8, 256));
+  // Stage widths grow (1024, 1536, 2048, ... up to ~N/6): the first output
+  // blocks become final after a short H2D so the D2H engine -- the critical
+  // path, 4.8 GB at C5 -- starts early; later stages are wide enough to fill
+  // the GPU.  PS_STAGE_W forces a uniform width (experiments).
   std::vector<long long> cols;
-  for (long long x = 0; x < g.N; x += W) cols.push_back(x);
+  if (w_env > 0) {
+    const long long W = round_up(w_env, 256);
+    for (long long x = 0; x < g.N; x += W) cols.push_back(x);
+  } else {
+    const long long wmax = std::max<long long>(1024, round_up((g.N + 5) / 6, 256));
+    long long w = 1024;
+    for (long long x = 0; x < g.N; x += w, w = std::min(wmax, w + 512)) cols.push_back(x);
+  }
   cols.push_back(g.N);
   const int S = (int)cols.size() - 1;
   PS_TRY(ensure_pipeline(c, S));
@@ -953,8 +966,10 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     PS_CUDA(cudaStreamWaitEvent(sc, pool_event(c, 3 * s), 0));
     PS_TRY(launch_stage(c, k, s, sc));
     if (trace) trace->rec(sc, "gram", s);
-    PS_CUDA(cudaMemcpyAsync(&c->h_cnt[s], &c->d_status->n_illcond, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            sc));
+    // the refine-queue count reaches the host through a store into mapped
+    // pinned memory: a cudaMemcpyAsync here would wait behind the bulk D2H
+    // copies of earlier stages and stall the next Gram stage behind it
+    PS_CUDA(launch_copy_u64(&c->d_status->n_illcond, &c->d_cnt[s], sc));
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s + 1), sc));
   }
   // ---- refine + copy-out per stage ------------------------------------------
@@ -972,7 +987,8 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     prev = n;
     PS_CUDA(cudaStreamWaitEvent(so, ready, 0));
     const long long c0 = cols[s], c1 = cols[s + 1];
-    for (int m = 0; m < 5; ++m) {
+    static const bool no_d2h = std::getenv("PS_PIPE_NO_D2H") != nullptr;  // experiment: Gram-only timeline
+    for (int m = 0; m < 5 && !no_d2h; ++m) {
       if (!houts[m]) continue;
       for (long long sl = 0; sl < k.slots; ++sl) {
         const size_t base = (size_t)sl * g.N * g.N * oes;

@@ -984,6 +984,19 @@ cudaError_t launch_reflect_pad(const SrcDesc& src, long long row0, long long nro
   return cudaGetLastError();
 }
 
+// *dst = *src by one thread: dst may be mapped pinned host memory, so a
+// counter reaches the host without a copy-engine transfer (which would queue
+// behind bulk D2H copies of other streams)
+__global__ void copy_u64_kernel(const unsigned long long* src, volatile unsigned long long* dst) {
+  *dst = *src;
+  __threadfence_system();
+}
+
+cudaError_t launch_copy_u64(const unsigned long long* src, unsigned long long* dst, cudaStream_t st) {
+  copy_u64_kernel<<<1, 1, 0, st>>>(src, dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_welch_segments(const SrcDesc& src, long long rows, int nseg, int W, int hop, const double* win,
                                   void* seg, int dst_double, cudaStream_t st) {
   const int g = grid_for(rows * nseg * (long long)W, 256);

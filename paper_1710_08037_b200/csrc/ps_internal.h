@@ -111,6 +111,8 @@ cudaError_t launch_spectrum_mul(void* spec, long long nrows, long long nb, const
 cudaError_t launch_zero_tail(void* y, long long nrows, long long L, long long Lf, int is_double, cudaStream_t st);
 cudaError_t launch_trim_rows(const void* y, long long nrows, long long ld, long long pad, long long T, void* out,
                              int is_double, cudaStream_t st);
+// *dst = *src on the device (dst may be mapped pinned host memory)
+cudaError_t launch_copy_u64(const unsigned long long* src, unsigned long long* dst, cudaStream_t st);
 // Welch coherence front end: tapered segments, per-bin normalised Gram operand
 // rows, and the max-over-bins band reduction
 cudaError_t launch_welch_segments(const SrcDesc& src, long long rows, int nseg, int W, int hop, const double* win,
