@@ -709,6 +709,11 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   p.status = c->d_status;
   p.illcond_tol = 4e-6f;  // 2.5x margin below the 1e-5 split-path tolerance
   p.kc_blocks = kc_blocks_default();
+  static const int dbg = [] {
+    const char* s = std::getenv("PS_DEBUG_EPI");
+    return s ? std::atoi(s) : 0;
+  }();
+  p.debug_flags = dbg;
   if (g.split && k.outs[2]) {
     const int cap = 1 << 22;  // queued ill-conditioned ciPLV (pair, round) entries
     PS_TRY(ensure(c->refine, (size_t)cap * sizeof(RefineEntry)));

@@ -28,14 +28,19 @@ __device__ __forceinline__ PairMetrics<S> pair_metrics(S gre, S gim, S inv_t) {
   PairMetrics<S> m;
   const S cre = gre * inv_t, cim = gim * inv_t;
   const S are = fabs(cre), aim = fabs(cim);
-  S plv = sqrt(cre * cre + cim * cim);
+  S plv;
   S ci;
   if (SPLIT) {
+    // MUFU.RSQ-based magnitude and ciPLV denominator: ~2 ulp, far below the
+    // 1e-5 budget, and no IEEE sqrt / division sequences in the epilogue
+    const S ss = cre * cre + cim * cim;
+    plv = ss * rsqrtf(fmaxf(ss, S(1e-30)));  // < 1e-15 off below the clamp, exact 0 at 0
     plv = plv > S(1) ? S(1) : plv;
     const S d = (S(1) - are) * (S(1) + are);
-    ci = d > S(0) ? aim * rsqrtf(d) : S(0);  // MUFU.RSQ: ~2 ulp, far below the 1e-5 budget
+    ci = d > S(0) ? aim * rsqrtf(d) : S(0);
     ci = ci > S(1) ? S(1) : ci;
   } else {
+    plv = sqrt(cre * cre + cim * cim);
     ci = (are >= S(1) - S(1e-12)) ? S(0) : aim / sqrt(S(1) - cre * cre);
   }
   m.plv = plv;
@@ -157,8 +162,8 @@ __device__ __forceinline__ void emit4_all(const GramParams& p, long long slot, i
       a = make_float4(a.x / d, a.y / d, a.z / d, a.w / d);
     }
     float* base = outs[q] + off;
-    *reinterpret_cast<float4*>(base + (long long)i * N + j0) = a;
-    if (last) {
+    if (!(p.debug_flags & 8)) *reinterpret_cast<float4*>(base + (long long)i * N + j0) = a;
+    if (last && !(p.debug_flags & 4)) {
       const float s = q == 4 ? -1.f : 1.f;
       base[(long long)(j0 + 0) * N + i] = s * a.x;
       base[(long long)(j0 + 1) * N + i] = s * a.y;

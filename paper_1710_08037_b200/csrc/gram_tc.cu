@@ -102,6 +102,51 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
   const long long Tobs = (long long)p.T * ri.nu;
   const float inv_t = 1.0f / static_cast<float>(Tobs);
   unsigned illc = 0;
+  // Interior warp block: all 32 rows of this warp lie strictly above all
+  // HALF columns of its slice and inside the matrix -- no per-pair diagonal /
+  // bounds / mask logic (every tile off the diagonal band takes this path).
+  const int lane = threadIdx.x & 31;
+  const int ib = i - lane, jb = w.J * BN + h * HALF;
+  const bool interior = !any_masked && (p.N & 3) == 0 && ib + 31 < jb && jb + HALF <= p.N;
+  if (interior) {
+    // ill-conditioning test of the general path, 1e-6 (|cim| are / d + 1) >
+    // tol sqrt(d), multiplied through by d / 1e-6 (d > 0): no division
+    const float kt = p.illcond_tol * 1e6f;
+#pragma unroll 1
+    for (int g = 0; g < HALF; g += 4) {
+      uint32_t vre[4], vim[4];
+      ptx::tmem_ld_32x32b_x4(ta + g, vre);
+      ptx::tmem_ld_32x32b_x4(ta + BN + g, vim);
+      ptx::tmem_wait_ld();
+      const int j0 = jb + g;
+      PairMetrics<float> m4[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        m4[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_t);
+        const float are = fabsf(m4[e].cre);
+        const float d = (1.0f - are) * (1.0f + are);
+        if (d > 0.0f && m4[e].iplv * are + d > kt * d * d * rsqrtf(d)) {
+          ++illc;
+          if (p.refine) {
+            const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
+            if (k < (unsigned long long)p.refine_cap) {
+              RefineEntry en;
+              en.slot = (int)ri.slot;
+              en.i = i;
+              en.j = j0 + e;
+              en.u0 = ri.u0;
+              en.nu = ri.nu;
+              en.approx = m4[e].ciplv;
+              p.refine[k] = en;
+            }
+          }
+        }
+      }
+      emit4_all(p, ri.slot, i, j0, m4, ri.first, ri.last);
+    }
+    if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+    return;
+  }
 #pragma unroll 1
   for (int g = 0; g < HALF; g += 4) {
     uint32_t vre[4], vim[4];
@@ -343,16 +388,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
           ptx::tc_fence_after();
           const uint32_t ta = tmem + lane_base + (uint32_t)buf * BUF_COLS + (uint32_t)(h * HALF);
-          add_chunk(sre, ta);
-          add_chunk(sim, ta + BN);
+          // single-chunk rounds (short K: over_trials, coherence, T <= 128):
+          // the chunk accumulator already is the round's sum (0 + x = x), so
+          // it is emitted in place -- no drain / park round trip through TMEM
+          const bool direct = nchunks == 1 && !p.pool;
+          if (!direct) {
+            add_chunk(sre, ta);
+            add_chunk(sim, ta + BN);
+          }
           if (c == nchunks - 1 && (!p.pool || r == r1 - 1)) {
             // Round complete: park the fp32 sums back in this (still owned)
             // TMEM buffer and emit from there with a compact loop, so the
             // 64 register sums are dead during the store-heavy epilogue.
-            store_sums(sre, ta);
-            store_sums(sim, ta + BN);
-            ptx::tmem_wait_st();
-            emit_round(p, w, r, r0, r1, ta, i, h, any_masked);
+            if (!direct) {
+              store_sums(sre, ta);
+              store_sums(sim, ta + BN);
+              ptx::tmem_wait_st();
+            }
+            if (!(p.debug_flags & 1)) emit_round(p, w, r, r0, r1, ta, i, h, any_masked);
 #pragma unroll
             for (int k = 0; k < HALF; ++k) sre[k] = sim[k] = 0.0f;  // sums dead across the emission
           }

@@ -785,35 +785,62 @@ __global__ void group_reduce_kernel(const S* ws, int G, long long slot_elems, lo
 // Gram's K axis runs over trials.  src [P][B*R][N][Tp] -> dst [P][B*T][N][Rp]
 // (P = 4 fp16 planes or 2 f64 planes), trial padding zeroed; maskcount_dst
 // [(b*T + t)*N + n] = number of masked trials (masked samples are exactly 0 in
-// every plane).  One thread per (b, n, t); reads are coalesced along t.
+// every plane).
+// One block per (band, signal, 32-sample tile): the [R][32] slab of every
+// plane goes through shared memory in 32 x 32 tiles, so reads run along t and
+// writes along r (both coalesced); a trial is masked at sample t when all its
+// planes are zero there (warp ballot per written row).
+constexpr int kTrTile = 32;
 template <typename E, int P>
-__global__ void transpose_trials_kernel(const E* __restrict__ src, long long sps, int Tp, E* __restrict__ dst,
-                                        long long dps, int Rp, int B, int R, int N, int T,
-                                        int* __restrict__ maskcount_dst) {
-  const long long total = (long long)B * N * T;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int t = (int)(e % T);
-    const long long bn = e / T;
-    const int n = (int)(bn % N);
-    const int b = (int)(bn / N);
-    const long long drow = ((long long)(b * T + t) * N + n) * Rp;
-    int masked = 0;
-    for (int r = 0; r < R; ++r) {
+__global__ void __launch_bounds__(kTrTile * 8) transpose_trials_kernel(
+    const E* __restrict__ src, long long sps, int Tp, E* __restrict__ dst, long long dps, int Rp, int B, int R, int N,
+    int T, int* __restrict__ maskcount_dst) {
+  __shared__ E tile[P][kTrTile][kTrTile + 1];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int ntt = (T + kTrTile - 1) / kTrTile;
+  const long long blk = blockIdx.x;
+  const int tt = (int)(blk % ntt);
+  const long long bn = blk / ntt;
+  const int n = (int)(bn % N);
+  const int b = (int)(bn / N);
+  const int t0 = tt * kTrTile;
+  int masked = 0;  // per written row t = t0 + ty + k*8, accumulated by lane 0 of the warp
+  int mk[kTrTile / 8] = {};
+  for (int r0 = 0; r0 < Rp; r0 += kTrTile) {
+#pragma unroll
+    for (int k = 0; k < kTrTile / 8; ++k) {
+      const int r = r0 + ty + 8 * k, t = t0 + tx;
       const long long sidx = ((long long)(b * R + r) * N + n) * Tp + t;
+#pragma unroll
+      for (int pl = 0; pl < P; ++pl) tile[pl][ty + 8 * k][tx] = (r < R && t < T) ? src[pl * sps + sidx] : E(0.0f);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kTrTile / 8; ++k) {
+      const int t = t0 + ty + 8 * k, r = r0 + tx;
       bool zero = true;
+      E v[P];
 #pragma unroll
       for (int pl = 0; pl < P; ++pl) {
-        const E v = src[pl * sps + sidx];
-        dst[pl * dps + drow + r] = v;
-        zero = zero && (static_cast<float>(v) == 0.0f);
+        v[pl] = tile[pl][tx][ty + 8 * k];
+        zero = zero && (static_cast<float>(v[pl]) == 0.0f);
       }
-      masked += zero ? 1 : 0;
-    }
-    for (int r = R; r < Rp; ++r)
+      if (t < T && r < Rp) {
+        const long long didx = ((long long)(b * T + t) * N + n) * Rp + r;
 #pragma unroll
-      for (int pl = 0; pl < P; ++pl) dst[pl * dps + drow + r] = E(0.0f);
-    maskcount_dst[(long long)(b * T + t) * N + n] = masked;
+        for (int pl = 0; pl < P; ++pl) dst[pl * dps + didx] = v[pl];
+      }
+      mk[k] += __popc(__ballot_sync(0xffffffffu, zero && r < R));
+    }
+    __syncthreads();
+  }
+  (void)masked;
+  if (tx == 0) {
+#pragma unroll
+    for (int k = 0; k < kTrTile / 8; ++k) {
+      const int t = t0 + ty + 8 * k;
+      if (t < T) maskcount_dst[(long long)(b * T + t) * N + n] = mk[k];
+    }
   }
 }
 
@@ -1249,15 +1276,18 @@ cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nr
 
 cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void* dst, long long dps, int Rp, int B,
                                     int R, int N, int T, int split, int* maskcount_dst, cudaStream_t st) {
-  const int g = grid_for((long long)B * N * T, 256);
+  const long long blocks = (long long)B * N * ((T + kTrTile - 1) / kTrTile);
+  if (blocks <= 0) return cudaSuccess;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const unsigned g = (unsigned)blocks;
   if (split)
-    transpose_trials_kernel<__half, 4><<<g, 256, 0, st>>>(static_cast<const __half*>(src), sps, Tp,
-                                                          static_cast<__half*>(dst), dps, Rp, B, R, N, T,
-                                                          maskcount_dst);
+    transpose_trials_kernel<__half, 4><<<g, kTrTile * 8, 0, st>>>(static_cast<const __half*>(src), sps, Tp,
+                                                                  static_cast<__half*>(dst), dps, Rp, B, R, N, T,
+                                                                  maskcount_dst);
   else
-    transpose_trials_kernel<double, 2><<<g, 256, 0, st>>>(static_cast<const double*>(src), sps, Tp,
-                                                          static_cast<double*>(dst), dps, Rp, B, R, N, T,
-                                                          maskcount_dst);
+    transpose_trials_kernel<double, 2><<<g, kTrTile * 8, 0, st>>>(static_cast<const double*>(src), sps, Tp,
+                                                                  static_cast<double*>(dst), dps, Rp, B, R, N, T,
+                                                                  maskcount_dst);
   return cudaGetLastError();
 }
 

@@ -81,6 +81,7 @@ struct GramParams {
   RefineEntry* refine;         // queue of flagged pairs (nullptr: count only)
   int refine_cap;
   int kc_blocks;               // split kernel: K blocks per TMEM accumulation chunk (drain period)
+  int debug_flags;             // experiments only (PS_DEBUG_EPI): 1 = skip the metric emission
 };
 
 // ---- launchers (return cudaError_t) --------------------------------------
