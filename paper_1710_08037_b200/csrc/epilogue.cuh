@@ -173,6 +173,45 @@ __device__ __forceinline__ void emit4_all(const GramParams& p, long long slot, i
   }
 }
 
+// 32-byte global accesses (STG.E.256 / LDG.E.256 on sm_100a)
+__device__ __forceinline__ void st_v8(float* p, const float (&v)[8]) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+// Eight consecutive columns j0..j0+7 of row i in the FIRST round of their
+// slot (plain stores, nothing to accumulate), all strictly above the diagonal
+// and inside (N % 8 == 0, j0 % 8 == 0): one 32-byte store per metric for the
+// direct part (a full sector per lane), coalesced mirror stores.
+__device__ __forceinline__ void emit8_first(const GramParams& p, long long slot, int i, int j0,
+                                            const PairMetrics<float> (&m)[8], bool last) {
+  const long long N = p.N;
+  const long long off = slot * N * N;
+  float* outs[5] = {static_cast<float*>(p.out_plv), static_cast<float*>(p.out_iplv),
+                    static_cast<float*>(p.out_ciplv), static_cast<float*>(p.out_cre),
+                    static_cast<float*>(p.out_cim)};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    if (!outs[q]) continue;
+    float* base = outs[q] + off;
+    float a[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      a[e] = q == 0 ? m[e].plv : q == 1 ? m[e].iplv : q == 2 ? m[e].ciplv : q == 3 ? m[e].cre : m[e].cim;
+    if (last && p.mean_div != 1) {
+      const float d = (float)p.mean_div;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) a[e] = a[e] / d;
+    }
+    if (!(p.debug_flags & 8)) st_v8(base + (long long)i * N + j0, a);
+    if (last && !(p.debug_flags & 4)) {
+      const float s = q == 4 ? -1.f : 1.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) base[(long long)(j0 + e) * N + i] = s * a[e];
+    }
+  }
+}
+
 // Round bookkeeping common to both kernels: which slot a (item, trial) round
 // writes and whether it is the first / last contribution to that slot.
 struct RoundInfo {

@@ -112,6 +112,48 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
     // ill-conditioning test of the general path, 1e-6 (|cim| are / d + 1) >
     // tol sqrt(d), multiplied through by d / 1e-6 (d > 0): no division
     const float kt = p.illcond_tol * 1e6f;
+    auto illcond = [&](const PairMetrics<float>& m, int j) {
+      const float are = fabsf(m.cre);
+      const float d = (1.0f - are) * (1.0f + are);
+      if (d > 0.0f && m.iplv * are + d > kt * d * d * rsqrtf(d)) {
+        ++illc;
+        if (p.refine) {
+          const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
+          if (k < (unsigned long long)p.refine_cap) {
+            RefineEntry en;
+            en.slot = (int)ri.slot;
+            en.i = i;
+            en.j = j;
+            en.u0 = ri.u0;
+            en.nu = ri.nu;
+            en.approx = m.ciplv;
+            p.refine[k] = en;
+          }
+        }
+      }
+    };
+    if (ri.first && (p.N & 7) == 0) {
+      // first round of the slot: 8 columns per step, 32-byte direct stores
+#pragma unroll 1
+      for (int g = 0; g < HALF; g += 8) {
+        uint32_t vre[8], vim[8];
+        ptx::tmem_ld_32x32b_x4(ta + g, *reinterpret_cast<uint32_t(*)[4]>(&vre[0]));
+        ptx::tmem_ld_32x32b_x4(ta + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vre[4]));
+        ptx::tmem_ld_32x32b_x4(ta + BN + g, *reinterpret_cast<uint32_t(*)[4]>(&vim[0]));
+        ptx::tmem_ld_32x32b_x4(ta + BN + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vim[4]));
+        ptx::tmem_wait_ld();
+        const int j0 = jb + g;
+        PairMetrics<float> m8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          m8[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_t);
+          illcond(m8[e], j0 + e);
+        }
+        emit8_first(p, ri.slot, i, j0, m8, ri.last);
+      }
+      if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+      return;
+    }
 #pragma unroll 1
     for (int g = 0; g < HALF; g += 4) {
       uint32_t vre[4], vim[4];
