@@ -11,12 +11,15 @@ point raises NativeLibraryError.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
 from . import errors
 
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
+if os.environ.get("PS_LIB_VARIANT"):  # A/B experiments: libphasesync_cuda.<variant>.so next to the default
+    LIB_PATH = LIB_PATH.with_name(f"libphasesync_cuda.{os.environ['PS_LIB_VARIANT']}.so")
 ABI_VERSION = 3
 
 # ps_status -> exception class (include/phasesync.h)
