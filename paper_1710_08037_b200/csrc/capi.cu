@@ -81,6 +81,7 @@ struct ps_ctx {
   Buf xw, spec, hbuf, planes, rowstat, maskcount, items, gws, hin, hout, refine, refine_sorted, planes_t, maskcount_t;
   Buf fir_taps, fir_spec;  // band-pass front end: padded taps, filter spectrum (double)
   Buf cohws;               // coherence: per-bin matrices before the max-over-bins reduction
+  Buf lockbuf;             // Gram producer lockstep counters (one launch at a time per ctx)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
   std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
@@ -777,6 +778,34 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
   if (p.n_items <= 0) return PS_OK;
   const int cta_per_group = k.g.split ? split_cta_group() : 1;
   const int grid = std::min(p.n_items, c->num_sms / cta_per_group);
+  // producer lockstep (GramParams::lock_cnt): needs the same number of K
+  // blocks in every item; PS_LOCKSTEP="group,lag" in K blocks ("0" = off)
+  static const std::pair<int, int> lk = [] {
+    const char* s = std::getenv("PS_LOCKSTEP");
+    int g = 32, l = 2;
+    if (s) {
+      g = std::atoi(s);
+      const char* comma = std::strchr(s, ',');
+      if (comma) l = std::max(1, std::atoi(comma + 1));
+    }
+    return std::make_pair(g, l);
+  }();
+  p.lock_cnt = nullptr;
+  const bool uniform = k.pool || (k.g.R % k.Rg) == 0;
+  if (k.g.split && lk.first > 0 && uniform) {
+    const long long rounds = k.pool ? k.g.R : k.Rg;
+    const long long nk = (k.g.T + kSplitBK - 1) / kSplitBK;
+    const long long per_cta = (long long)((p.n_items + grid - 1) / grid) * rounds * nk;
+    const long long ngroups = per_cta / lk.first + 2;
+    // sized generously once: a reallocation would synchronise the device and
+    // break the overlap of the pipelined host path's stages
+    PS_TRY(ensure(c->lockbuf, (size_t)std::max<long long>(ngroups, 1 << 16) * sizeof(int)));
+    PS_CUDA(cudaMemsetAsync(c->lockbuf.p, 0, (size_t)ngroups * sizeof(int), st));
+    p.lock_cnt = static_cast<int*>(c->lockbuf.p);
+    p.lock_group = lk.first;
+    p.lock_lag = lk.second;
+    p.lock_rounds = (int)rounds;
+  }
   if (k.g.split) PS_CUDA(launch_gram_split(k.ta, k.tb, p, grid, st));
   else PS_CUDA(launch_gram_f64(p, grid, st));
   c->launches++;
@@ -1092,7 +1121,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
-                 &c->fir_spec, &c->cohws})
+                 &c->fir_spec, &c->cohws, &c->lockbuf})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);

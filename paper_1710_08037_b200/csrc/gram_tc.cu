@@ -305,15 +305,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // lockstep bookkeeping (see GramParams::lock_cnt)
+      const bool lock = p.lock_cnt != nullptr;
+      const long long S = p.lock_group;
+      const long long rk = (long long)p.lock_rounds * nk;                 // K blocks per item
+      const int c_full = (p.n_items + ngrp - 1) / ngrp;                    // items of the busiest groups
+      const int n_full = p.n_items - (c_full - 1) * ngrp;                  // groups with c_full items
+      auto expected = [&](long long g) -> int {                            // producers that pass group g
+        const long long e0 = g * S;
+        if (e0 < (long long)(c_full - 1) * rk) return CG * ngrp;
+        if (e0 < (long long)c_full * rk) return CG * n_full;
+        return 0;
+      };
+      long long e = 0;  // K blocks issued by this producer
       for (int it = grp; it < p.n_items; it += ngrp) {
         const Item w = p.items[it];
         const int r0 = p.pool ? 0 : w.g * p.Rg;
         const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
-        const int rowA = w.I * G::UMMA_M + (int)rank * BMC;
-        const int rowB = w.J * BN + (int)rank * G::BNC;
+        // (debug_flags & 16: every item streams panel 0 -- operands L2-resident,
+        // results meaningless; measures the kernel without DRAM operand traffic)
+        const bool l2only = (p.debug_flags & 16) != 0;
+        const int rowA = (l2only ? 0 : w.I * G::UMMA_M) + (int)rank * BMC;
+        const int rowB = (l2only ? 0 : w.J * BN) + (int)rank * G::BNC;
         for (int r = r0; r < r1; ++r) {
           const int u = w.b * p.R + r;
           for (int kb = 0; kb < nk; ++kb) {
+            if (lock && e > 0 && e % S == 0) {
+              const long long g = e / S;
+              atomicAdd(&p.lock_cnt[g - 1], 1);  // group g-1 fully issued
+              if (g - p.lock_lag >= 0) {
+                const long long gw = g - p.lock_lag;
+                const int need = expected(gw);
+                const long long t0 = clock64();
+                while (ptx::ld_acquire_gpu(&p.lock_cnt[gw]) < need) {
+                  __nanosleep(256);
+                  if (clock64() - t0 > 2000000000LL) break;  // ~1 s: pacing only, never a hang
+                }
+              }
+            }
+            ++e;
             ptx::mbar_wait(&empty[stage], phase ^ 1u, tflag);
             uint8_t* sa = smem + stage * G::STAGE_BYTES;
             if (CG == 1) {
@@ -333,6 +363,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
+      if (lock && e > 0) atomicAdd(&p.lock_cnt[(e - 1) / S], 1);  // last (possibly partial) group
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (rank 0) =====================

@@ -82,6 +82,15 @@ struct GramParams {
   int refine_cap;
   int kc_blocks;               // split kernel: K blocks per TMEM accumulation chunk (drain period)
   int debug_flags;             // experiments only (PS_DEBUG_EPI): 1 = skip the metric emission
+  // Producer lockstep (split kernel): every producer publishes each group of
+  // lock_group issued K blocks in lock_cnt[group] and may not run more than
+  // lock_lag groups ahead of the slowest producer, so the CTAs that share an
+  // operand panel stream it through L2 together (one DRAM read per panel
+  // slice instead of one per CTA).  lock_cnt == nullptr disables it.
+  int* lock_cnt;
+  int lock_group;
+  int lock_lag;
+  int lock_rounds;             // rounds per item (uniform across items when enabled)
 };
 
 // ---- launchers (return cudaError_t) --------------------------------------
