@@ -82,6 +82,7 @@ struct ps_ctx {
   Buf fir_taps, fir_spec;  // band-pass front end: padded taps, filter spectrum (double)
   Buf cohws;               // coherence: per-bin matrices before the max-over-bins reduction
   Buf lockbuf;             // Gram producer lockstep counters (one launch at a time per ctx)
+  Buf hscale;              // per-row factors restoring H after scaled packing (odd T)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
   std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
@@ -202,6 +203,7 @@ SrcDesc make_src(const ps_plv_args* a, const Geometry& g, const void* ptr) {
   s.hbuf = nullptr;
   s.h_row0 = 0;
   s.h_ld = g.T;
+  s.h_scale = nullptr;
   return s;
 }
 
@@ -254,15 +256,27 @@ long long hilbert_chunk_rows(const Geometry& g) {
 }
 
 // Hilbert stage for rows [row0, row0+nr): leaves H{x} (compute type) in c->hbuf.
+// For odd T cuFFT's batched R2C transforms two rows as one complex sequence,
+// so a row's rounding error scales with its partner's magnitude: the rows are
+// then packed with a per-row power-of-two scale first and *h_scale receives
+// the per-row factors that restore H (SrcDesc::h_scale; nullptr otherwise).
 ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const SrcDesc& src, long long row0,
-                        long long nr, cudaStream_t st, bool* copied) {
+                        long long nr, cudaStream_t st, bool* copied, const void** h_scale) {
   const size_t es = g.cdouble ? 8 : 4;
   const long long nb = g.T / 2 + 1;
   PS_TRY(ensure(c->spec, (size_t)nr * nb * 2 * es));
   PS_TRY(ensure(c->hbuf, (size_t)nr * g.T * es));
   const void* in = nullptr;
   long long idist = g.T;
-  if (fft_direct(a, g)) {
+  *h_scale = nullptr;
+  if (g.T % 2 == 1) {
+    PS_TRY(ensure(c->xw, (size_t)nr * g.T * es));
+    PS_TRY(ensure(c->hscale, (size_t)nr * es));
+    PS_CUDA(launch_pack_real_scaled(src, row0, nr, c->xw.p, c->hscale.p, g.cdouble ? 1 : 0, st));
+    c->launches++;
+    in = c->xw.p;
+    *h_scale = c->hscale.p;
+  } else if (fft_direct(a, g)) {
     in = static_cast<const char*>(src.ptr) + (size_t)row0 * a->stride_signal * es;
     idist = a->stride_signal;
   } else {
@@ -300,8 +314,10 @@ struct FirGeom {
   long long P = 0, L = 0, Lf = 0, nt = 0;
 };
 
-long long next_fast_len(long long n) {  // smallest 2^a 3^b 5^c 7^d >= n
-  for (long long m = std::max(n, 1LL);; ++m) {
+long long next_fast_len(long long n) {  // smallest EVEN 2^a 3^b 5^c 7^d >= n
+  // (even: cuFFT's odd-length R2C pairs two rows of the batch into one complex
+  // transform, which would couple the rounding error of rows of unequal scale)
+  for (long long m = std::max(n + (n & 1), 2LL);; m += 2) {
     long long r = m;
     for (long long f : {2LL, 3LL, 5LL, 7LL})
       while (r % f == 0) r /= f;
@@ -333,6 +349,7 @@ ps_status prep_begin(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cudaStr
   if (a->input_kind != PS_INPUT_REAL) return PS_OK;
   const size_t es = g.cdouble ? 8 : 4;
   const long long rc = std::min(prep_chunk_rows(a, g), g.rows);
+  PS_TRY(ensure(c->hscale, (size_t)rc * es));
   if (!a->fir) {
     PS_TRY(ensure(c->spec, (size_t)rc * (g.T / 2 + 1) * 2 * es));
     PS_TRY(ensure(c->hbuf, (size_t)rc * g.T * es));
@@ -389,16 +406,22 @@ ps_status bandpass_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, con
   PS_CUDA(launch_spectrum_mul(c->spec.p, nr, nbf, c->fir_spec.p, 1, inv_lf, dbl, st));
   PS_CUFFT(c2r(inv, c->xw.p));
   c->launches += 5;
+  const bool odd = (f.L & 1) != 0;
   if (hilbert) {  // analytic signal of the padded record (length L), before the trim
     cufftHandle fl, il;
     PS_TRY(get_plan(c, (int)f.L, nr, f.Lf, g.cdouble, 0, &fl));
     PS_TRY(get_plan(c, (int)f.L, nr, f.L, g.cdouble, 1, &il));
     PS_CUFFT(cufftSetStream(fl, st));
     PS_CUFFT(cufftSetStream(il, st));
+    if (odd) {  // odd L: rows scaled by powers of two around the paired R2C (see hilbert_chunk)
+      PS_TRY(ensure(c->hscale, (size_t)nr * es));
+      PS_CUDA(launch_scale_rows(c->xw.p, nr, f.L, f.Lf, c->hscale.p, 0, dbl, st));
+    }
     PS_CUFFT(r2c(fl, c->xw.p));
     PS_CUDA(launch_hilbert_spectrum(c->spec.p, nr, (int)f.L, dbl, st));
     PS_CUFFT(c2r(il, c->hbuf.p));
-    c->launches++;
+    if (odd) PS_CUDA(launch_scale_rows(c->xw.p, nr, f.L, f.Lf, c->hscale.p, 1, dbl, st));
+    c->launches += odd ? 3 : 1;
   }
   SrcDesc s = src;
   s.ptr = static_cast<const char*>(c->xw.p) + (f.P - row0 * f.Lf) * (long long)es;
@@ -411,6 +434,7 @@ ps_status bandpass_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, con
   s.hbuf = static_cast<const char*>(c->hbuf.p) + f.P * (long long)es;
   s.h_row0 = row0;
   s.h_ld = f.L;
+  s.h_scale = (hilbert && odd) ? c->hscale.p : nullptr;
   *fs = s;
   return PS_OK;
 }
@@ -495,7 +519,7 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
       continue;
     }
     if (a->input_kind == PS_INPUT_REAL) {
-      PS_TRY(hilbert_chunk(c, a, g, src, row0, nr, st, copied));
+      PS_TRY(hilbert_chunk(c, a, g, src, row0, nr, st, copied, &src.h_scale));
       src.hbuf = c->hbuf.p;
       src.h_row0 = row0;
     }
@@ -1121,7 +1145,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
-                 &c->fir_spec, &c->cohws, &c->lockbuf})
+                 &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1482,7 +1506,7 @@ ps_status ps_analytic_signal(ps_ctx* c, const ps_plv_args* a0, void* out) {
     if (a.fir) {
       PS_TRY(bandpass_chunk(c, &a, g, src, row0, nr, true, st, &s));
     } else {
-      PS_TRY(hilbert_chunk(c, &a, g, src, row0, nr, st, &copied));
+      PS_TRY(hilbert_chunk(c, &a, g, src, row0, nr, st, &copied, &s.h_scale));
       s.hbuf = c->hbuf.p;
       s.h_row0 = row0;
     }

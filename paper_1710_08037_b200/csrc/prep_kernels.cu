@@ -37,6 +37,7 @@ __device__ __forceinline__ void load_a(const SrcDesc& s, long long roff, long lo
   if (KIND == 0) {
     re = static_cast<S>(static_cast<const IT*>(s.ptr)[roff + t * s.s_samp]);
     im = static_cast<const S*>(s.hbuf)[(r - s.h_row0) * s.h_ld + t];
+    if (s.h_scale) im *= static_cast<const S*>(s.h_scale)[r - s.h_row0];
   } else {
     const IT* p = static_cast<const IT*>(s.ptr) + 2 * (roff + t * s.s_samp);
     re = static_cast<S>(p[0]);
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
   float amin = FLT_MAX, amax = 0.0f;
   bool bad = false;
   const long long obase = r * pitch;
+  const float hs = (KIND == 0 && src.h_scale) ? static_cast<const float*>(src.h_scale)[r - src.h_row0] : 1.0f;
 #pragma unroll
   for (int g = 0; g < kVecPer; ++g) {
     const long long t0 = (long long)ch * kVecSamplesPerBlock + ((long long)g * kNormThreads + threadIdx.x) * 4;
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
         const float4 h = *reinterpret_cast<const float4*>(static_cast<const float*>(src.hbuf) +
                                                           (r - src.h_row0) * src.h_ld + t0);
         re[0] = x.x; re[1] = x.y; re[2] = x.z; re[3] = x.w;
-        im[0] = h.x; im[1] = h.y; im[2] = h.z; im[3] = h.w;
+        im[0] = h.x * hs; im[1] = h.y * hs; im[2] = h.z * hs; im[3] = h.w * hs;
       } else {
         const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + 2 * (roff + t0));
         const float4 a = p[0], b = p[1];
@@ -724,6 +726,66 @@ __global__ void pack_real_kernel(SrcDesc src, long long row0, long long nrows, O
   }
 }
 
+// Packing copy with per-row power-of-two scaling (max |x| -> [1, 2)), for
+// lengths at which cuFFT's R2C pairs two rows of a batch into one complex
+// transform (odd T): without it the rounding error of a large row leaks into
+// its partner.  inv_scale[rl] = 1 / scale, applied to H downstream (SrcDesc::
+// h_scale); exact, since the factors are powers of two.  One block per row.
+template <typename IT, typename OT>
+__global__ void __launch_bounds__(256) pack_real_scaled_kernel(SrcDesc src, long long row0, long long nrows, OT* dst,
+                                                               OT* inv_scale) {
+  __shared__ double red[8];
+  const long long T = src.T;
+  for (long long rl = blockIdx.x; rl < nrows; rl += gridDim.x) {
+    const IT* x = static_cast<const IT*>(src.ptr) + row_offset(src, row0 + rl);
+    double m = 0.0;
+    for (long long t = threadIdx.x; t < T; t += blockDim.x) m = fmax(m, fabs((double)x[t * src.s_samp]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    for (int w = 0; w < 8; ++w) m = fmax(m, red[w]);
+    __syncthreads();
+    int e = 0;
+    if (m > 0.0 && m <= DBL_MAX) frexp(m, &e);
+    const int lim = sizeof(OT) == 4 ? 126 : 1000;
+    const int sh = min(lim, max(-lim, 1 - e));
+    const OT s = (OT)ldexp(1.0, sh);
+    for (long long t = threadIdx.x; t < T; t += blockDim.x) dst[rl * T + t] = static_cast<OT>(x[t * src.s_samp]) * s;
+    if (threadIdx.x == 0) inv_scale[rl] = (OT)ldexp(1.0, -sh);
+  }
+}
+
+// In-place per-row power-of-two scaling of y[rl][0..L) (row stride ld):
+// undo == 0: scale max |y| into [1, 2) and store the inverse factor;
+// undo == 1: multiply by the stored inverse factor (exact restore).
+template <typename S>
+__global__ void __launch_bounds__(256) scale_rows_kernel(S* y, long long nrows, long long L, long long ld, S* inv_scale,
+                                                         int undo) {
+  __shared__ double red[8];
+  for (long long rl = blockIdx.x; rl < nrows; rl += gridDim.x) {
+    S* row = y + rl * ld;
+    if (undo) {
+      const S f = inv_scale[rl];
+      for (long long t = threadIdx.x; t < L; t += blockDim.x) row[t] *= f;
+      continue;
+    }
+    double m = 0.0;
+    for (long long t = threadIdx.x; t < L; t += blockDim.x) m = fmax(m, fabs((double)row[t]));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    for (int w = 0; w < 8; ++w) m = fmax(m, red[w]);
+    __syncthreads();
+    int e = 0;
+    if (m > 0.0 && m <= DBL_MAX) frexp(m, &e);
+    const int lim = sizeof(S) == 4 ? 126 : 1000;
+    const int sh = min(lim, max(-lim, 1 - e));
+    const S s = (S)ldexp(1.0, sh);
+    for (long long t = threadIdx.x; t < L; t += blockDim.x) row[t] *= s;
+    if (threadIdx.x == 0) inv_scale[rl] = (S)ldexp(1.0, -sh);
+  }
+}
+
 // K2: one-sided Hilbert multiplier on the half spectrum, scaled by 1/T so the
 // C2R output is H{x} directly: Y_k = -i X_k / T for strictly positive bins,
 // Y_0 = Y_{T/2} = 0.
@@ -1111,6 +1173,30 @@ cudaError_t launch_pack_real(const SrcDesc& src, long long row0, long long nrows
     if (dst_double) pack_real_kernel<float, double><<<g, 256, 0, st>>>(src, row0, nrows, (double*)dst);
     else pack_real_kernel<float, float><<<g, 256, 0, st>>>(src, row0, nrows, (float*)dst);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pack_real_scaled(const SrcDesc& src, long long row0, long long nrows, void* dst, void* inv_scale,
+                                    int dst_double, cudaStream_t st) {
+  const unsigned g = (unsigned)(nrows < 148 * 16 ? nrows : 148 * 16);
+  if (nrows <= 0) return cudaSuccess;
+  if (src.is_double) {
+    if (!dst_double) return cudaErrorInvalidValue;
+    pack_real_scaled_kernel<double, double><<<g, 256, 0, st>>>(src, row0, nrows, (double*)dst, (double*)inv_scale);
+  } else if (dst_double) {
+    pack_real_scaled_kernel<float, double><<<g, 256, 0, st>>>(src, row0, nrows, (double*)dst, (double*)inv_scale);
+  } else {
+    pack_real_scaled_kernel<float, float><<<g, 256, 0, st>>>(src, row0, nrows, (float*)dst, (float*)inv_scale);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale_rows(void* y, long long nrows, long long L, long long ld, void* inv_scale, int undo,
+                              int is_double, cudaStream_t st) {
+  if (nrows <= 0) return cudaSuccess;
+  const unsigned g = (unsigned)(nrows < 148 * 16 ? nrows : 148 * 16);
+  if (is_double) scale_rows_kernel<double><<<g, 256, 0, st>>>((double*)y, nrows, L, ld, (double*)inv_scale, undo);
+  else scale_rows_kernel<float><<<g, 256, 0, st>>>((float*)y, nrows, L, ld, (float*)inv_scale, undo);
   return cudaGetLastError();
 }
 

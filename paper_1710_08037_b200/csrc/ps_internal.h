@@ -39,6 +39,7 @@ struct SrcDesc {
   const void* hbuf;          // H{x} for real input: [rows_in_chunk][T] scalar
   long long h_row0;          // first row held in hbuf
   long long h_ld;            // hbuf row stride (elements; T unless band-pass padded)
+  const void* h_scale;       // per-row factor on hbuf values ([rows_in_chunk], hbuf type), nullptr = 1
 };
 
 // An ill-conditioned ciPLV value of the split path queued for exact FP64
@@ -96,6 +97,12 @@ struct GramParams {
 // ---- launchers (return cudaError_t) --------------------------------------
 cudaError_t launch_pack_real(const SrcDesc& src, long long row0, long long nrows,
                              void* dst, int dst_double, cudaStream_t st);
+// packing copy scaled per row by a power of two (odd T: cuFFT pairs rows)
+cudaError_t launch_pack_real_scaled(const SrcDesc& src, long long row0, long long nrows, void* dst, void* inv_scale,
+                                    int dst_double, cudaStream_t st);
+// in-place per-row power-of-two scaling of [rows][L] (stride ld) / its undo
+cudaError_t launch_scale_rows(void* y, long long nrows, long long L, long long ld, void* inv_scale, int undo,
+                              int is_double, cudaStream_t st);
 cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_double,
                                     cudaStream_t st);
 // fmt: 0 split fp16 planes, 1 f64 planes, 2 complex interleaved (compute type)

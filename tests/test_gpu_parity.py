@@ -318,6 +318,58 @@ def test_fused_hilbert_t4096_bands():
     assert not res["plv"].meta["input_copied"]
 
 
+@pytest.mark.parametrize("T", [16, 30, 250, 1000, 2000, 2250, 4095, 4096, 10000, 12000])
+def test_real_input_lengths_unequal_scales(T):
+    # fp32 real rows, samples contiguous, odd and even T (4096: the fused
+    # radix-16 kernel; others: the cuFFT chain, odd T with per-row scaling),
+    # neighbouring rows 1e5 apart in scale and a zero stretch
+    rng = np.random.default_rng(T)
+    R = 2
+    x = np.ascontiguousarray(rng.standard_normal((R, 7, T)).astype(np.float32)).transpose(1, 2, 0)
+    x[3] *= 1e5          # rows sharing one packed FFT at very different scales
+    x[4, :T // 5] = 0.0  # a zero stretch (amplitude-floor fixup path)
+    ref = O.plv_family(x.astype(np.float64), input_kind="real")
+    res = C.plv_family(x, input_kind="real", precision="split")
+    check(res, ref, "split", f"real T={T}")
+    m = O.normalize_phasors(O.analytic_signal(x.astype(np.float64), axis=1))[1]
+    assert res["plv"].meta["n_masked_samples"] == int(m.sum())
+
+
+@pytest.mark.parametrize("prec,dt", [("split", np.float32), ("fp64", np.float64), ("fp64", np.float32)])
+@pytest.mark.parametrize("T", [1001, 2047])
+def test_odd_T_cufft_rows_of_unequal_scale(T, prec, dt):
+    # odd T: cuFFT's batched R2C pairs rows into one complex transform; rows
+    # are packed with per-row power-of-two scales so a 1e6-times larger
+    # neighbour does not leak its rounding error into a row
+    rng = np.random.default_rng(T + 1)
+    x = np.ascontiguousarray(rng.standard_normal((2, 9, T)).astype(dt)).transpose(1, 2, 0)
+    x[1] *= 1e6
+    x[4] *= 1e-6
+    ref = O.plv_family(x.astype(np.float64), input_kind="real")
+    res = C.plv_family(x, input_kind="real", precision=prec)
+    check(res, ref, prec, f"odd T={T} {np.dtype(dt).name}")
+    a = signalprep.analytic_signal(x).data
+    ar = O.analytic_signal(x.astype(np.float64), axis=1)
+    rel = np.max(np.abs(a - ar), axis=(1, 2)) / np.max(np.abs(ar), axis=(1, 2))
+    assert np.all(rel <= (1e-13 if dt is np.float64 else 2e-6)), rel
+    assert np.array_equal(a.real, x)  # Re(a) == x bit-exactly
+
+
+def test_bandpass_odd_padded_length_unequal_scales():
+    # L = T + 2 pad odd: the length-L Hilbert FFT of the filtered record uses
+    # the same per-row scaling
+    rng = np.random.default_rng(77)
+    x = np.ascontiguousarray(rng.standard_normal((1, 6, 1201))).transpose(1, 2, 0)
+    x[2] *= 1e6
+    f = _fir(order=100, lo=0.2, hi=0.4)
+    a = signalprep.analytic_signal(x, fir=f, pad_samples=300).data
+    ar = O.bandpass_analytic(x, f.taps, 300)
+    rel = np.max(np.abs(a - ar), axis=(1, 2)) / np.max(np.abs(ar), axis=(1, 2))
+    assert np.all(rel <= 1e-13), rel
+    res = C.plv_family(x, input_kind="real", precision="fp64", fir=f, pad_samples=300)
+    check(res, O.plv_family(x, input_kind="real", fir=(f.taps, 300)), "fp64", "bandpass odd L")
+
+
 def test_fused_hilbert_mixed_row_scales():
     # rows sharing one packed FFT differ by 1e10 in amplitude
     rng = np.random.default_rng(41)
