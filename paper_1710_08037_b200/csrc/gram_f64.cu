@@ -8,6 +8,7 @@
 //   CTA tile 64 x 64, 8 warps (2 x 4), warp tile 32 x 16 = 4 x 2 m8n8 tiles,
 //   K staged 16 samples at a time in shared memory with cp.async double
 //   buffering (rows padded to 20 doubles: conflict-free fragment loads).
+#include <algorithm>
 #include <cstdint>
 
 #include "epilogue.cuh"
@@ -171,7 +172,17 @@ cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(gram_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
   if (p.n_items <= 0) return cudaSuccess;
-  gram_f64_kernel<<<grid, NTHREADS, SMEM_BYTES, st>>>(p);
+  // `grid` is one CTA per SM; fill every resident slot (2 CTAs / SM: 80 KB of
+  // shared memory each) so the DMMA pipeline has 16 warps per SM to hide
+  // its latency
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gram_f64_kernel, NTHREADS, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    per_sm = per_sm < 1 ? 1 : per_sm;
+  }
+  const long long g = std::min<long long>((long long)grid * per_sm, p.n_items);
+  gram_f64_kernel<<<(unsigned)g, NTHREADS, SMEM_BYTES, st>>>(p);
   return cudaGetLastError();
 }
 
