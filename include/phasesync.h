@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 3
+#define PS_ABI_VERSION 4
 
 typedef enum ps_status {
   PS_OK = 0,
@@ -140,6 +140,11 @@ typedef struct ps_plv_result {
   float ms_normalize;
   float ms_gram;
   float ms_finish;
+  /* Host entry point only: bytes actually moved over the host link by the
+   * call (the pipelined path transfers one triangle's column blocks and
+   * mirrors the rest on the host). */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
 } ps_plv_result;
 
 /* ABI version check (PS_ABI_VERSION). */

@@ -20,7 +20,7 @@ from . import errors
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
 if os.environ.get("PS_LIB_VARIANT"):  # A/B experiments: libphasesync_cuda.<variant>.so next to the default
     LIB_PATH = LIB_PATH.with_name(f"libphasesync_cuda.{os.environ['PS_LIB_VARIANT']}.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # ps_status -> exception class (include/phasesync.h)
 PS_OK = 0
@@ -116,6 +116,8 @@ class PlvResult(ctypes.Structure):
         ("ms_normalize", ctypes.c_float),
         ("ms_gram", ctypes.c_float),
         ("ms_finish", ctypes.c_float),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
     ]
 
     def as_dict(self) -> dict:

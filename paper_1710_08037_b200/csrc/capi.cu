@@ -15,7 +15,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <atomic>
 #include <memory>
+#include <thread>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -919,6 +921,49 @@ ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
   return PS_OK;
 }
 
+// Host-side mirror of the pipelined copy-out: for every matrix, rows
+// [c0, c1) x cols [0, c0) := (+/-) transpose of rows [0, c0) x cols [c0, c1),
+// which the device already delivered.  Cache-blocked (64 x 64) and split over
+// host threads by row bands; PS_HOST_THREADS caps the thread count.
+template <typename S>
+void mirror_rows(S* M, long long N, long long r0, long long r1, long long c0, bool neg) {
+  constexpr long long Bk = 64;
+  for (long long rb = r0; rb < r1; rb += Bk)
+    for (long long cb = 0; cb < c0; cb += Bk) {
+      const long long re = std::min(rb + Bk, r1), ce = std::min(cb + Bk, c0);
+      for (long long r = rb; r < re; ++r) {
+        S* dst = M + r * N;
+        if (neg)
+          for (long long cc = cb; cc < ce; ++cc) dst[cc] = -M[cc * N + r];
+        else
+          for (long long cc = cb; cc < ce; ++cc) dst[cc] = M[cc * N + r];
+      }
+    }
+}
+
+void host_mirror_rows(const std::vector<std::pair<char*, bool>>& mats, int dbl, long long N, long long c0,
+                      long long c1) {
+  static const int nthreads = [] {
+    const char* s = std::getenv("PS_HOST_THREADS");
+    int n = s ? std::atoi(s) : (int)std::thread::hardware_concurrency();
+    return std::max(1, std::min(n, 64));
+  }();
+  const long long rows = c1 - c0;
+  const int nt = (int)std::max(1LL, std::min<long long>(nthreads, rows / 16));
+  auto work = [&](int t) {
+    const long long a = c0 + rows * t / nt, b = c0 + rows * (t + 1) / nt;
+    for (const auto& mb : mats) {
+      if (dbl) mirror_rows(reinterpret_cast<double*>(mb.first), N, a, b, c0, mb.second);
+      else mirror_rows(reinterpret_cast<float*>(mb.first), N, a, b, c0, mb.second);
+    }
+  };
+  std::vector<std::thread> th;
+  th.reserve(nt);
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+}
+
 // PS_PIPE_TRACE=1: per-stage event timeline of the pipelined host path on stderr
 struct PipeTrace {
   cudaEvent_t t0 = nullptr;
@@ -1000,6 +1045,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   ps_plv_args d = *a;
   d.input = c->hin.p;
   const long long U = g.B * g.R;
+  size_t h2d_bytes = 0;
   static const bool want_trace = std::getenv("PS_PIPE_TRACE") != nullptr;
   std::unique_ptr<PipeTrace> trace_holder(want_trace ? new PipeTrace(si) : nullptr);
   PipeTrace* trace = trace_holder.get();
@@ -1011,6 +1057,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
       const long long len = (cols[s + 1] - 1 - cols[s]) * a->stride_signal + (g.T - 1) * a->stride_sample + 1;
       PS_CUDA(cudaMemcpyAsync(static_cast<char*>(c->hin.p) + off * esz, static_cast<const char*>(a->input) + off * esz,
                               (size_t)len * esz, cudaMemcpyHostToDevice, si));
+      h2d_bytes += (size_t)len * esz;
     }
     if (trace) trace->rec(si, "h2d", s);
     for (long long u = 0; u < U; ++u)
@@ -1031,7 +1078,58 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s + 1), sc));
   }
   // ---- refine + copy-out per stage ------------------------------------------
+  // Both halves of every stage block cross the link by default.  With
+  // PS_HOST_MIRROR=1 only the block rows [0, c1) x cols [c0, c1) do, and a
+  // host worker fills the mirror rows [c0, c1) x cols [0, c0) with a
+  // multi-threaded cache-blocked transpose behind the D2H events (the outputs
+  // are exactly symmetric / antisymmetric): half the D2H bytes, but on the
+  // 16-core GPU hosts measured so far the transposes (~20 GB/s while the DMA
+  // writes the same memory) are slower than the link they relieve
+  // (DESIGN.md "E2E").
+  static const bool host_mirror = [] {
+    const char* s = std::getenv("PS_HOST_MIRROR");
+    return s && std::string(s) == "1";
+  }();
+  auto mirror_stage = [&](int s) {
+    const long long c0 = cols[s], c1 = cols[s + 1];
+    if (c0 == 0) return;
+    std::vector<std::pair<char*, bool>> mats;
+    for (int m = 0; m < 5; ++m) {
+      if (!houts[m]) continue;
+      for (long long sl = 0; sl < k.slots; ++sl)
+        mats.emplace_back(static_cast<char*>(houts[m]) + (size_t)sl * g.N * g.N * oes, m == 4);
+    }
+    host_mirror_rows(mats, g.split ? 0 : 1, g.N, c0, c1);
+  };
+  size_t d2h_bytes = 0;
   unsigned long long prev = 0;
+  static const bool no_d2h_env = std::getenv("PS_PIPE_NO_D2H") != nullptr;  // experiment: Gram-only timeline
+  // the mirror runs on a worker thread, stage by stage behind the D2H events,
+  // so the issue of later copies never waits for the host transposes
+  pool_event(c, 4 * (size_t)S + 2);  // create every event before the worker reads the pool
+  std::atomic<int> issued{0};
+  std::atomic<bool> abort_worker{false};
+  std::thread worker;
+  if (host_mirror && !no_d2h_env)
+    worker = std::thread([&, dev = c->device] {
+      cudaSetDevice(dev);
+      for (int s = 0; s < S; ++s) {
+        while (issued.load(std::memory_order_acquire) <= s) {
+          if (abort_worker.load()) return;
+          std::this_thread::yield();
+        }
+        if (cudaEventSynchronize(pool_event(c, 3 * S + 1 + s)) != cudaSuccess) return;
+        mirror_stage(s);
+      }
+    });
+  struct Joiner {
+    std::thread& t;
+    std::atomic<bool>& abort;
+    ~Joiner() {
+      abort.store(true);
+      if (t.joinable()) t.join();
+    }
+  } joiner{worker, abort_worker};
   for (int s = 0; s < S; ++s) {
     cudaEvent_t ready = pool_event(c, 3 * s + 1);
     PS_CUDA(cudaEventSynchronize(ready));
@@ -1056,16 +1154,23 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
         // rows [0, c1) x cols [c0, c1)
         PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * oes, pitch, dsrc + (size_t)c0 * oes, pitch,
                                   (size_t)(c1 - c0) * oes, (size_t)c1, cudaMemcpyDeviceToHost, so));
+        d2h_bytes += (size_t)(c1 - c0) * oes * (size_t)c1;
         // rows [c0, c1) x cols [0, c0)
-        if (c0 > 0)
+        if (c0 > 0 && !host_mirror) {
           PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * pitch, pitch, dsrc + (size_t)c0 * pitch, pitch,
                                     (size_t)c0 * oes, (size_t)(c1 - c0), cudaMemcpyDeviceToHost, so));
+          d2h_bytes += (size_t)c0 * oes * (size_t)(c1 - c0);
+        }
       }
     }
+    cudaEvent_t copied_ev = pool_event(c, 3 * S + 1 + s);
+    PS_CUDA(cudaEventRecord(copied_ev, so));
+    issued.store(s + 1, std::memory_order_release);
     if (trace && s + 1 < S) trace->rec(so, "d2h", s);
   }
   if (trace) trace->rec(so, "d2h", S - 1);
   PS_CUDA(cudaStreamSynchronize(so));
+  if (worker.joinable()) worker.join();  // all mirrors done
   if (trace) trace->dump();
   ps_status st = read_status(c, so);
   if (res) {
@@ -1075,6 +1180,8 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
+    res->h2d_bytes = (int64_t)h2d_bytes;
+    res->d2h_bytes = (int64_t)d2h_bytes;
   }
   std::memcpy(k.outs, houts, sizeof(houts));
   return st;
@@ -1480,6 +1587,10 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
       PS_CUDA(cudaMemcpyAsync(houts[m], static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes, out_bytes,
                               cudaMemcpyDeviceToHost, st));
   PS_CUDA(cudaStreamSynchronize(st));
+  if (res) {
+    res->h2d_bytes = (int64_t)span * esz;
+    res->d2h_bytes = (int64_t)out_bytes * q;
+  }
   return PS_OK;
 }
 
