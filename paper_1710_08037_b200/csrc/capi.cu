@@ -1086,20 +1086,26 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   // 16-core GPU hosts measured so far the transposes (~20 GB/s while the DMA
   // writes the same memory) are slower than the link they relieve
   // (DESIGN.md "E2E").
-  static const bool host_mirror = [] {
+  // PS_HOST_MIRROR=k mirrors the first k output matrices (metric order, then
+  // slot) on the host and ships the others whole -- a partial split of the
+  // mirroring between the link and the host's memory bandwidth.
+  static const int mirror_count = [] {
     const char* s = std::getenv("PS_HOST_MIRROR");
-    return s && std::string(s) == "1";
+    return s ? std::max(0, std::atoi(s)) : 0;
   }();
+  const bool host_mirror = mirror_count > 0;
+  auto mirrored = [&](long long q) { return q < mirror_count; };
   auto mirror_stage = [&](int s) {
     const long long c0 = cols[s], c1 = cols[s + 1];
     if (c0 == 0) return;
     std::vector<std::pair<char*, bool>> mats;
+    long long q = 0;
     for (int m = 0; m < 5; ++m) {
       if (!houts[m]) continue;
-      for (long long sl = 0; sl < k.slots; ++sl)
-        mats.emplace_back(static_cast<char*>(houts[m]) + (size_t)sl * g.N * g.N * oes, m == 4);
+      for (long long sl = 0; sl < k.slots; ++sl, ++q)
+        if (mirrored(q)) mats.emplace_back(static_cast<char*>(houts[m]) + (size_t)sl * g.N * g.N * oes, m == 4);
     }
-    host_mirror_rows(mats, g.split ? 0 : 1, g.N, c0, c1);
+    if (!mats.empty()) host_mirror_rows(mats, g.split ? 0 : 1, g.N, c0, c1);
   };
   size_t d2h_bytes = 0;
   unsigned long long prev = 0;
@@ -1144,9 +1150,10 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     PS_CUDA(cudaStreamWaitEvent(so, ready, 0));
     const long long c0 = cols[s], c1 = cols[s + 1];
     static const bool no_d2h = std::getenv("PS_PIPE_NO_D2H") != nullptr;  // experiment: Gram-only timeline
+    long long q = 0;
     for (int m = 0; m < 5 && !no_d2h; ++m) {
       if (!houts[m]) continue;
-      for (long long sl = 0; sl < k.slots; ++sl) {
+      for (long long sl = 0; sl < k.slots; ++sl, ++q) {
         const size_t base = (size_t)sl * g.N * g.N * oes;
         char* hdst = static_cast<char*>(houts[m]) + base;
         const char* dsrc = static_cast<const char*>(k.outs[m]) + base;
@@ -1156,7 +1163,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
                                   (size_t)(c1 - c0) * oes, (size_t)c1, cudaMemcpyDeviceToHost, so));
         d2h_bytes += (size_t)(c1 - c0) * oes * (size_t)c1;
         // rows [c0, c1) x cols [0, c0)
-        if (c0 > 0 && !host_mirror) {
+        if (c0 > 0 && !mirrored(q)) {
           PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * pitch, pitch, dsrc + (size_t)c0 * pitch, pitch,
                                     (size_t)c0 * oes, (size_t)(c1 - c0), cudaMemcpyDeviceToHost, so));
           d2h_bytes += (size_t)c0 * oes * (size_t)(c1 - c0);
