@@ -844,7 +844,11 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
 ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long long hi, cudaStream_t st) {
   if (hi <= lo || !k.g.split || !k.outs[2]) return PS_OK;
   if (hi > (unsigned long long)k.p.refine_cap)
-    return fail(PS_E_INTERNAL, "ciPLV refinement queue overflow (" + std::to_string(hi) + " pairs)");
+    return fail(PS_E_UNSUPPORTED,
+                "more than " + std::to_string(k.p.refine_cap) + " ill-conditioned ciPLV pair-rounds (" +
+                    std::to_string(hi) +
+                    "; |Re| within ~1e-3 of 1 for a large share of pairs): the split path cannot meet 1e-5 for "
+                    "them cheaply -- use precision='fp64' for this input");
   std::vector<RefineEntry> ent(hi - lo);
   PS_CUDA(cudaMemcpyAsync(ent.data(), static_cast<RefineEntry*>(c->refine.p) + lo, ent.size() * sizeof(RefineEntry),
                           cudaMemcpyDeviceToHost, st));

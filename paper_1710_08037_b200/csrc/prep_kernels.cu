@@ -1218,18 +1218,17 @@ cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long n
                                  long long plane_stride, unsigned long long* rowstat, long long rows_total,
                                  double amp_floor, DevStatus* status, cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
-  static int per_sm = 0, n_sms = 0;
-  if (per_sm == 0) {
-    cudaError_t e = cudaFuncSetAttribute(hilbert_fused4096_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kFftSmemBytes);
-    if (e != cudaSuccess) return e;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hilbert_fused4096_kernel, kFftThreads, kFftSmemBytes);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  // the attribute is per device: set it on every launch (cheap), so a process
+  // driving several GPUs gets it on each
+  cudaError_t e = cudaFuncSetAttribute(hilbert_fused4096_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kFftSmemBytes);
+  if (e != cudaSuccess) return e;
+  int dev = 0, n_sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hilbert_fused4096_kernel, kFftThreads, kFftSmemBytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
   const long long npairs = (nrows + 1) / 2;
   const long long cap = (long long)per_sm * n_sms;
   const unsigned grid = (unsigned)(npairs < cap ? npairs : cap);
