@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         return 0;
       };
       long long e = 0;  // K blocks issued by this producer
+      bool pace = true;  // cleared after a pacing timeout (counters are still published)
       for (int it = grp; it < p.n_items; it += ngrp) {
         const Item w = p.items[it];
         const int r0 = p.pool ? 0 : w.g * p.Rg;
@@ -333,13 +334,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (lock && e > 0 && e % S == 0) {
               const long long g = e / S;
               atomicAdd(&p.lock_cnt[g - 1], 1);  // group g-1 fully issued
-              if (g - p.lock_lag >= 0) {
+              if (pace && g - p.lock_lag >= 0) {
                 const long long gw = g - p.lock_lag;
                 const int need = expected(gw);
                 const long long t0 = clock64();
                 while (ptx::ld_acquire_gpu(&p.lock_cnt[gw]) < need) {
                   __nanosleep(256);
-                  if (clock64() - t0 > 2000000000LL) break;  // ~1 s: pacing only, never a hang
+                  // pacing only, never a hang: if the others do not show up
+                  // within ~0.2 s (CTAs not co-resident, e.g. the GPU is
+                  // shared) this producer stops pacing for the rest of the launch
+                  if (clock64() - t0 > 400000000LL) {
+                    pace = false;
+                    break;
+                  }
                 }
               }
             }
