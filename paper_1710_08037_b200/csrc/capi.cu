@@ -1036,6 +1036,9 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   std::memcpy(houts, k.outs, sizeof(houts));
   int nout = 0;
   for (int m = 0; m < 5; ++m) nout += houts[m] ? 1 : 0;
+  // output slots per metric, as plan_call will set k.slots (needed before it:
+  // the device outputs it builds the parameters from are allocated here)
+  k.slots = a->trial_reduce == PS_TRIALS_NONE ? g.B * g.R : g.B;
   const size_t out_bytes = (size_t)k.slots * g.N * g.N * oes;
   PS_TRY(ensure(c->hout, out_bytes * std::max(nout, 1)));
   {

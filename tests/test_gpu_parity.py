@@ -105,6 +105,32 @@ def test_pipelined_host_path_matches_device_path(kind):
         assert maxerr(h[m].values[np.ix_(idx, idx)], ref[m]) <= TOL["split"], m
 
 
+@pytest.mark.parametrize("kind", ["analytic", "real"])
+def test_pipelined_host_path_bands_and_trials(kind):
+    # the pipelined host path with several (band, trial) units and trial means:
+    # output slots per band (regression: they were sized for one slot)
+    import torch
+
+    rng = np.random.default_rng(13)
+    B, R, N, T = 2, 3, 2304, 256
+    if kind == "analytic":
+        x = (rng.standard_normal((B, R, N, T)) + 1j * rng.standard_normal((B, R, N, T))).astype(np.complex64)
+    else:
+        x = rng.standard_normal((B, R, N, T)).astype(np.float32)
+    xv = np.transpose(x, (0, 2, 3, 1))
+    h = C.plv_family(xv, input_kind=kind, bands=True)
+    assert h["plv"].values.shape == (B, N, N)
+    if kind == "analytic":  # same planes on both paths: bit-identical
+        d = C.plv_family(torch.from_numpy(x).cuda().permute(0, 2, 3, 1), input_kind=kind, bands=True)
+        for m in METRICS:
+            assert np.array_equal(h[m].values, d[m].values.cpu().numpy()), m
+    idx = np.sort(rng.choice(N, size=64, replace=False))
+    for b in range(B):
+        ref = O.plv_family(xv[b][idx], input_kind=kind)
+        for m in METRICS:
+            assert maxerr(h[m].values[b][np.ix_(idx, idx)], ref[m]) <= TOL["split"], (b, m)
+
+
 def test_staged_input_matches_device_path():
     # ps_plv_family_staged: rows arrive chunk by chunk (here: async copies on a
     # side stream standing in for the per-chunk NCCL broadcast of N>1 runs)
