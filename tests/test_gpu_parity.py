@@ -131,6 +131,33 @@ def test_pipelined_host_path_bands_and_trials(kind):
             assert maxerr(h[m].values[b][np.ix_(idx, idx)], ref[m]) <= TOL["split"], (b, m)
 
 
+@pytest.mark.parametrize("prec,reduce_", [("fp64", "mean"), ("split", "none"), ("split", "pool"), ("fp64", "none")])
+def test_pipelined_host_path_variants(prec, reduce_):
+    # precision / trial-reduce combinations of the pipelined host path against
+    # the device path (same planes, same kernels: bit-identical) and the oracle
+    import torch
+
+    rng = np.random.default_rng(14)
+    R, N, T = 2, 3072, 96  # N >= 2048 and >= 148 output tiles: the pipelined path
+    from paper_1710_08037_b200 import _native
+
+    assert _native.tile_count(N, prec) >= 148
+    z = np.exp(1j * rng.uniform(0, 2 * np.pi, (R, N, T))).astype(np.complex128)
+    z[:, ::50] *= np.exp(1j * 0.3)
+    zv = np.transpose(z, (1, 2, 0))
+    metrics = ("plv", "iplv", "ciplv", "cre", "cim")
+    h = C.plv_family(zv, input_kind="phasor", precision=prec, trial_reduce=reduce_, metrics=metrics)
+    d = C.plv_family(torch.from_numpy(z).cuda().permute(1, 2, 0), input_kind="phasor", precision=prec,
+                     trial_reduce=reduce_, metrics=metrics)
+    for m in metrics:
+        assert np.array_equal(h[m].values, d[m].values.cpu().numpy()), m
+    idx = np.sort(rng.choice(N, size=48, replace=False))
+    ref = O.plv_family(zv[idx], input_kind="phasor", trial_reduce=reduce_)
+    for m in METRICS:
+        got = h[m].values[np.ix_(idx, idx)] if reduce_ != "none" else h[m].values[np.ix_(idx, idx)]
+        assert maxerr(got, ref[m]) <= TOL[prec], m
+
+
 def test_staged_input_matches_device_path():
     # ps_plv_family_staged: rows arrive chunk by chunk (here: async copies on a
     # side stream standing in for the per-chunk NCCL broadcast of N>1 runs)
