@@ -136,7 +136,9 @@ typedef struct ps_plv_result {
   int64_t n_refined_pairs;     /* ill-conditioned ciPLV pairs recomputed in FP64 */
   int32_t input_copied;        /* 1 if the input layout forced a packing copy */
   int32_t n_kernel_launches;   /* kernels of this library launched by the call */
-  float ms_hilbert;            /* device time per stage (when timing enabled) */
+  float ms_hilbert;            /* reserved (0): the Hilbert stage is interleaved with, and
+                                  counted in, ms_normalize */
+                               /* device time per stage (ps_ctx_set_timing): */
   float ms_normalize;
   float ms_gram;
   float ms_finish;
