@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -37,6 +38,17 @@ METRIC = "pair·samples/s for PLV+iPLV+ciPLV at 1/2/4/8 GPU; % tensor/HBM roofli
 UNIT = "pair·samples/s"
 FLOPS_PER_PAIR_SAMPLE = 8  # complex MAC
 FP64_DGEMM_TFLOPS = 35.5   # FP64 roofline for --precision fp64 (tools/fp64_peak.py, K6)
+
+
+def finite(obj):
+    """JSON-safe copy: non-finite floats become null (strict JSON parsers)."""
+    if isinstance(obj, dict):
+        return {k: finite(v) for k, v in obj.items()}
+    if isinstance(obj, (list, tuple)):
+        return [finite(v) for v in obj]
+    if isinstance(obj, float) and not math.isfinite(obj):
+        return None
+    return obj
 
 
 def peaks():
@@ -275,8 +287,12 @@ def main():
     pk = peaks()
     my_tiles = sum(1 for t in range(_native.tile_count(N, args.precision)) if t % world == rank)
     frac_tiles = my_tiles / max(1, _native.tile_count(N, args.precision))
-    gram_avg = float(np.mean(gram_ms)) if gram_ms else float("nan")
+    gram_avg = float(np.mean(gram_ms)) if gram_ms else 0.0
     algo_flops = FLOPS_PER_PAIR_SAMPLE * work * frac_tiles
+    # (the library reports the Gram's CUDA-event time; without it, fall back
+    # to the whole step so the JSON never carries inf / nan)
+    if not gram_avg > 0.0:
+        gram_avg = ms_step
     achieved = algo_flops / (gram_avg / 1e3) / 1e12
     passes = 1 if fp64 else 3
     peak = pk["bf16_tflops"] / passes if not fp64 else FP64_DGEMM_TFLOPS
@@ -352,7 +368,7 @@ def main():
                 "gpu_launches": launches, "clocks": clocks,
                 "stages_ms": {"normalize": float(info["ms_normalize"]), "gram": gram_avg,
                               "finish": float(info["ms_finish"])}}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(finite(line)), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

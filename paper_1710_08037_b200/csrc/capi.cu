@@ -85,6 +85,7 @@ struct ps_ctx {
   Buf cohws;               // coherence: per-bin matrices before the max-over-bins reduction
   Buf lockbuf;             // Gram producer lockstep counters (one launch at a time per ctx)
   Buf hscale;              // per-row factors restoring H after scaled packing (odd T)
+  std::vector<cudaEvent_t> tev;  // timing events of the staged path (2 per stage)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
   std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
@@ -1274,6 +1275,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evpool) cudaEventDestroy(e);
+  for (auto& e : c->tev) cudaEventDestroy(e);
   for (cudaStream_t s : {c->s_in, c->s_comp, c->s_ref, c->s_out})
     if (s) cudaStreamDestroy(s);
   if (c->h_cnt) cudaFreeHost(c->h_cnt);
@@ -1523,9 +1525,19 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
                           u * g.N + cols[s], u * g.N + cols[s + 1], st, &copied));
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), st));
   }
+  // timing: the Gram stages' kernel time only (each stage's start event is
+  // recorded after its wait for the input chunk), summed below
+  if (c->timing)
+    while ((int)c->tev.size() < 2 * n_stages) {
+      cudaEvent_t e;
+      PS_CUDA(cudaEventCreate(&e));
+      c->tev.push_back(e);
+    }
   for (int s = 0; s < n_stages; ++s) {
     PS_CUDA(cudaStreamWaitEvent(c->s_comp, pool_event(c, 3 * s), 0));
+    if (c->timing) PS_CUDA(cudaEventRecord(c->tev[2 * s], c->s_comp));
     PS_TRY(launch_stage(c, k, s, c->s_comp));
+    if (c->timing) PS_CUDA(cudaEventRecord(c->tev[2 * s + 1], c->s_comp));
   }
   cudaEvent_t done = pool_event(c, 3 * n_stages);
   PS_CUDA(cudaEventRecord(done, c->s_comp));
@@ -1539,6 +1551,16 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
+    if (c->timing) {
+      PS_CUDA(cudaEventSynchronize(done));
+      float tot = 0.f;
+      for (int q = 0; q < n_stages; ++q) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->tev[2 * q], c->tev[2 * q + 1]);
+        tot += ms;
+      }
+      res->ms_gram = tot;
+    }
   }
   return s;
 }

@@ -80,6 +80,7 @@ def broadcast_input_staged(rows_view, cols, src: int = 0, group=None, stream=Non
     import torch.distributed as dist
 
     stream = stream or torch.cuda.Stream()
+    stream.wait_stream(torch.cuda.current_stream())  # earlier work on the buffer is ordered first
     events = []
     with torch.cuda.stream(stream):
         for c0, c1 in zip(cols[:-1], cols[1:]):

@@ -180,7 +180,8 @@ def test_staged_input_matches_device_path():
             ev = torch.cuda.Event()
             ev.record(side)
             events.append(ev)
-    got = C.plv_family(dst, input_kind="analytic", stages=(cols, events))
+    got = C.plv_family(dst, input_kind="analytic", stages=(cols, events), timing=True)
+    assert got["plv"].meta["ms_gram"] > 0.0  # bench.py's roofline reads it on the N > 1 path
     for m in METRICS:
         assert torch.equal(got[m].values, ref[m].values), m
     # sharded + staged: the union of two shards equals the full result
