@@ -85,6 +85,7 @@ struct ps_ctx {
   Buf cohws;               // coherence: per-bin matrices before the max-over-bins reduction
   Buf lockbuf;             // Gram producer lockstep counters (one launch at a time per ctx)
   Buf hscale;              // per-row factors restoring H after scaled packing (odd T)
+  Buf sortws;              // device-side ordering of the ciPLV refinement queue
   std::vector<cudaEvent_t> tev;  // timing events of the staged path (2 per stage)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
@@ -850,6 +851,34 @@ ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long 
                     std::to_string(hi) +
                     "; |Re| within ~1e-3 of 1 for a large share of pairs): the split path cannot meet 1e-5 for "
                     "them cheaply -- use precision='fp64' for this input");
+  const bool single_round = k.pool || k.g.R == 1 || k.slot_mode == 0;
+  {  // device-side ordering when the packed (slot, i, j) key fits 64 bits
+    auto bits = [](long long v) {
+      int b = 1;
+      while ((1LL << b) < v) ++b;
+      return b;
+    };
+    const int ib = bits(k.g.N), sb = bits(std::max<long long>(k.slots, 2));
+    if (sb + 2 * ib <= 64 && hi - lo < (1ULL << 30)) {
+      const int n = (int)(hi - lo);
+      const size_t ebytes = (size_t)round_up((long long)n * (long long)sizeof(RefineEntry), 256);
+      const size_t xbytes = (size_t)round_up((long long)n * 8, 256);
+      PS_TRY(ensure(c->refine_sorted, ebytes + xbytes + (size_t)(n + 1) * sizeof(int) + 256));
+      const size_t wsb = refine_sort_ws_bytes(n);
+      PS_TRY(ensure(c->sortws, wsb));
+      RefineEntry* d_ent = static_cast<RefineEntry*>(c->refine_sorted.p);
+      double* d_exact = reinterpret_cast<double*>(static_cast<char*>(c->refine_sorted.p) + ebytes);
+      int* d_grp = reinterpret_cast<int*>(static_cast<char*>(c->refine_sorted.p) + ebytes + xbytes);
+      GramParams pr = k.p;
+      pr.out_ciplv = k.outs[2];
+      PS_CUDA(launch_refine_sorted(pr, static_cast<RefineEntry*>(c->refine.p) + lo, n, k.slot_mode == 2 ? k.G : 1, ib,
+                                   c->sortws.p, c->sortws.n, d_ent, d_exact, d_grp, single_round ? 1 : 0,
+                                   (int)k.g.R, st));
+      c->launches += 8;
+      PS_CUDA(cudaStreamSynchronize(st));
+      return PS_OK;
+    }
+  }
   std::vector<RefineEntry> ent(hi - lo);
   PS_CUDA(cudaMemcpyAsync(ent.data(), static_cast<RefineEntry*>(c->refine.p) + lo, ent.size() * sizeof(RefineEntry),
                           cudaMemcpyDeviceToHost, st));
@@ -875,7 +904,6 @@ ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long 
   PS_CUDA(cudaMemcpyAsync(d_grp, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   GramParams pr = k.p;
   pr.out_ciplv = k.outs[2];
-  const bool single_round = k.pool || k.g.R == 1 || k.slot_mode == 0;
   PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, (int)ent.size(), d_exact, single_round ? 1 : 0, (int)k.g.R,
                         st));
   c->launches += 2;
@@ -1267,7 +1295,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
-                 &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale})
+                 &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale, &c->sortws})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);

@@ -156,6 +156,14 @@ cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);
 // `div` rounds gets (exact - approx) / div added).
 cudaError_t launch_refine(const GramParams& p, const RefineEntry* entries, const int* groups, int n_groups,
                           int n_entries, double* exact, int overwrite, int div, cudaStream_t st);
+// Same, with the queue ordered on the device (entries modified in place:
+// slot /= slot_div; sorted copy in `sorted`, group starts in `groups`,
+// n + 1 ints).  ib = bits of the signal index; the packed key needs
+// bits(slot) + 2 ib <= 64.
+size_t refine_sort_ws_bytes(int n);
+cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, void* ws,
+                                 size_t ws_bytes, RefineEntry* sorted, double* exact, int* groups, int overwrite,
+                                 int div, cudaStream_t st);
 
 // split Gram variant: 2 = CTA pair (cta_group::2, 256-row panels), 1 = single
 // CTA (128-row panels).  PS_CTA_GROUP=1 selects the latter.

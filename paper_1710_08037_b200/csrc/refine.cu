@@ -13,6 +13,10 @@
 //     queue, so corrections are summed in trial order (deterministic).
 #include <cuda_fp16.h>
 
+#include <algorithm>
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+
 #include "epilogue.cuh"
 #include "ps_internal.h"
 
@@ -77,8 +81,9 @@ __global__ void refine_exact_kernel(const GramParams p, const RefineEntry* __res
 
 __global__ void refine_apply_kernel(const GramParams p, const RefineEntry* __restrict__ e,
                                     const double* __restrict__ exact, const int* __restrict__ groups, int n_groups,
-                                    int overwrite, int div) {
+                                    const int* __restrict__ d_n_groups, int overwrite, int div) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (d_n_groups) n_groups = *d_n_groups;
   if (g >= n_groups || !p.out_ciplv) return;
   const int k0 = groups[g], k1 = groups[g + 1];
   double corr = 0.0, sum = 0.0;
@@ -98,6 +103,46 @@ __global__ void refine_apply_kernel(const GramParams p, const RefineEntry* __res
   o[b] = v;
 }
 
+// ---- device-side ordering of the refinement queue ---------------------------
+// Entries arrive in atomicAdd order; corrections must be applied per output
+// location in trial order (deterministic).  Sort on the device: a stable LSD
+// radix sort by u0, then by the packed (slot, i, j) key, then group starts by
+// flagging key changes -- no host round trip (the host sort dominated calls
+// with ~1e5-1e6 leakage-coupled pairs).
+__global__ void refine_keys_kernel(RefineEntry* __restrict__ e, int n, int slot_div, uint32_t* __restrict__ ku0,
+                                   int* __restrict__ idx) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  RefineEntry en = e[q];
+  if (slot_div > 1) {
+    en.slot /= slot_div;  // workspace slot b*G+g -> final output slot b
+    e[q].slot = en.slot;
+  }
+  ku0[q] = (uint32_t)en.u0;
+  idx[q] = q;
+}
+
+__device__ __forceinline__ unsigned long long pos_key(const RefineEntry& en, int ib) {
+  return ((unsigned long long)en.slot << (2 * ib)) | ((unsigned long long)en.i << ib) | (unsigned long long)en.j;
+}
+
+__global__ void refine_poskey_kernel(const RefineEntry* __restrict__ e, const int* __restrict__ idx1, int n, int ib,
+                                     unsigned long long* __restrict__ kpos) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < n) kpos[q] = pos_key(e[idx1[q]], ib);
+}
+
+__global__ void refine_gather_kernel(const RefineEntry* __restrict__ e, const int* __restrict__ idx2,
+                                     const unsigned long long* __restrict__ kpos2, int n,
+                                     RefineEntry* __restrict__ sorted, uint8_t* __restrict__ flags) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  sorted[q] = e[idx2[q]];
+  flags[q] = (q == 0 || kpos2[q] != kpos2[q - 1]) ? 1 : 0;
+}
+
+__global__ void refine_terminate_kernel(int* groups, const int* d_n_groups, int n) { groups[*d_n_groups] = n; }
+
 }  // namespace
 
 cudaError_t launch_refine(const GramParams& p, const RefineEntry* entries, const int* groups, int n_groups,
@@ -106,7 +151,62 @@ cudaError_t launch_refine(const GramParams& p, const RefineEntry* entries, const
   const int threads = 256;
   refine_exact_kernel<<<(n_entries * 32 + threads - 1) / threads, threads, 0, st>>>(p, entries, n_entries, exact);
   refine_apply_kernel<<<(n_groups + threads - 1) / threads, threads, 0, st>>>(p, entries, exact, groups, n_groups,
-                                                                              overwrite, div);
+                                                                              nullptr, overwrite, div);
+  return cudaGetLastError();
+}
+
+size_t refine_sort_ws_bytes(int n) {
+  size_t a = 0, b = 0, c = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, a, (const uint32_t*)nullptr, (uint32_t*)nullptr, (const int*)nullptr,
+                                  (int*)nullptr, n);
+  cub::DeviceRadixSort::SortPairs(nullptr, b, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                  (const int*)nullptr, (int*)nullptr, n);
+  cub::DeviceSelect::Flagged(nullptr, c, thrust::counting_iterator<int>(0), (const uint8_t*)nullptr, (int*)nullptr,
+                             (int*)nullptr, n);
+  const size_t cubb = std::max(a, std::max(b, c));
+  // ku0, ku0s (4 n) + idx, idx1, idx2 (4 n) + kpos, kpos2 (8 n) + flags (n) + n_groups + cub
+  // (each of the 9 carve-outs is rounded up to 256 bytes)
+  return (size_t)n * (4 * 2 + 4 * 3 + 8 * 2 + 1) + 10 * 256 + 256 + cubb;
+}
+
+cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, void* ws,
+                                 size_t ws_bytes, RefineEntry* sorted, double* exact, int* groups, int overwrite,
+                                 int div, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  char* w = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) {
+    char* r = w;
+    w += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  uint32_t* ku0 = reinterpret_cast<uint32_t*>(take((size_t)n * 4));
+  uint32_t* ku0s = reinterpret_cast<uint32_t*>(take((size_t)n * 4));
+  int* idx = reinterpret_cast<int*>(take((size_t)n * 4));
+  int* idx1 = reinterpret_cast<int*>(take((size_t)n * 4));
+  int* idx2 = reinterpret_cast<int*>(take((size_t)n * 4));
+  unsigned long long* kpos = reinterpret_cast<unsigned long long*>(take((size_t)n * 8));
+  unsigned long long* kpos2 = reinterpret_cast<unsigned long long*>(take((size_t)n * 8));
+  uint8_t* flags = reinterpret_cast<uint8_t*>(take((size_t)n));
+  int* d_ng = reinterpret_cast<int*>(take(64));
+  const size_t used = (size_t)(w - static_cast<char*>(ws));
+  if (used > ws_bytes) return cudaErrorInvalidValue;
+  size_t cub_bytes = ws_bytes - used;
+  void* cub_ws = w;
+  const int threads = 256, blocks = (n + threads - 1) / threads;
+  refine_keys_kernel<<<blocks, threads, 0, st>>>(entries, n, slot_div, ku0, idx);
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, ku0, ku0s, idx, idx1, n, 0, 32, st);
+  if (e != cudaSuccess) return e;
+  refine_poskey_kernel<<<blocks, threads, 0, st>>>(entries, idx1, n, ib, kpos);
+  cub_bytes = ws_bytes - used;
+  e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, kpos, kpos2, idx1, idx2, n, 0, 64, st);
+  if (e != cudaSuccess) return e;
+  refine_gather_kernel<<<blocks, threads, 0, st>>>(entries, idx2, kpos2, n, sorted, flags);
+  cub_bytes = ws_bytes - used;
+  e = cub::DeviceSelect::Flagged(cub_ws, cub_bytes, thrust::counting_iterator<int>(0), flags, groups, d_ng, n, st);
+  if (e != cudaSuccess) return e;
+  refine_terminate_kernel<<<1, 1, 0, st>>>(groups, d_ng, n);
+  refine_exact_kernel<<<(n * 32 + threads - 1) / threads, threads, 0, st>>>(p, sorted, n, exact);
+  refine_apply_kernel<<<blocks, threads, 0, st>>>(p, sorted, exact, groups, n, d_ng, overwrite, div);
   return cudaGetLastError();
 }
 
