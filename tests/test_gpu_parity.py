@@ -460,6 +460,22 @@ def test_float32_trial_fastest_layout_copies():
     assert res["plv"].meta["input_copied"]
 
 
+@pytest.mark.parametrize("reduce_", ["mean", "none"])
+def test_heavy_zero_lag_leakage_split_accuracy(reduce_):
+    # clusters of signals sharing one source at zero lag (|Re| -> 1 for every
+    # within-cluster pair): tens of thousands of ill-conditioned ciPLV pairs,
+    # all refined in FP64 on the device; split results within 1e-5
+    rng = np.random.default_rng(61)
+    N, T, R, K = 512, 2048, 2, 32
+    src = rng.standard_normal((N // K, T, R)) + 1j * rng.standard_normal((N // K, T, R))
+    a = src[np.arange(N) // K] + 0.05 * (rng.standard_normal((N, T, R)) + 1j * rng.standard_normal((N, T, R)))
+    a = a.astype(np.complex64)
+    ref = O.plv_family(a, input_kind="analytic", trial_reduce=reduce_)
+    res = C.plv_family(a, input_kind="analytic", precision="split", trial_reduce=reduce_)
+    check(res, ref, "split", f"leakage {reduce_}")
+    assert res["plv"].meta["n_refined_pairs"] > 10000
+
+
 def test_signed_coherency_outputs():
     z = O.make_surrogate(40, 500, 1, seed=8)
     raw = O.plv_family(z, input_kind="phasor", raw=True)["cgram"][:, :, 0]
