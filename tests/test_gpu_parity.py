@@ -460,6 +460,40 @@ def test_float32_trial_fastest_layout_copies():
     assert res["plv"].meta["input_copied"]
 
 
+def test_combinations_bands_with_bandpass_over_trials_and_pipelined_bandpass():
+    import torch
+
+    rng = np.random.default_rng(62)
+    f = _fir(order=60, lo=0.2, hi=0.5)
+    # band-pass front end with a band axis (device and host paths)
+    x = rng.standard_normal((2, 40, 700, 3)).astype(np.float32)        # [B, N, T, R]
+    res = C.plv_family(x, input_kind="real", bands=True, fir=f, pad_samples=80)
+    for b in range(2):
+        ref = O.plv_family(x[b].astype(np.float64), input_kind="real", fir=(f.taps, 80))
+        for m in METRICS:
+            assert maxerr(res[m].values[b], ref[m]) <= TOL["split"], (b, m)
+    # time-resolved mode with a band axis
+    z = np.exp(1j * rng.uniform(0, 6.3, (2, 30, 20, 9)))                # [B, N, T, R]
+    tr = C.plv_family(z, input_kind="phasor", bands=True, mode="over_trials", precision="fp64")
+    assert tr["plv"].values.shape == (2, 30, 30, 20)
+    for b in range(2):
+        zz, mk = O.phasors_from_unit(z[b])
+        ref = O.plv_family_over_trials(zz, mk)
+        for m in METRICS:
+            assert maxerr(tr[m].values[b], ref[m]) <= TOL["fp64"], (b, m)
+    # band-pass on the pipelined host path (N >= 2048 and >= 148 tiles)
+    N = 3072
+    xp = rng.standard_normal((N, 400)).astype(np.float32)
+    h = C.plv_family(xp, input_kind="real", fir=f, pad_samples=100)
+    d = C.plv_family(torch.from_numpy(xp).cuda(), input_kind="real", fir=f, pad_samples=100)
+    for m in METRICS:
+        assert np.array_equal(h[m].values, d[m].values.cpu().numpy()), m
+    idx = np.sort(rng.choice(N, size=40, replace=False))
+    ref = O.plv_family(xp[idx][:, :, None], input_kind="real", fir=(f.taps, 100))
+    for m in METRICS:
+        assert maxerr(h[m].values[np.ix_(idx, idx)], ref[m]) <= TOL["split"], m
+
+
 @pytest.mark.parametrize("reduce_", ["mean", "none"])
 def test_heavy_zero_lag_leakage_split_accuracy(reduce_):
     # clusters of signals sharing one source at zero lag (|Re| -> 1 for every
