@@ -154,6 +154,9 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(W.CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--precision", default="split", choices=["split", "fp64"])
+    ap.add_argument("--layout", default=None, choices=["full", "upper"],
+                    help="output layout (default: 'upper' for c5, whose BASELINE config asks for the upper "
+                         "triangle of each metric; 'full' otherwise)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stage-bcast", dest="stage_bcast", action="store_false",
@@ -164,10 +167,13 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     N, T, R, B, dt, kind = W.CONFIGS[args.config]
+    layout = args.layout or ("upper" if args.config == "c5" else "full")
     work = W.pair_samples(N, T, R, B)
     cfg = {"workload": f"{args.config}: {W.DESCRIPTIONS[args.config]}", "n_signals": N, "n_samples": T,
            "n_trials": R, "n_bands": B, "input": dt, "input_kind": kind, "trial_reduce": "mean",
            "precision": args.precision, "pair_samples_per_step": work,
+           "output_layout": layout + (" (i <= j of each [N][N] matrix, BASELINE configs[4])" if layout == "upper"
+                                      else " (both triangles)"),
            "l2": "inputs larger than L2 (126 MB) every step",
            "parallelism": f"output-tile shards x{world}" + (
                (" + chunked NCCL broadcast of the input from rank 0, overlapped with compute" if R == 1 and B == 1
@@ -244,11 +250,11 @@ def main():
         if staged:
             events = sharding.broadcast_input_staged(rows_view, cols, src=0, stream=comm)
             return C.plv_family(xv, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
-                                out=outs, timing=timing, stages=(cols, events))
+                                out=outs, timing=timing, stages=(cols, events), layout=layout)
         if world > 1 and R == 1 and B == 1:
             sharding.broadcast_input(bcast_t, src=0)
         return C.plv_family(xv, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
-                            out=outs, timing=timing)
+                            out=outs, timing=timing, layout=layout)
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -325,13 +331,14 @@ def main():
         xin_view = np.transpose(xin_np, (1, 2, 0)) if not bands else np.transpose(xin_np, (0, 2, 3, 1))
         hout = {m: torch.zeros((B, N, N), dtype=odt, pin_memory=True).numpy() for m in ("plv", "iplv", "ciplv")}
         for _ in range(1):
-            C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard, out=hout)
+            C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard, out=hout,
+                         layout=layout)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             r_e = C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
-                               out=hout)
+                               out=hout, layout=layout)
         dt_e = (time.perf_counter() - t0) / args.steps
         meta_e = next(iter(r_e.values())).meta
         if world > 1:

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 4
+#define PS_ABI_VERSION 5
 
 typedef enum ps_status {
   PS_OK = 0,
@@ -122,13 +122,21 @@ typedef struct ps_plv_args {
    * 153-157,173,186-189).  Over trials, outputs are [n_bands][n_samples][N][N]
    * and trial_reduce is ignored. */
   int32_t mode;
-  int32_t reserved0;
+  /* PS_LAYOUT_FULL (default): both triangles written (symmetric; CIM
+   * antisymmetric).  PS_LAYOUT_UPPER: only entries (i, j) with i <= j of each
+   * [N][N] slot are written -- the output BASELINE configs[4] asks for ("the
+   * 20,000 x 20,000 upper triangle for each metric"); the strictly lower
+   * triangle is left as the caller allocated it (device outputs); the host
+   * entry point does not transfer it except inside the diagonal blocks of its
+   * copy-out, which read 0 there.  Halves output writes and D2H bytes. */
+  int32_t out_layout;
   /* Optional band-pass front end (real input only; NULL = input is already
    * band-limited, the configs' case). */
   const ps_fir* fir;
 } ps_plv_args;
 
 enum { PS_MODE_OVER_SAMPLES = 0, PS_MODE_OVER_TRIALS = 1 };
+enum { PS_LAYOUT_FULL = 0, PS_LAYOUT_UPPER = 1 };
 
 typedef struct ps_plv_result {
   int64_t n_observations;      /* T used for normalisation (R*T for POOL) */

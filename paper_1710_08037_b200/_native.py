@@ -20,7 +20,8 @@ from . import errors
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
 if os.environ.get("PS_LIB_VARIANT"):  # A/B experiments: libphasesync_cuda.<variant>.so next to the default
     LIB_PATH = LIB_PATH.with_name(f"libphasesync_cuda.{os.environ['PS_LIB_VARIANT']}.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
+LAYOUTS = {"full": 0, "upper": 1}
 
 # ps_status -> exception class (include/phasesync.h)
 PS_OK = 0
@@ -85,7 +86,7 @@ class PlvArgs(ctypes.Structure):
         ("shard_count", ctypes.c_int32),
         ("stream", ctypes.c_void_p),
         ("mode", ctypes.c_int32),
-        ("reserved0", ctypes.c_int32),
+        ("out_layout", ctypes.c_int32),
         ("fir", ctypes.POINTER(Fir)),
     ]
 

@@ -55,7 +55,7 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
                precision: str = "split", trial_reduce: str = "mean", amp_floor: float = 1e-6,
                bands: bool = False, shard: tuple[int, int] = (0, 1), out: dict | None = None,
                timing: bool = False, stages=None, mode: str = "over_samples", fir=None,
-               pad_samples: int = 0) -> dict:
+               pad_samples: int = 0, layout: str = "full") -> dict:
     """All requested PLV-family metrics from one Gram per trial.
 
     x: RealEpochs / AnalyticEpochs / PhasorEpochs data, shape [N, T], [N, T, R]
@@ -80,8 +80,14 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
        reflection-padded by pad_samples, analytic signal before the trim
        (SURVEY 3.2, 8(f) #1), fused into the Hilbert
        stage of the same call.
+    layout: 'full' (both triangles, default) or 'upper' (only i <= j of every
+       matrix is computed and, for host arrays, transferred -- BASELINE
+       configs[4]'s output; the strictly lower triangle is zero when the
+       outputs are allocated here).
     Returns {metric: ConnectivityMatrix}.
     """
+    if layout not in _native.LAYOUTS:
+        raise ValueError(f"layout must be one of {sorted(_native.LAYOUTS)}")
     if mode not in ("over_samples", "over_trials"):
         raise ValueError("mode must be 'over_samples' or 'over_trials'")
     over_trials = mode == "over_trials"
@@ -117,6 +123,8 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     a.trial_reduce = _native.TRIAL_REDUCE[trial_reduce]
     a.shard_index, a.shard_count = int(shard[0]), int(shard[1])
     a.mode = 1 if over_trials else 0
+    a.out_layout = _native.LAYOUTS[layout]
+    zero_init = shard[1] > 1 or layout == "upper"
     fir_keep = None
     if fir is not None:
         from .signalprep import fir_struct
@@ -133,7 +141,7 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
         for m in metrics:
             o = None if out is None else out.get(m)
             if o is None:
-                o = (torch.zeros if shard[1] > 1 else torch.empty)((slots, N, N), dtype=tdt, device=dev)
+                o = (torch.zeros if zero_init else torch.empty)((slots, N, N), dtype=tdt, device=dev)
             elif o.dtype != tdt or not o.is_contiguous() or o.numel() != slots * N * N:
                 raise ValueError(f"out[{m!r}] must be a contiguous {tdt} tensor with {slots * N * N} elements")
             outs[m] = o
@@ -158,7 +166,7 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
         for m in metrics:
             o = None if out is None else out.get(m)
             if o is None:
-                o = (np.zeros if shard[1] > 1 else np.empty)((slots, N, N), dtype=ndt)
+                o = (np.zeros if zero_init else np.empty)((slots, N, N), dtype=ndt)
             elif o.dtype != ndt or not o.flags.c_contiguous or o.size != slots * N * N:
                 raise ValueError(f"out[{m!r}] must be a C-contiguous {ndt.__name__} array with {slots * N * N} "
                                  "elements")
@@ -173,6 +181,7 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
     info["input_copied"] = bool(info["input_copied"]) or d.copied
     info["precision"] = precision
     info["trial_reduce"] = trial_reduce
+    info["layout"] = layout
     result = {}
     for m in metrics:
         v = outs[m]
@@ -265,7 +274,7 @@ def welch_bins(window_len: int, band) -> tuple[int, int]:
 
 def coherence_matrix(x, cfg: WelchConfig, band, *, mode: str = "max", metrics: Iterable[str] = ("coh",),
                      precision: str = "split", bands: bool = False, shard: tuple[int, int] = (0, 1),
-                     timing: bool = False) -> dict:
+                     timing: bool = False, layout: str = "full") -> dict:
     """All-pairs Welch coherence aggregated over `band`:
     band_coherence(coherence_welch(x_i, x_j), band, mode) for every pair, from
     one Gram over segments per frequency bin on the sm_100a path.
@@ -277,10 +286,13 @@ def coherence_matrix(x, cfg: WelchConfig, band, *, mode: str = "max", metrics: I
        (COH_MEAN) or 'none' (one matrix per bin: values [N, N, n_bins]).
     metrics: 'coh' (|C|, Eq 12), 'icoh' (|Im C|, imaginary coherency), 'cre' /
        'cim' (signed coherency parts).
+    layout: 'full' or 'upper' (only i <= j computed; lower triangle zero).
     Returns {metric: ConnectivityMatrix}.
     """
     import torch
 
+    if layout not in _native.LAYOUTS:
+        raise ValueError(f"layout must be one of {sorted(_native.LAYOUTS)}")
     if mode not in BAND_REDUCE:
         raise ValueError("mode must be 'max', 'mean' or 'none'")
     if cfg.taper != "hamming":
@@ -309,6 +321,7 @@ def coherence_matrix(x, cfg: WelchConfig, band, *, mode: str = "max", metrics: I
     a.amp_floor = 0.0
     a.precision = _native.PRECISIONS[precision]
     a.shard_index, a.shard_count = int(shard[0]), int(shard[1])
+    a.out_layout = _native.LAYOUTS[layout]
     w = _native.Welch()
     w.window_len, w.overlap = int(cfg.window_len), int(cfg.overlap)
     w.band_low, w.band_high = float(band[0]), float(band[1])
@@ -330,7 +343,7 @@ def coherence_matrix(x, cfg: WelchConfig, band, *, mode: str = "max", metrics: I
         _native.check(_native.lib().ps_coherence(ctx.handle, ctypes.byref(a), ctypes.byref(w), ctypes.byref(res)))
     info = res.as_dict()
     info.update(window_len=cfg.window_len, overlap=cfg.overlap, band=tuple(band), band_reduce=mode,
-                first_bin=k0, n_bins=nb, precision=precision)
+                first_bin=k0, n_bins=nb, precision=precision, layout=layout)
     names = {"coh": "COH_" + mode.upper(), "icoh": "ICOH_" + mode.upper()}
     result = {}
     for m in metrics:

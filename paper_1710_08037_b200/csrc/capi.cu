@@ -163,6 +163,8 @@ ps_status validate(const ps_plv_args* a, Geometry& g) {
     return fail(PS_E_INVALID, "unknown precision");
   if (a->trial_reduce < 0 || a->trial_reduce > 2) return fail(PS_E_INVALID, "unknown trial_reduce");
   if (a->mode != PS_MODE_OVER_SAMPLES && a->mode != PS_MODE_OVER_TRIALS) return fail(PS_E_INVALID, "unknown mode");
+  if (a->out_layout != PS_LAYOUT_FULL && a->out_layout != PS_LAYOUT_UPPER)
+    return fail(PS_E_INVALID, "unknown out_layout");
   if (!(a->amp_floor >= 0.0)) return fail(PS_E_INVALID, "amp_floor must be >= 0");
   if (a->n_signals > (1 << 30) || a->n_samples > (1LL << 31) - 1)
     return fail(PS_E_SHAPE, "n_signals / n_samples exceed the supported range");
@@ -738,6 +740,7 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   p.status = c->d_status;
   p.illcond_tol = 4e-6f;  // 2.5x margin below the 1e-5 split-path tolerance
   p.kc_blocks = kc_blocks_default();
+  p.upper_only = a->out_layout == PS_LAYOUT_UPPER ? 1 : 0;
   static const int dbg = [] {
     const char* s = std::getenv("PS_DEBUG_EPI");
     return s ? std::atoi(s) : 0;
@@ -1061,6 +1064,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
   PS_TRY(ensure(c->planes, plane_bytes));
   const size_t oes = g.split ? 4 : 8;
+  const bool upper = a->out_layout == PS_LAYOUT_UPPER;
   void* houts[5];
   std::memcpy(houts, k.outs, sizeof(houts));
   int nout = 0;
@@ -1105,6 +1109,14 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   // ---- Gram per stage ------------------------------------------------------
   for (int s = 0; s < S; ++s) {
     PS_CUDA(cudaStreamWaitEvent(sc, pool_event(c, 3 * s), 0));
+    if (upper) {  // the copy-out of the diagonal block carries its lower part: make it 0, not stale
+      const long long c0 = cols[s], c1 = cols[s + 1];
+      for (int m = 0; m < 5; ++m)
+        if (k.outs[m])
+          for (long long sl = 0; sl < k.slots; ++sl)
+            PS_CUDA(cudaMemset2DAsync(static_cast<char*>(k.outs[m]) + ((size_t)sl * g.N * g.N + c0 * g.N + c0) * oes,
+                                      (size_t)g.N * oes, 0, (size_t)(c1 - c0) * oes, (size_t)(c1 - c0), sc));
+    }
     PS_TRY(launch_stage(c, k, s, sc));
     if (trace) trace->rec(sc, "gram", s);
     // the refine-queue count reaches the host through a store into mapped
@@ -1129,7 +1141,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     const char* s = std::getenv("PS_HOST_MIRROR");
     return s ? std::max(0, std::atoi(s)) : 0;
   }();
-  const bool host_mirror = mirror_count > 0;
+  const bool host_mirror = mirror_count > 0 && !upper;
   auto mirrored = [&](long long q) { return q < mirror_count; };
   auto mirror_stage = [&](int s) {
     const long long c0 = cols[s], c1 = cols[s + 1];
@@ -1198,8 +1210,8 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
         PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * oes, pitch, dsrc + (size_t)c0 * oes, pitch,
                                   (size_t)(c1 - c0) * oes, (size_t)c1, cudaMemcpyDeviceToHost, so));
         d2h_bytes += (size_t)(c1 - c0) * oes * (size_t)c1;
-        // rows [c0, c1) x cols [0, c0)
-        if (c0 > 0 && !mirrored(q)) {
+        // rows [c0, c1) x cols [0, c0) (strictly lower: not part of the upper layout)
+        if (c0 > 0 && !mirrored(q) && !upper) {
           PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * pitch, pitch, dsrc + (size_t)c0 * pitch, pitch,
                                     (size_t)c0 * oes, (size_t)(c1 - c0), cudaMemcpyDeviceToHost, so));
           d2h_bytes += (size_t)c0 * oes * (size_t)(c1 - c0);
@@ -1360,7 +1372,8 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   PS_TRY(launch_stage(c, k, 0, st));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, (int)g.R, g.split ? 0 : 1, st));
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, (int)g.R, g.split ? 0 : 1, st,
+                                    a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
   ps_status s = read_status(c, st);
@@ -1487,7 +1500,8 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
   PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
   PS_TRY(launch_stage(c, k, 0, st));
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, gt.B * k.nn, (int)gt.R, gt.split ? 0 : 1, st));
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, gt.B * k.nn, (int)gt.R, gt.split ? 0 : 1, st,
+                                    a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
@@ -1496,7 +1510,8 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
   if (s == PS_OK && w->reduce == PS_BAND_MAX) {
     for (int m = 0; m < 5; ++m)
       if (k.outs[m]) {
-        PS_CUDA(launch_band_max(k.outs[m], g.B, nb, nn, user_outs[m], fp64 ? 1 : 0, st));
+        PS_CUDA(launch_band_max(k.outs[m], g.B, nb, nn, user_outs[m], fp64 ? 1 : 0, st,
+                                        a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
         c->launches++;
       }
     PS_CUDA(cudaStreamSynchronize(st));
@@ -1643,6 +1658,8 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
     if (((a->metrics >> m) & 1u) && houts[m]) *douts[m] = static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes;
     else *douts[m] = nullptr;
   }
+  if (a->out_layout == PS_LAYOUT_UPPER)  // the full-matrix copy-out carries the lower triangle: 0, not stale
+    PS_CUDA(cudaMemsetAsync(c->hout.p, 0, out_bytes * q, st));
   ps_status s = ps_plv_family(c, &d, res);
   if (s != PS_OK) return s;
   q = 0;

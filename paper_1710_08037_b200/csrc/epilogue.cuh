@@ -110,12 +110,12 @@ __device__ __forceinline__ long long effective_T(const GramParams& p, int u0, in
 // antisymmetric signed imaginary part).
 template <typename S>
 __device__ __forceinline__ void emit(S* base, long long N, int i, int j, S v, bool first, bool last, int div,
-                                     bool anti) {
+                                     bool anti, bool mirror) {
   const long long idx = (long long)i * N + j;
   S acc = first ? v : base[idx] + v;
   if (last && div != 1) acc = acc / S(div);
   base[idx] = acc;
-  if (last && i != j) base[(long long)j * N + i] = anti ? -acc : acc;
+  if (mirror && last && i != j) base[(long long)j * N + i] = anti ? -acc : acc;
 }
 
 template <typename S>
@@ -123,12 +123,12 @@ __device__ __forceinline__ void emit_all(const GramParams& p, long long slot, in
                                          const PairMetrics<S>& m, bool first, bool last) {
   const long long off = slot * (long long)p.N * p.N;
   const long long N = p.N;
-  if (p.out_plv) emit<S>(static_cast<S*>(p.out_plv) + off, N, i, j, m.plv, first, last, p.mean_div, false);
-  if (p.out_iplv) emit<S>(static_cast<S*>(p.out_iplv) + off, N, i, j, m.iplv, first, last, p.mean_div, false);
+  if (p.out_plv) emit<S>(static_cast<S*>(p.out_plv) + off, N, i, j, m.plv, first, last, p.mean_div, false, !p.upper_only);
+  if (p.out_iplv) emit<S>(static_cast<S*>(p.out_iplv) + off, N, i, j, m.iplv, first, last, p.mean_div, false, !p.upper_only);
   if (p.out_ciplv)
-    emit<S>(static_cast<S*>(p.out_ciplv) + off, N, i, j, m.ciplv, first, last, p.mean_div, false);
-  if (p.out_cre) emit<S>(static_cast<S*>(p.out_cre) + off, N, i, j, m.cre, first, last, p.mean_div, false);
-  if (p.out_cim) emit<S>(static_cast<S*>(p.out_cim) + off, N, i, j, m.cim, first, last, p.mean_div, true);
+    emit<S>(static_cast<S*>(p.out_ciplv) + off, N, i, j, m.ciplv, first, last, p.mean_div, false, !p.upper_only);
+  if (p.out_cre) emit<S>(static_cast<S*>(p.out_cre) + off, N, i, j, m.cre, first, last, p.mean_div, false, !p.upper_only);
+  if (p.out_cim) emit<S>(static_cast<S*>(p.out_cim) + off, N, i, j, m.cim, first, last, p.mean_div, true, !p.upper_only);
 }
 
 // Four consecutive columns j0..j0+3 of row i, all strictly above the diagonal
@@ -163,7 +163,7 @@ __device__ __forceinline__ void emit4_all(const GramParams& p, long long slot, i
     }
     float* base = outs[q] + off;
     if (!(p.debug_flags & 8)) *reinterpret_cast<float4*>(base + (long long)i * N + j0) = a;
-    if (last && !(p.debug_flags & 4)) {
+    if (last && !p.upper_only && !(p.debug_flags & 4)) {
       const float s = q == 4 ? -1.f : 1.f;
       base[(long long)(j0 + 0) * N + i] = s * a.x;
       base[(long long)(j0 + 1) * N + i] = s * a.y;
@@ -204,7 +204,7 @@ __device__ __forceinline__ void emit8_first(const GramParams& p, long long slot,
       for (int e = 0; e < 8; ++e) a[e] = a[e] / d;
     }
     if (!(p.debug_flags & 8)) st_v8(base + (long long)i * N + j0, a);
-    if (last && !(p.debug_flags & 4)) {
+    if (last && !p.upper_only && !(p.debug_flags & 4)) {
       const float s = q == 4 ? -1.f : 1.f;
 #pragma unroll
       for (int e = 0; e < 8; ++e) base[(long long)(j0 + e) * N + i] = s * a[e];

@@ -831,11 +831,12 @@ __global__ void analytic_out_kernel(SrcDesc src, long long row0, long long nrows
 // out_m[i] = sum_g ws_m[g][i] / R  (deterministic fixed-order trial-group sum)
 template <typename S>
 __global__ void group_reduce_kernel(const S* ws, int G, long long slot_elems, long long elems, int R,
-                                    S* out) {
+                                    S* out, long long upper_n) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < elems;
        e += (long long)gridDim.x * blockDim.x) {
     // slot layout of ws: [band][G][N*N]; elems = B*N*N, slot_elems = N*N
     const long long b = e / slot_elems, i = e % slot_elems;
+    if (upper_n && i / upper_n > i % upper_n) continue;  // PS_LAYOUT_UPPER: lower triangle untouched
     const S* p = ws + (b * G) * slot_elems + i;
     S acc = p[0];
     for (int g = 1; g < G; ++g) acc += p[g * slot_elems];
@@ -1034,11 +1035,12 @@ __global__ void coherence_planes_kernel(const C* __restrict__ spec, int nbW, lon
 
 // out[b][e] = max_kb ws[b * nb + kb][e]
 template <typename S>
-__global__ void band_max_kernel(const S* ws, long long B, long long nb, long long nn, S* out) {
+__global__ void band_max_kernel(const S* ws, long long B, long long nb, long long nn, S* out, long long upper_n) {
   const long long total = B * nn;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long b = e / nn, i = e % nn;
+    if (upper_n && i / upper_n > i % upper_n) continue;  // PS_LAYOUT_UPPER
     S m = ws[(b * nb) * nn + i];
     for (long long kb = 1; kb < nb; ++kb) {
       const S v = ws[(b * nb + kb) * nn + i];
@@ -1127,10 +1129,10 @@ cudaError_t launch_coherence_planes(const void* spec, int spec_double, int nbW, 
 }
 
 cudaError_t launch_band_max(const void* ws, long long B, long long nb, long long nn, void* out, int is_double,
-                            cudaStream_t st) {
+                            cudaStream_t st, long long upper_n) {
   const int g = grid_for(B * nn, 256);
-  if (is_double) band_max_kernel<double><<<g, 256, 0, st>>>((const double*)ws, B, nb, nn, (double*)out);
-  else band_max_kernel<float><<<g, 256, 0, st>>>((const float*)ws, B, nb, nn, (float*)out);
+  if (is_double) band_max_kernel<double><<<g, 256, 0, st>>>((const double*)ws, B, nb, nn, (double*)out, upper_n);
+  else band_max_kernel<float><<<g, 256, 0, st>>>((const float*)ws, B, nb, nn, (float*)out, upper_n);
   return cudaGetLastError();
 }
 
@@ -1377,7 +1379,7 @@ cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void
 }
 
 cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs, void* const* outs,
-                                long long elems_per_out, int R, int is_double, cudaStream_t st) {
+                                long long elems_per_out, int R, int is_double, cudaStream_t st, long long upper_n) {
   // ws holds n_outputs consecutive blocks of [B][G][slot_elems]
   const int g = grid_for(elems_per_out, 256);
   const long long ws_block = elems_per_out * G;
@@ -1385,10 +1387,10 @@ cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int
     if (!outs[m]) continue;
     if (is_double)
       group_reduce_kernel<double><<<g, 256, 0, st>>>((const double*)ws + m * ws_block, G, slot_elems,
-                                                      elems_per_out, R, (double*)outs[m]);
+                                                      elems_per_out, R, (double*)outs[m], upper_n);
     else
       group_reduce_kernel<float><<<g, 256, 0, st>>>((const float*)ws + m * ws_block, G, slot_elems,
-                                                     elems_per_out, R, (float*)outs[m]);
+                                                     elems_per_out, R, (float*)outs[m], upper_n);
   }
   return cudaGetLastError();
 }

@@ -83,6 +83,7 @@ struct GramParams {
   int refine_cap;
   int kc_blocks;               // split kernel: K blocks per TMEM accumulation chunk (drain period)
   int debug_flags;             // experiments only (PS_DEBUG_EPI): 1 = skip the metric emission
+  int upper_only;              // PS_LAYOUT_UPPER: no mirror (j, i) writes
   // Producer lockstep (split kernel): every producer publishes each group of
   // lock_group issued K blocks in lock_cnt[group] and may not run more than
   // lock_lag groups ahead of the slowest producer, so the CTAs that share an
@@ -137,8 +138,9 @@ cudaError_t launch_welch_segments(const SrcDesc& src, long long rows, int nseg, 
 cudaError_t launch_coherence_planes(const void* spec, int spec_double, int nbW, long long B, long long R, long long N,
                                     int nseg, int k0, int nb, int K, int Kp, void* planes, long long ps, int split,
                                     cudaStream_t st);
+// upper_n = N for PS_LAYOUT_UPPER (strictly lower entries skipped), 0 = all
 cudaError_t launch_band_max(const void* ws, long long B, long long nb, long long nn, void* out, int is_double,
-                            cudaStream_t st);
+                            cudaStream_t st, long long upper_n);
 cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nrows,
                                 void* out, cudaStream_t st);
 // Eq 8 (over trials): planes [P][B*R][N][Tp] -> [P][B*T][N][Rp] + masked-trial counts
@@ -146,7 +148,7 @@ cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void
                                     int R, int N, int T, int split, int* maskcount_dst, cudaStream_t st);
 cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs,
                                 void* const* outs, long long elems_per_out, int R,
-                                int is_double, cudaStream_t st);
+                                int is_double, cudaStream_t st, long long upper_n);
 cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p,
                               int grid, cudaStream_t st);
 cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);

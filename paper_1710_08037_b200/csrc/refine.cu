@@ -100,7 +100,7 @@ __global__ void refine_apply_kernel(const GramParams p, const RefineEntry* __res
                   : (k1 - k0 == div) ? (float)(sum / (double)div)
                                      : (float)((double)o[a] + corr / (double)div);
   o[a] = v;
-  o[b] = v;
+  if (!p.upper_only) o[b] = v;
 }
 
 // ---- device-side ordering of the refinement queue ---------------------------

@@ -1,0 +1,127 @@
+"""GPU: PS_LAYOUT_UPPER (BASELINE configs[4]: "the upper triangle for each
+metric") against PS_LAYOUT_FULL on the same inputs.
+
+The upper entries (i <= j) must be bit-identical to the full layout's (the
+same tiles, epilogue, trial-group reduction and FP64 refinement produce them;
+only the mirror writes and their transfer are skipped), and the strictly lower
+triangle must be left as allocated (zero here) -- on the device path, the host
+non-pipelined path, the host pipelined path, the trial-group reduction, the
+refine queue, time-resolved mode and Welch coherence.
+"""
+import numpy as np
+import pytest
+
+from oracle import plv_oracle as O
+from paper_1710_08037_b200 import connectivity as C
+
+pytestmark = pytest.mark.gpu
+
+ALL = ("plv", "iplv", "ciplv", "cre", "cim")
+
+
+def _np(v):
+    return v.cpu().numpy() if hasattr(v, "cpu") else np.asarray(v)
+
+
+def _same_upper(full, upper, label):
+    """full / upper: arrays [..., N, N] or TimeResolved / per-trial [N, N, K]."""
+    f, u = _np(full), _np(upper)
+    assert f.shape == u.shape, label
+    if f.shape[-1] != f.shape[-2]:  # [..., N, N, K] (per trial / sample / bin) -> [K, ..., N, N]
+        f, u = np.moveaxis(f, -1, 0), np.moveaxis(u, -1, 0)
+    N = f.shape[-1]
+    iu = np.triu_indices(N)
+    il = np.tril_indices(N, -1)
+    fu, uu = f[..., iu[0], iu[1]], u[..., iu[0], iu[1]]
+    assert np.array_equal(fu, uu), (label, float(np.max(np.abs(fu - uu))))
+    assert not np.any(u[..., il[0], il[1]]), (label, "lower triangle written")
+
+
+def _both(x, label, **kw):
+    full = C.plv_family(x, layout="full", **kw)
+    upper = C.plv_family(x, layout="upper", **kw)
+    assert upper[next(iter(upper))].meta["layout"] == "upper"
+    for m in full:
+        _same_upper(full[m].values, upper[m].values, f"{label}:{m}")
+    return full, upper
+
+
+@pytest.mark.parametrize("prec", ["split", "fp64"])
+def test_device_upper_matches_full(prec):
+    import torch
+
+    z = O.make_surrogate(300, 700, 3, seed=81)
+    x = torch.from_numpy(z).cuda()
+    _both(x, f"device-{prec}", input_kind="phasor", precision=prec, metrics=ALL)
+    _both(x, f"device-{prec}-none", input_kind="phasor", precision=prec, metrics=ALL, trial_reduce="none")
+    _both(x, f"device-{prec}-pool", input_kind="phasor", precision=prec, metrics=ALL, trial_reduce="pool")
+
+
+def test_device_upper_leaves_caller_lower_untouched():
+    import torch
+
+    z = O.make_surrogate(200, 400, 1, seed=82)
+    x = torch.from_numpy(z).cuda()
+    out = {m: torch.full((1, 200, 200), 7.0, dtype=torch.float32, device="cuda") for m in ("plv", "ciplv")}
+    C.plv_family(x, input_kind="phasor", metrics=("plv", "ciplv"), layout="upper", out=out)
+    ref = C.plv_family(x, input_kind="phasor", metrics=("plv", "ciplv"))
+    il = np.tril_indices(200, -1)
+    iu = np.triu_indices(200)
+    for m in out:
+        o = out[m][0].cpu().numpy()
+        assert np.all(o[il] == 7.0), m
+        assert np.array_equal(o[iu], ref[m].values.cpu().numpy()[iu]), m
+
+
+def test_host_paths_upper_match_full():
+    rng = np.random.default_rng(83)
+    # non-pipelined host path (small N)
+    x = rng.standard_normal((256, 900, 2)).astype(np.float32)
+    _both(x, "host-small", input_kind="real", metrics=ALL)
+    # pipelined host path (N >= 2048, >= 148 tiles): growing stages, diagonal blocks
+    xp = rng.standard_normal((4100, 300)).astype(np.float32)
+    full, upper = _both(xp, "host-pipelined", input_kind="real", metrics=("plv", "iplv", "ciplv"))
+    assert upper["plv"].meta["d2h_bytes"] < 0.7 * full["plv"].meta["d2h_bytes"]
+    # pipelined, FP64
+    _both(xp[:2304].astype(np.float64), "host-pipelined-fp64", input_kind="real", precision="fp64",
+          metrics=("plv", "cim"))
+
+
+def test_upper_with_trial_groups_and_refinement():
+    # zero-lag clusters: many ill-conditioned ciPLV pairs refined in FP64 (the
+    # refine writes must respect the layout too); R = 6 small N -> the trial-
+    # group reduction path
+    rng = np.random.default_rng(84)
+    N, T, R, K = 384, 1024, 6, 32
+    src = rng.standard_normal((N // K, T, R)) + 1j * rng.standard_normal((N // K, T, R))
+    a = src[np.arange(N) // K] + 0.05 * (rng.standard_normal((N, T, R)) + 1j * rng.standard_normal((N, T, R)))
+    a = a.astype(np.complex64)
+    full, upper = _both(a, "refine-mean", input_kind="analytic", metrics=ALL)
+    assert upper["ciplv"].meta["n_refined_pairs"] > 1000
+    _both(a[:, :, :2], "refine-none", input_kind="analytic", metrics=ALL, trial_reduce="none")
+    ref = O.plv_family(a.astype(np.complex128), input_kind="analytic")
+    iu = np.triu_indices(N)
+    for m in ("plv", "iplv", "ciplv"):
+        assert np.max(np.abs(upper[m].values[iu] - ref[m][iu])) <= 1e-5, m
+
+
+def test_upper_over_trials():
+    z = np.exp(1j * np.random.default_rng(85).uniform(0, 6.3, (2, 40, 25, 11)))  # [B, N, T, R]
+    _both(z, "over-trials", input_kind="phasor", bands=True, mode="over_trials", metrics=ALL)
+    _both(z[0], "over-trials-fp64", input_kind="phasor", mode="over_trials", precision="fp64")
+
+
+@pytest.mark.parametrize("mode", ["max", "mean", "none"])
+def test_upper_coherence(mode):
+    rng = np.random.default_rng(86)
+    x = rng.standard_normal((70, 1024, 2))
+    cfg = C.WelchConfig(window_len=128, overlap=64)
+    full = C.coherence_matrix(x, cfg, (0.3, 0.9), mode=mode, metrics=("coh", "icoh", "cim"))
+    upper = C.coherence_matrix(x, cfg, (0.3, 0.9), mode=mode, metrics=("coh", "icoh", "cim"), layout="upper")
+    for m in full:
+        _same_upper(full[m].values, upper[m].values, f"coh-{mode}:{m}")
+
+
+def test_bad_layout_rejected():
+    with pytest.raises(ValueError):
+        C.plv_family(np.zeros((4, 16), np.float32), layout="lower")
