@@ -17,6 +17,7 @@
 #include <map>
 #include <atomic>
 #include <memory>
+#include <chrono>
 #include <thread>
 #include <mutex>
 #include <string>
@@ -101,6 +102,13 @@ struct ps_ctx {
   unsigned long long* h_cnt = nullptr;  // mapped pinned per-stage refine-queue counters
   unsigned long long* d_cnt = nullptr;  // device alias of h_cnt
   int h_cnt_cap = 0;
+  // streamed copy-out of the pipelined host path (upper layout)
+  Buf sbinfo;                    // device: item_sb[items] | sb_need[sb] | sb_cnt[sb]
+  Buf rpick;                     // device: (index, value) of refined ciPLV entries
+  std::vector<int> h_sbinfo;     // host staging of item_sb | sb_need
+  int* h_sbflag = nullptr;       // mapped pinned per-sub-block ready flags
+  int* d_sbflag = nullptr;       // device alias of h_sbflag
+  int h_sbflag_cap = 0;
 };
 
 namespace {
@@ -626,12 +634,21 @@ int kc_blocks_default() {
   return kcb;
 }
 
+// Supertile edge (in ownership tiles) of the item raster order within a stage.
+int raster_tiles() {
+  static const int S = [] {
+    const char* s = std::getenv("PS_RASTER");
+    return s ? std::max(1, std::atoi(s)) : 12;
+  }();
+  return S;
+}
+
 // Work items, grouped by stage: stage s holds the tiles whose column panel
 // starts in [cols[s], cols[s+1]) (one stage covering everything when `cols` is
 // empty).  Ownership (sharding) uses the canonical J-major tile enumeration
 // of ps_pair_shard; within a stage items run in 12 x 12 supertile raster order.
 ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<long long>& cols, bool force_g1,
-                    cudaStream_t st) {
+                    cudaStream_t st, int row_band = 0) {
   const Geometry& g = k.g;
   const int bm = g.split ? kSplitBM : kF64BM;
   const int bn = g.split ? kSplitBN : kF64BN;
@@ -641,20 +658,27 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   for (size_t t = 0; t < tiles.size(); ++t)
     if ((int)(t % k.shard_count) == k.shard_index) mine.push_back(tiles[t]);
   const int n_stages = cols.empty() ? 1 : (int)cols.size() - 1;
-  auto stage_of = [&](int J) -> int {
+  // Column stages (row_band == 0): stage s holds the tiles whose column panel
+  // starts in [cols[s], cols[s+1]).  Row stages (row_band > 0, the streamed
+  // copy-out of the upper layout): stage s holds the tiles whose row panel
+  // starts in [cols[n-1-s], cols[n-s]) -- the last signals come first, and a
+  // finished row band is final over the whole upper part of its rows.
+  auto stage_of = [&](const std::pair<int, int>& t) -> int {
     if (cols.empty()) return 0;
-    const long long j0 = (long long)J * bn;
+    const long long x0 = row_band > 0 ? (long long)t.first * bm : (long long)t.second * bn;
     int s = 0;
-    while (s + 1 < n_stages && j0 >= cols[s + 1]) ++s;
-    return s;
+    while (s + 1 < n_stages && x0 >= cols[s + 1]) ++s;
+    return row_band > 0 ? n_stages - 1 - s : s;
   };
-  static const int S = [] {
-    const char* s = std::getenv("PS_RASTER");
-    return s ? std::max(1, std::atoi(s)) : 12;
-  }();
+  const int S = row_band > 0 ? row_band : raster_tiles();
+  // row stages: bands of S row panels, J-major within a band (a finished band
+  // is one output block of full upper rows); the in-flight window (~74
+  // consecutive items: ~74/S column panels x S row panels) stays L2-sized.
+  // Column stages: S x S supertile raster.
   std::stable_sort(mine.begin(), mine.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
-    return std::make_tuple(stage_of(x.second), x.second / S, x.first / S, x.second, x.first) <
-           std::make_tuple(stage_of(y.second), y.second / S, y.first / S, y.second, y.first);
+    const int xs = row_band > 0 ? 0 : x.second / S, ys = row_band > 0 ? 0 : y.second / S;
+    return std::make_tuple(stage_of(x), xs, x.first / S, x.second, x.first) <
+           std::make_tuple(stage_of(y), ys, y.first / S, y.second, y.first);
   });
   k.pool = a->trial_reduce == PS_TRIALS_POOL;
   if (k.pool || g.R == 1) {
@@ -693,7 +717,7 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   size_t t0 = 0;
   for (int s = 0; s < n_stages; ++s) {
     size_t t1 = t0;
-    while (t1 < mine.size() && stage_of(mine[t1].second) == s) ++t1;
+    while (t1 < mine.size() && stage_of(mine[t1]) == s) ++t1;
     for (int b = 0; b < g.B; ++b)
       for (int gi = 0; gi < k.G; ++gi)
         for (size_t t = t0; t < t1; ++t)
@@ -805,6 +829,7 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
   GramParams p = k.p;
   const int i0 = k.stage_off[s], i1 = k.stage_off[s + 1];
   p.items = k.p.items + i0;
+  if (p.item_sb) p.item_sb += i0;
   p.n_items = i1 - i0;
   if (p.n_items <= 0) return PS_OK;
   const int cta_per_group = k.g.split ? split_cta_group() : 1;
@@ -948,6 +973,7 @@ ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
   }
   if (c->h_cnt_cap < n_stages) {
     if (c->h_cnt) cudaFreeHost(c->h_cnt);
+  if (c->h_sbflag) cudaFreeHost(c->h_sbflag);
     c->h_cnt = nullptr;
     PS_CUDA(cudaHostAlloc(&c->h_cnt, (size_t)n_stages * sizeof(unsigned long long),
                           cudaHostAllocMapped | cudaHostAllocPortable));
@@ -1001,38 +1027,49 @@ void host_mirror_rows(const std::vector<std::pair<char*, bool>>& mats, int dbl, 
 }
 
 // PS_PIPE_TRACE=1: per-stage event timeline of the pipelined host path on stderr
+// (each line: device time of the event, host time at which it was enqueued)
 struct PipeTrace {
   cudaEvent_t t0 = nullptr;
-  std::vector<std::tuple<cudaEvent_t, const char*, int>> ev;
+  std::chrono::steady_clock::time_point h0;
+  std::vector<std::tuple<cudaEvent_t, const char*, int, double>> ev;
   explicit PipeTrace(cudaStream_t st) {
     cudaEventCreate(&t0);
     cudaEventRecord(t0, st);
+    h0 = std::chrono::steady_clock::now();
   }
   void rec(cudaStream_t st, const char* what, int s) {
     cudaEvent_t e;
     cudaEventCreate(&e);
     cudaEventRecord(e, st);
-    ev.emplace_back(e, what, s);
+    const double hms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    ev.emplace_back(e, what, s, hms);
   }
   void dump() {
     for (auto& x : ev) {
       cudaEventSynchronize(std::get<0>(x));
       float ms = 0.f;
       cudaEventElapsedTime(&ms, t0, std::get<0>(x));
-      std::fprintf(stderr, "[pipe] %-6s stage %2d  %8.2f ms\n", std::get<1>(x), std::get<2>(x), ms);
+      std::fprintf(stderr, "[pipe] %-6s stage %2d  %8.2f ms  (host %8.2f ms)\n", std::get<1>(x), std::get<2>(x), ms,
+                   std::get<3>(x));
       cudaEventDestroy(std::get<0>(x));
     }
     cudaEventDestroy(t0);
   }
 };
 
-// E2E host path, pipelined over column stages (the "growing square"):
-// stage s owns output columns [cols[s], cols[s+1]).  Its Gram tiles need
-// only signal rows < cols[s+1], and once they are done the output block
-// rows [0, cols[s+1]) x cols [cols[s], cols[s+1]) plus its mirror
-// rows [cols[s], cols[s+1]) x cols [0, cols[s]) is final.  So the H2D of
-// stage s+1's input rows, the Gram of stage s and the D2H of stage s-1's
-// output blocks run concurrently on separate streams.
+// E2E host path, pipelined over stages of signals (the "growing square"):
+// the H2D + normalisation of stage s+1's signals, the Gram of stage s and the
+// D2H of finished output run concurrently on separate streams.
+//  * Full layout -- column stages: stage s owns output columns
+//    [cols[s], cols[s+1]); its tiles need only signals < cols[s+1], and once
+//    they are done the block rows [0, cols[s+1]) x cols [cols[s], cols[s+1])
+//    plus its mirror is final and is copied out.
+//  * Upper layout -- row stages from the last signals up: stage s owns the
+//    tiles of rows [lo(s), hi(s)) (all their columns have arrived), and the
+//    output is streamed per finished row band: the upper part of a band's
+//    rows, cols [i, N), is final when the band's tiles are emitted, and long
+//    contiguous host rows are what the copy engine moves fastest (55 GB/s
+//    against 35-45 GB/s for the 10-14 KB rows of column blocks).
 ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long span, long long esz,
                          ps_plv_result* res) {
   const Geometry& g = k.g;
@@ -1040,21 +1077,78 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     const char* s = std::getenv("PS_STAGE_W");  // experiment override (signals per stage)
     return s ? std::atoll(s) : 0LL;
   }();
-  // Stage widths grow (1024, 1536, 2048, ... up to ~N/6): the first output
+  // Column stages grow (1024, 1536, 2048, ... up to ~N/6): the first output
   // blocks become final after a short H2D so the D2H engine -- the critical
   // path, 4.8 GB at C5 -- starts early; later stages are wide enough to fill
-  // the GPU.  PS_STAGE_W forces a uniform width (experiments).
-  std::vector<long long> cols;
-  if (w_env > 0) {
-    const long long W = round_up(w_env, 256);
-    for (long long x = 0; x < g.N; x += W) cols.push_back(x);
+  // the GPU.  Row stages: see below.  PS_STAGE_W forces a uniform width and
+  // PS_STAGE_COLS an explicit list (experiments).
+  static const std::vector<long long> w_list = [] {
+    // experiment override: PS_STAGE_COLS="w0,w1,..." explicit stage widths
+    // (rounded up to 256), the last one repeated until N is covered
+    std::vector<long long> v;
+    const char* s = std::getenv("PS_STAGE_COLS");
+    while (s && *s) {
+      const long long w = std::atoll(s);
+      if (w > 0) v.push_back(round_up(w, 256));
+      s = std::strchr(s, ',');
+      if (s) ++s;
+    }
+    return v;
+  }();
+  const bool upper = a->out_layout == PS_LAYOUT_UPPER;
+  static const bool no_stream_env = std::getenv("PS_PIPE_NO_STREAM") != nullptr;  // experiment: column stages
+  // upper layout: row stages from the last signals up, output streamed per
+  // finished row band (see below); full layout: column stages
+  const bool stream_out = upper && !no_stream_env;
+  static const int band_env = [] {
+    const char* s = std::getenv("PS_SB_BAND");  // row panels per streamed output band
+    return s ? std::max(1, std::atoi(s)) : 4;
+  }();
+  // stage widths in processing order
+  std::vector<long long> widths;
+  if (!w_list.empty()) {
+    widths = w_list;
+  } else if (w_env > 0) {
+    widths.push_back(round_up(w_env, 256));
+  } else if (stream_out) {
+    // grow by 1024 up to ~N/6 (the Gram of a stage should cover the copy-in
+    // of the next one), then finish with 2/3 + 1/3 of the last <= 4096
+    // signals: the final stage's Gram and its last band's D2H are the tail
+    const long long wmax = std::max<long long>(1024, round_up((g.N + 5) / 6, 256));
+    long long rem = g.N, w = 1024;
+    while (rem > 4096) {
+      const long long take = std::min(w, rem - 3072);
+      widths.push_back(take);
+      rem -= take;
+      w = std::min(wmax, w + 1024);
+    }
+    if (rem > 1024) widths.push_back(rem - 1024);
+    widths.push_back(std::min<long long>(rem, 1024));
   } else {
     const long long wmax = std::max<long long>(1024, round_up((g.N + 5) / 6, 256));
-    long long w = 1024;
-    for (long long x = 0; x < g.N; x += w, w = std::min(wmax, w + 512)) cols.push_back(x);
+    for (long long w = 1024, x = 0; x < g.N; x += w, w = std::min(wmax, w + 512)) widths.push_back(w);
+  }
+  // cut points 0 = cols[0] < ... < cols[S] = N, every inner cut a multiple of
+  // 256 counted from 0 (row / column panels never straddle a stage)
+  std::vector<long long> cols;
+  if (stream_out) {
+    std::vector<long long> cuts;
+    long long x = g.N;
+    for (size_t i = 0; x > 0; ++i) {
+      const long long w = widths[std::min(i, widths.size() - 1)];
+      x = std::max(0LL, (x - w + 128) / 256 * 256);
+      if (x < 256) x = 0;
+      cuts.push_back(x);
+    }
+    cols.assign(cuts.rbegin(), cuts.rend());
+  } else {
+    for (long long x = 0, i = 0; x < g.N; x += widths[std::min<size_t>(i, widths.size() - 1)], ++i) cols.push_back(x);
   }
   cols.push_back(g.N);
   const int S = (int)cols.size() - 1;
+  // signal range of processing stage s
+  auto lo = [&](int s) { return stream_out ? cols[S - 1 - s] : cols[s]; };
+  auto hi = [&](int s) { return stream_out ? cols[S - s] : cols[s + 1]; };
   PS_TRY(ensure_pipeline(c, S));
   cudaStream_t si = c->s_in, sc = c->s_comp, sr = c->s_ref, so = c->s_out;
   c->launches = 0;
@@ -1064,7 +1158,6 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
   PS_TRY(ensure(c->planes, plane_bytes));
   const size_t oes = g.split ? 4 : 8;
-  const bool upper = a->out_layout == PS_LAYOUT_UPPER;
   void* houts[5];
   std::memcpy(houts, k.outs, sizeof(houts));
   int nout = 0;
@@ -1081,7 +1174,76 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   PS_TRY(prep_begin(c, a, g, si));  // Hilbert workspace sized once (no realloc mid-pipeline)
   PS_TRY(reset_status(c, si));
   PS_TRY(init_row_state(c, g, si));
-  PS_TRY(plan_call(c, a, k, cols, /*force_g1=*/true, si));
+  PS_TRY(plan_call(c, a, k, cols, /*force_g1=*/true, si, /*row_band=*/stream_out ? band_env : 0));
+  // ---- streamed copy-out (upper layout) ------------------------------------
+  // Row stages run from the last signals up and, within a stage, band by band
+  // (band_env row panels, J-major inside a band).  Once a band's tiles are
+  // emitted, the upper part of its rows -- cols [i, N) of every row i, i.e.
+  // long contiguous host rows, the shape the copy engine moves fastest -- is
+  // final: that is one output sub-block.  The split kernel publishes a
+  // sub-block in mapped host memory as soon as its last item is emitted, so
+  // its D2H starts while the stage's other bands are still being computed;
+  // the FP64 kernel (no counters) releases a stage's sub-blocks with the
+  // stage's completion event.
+  struct SubBlock {
+    long long slot, r0, r1, c0, c1;
+  };
+  std::vector<SubBlock> sbs;
+  std::vector<int> sb_first(S + 1, 0);  // sub-blocks of stage s: [sb_first[s], sb_first[s + 1])
+  if (stream_out) {
+    const int exec_rows = g.split ? split_panel_rows() : kF64BM;
+    const int sub = g.split ? kSplitBM / exec_rows : 1;
+    const int n_items = k.stage_off[S];
+    std::vector<int>& info = c->h_sbinfo;
+    info.assign((size_t)n_items, 0);
+    std::vector<int> need;
+    const int arrivals = g.split ? split_epi_arrivals() : 1;
+    for (int s = 0; s < S; ++s) {
+      sb_first[s] = (int)sbs.size();
+      long long prev_key = -1;
+      for (int n = k.stage_off[s]; n < k.stage_off[s + 1]; ++n) {
+        const Item& w = c->h_items[n];
+        const long long slot = k.slot_mode == 0 ? (long long)w.b * g.R + w.g : (long long)w.b;
+        const long long key = slot * 4096 + (w.I / sub) / band_env;  // (slot, row band)
+        const long long r0 = (long long)w.I * exec_rows, r1 = std::min<long long>(r0 + exec_rows, g.N);
+        if (key != prev_key) {
+          sbs.push_back(SubBlock{slot, r0, r1, r0, g.N});
+          need.push_back(0);
+          prev_key = key;
+        }
+        SubBlock& b = sbs.back();
+        b.r0 = std::min(b.r0, r0);
+        b.r1 = std::max(b.r1, r1);
+        b.c0 = b.r0;  // upper part of rows [r0, r1): cols [i, N)
+        need.back() += arrivals;
+        info[(size_t)n] = (int)sbs.size() - 1;
+      }
+    }
+    sb_first[S] = (int)sbs.size();
+    const int n_sb = (int)sbs.size();
+    if (g.split && n_sb > 0) {
+      info.insert(info.end(), need.begin(), need.end());
+      const size_t ibytes = info.size() * sizeof(int);
+      PS_TRY(ensure(c->sbinfo, ibytes + (size_t)n_sb * sizeof(int)));
+      PS_CUDA(cudaMemcpyAsync(c->sbinfo.p, info.data(), ibytes, cudaMemcpyHostToDevice, si));
+      PS_CUDA(cudaMemsetAsync(static_cast<char*>(c->sbinfo.p) + ibytes, 0, (size_t)n_sb * sizeof(int), si));
+      if (c->h_sbflag_cap < n_sb) {
+        if (c->h_sbflag) cudaFreeHost(c->h_sbflag);
+        c->h_sbflag = nullptr;
+        c->h_sbflag_cap = 0;
+        const int cap = std::max(n_sb, 1024);
+        PS_CUDA(cudaHostAlloc(&c->h_sbflag, (size_t)cap * sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+        PS_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->d_sbflag), c->h_sbflag, 0));
+        c->h_sbflag_cap = cap;
+      }
+      std::memset(c->h_sbflag, 0, (size_t)n_sb * sizeof(int));
+      int* base = static_cast<int*>(c->sbinfo.p);
+      k.p.item_sb = base;
+      k.p.sb_need = base + n_items;
+      k.p.sb_cnt = base + n_items + n_sb;
+      k.p.sb_flag = c->d_sbflag;
+    }
+  }
   ps_plv_args d = *a;
   d.input = c->hin.p;
   const long long U = g.B * g.R;
@@ -1093,8 +1255,8 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   for (int s = 0; s < S; ++s) {
     for (long long u = 0; u < U; ++u) {
       const long long b = u / g.R, t = u % g.R;
-      const long long off = b * a->stride_band + t * a->stride_trial + cols[s] * a->stride_signal;
-      const long long len = (cols[s + 1] - 1 - cols[s]) * a->stride_signal + (g.T - 1) * a->stride_sample + 1;
+      const long long off = b * a->stride_band + t * a->stride_trial + lo(s) * a->stride_signal;
+      const long long len = (hi(s) - 1 - lo(s)) * a->stride_signal + (g.T - 1) * a->stride_sample + 1;
       PS_CUDA(cudaMemcpyAsync(static_cast<char*>(c->hin.p) + off * esz, static_cast<const char*>(a->input) + off * esz,
                               (size_t)len * esz, cudaMemcpyHostToDevice, si));
       h2d_bytes += (size_t)len * esz;
@@ -1102,7 +1264,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     if (trace) trace->rec(si, "h2d", s);
     for (long long u = 0; u < U; ++u)
       PS_TRY(prepare_rows(c, &d, g, c->hin.p, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride,
-                          u * g.N + cols[s], u * g.N + cols[s + 1], si, &copied));
+                          u * g.N + lo(s), u * g.N + hi(s), si, &copied));
     if (trace) trace->rec(si, "norm", s);
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), si));
   }
@@ -1110,7 +1272,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   for (int s = 0; s < S; ++s) {
     PS_CUDA(cudaStreamWaitEvent(sc, pool_event(c, 3 * s), 0));
     if (upper) {  // the copy-out of the diagonal block carries its lower part: make it 0, not stale
-      const long long c0 = cols[s], c1 = cols[s + 1];
+      const long long c0 = lo(s), c1 = hi(s);
       for (int m = 0; m < 5; ++m)
         if (k.outs[m])
           for (long long sl = 0; sl < k.slots; ++sl)
@@ -1125,107 +1287,210 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     PS_CUDA(launch_copy_u64(&c->d_status->n_illcond, &c->d_cnt[s], sc));
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s + 1), sc));
   }
-  // ---- refine + copy-out per stage ------------------------------------------
-  // Both halves of every stage block cross the link by default.  With
-  // PS_HOST_MIRROR=1 only the block rows [0, c1) x cols [c0, c1) do, and a
-  // host worker fills the mirror rows [c0, c1) x cols [0, c0) with a
-  // multi-threaded cache-blocked transpose behind the D2H events (the outputs
-  // are exactly symmetric / antisymmetric): half the D2H bytes, but on the
-  // 16-core GPU hosts measured so far the transposes (~20 GB/s while the DMA
-  // writes the same memory) are slower than the link they relieve
-  // (DESIGN.md "E2E").
-  // PS_HOST_MIRROR=k mirrors the first k output matrices (metric order, then
-  // slot) on the host and ships the others whole -- a partial split of the
-  // mirroring between the link and the host's memory bandwidth.
-  static const int mirror_count = [] {
-    const char* s = std::getenv("PS_HOST_MIRROR");
-    return s ? std::max(0, std::atoi(s)) : 0;
-  }();
-  const bool host_mirror = mirror_count > 0 && !upper;
-  auto mirrored = [&](long long q) { return q < mirror_count; };
-  auto mirror_stage = [&](int s) {
-    const long long c0 = cols[s], c1 = cols[s + 1];
-    if (c0 == 0) return;
-    std::vector<std::pair<char*, bool>> mats;
-    long long q = 0;
-    for (int m = 0; m < 5; ++m) {
-      if (!houts[m]) continue;
-      for (long long sl = 0; sl < k.slots; ++sl, ++q)
-        if (mirrored(q)) mats.emplace_back(static_cast<char*>(houts[m]) + (size_t)sl * g.N * g.N * oes, m == 4);
-    }
-    if (!mats.empty()) host_mirror_rows(mats, g.split ? 0 : 1, g.N, c0, c1);
-  };
   size_t d2h_bytes = 0;
-  unsigned long long prev = 0;
-  static const bool no_d2h_env = std::getenv("PS_PIPE_NO_D2H") != nullptr;  // experiment: Gram-only timeline
-  // the mirror runs on a worker thread, stage by stage behind the D2H events,
-  // so the issue of later copies never waits for the host transposes
-  pool_event(c, 4 * (size_t)S + 2);  // create every event before the worker reads the pool
-  std::atomic<int> issued{0};
-  std::atomic<bool> abort_worker{false};
-  std::thread worker;
-  if (host_mirror && !no_d2h_env)
-    worker = std::thread([&, dev = c->device] {
-      cudaSetDevice(dev);
-      for (int s = 0; s < S; ++s) {
-        while (issued.load(std::memory_order_acquire) <= s) {
-          if (abort_worker.load()) return;
-          std::this_thread::yield();
-        }
-        if (cudaEventSynchronize(pool_event(c, 3 * S + 1 + s)) != cudaSuccess) return;
-        mirror_stage(s);
+  if (!stream_out) {
+    // ---- refine + copy-out per stage ------------------------------------------
+    // Both halves of every stage block cross the link by default.  With
+    // PS_HOST_MIRROR=1 only the block rows [0, c1) x cols [c0, c1) do, and a
+    // host worker fills the mirror rows [c0, c1) x cols [0, c0) with a
+    // multi-threaded cache-blocked transpose behind the D2H events (the outputs
+    // are exactly symmetric / antisymmetric): half the D2H bytes, but on the
+    // 16-core GPU hosts measured so far the transposes (~20 GB/s while the DMA
+    // writes the same memory) are slower than the link they relieve
+    // (DESIGN.md "E2E").
+    // PS_HOST_MIRROR=k mirrors the first k output matrices (metric order, then
+    // slot) on the host and ships the others whole -- a partial split of the
+    // mirroring between the link and the host's memory bandwidth.
+    static const int mirror_count = [] {
+      const char* s = std::getenv("PS_HOST_MIRROR");
+      return s ? std::max(0, std::atoi(s)) : 0;
+    }();
+    const bool host_mirror = mirror_count > 0 && !upper;
+    auto mirrored = [&](long long q) { return q < mirror_count; };
+    auto mirror_stage = [&](int s) {
+      const long long c0 = cols[s], c1 = cols[s + 1];
+      if (c0 == 0) return;
+      std::vector<std::pair<char*, bool>> mats;
+      long long q = 0;
+      for (int m = 0; m < 5; ++m) {
+        if (!houts[m]) continue;
+        for (long long sl = 0; sl < k.slots; ++sl, ++q)
+          if (mirrored(q)) mats.emplace_back(static_cast<char*>(houts[m]) + (size_t)sl * g.N * g.N * oes, m == 4);
       }
-    });
-  struct Joiner {
-    std::thread& t;
-    std::atomic<bool>& abort;
-    ~Joiner() {
-      abort.store(true);
-      if (t.joinable()) t.join();
+      if (!mats.empty()) host_mirror_rows(mats, g.split ? 0 : 1, g.N, c0, c1);
+    };
+
+    unsigned long long prev = 0;
+    static const bool no_d2h_env = std::getenv("PS_PIPE_NO_D2H") != nullptr;  // experiment: Gram-only timeline
+    // the mirror runs on a worker thread, stage by stage behind the D2H events,
+    // so the issue of later copies never waits for the host transposes
+    pool_event(c, 4 * (size_t)S + 2);  // create every event before the worker reads the pool
+    std::atomic<int> issued{0};
+    std::atomic<bool> abort_worker{false};
+    std::thread worker;
+    if (host_mirror && !no_d2h_env)
+      worker = std::thread([&, dev = c->device] {
+        cudaSetDevice(dev);
+        for (int s = 0; s < S; ++s) {
+          while (issued.load(std::memory_order_acquire) <= s) {
+            if (abort_worker.load()) return;
+            std::this_thread::yield();
+          }
+          if (cudaEventSynchronize(pool_event(c, 3 * S + 1 + s)) != cudaSuccess) return;
+          mirror_stage(s);
+        }
+      });
+    struct Joiner {
+      std::thread& t;
+      std::atomic<bool>& abort;
+      ~Joiner() {
+        abort.store(true);
+        if (t.joinable()) t.join();
+      }
+    } joiner{worker, abort_worker};
+    for (int s = 0; s < S; ++s) {
+      cudaEvent_t ready = pool_event(c, 3 * s + 1);
+      PS_CUDA(cudaEventSynchronize(ready));
+      const unsigned long long n = c->h_cnt[s];
+      if (n > prev && k.outs[2] && g.split) {
+        PS_CUDA(cudaStreamWaitEvent(sr, ready, 0));
+        PS_TRY(refine_range(c, k, prev, n, sr));
+        ready = pool_event(c, 3 * s + 2);
+        PS_CUDA(cudaEventRecord(ready, sr));
+      }
+      prev = n;
+      PS_CUDA(cudaStreamWaitEvent(so, ready, 0));
+      const long long c0 = cols[s], c1 = cols[s + 1];
+      static const bool no_d2h = std::getenv("PS_PIPE_NO_D2H") != nullptr;  // experiment: Gram-only timeline
+      long long q = 0;
+      for (int m = 0; m < 5 && !no_d2h; ++m) {
+        if (!houts[m]) continue;
+        for (long long sl = 0; sl < k.slots; ++sl, ++q) {
+          const size_t base = (size_t)sl * g.N * g.N * oes;
+          char* hdst = static_cast<char*>(houts[m]) + base;
+          const char* dsrc = static_cast<const char*>(k.outs[m]) + base;
+          const size_t pitch = (size_t)g.N * oes;
+          // rows [0, c1) x cols [c0, c1)
+          PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * oes, pitch, dsrc + (size_t)c0 * oes, pitch,
+                                    (size_t)(c1 - c0) * oes, (size_t)c1, cudaMemcpyDeviceToHost, so));
+          d2h_bytes += (size_t)(c1 - c0) * oes * (size_t)c1;
+          // rows [c0, c1) x cols [0, c0) (strictly lower: not part of the upper layout)
+          if (c0 > 0 && !mirrored(q) && !upper) {
+            PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * pitch, pitch, dsrc + (size_t)c0 * pitch, pitch,
+                                      (size_t)c0 * oes, (size_t)(c1 - c0), cudaMemcpyDeviceToHost, so));
+            d2h_bytes += (size_t)c0 * oes * (size_t)(c1 - c0);
+          }
+        }
+      }
+      cudaEvent_t copied_ev = pool_event(c, 3 * S + 1 + s);
+      PS_CUDA(cudaEventRecord(copied_ev, so));
+      issued.store(s + 1, std::memory_order_release);
+      if (trace && s + 1 < S) trace->rec(so, "d2h", s);
     }
-  } joiner{worker, abort_worker};
-  for (int s = 0; s < S; ++s) {
-    cudaEvent_t ready = pool_event(c, 3 * s + 1);
-    PS_CUDA(cudaEventSynchronize(ready));
-    const unsigned long long n = c->h_cnt[s];
-    if (n > prev && k.outs[2] && g.split) {
-      PS_CUDA(cudaStreamWaitEvent(sr, ready, 0));
-      PS_TRY(refine_range(c, k, prev, n, sr));
-      ready = pool_event(c, 3 * s + 2);
-      PS_CUDA(cudaEventRecord(ready, sr));
-    }
-    prev = n;
-    PS_CUDA(cudaStreamWaitEvent(so, ready, 0));
-    const long long c0 = cols[s], c1 = cols[s + 1];
+    if (trace) trace->rec(so, "d2h", S - 1);
+    PS_CUDA(cudaStreamSynchronize(so));
+    if (worker.joinable()) worker.join();  // all mirrors done
+  } else {
+    // ---- streamed copy-out: ship each sub-block as soon as it is final -----
     static const bool no_d2h = std::getenv("PS_PIPE_NO_D2H") != nullptr;  // experiment: Gram-only timeline
-    long long q = 0;
-    for (int m = 0; m < 5 && !no_d2h; ++m) {
-      if (!houts[m]) continue;
-      for (long long sl = 0; sl < k.slots; ++sl, ++q) {
-        const size_t base = (size_t)sl * g.N * g.N * oes;
+    const size_t pitch = (size_t)g.N * oes;
+    // upper part of sub-block b for metric m: rows above the diagonal block as
+    // one 2-D copy, the rows crossing it in 256-row strips [a, a+h) x [a, c1)
+    // (their few strictly-lower entries are zero on the device)
+    auto ship = [&](const SubBlock& b) -> ps_status {
+      for (int m = 0; m < 5 && !no_d2h; ++m) {
+        if (!houts[m]) continue;
+        const size_t base = (size_t)b.slot * g.N * g.N * oes;
         char* hdst = static_cast<char*>(houts[m]) + base;
         const char* dsrc = static_cast<const char*>(k.outs[m]) + base;
-        const size_t pitch = (size_t)g.N * oes;
-        // rows [0, c1) x cols [c0, c1)
-        PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * oes, pitch, dsrc + (size_t)c0 * oes, pitch,
-                                  (size_t)(c1 - c0) * oes, (size_t)c1, cudaMemcpyDeviceToHost, so));
-        d2h_bytes += (size_t)(c1 - c0) * oes * (size_t)c1;
-        // rows [c0, c1) x cols [0, c0) (strictly lower: not part of the upper layout)
-        if (c0 > 0 && !mirrored(q) && !upper) {
-          PS_CUDA(cudaMemcpy2DAsync(hdst + (size_t)c0 * pitch, pitch, dsrc + (size_t)c0 * pitch, pitch,
-                                    (size_t)c0 * oes, (size_t)(c1 - c0), cudaMemcpyDeviceToHost, so));
-          d2h_bytes += (size_t)c0 * oes * (size_t)(c1 - c0);
+        const long long rtop = std::min(b.r1, b.c0);
+        if (rtop > b.r0) {
+          const size_t off = (size_t)b.r0 * pitch + (size_t)b.c0 * oes;
+          PS_CUDA(cudaMemcpy2DAsync(hdst + off, pitch, dsrc + off, pitch, (size_t)(b.c1 - b.c0) * oes,
+                                    (size_t)(rtop - b.r0), cudaMemcpyDeviceToHost, so));
+          d2h_bytes += (size_t)(b.c1 - b.c0) * oes * (size_t)(rtop - b.r0);
+        }
+        for (long long r = std::max(b.r0, b.c0); r < b.r1; r += 256) {
+          const long long re = std::min(r + 256, b.r1);
+          const size_t off = (size_t)r * pitch + (size_t)r * oes;
+          PS_CUDA(cudaMemcpy2DAsync(hdst + off, pitch, dsrc + off, pitch, (size_t)(b.c1 - r) * oes, (size_t)(re - r),
+                                    cudaMemcpyDeviceToHost, so));
+          d2h_bytes += (size_t)(b.c1 - r) * oes * (size_t)(re - r);
         }
       }
+      return PS_OK;
+    };
+    const bool flags = k.p.sb_flag != nullptr;
+    // PS_PIPE_TRACE=2: one timeline event per shipped sub-block as well
+    static const bool trace_blocks_env = [] {
+      const char* e = std::getenv("PS_PIPE_TRACE");
+      return e && std::atoi(e) >= 2;
+    }();
+    const bool trace_blocks = trace && trace_blocks_env;
+    // PS_PIPE_POLL (experiment): 0 = release blocks per stage event only,
+    // 1 = poll the flags (yield), 2 = poll the flags (20 us sleeps)
+    static const int poll_mode = [] {
+      const char* e = std::getenv("PS_PIPE_POLL");
+      return e ? std::atoi(e) : 1;
+    }();
+    unsigned long long prev = 0;
+    std::vector<long long> patch_idx;  // refined ciPLV entries: flat index, final value
+    std::vector<float> patch_val;
+    for (int s = 0; s < S; ++s) {
+      cudaEvent_t done = pool_event(c, 3 * s + 1);
+      for (int q = sb_first[s]; q < sb_first[s + 1]; ++q) {
+        // ready: the kernel published the block, or the whole stage finished
+        if (poll_mode == 0 || !flags) {
+          PS_CUDA(cudaEventSynchronize(done));
+        } else {
+          int spins = 0;
+          while (reinterpret_cast<volatile int*>(c->h_sbflag)[q] == 0) {
+            // the stage event is the fallback (and error) path: queried only
+            // every 64 polls of the flag, which lives in host memory
+            if ((++spins & 63) == 0) {
+              const cudaError_t e = cudaEventQuery(done);
+              if (e == cudaSuccess) break;
+              if (e != cudaErrorNotReady) PS_CUDA(e);
+            }
+            if (poll_mode == 2) std::this_thread::sleep_for(std::chrono::microseconds(20));
+            else std::this_thread::yield();
+          }
+        }
+        PS_TRY(ship(sbs[(size_t)q]));
+        if (trace_blocks) trace->rec(so, "blk", q);
+      }
+      PS_CUDA(cudaEventSynchronize(done));
+      const unsigned long long n = c->h_cnt[s];
+      if (n > prev && k.outs[2] && g.split) {
+        // FP64 refinement of this stage's ill-conditioned ciPLV pairs (their
+        // blocks may already be on their way); the corrected values come back
+        // as (index, value) pairs and patch the host matrix after the last copy
+        PS_CUDA(cudaStreamWaitEvent(sr, done, 0));
+        PS_TRY(refine_range(c, k, prev, n, sr));
+        if (houts[2] && !no_d2h) {
+          const int m = (int)(std::min<unsigned long long>(n, (unsigned long long)k.p.refine_cap) - prev);
+          PS_TRY(ensure(c->rpick, (size_t)m * 12 + 256));
+          long long* d_idx = static_cast<long long*>(c->rpick.p);
+          float* d_val = reinterpret_cast<float*>(static_cast<char*>(c->rpick.p) + (size_t)m * 8);
+          PS_CUDA(launch_refine_pick(static_cast<const RefineEntry*>(c->refine.p) + prev, m,
+                                     static_cast<const float*>(k.outs[2]), g.N, d_idx, d_val, sr));
+          const size_t at = patch_idx.size();
+          patch_idx.resize(at + (size_t)m);
+          patch_val.resize(at + (size_t)m);
+          PS_CUDA(cudaMemcpyAsync(patch_idx.data() + at, d_idx, (size_t)m * 8, cudaMemcpyDeviceToHost, sr));
+          PS_CUDA(cudaMemcpyAsync(patch_val.data() + at, d_val, (size_t)m * 4, cudaMemcpyDeviceToHost, sr));
+          PS_CUDA(cudaStreamSynchronize(sr));
+          d2h_bytes += (size_t)m * 12;
+        }
+      }
+      prev = n;
+      if (trace && s + 1 < S) trace->rec(so, "d2h", s);
     }
-    cudaEvent_t copied_ev = pool_event(c, 3 * S + 1 + s);
-    PS_CUDA(cudaEventRecord(copied_ev, so));
-    issued.store(s + 1, std::memory_order_release);
-    if (trace && s + 1 < S) trace->rec(so, "d2h", s);
+    if (trace) trace->rec(so, "d2h", S - 1);
+    PS_CUDA(cudaStreamSynchronize(so));
+    float* hc = static_cast<float*>(houts[2]);
+    for (size_t q = 0; q < patch_idx.size(); ++q) hc[patch_idx[q]] = patch_val[q];
   }
-  if (trace) trace->rec(so, "d2h", S - 1);
-  PS_CUDA(cudaStreamSynchronize(so));
-  if (worker.joinable()) worker.join();  // all mirrors done
   if (trace) trace->dump();
   ps_status st = read_status(c, so);
   if (res) {
@@ -1307,7 +1572,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
-                 &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale, &c->sortws})
+                 &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale, &c->sortws, &c->sbinfo, &c->rpick})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);

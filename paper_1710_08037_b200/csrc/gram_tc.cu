@@ -499,6 +499,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           buf ^= 1;
         }
       }
+      if (p.sb_cnt) {  // item emitted by this warp: count it towards its output sub-block
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          const int sb = p.item_sb[it];
+          if (atomicAdd(&p.sb_cnt[sb], 1) == p.sb_need[sb] - 1) {
+            __threadfence_system();
+            p.sb_flag[sb] = 1;
+          }
+        }
+      }
     }
   }
 
@@ -547,6 +558,8 @@ int split_cta_group() {
 int split_panel_rows() { return split_cta_group() * BMC; }
 
 int split_b_box_rows() { return BN / split_cta_group(); }
+
+int split_epi_arrivals() { return NEPI_WARPS * split_cta_group(); }
 
 cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p, int groups,
                               cudaStream_t st) {

@@ -93,6 +93,15 @@ struct GramParams {
   int lock_group;
   int lock_lag;
   int lock_rounds;             // rounds per item (uniform across items when enabled)
+  // Streamed copy-out (split kernel, pipelined host path): item n belongs to
+  // output sub-block item_sb[n]; every epilogue warp that finished emitting an
+  // item fences its stores and counts in sb_cnt[sb]; the arrival that reaches
+  // sb_need[sb] publishes sb_flag[sb] = 1 into mapped host memory, so the host
+  // ships that block while the kernel keeps running.  sb_cnt == nullptr: off.
+  int* sb_cnt;
+  const int* item_sb;
+  const int* sb_need;
+  volatile int* sb_flag;
 };
 
 // ---- launchers (return cudaError_t) --------------------------------------
@@ -163,6 +172,9 @@ cudaError_t launch_refine(const GramParams& p, const RefineEntry* entries, const
 // n + 1 ints).  ib = bits of the signal index; the packed key needs
 // bits(slot) + 2 ib <= 64.
 size_t refine_sort_ws_bytes(int n);
+// (flat output index, final ciPLV value) of queued refine entries (split outputs)
+cudaError_t launch_refine_pick(const RefineEntry* entries, int n, const float* out, long long N, long long* idx,
+                               float* val, cudaStream_t st);
 cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, void* ws,
                                  size_t ws_bytes, RefineEntry* sorted, double* exact, int* groups, int overwrite,
                                  int div, cudaStream_t st);
@@ -172,6 +184,7 @@ cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int 
 int split_cta_group();
 int split_panel_rows();   // rows of one execution panel (= UMMA M)
 int split_b_box_rows();   // J-panel rows staged per CTA
+int split_epi_arrivals(); // epilogue warps per CTA group (arrivals per item on GramParams::sb_cnt)
 
 // tile geometry of the two Gram kernels (ownership / sharding granularity)
 constexpr int kSplitBM = 256;

@@ -210,4 +210,24 @@ cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int 
   return cudaGetLastError();
 }
 
+// Streamed copy-out of the pipelined host path: the final (refined) ciPLV
+// value at every queued entry, packed with its flat output index, so the host
+// can patch the blocks it already received without shipping them again.
+__global__ void refine_pick_kernel(const RefineEntry* __restrict__ e, int n, const float* __restrict__ out,
+                                   long long N, long long* __restrict__ idx, float* __restrict__ val) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const RefineEntry en = e[q];
+  const long long at = ((long long)en.slot * N + en.i) * N + en.j;
+  idx[q] = at;
+  val[q] = out[at];
+}
+
+cudaError_t launch_refine_pick(const RefineEntry* entries, int n, const float* out, long long N, long long* idx,
+                               float* val, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  refine_pick_kernel<<<(n + 255) / 256, 256, 0, st>>>(entries, n, out, N, idx, val);
+  return cudaGetLastError();
+}
+
 }  // namespace ps

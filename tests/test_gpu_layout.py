@@ -105,6 +105,40 @@ def test_upper_with_trial_groups_and_refinement():
         assert np.max(np.abs(upper[m].values[iu] - ref[m][iu])) <= 1e-5, m
 
 
+@pytest.mark.parametrize("R,reduce", [(1, "mean"), (3, "mean"), (2, "none")])
+def test_host_pipelined_upper_streamed_with_refinement(R, reduce):
+    # pipelined host path (N >= 2048, >= 148 tiles) with the upper layout: the
+    # output sub-blocks are shipped while the Gram kernel still runs, and the
+    # refined ciPLV entries (FP64, after their stage) come back as (index,
+    # value) pairs that patch the received blocks -- upper entries bit-
+    # identical to the full layout (which ships whole stage blocks after the
+    # refinement), lower triangle zero
+    rng = np.random.default_rng(87)
+    N, T, K = 3072, 192, 48
+    src = rng.standard_normal((N // K, T, R)) + 1j * rng.standard_normal((N // K, T, R))
+    a = src[np.arange(N) // K] + 0.05 * (rng.standard_normal((N, T, R)) + 1j * rng.standard_normal((N, T, R)))
+    # trials-first storage ([R, N, T] contiguous, viewed as [N, T, R]): unit
+    # sample stride, the layout the pipelined host path requires
+    a = np.transpose(np.ascontiguousarray(np.transpose(a, (2, 0, 1)).astype(np.complex64)), (1, 2, 0))
+    full, upper = _both(a, f"host-stream-{R}-{reduce}", input_kind="analytic", trial_reduce=reduce,
+                        metrics=("plv", "iplv", "ciplv", "cim"))
+    assert upper["ciplv"].meta["n_refined_pairs"] > 1000
+    # only the upper triangle (+ the strictly-lower corners of the 256-row
+    # strips crossing the diagonal: 255 / N of it) and 12 B per refined entry
+    # cross the link
+    slots = R if reduce == "none" else 1
+    exact = 4 * slots * N * (N + 1) // 2 * 4
+    patch = 12 * upper["ciplv"].meta["n_refined_pairs"]
+    assert exact <= upper["plv"].meta["d2h_bytes"] <= (1 + 256 / N) * exact + patch
+    ref = O.plv_family(a[:300].astype(np.complex128), input_kind="analytic", trial_reduce=reduce)
+    iu = np.triu_indices(300)
+    for m in ("plv", "iplv", "ciplv"):
+        v = upper[m].values
+        v = v[:300, :300] if v.ndim == 2 else v[:300, :300, :]
+        r = ref[m]
+        assert np.max(np.abs(v[iu] - r[iu])) <= 1e-5, m
+
+
 def test_upper_over_trials():
     z = np.exp(1j * np.random.default_rng(85).uniform(0, 6.3, (2, 40, 25, 11)))  # [B, N, T, R]
     _both(z, "over-trials", input_kind="phasor", bands=True, mode="over_trials", metrics=ALL)

@@ -14,6 +14,7 @@ from paper_1710_08037_b200 import connectivity as C  # noqa: E402
 from paper_1710_08037_b200 import workloads as W  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c5"
+layout = sys.argv[2] if len(sys.argv) > 2 else ("upper" if cfg == "c5" else "full")
 x = W.generate(cfg)
 N, T, R, B, dt, kind = W.CONFIGS[cfg]
 pin = torch.empty(x.shape[::-1][:0] + (R, N, T), dtype={"c64": torch.complex64, "f32": torch.float32,
@@ -21,12 +22,13 @@ pin = torch.empty(x.shape[::-1][:0] + (R, N, T), dtype={"c64": torch.complex64, 
 pin[...] = np.transpose(x, (2, 0, 1))
 xv = np.transpose(pin, (1, 2, 0))
 outs = {m: torch.zeros((1, N, N), dtype=torch.float32, pin_memory=True).numpy() for m in ("plv", "iplv", "ciplv")}
-C.plv_family(xv, input_kind=kind, out=outs)
+res = C.plv_family(xv, input_kind=kind, out=outs, layout=layout)
+meta = {k: res["plv"].meta[k] for k in ("n_refined_pairs", "n_kernel_launches", "h2d_bytes", "d2h_bytes")}
 ts = []
 for _ in range(3):
     t0 = time.perf_counter()
-    C.plv_family(xv, input_kind=kind, out=outs)
+    C.plv_family(xv, input_kind=kind, out=outs, layout=layout)
     ts.append(time.perf_counter() - t0)
-print(json.dumps({"cfg": cfg, "env": {k: v for k, v in os.environ.items() if k.startswith("PS_")},
+print(json.dumps({"cfg": cfg, "layout": layout, "env": {k: v for k, v in os.environ.items() if k.startswith("PS_")},
                   "ms": [round(t * 1e3, 2) for t in ts],
-                  "pair_samples_per_s": W.pair_samples(N, T, R, B) / min(ts)}), flush=True)
+                  "pair_samples_per_s": W.pair_samples(N, T, R, B) / min(ts), "meta": meta}), flush=True)
