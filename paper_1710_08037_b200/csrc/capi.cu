@@ -643,6 +643,15 @@ int raster_tiles() {
   return S;
 }
 
+// Row panels per streamed output band in the final row stage.
+int row_band_last(int row_band) {
+  static const int v = [] {
+    const char* s = std::getenv("PS_SB_BAND_LAST");
+    return s ? std::max(1, std::atoi(s)) : 0;
+  }();
+  return v > 0 ? v : std::max(1, row_band / 2);
+}
+
 // Work items, grouped by stage: stage s holds the tiles whose column panel
 // starts in [cols[s], cols[s+1]) (one stage covering everything when `cols` is
 // empty).  Ownership (sharding) uses the canonical J-major tile enumeration
@@ -671,14 +680,19 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     return row_band > 0 ? n_stages - 1 - s : s;
   };
   const int S = row_band > 0 ? row_band : raster_tiles();
+  // row stages: the final stage uses bands of half the size (its last band's
+  // Gram + copy-out is the tail of the call)
+  auto band_of = [&](int stage) { return stage == n_stages - 1 ? row_band_last(row_band) : S; };
   // row stages: bands of S row panels, J-major within a band (a finished band
   // is one output block of full upper rows); the in-flight window (~74
   // consecutive items: ~74/S column panels x S row panels) stays L2-sized.
   // Column stages: S x S supertile raster.
   std::stable_sort(mine.begin(), mine.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
+    const int sx = stage_of(x), sy = stage_of(y);
+    const int bx = row_band > 0 ? band_of(sx) : S, by = row_band > 0 ? band_of(sy) : S;
     const int xs = row_band > 0 ? 0 : x.second / S, ys = row_band > 0 ? 0 : y.second / S;
-    return std::make_tuple(stage_of(x), xs, x.first / S, x.second, x.first) <
-           std::make_tuple(stage_of(y), ys, y.first / S, y.second, y.first);
+    return std::make_tuple(sx, xs, x.first / bx, x.second, x.first) <
+           std::make_tuple(sy, ys, y.first / by, y.second, y.first);
   });
   k.pool = a->trial_reduce == PS_TRIALS_POOL;
   if (k.pool || g.R == 1) {
@@ -1204,7 +1218,8 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
       for (int n = k.stage_off[s]; n < k.stage_off[s + 1]; ++n) {
         const Item& w = c->h_items[n];
         const long long slot = k.slot_mode == 0 ? (long long)w.b * g.R + w.g : (long long)w.b;
-        const long long key = slot * 4096 + (w.I / sub) / band_env;  // (slot, row band)
+        const int band = s == S - 1 ? row_band_last(band_env) : band_env;
+        const long long key = slot * 4096 + (w.I / sub) / band;  // (slot, row band)
         const long long r0 = (long long)w.I * exec_rows, r1 = std::min<long long>(r0 + exec_rows, g.N);
         if (key != prev_key) {
           sbs.push_back(SubBlock{slot, r0, r1, r0, g.N});
