@@ -649,13 +649,16 @@ int row_band_last(int row_band) {
     const char* s = std::getenv("PS_SB_BAND_LAST");
     return s ? std::max(1, std::atoi(s)) : 0;
   }();
-  return v > 0 ? v : std::max(1, row_band / 2);
+  // never wider than an ownership band (a sharded call owns whole bands)
+  return v > 0 ? std::min(v, std::max(1, row_band)) : std::max(1, row_band / 2);
 }
 
 // Work items, grouped by stage: stage s holds the tiles whose column panel
 // starts in [cols[s], cols[s+1]) (one stage covering everything when `cols` is
 // empty).  Ownership (sharding) uses the canonical J-major tile enumeration
-// of ps_pair_shard; within a stage items run in 12 x 12 supertile raster order.
+// of ps_pair_shard -- except on the streamed host path (row stages), which
+// deals whole row bands; within a stage items run in 12 x 12 supertile raster
+// order (column stages) or band by band (row stages).
 ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<long long>& cols, bool force_g1,
                     cudaStream_t st, int row_band = 0) {
   const Geometry& g = k.g;
@@ -664,8 +667,32 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   std::vector<std::pair<int, int>> tiles;
   build_tiles(g.N, bm, bn, tiles);
   std::vector<std::pair<int, int>> mine;
-  for (size_t t = 0; t < tiles.size(); ++t)
-    if ((int)(t % k.shard_count) == k.shard_index) mine.push_back(tiles[t]);
+  if (row_band > 0 && k.shard_count > 1) {
+    // streamed host path, sharded: whole row bands per shard (so each shard
+    // ships long contiguous rows), dealt largest-work-first to the least
+    // loaded shard (band work ~ rows x (N - i)); deterministic for every shard
+    const long long band_rows = (long long)row_band * bm;
+    const int n_bands = (int)((g.N + band_rows - 1) / band_rows);
+    std::vector<std::pair<long long, int>> work(n_bands);
+    for (int b = 0; b < n_bands; ++b) {
+      const long long r0 = b * band_rows, r1 = std::min<long long>(r0 + band_rows, g.N);
+      work[b] = {(r1 - r0) * (g.N - (r0 + r1) / 2), b};
+    }
+    std::stable_sort(work.begin(), work.end(),
+                     [](const std::pair<long long, int>& x, const std::pair<long long, int>& y) { return x.first > y.first; });
+    std::vector<long long> load(k.shard_count, 0);
+    std::vector<int> owner(n_bands, 0);
+    for (const auto& wb : work) {
+      const int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+      owner[wb.second] = r;
+      load[r] += wb.first;
+    }
+    for (const auto& t : tiles)
+      if (owner[(int)(((long long)t.first * bm) / band_rows)] == k.shard_index) mine.push_back(t);
+  } else {
+    for (size_t t = 0; t < tiles.size(); ++t)
+      if ((int)(t % k.shard_count) == k.shard_index) mine.push_back(tiles[t]);
+  }
   const int n_stages = cols.empty() ? 1 : (int)cols.size() - 1;
   // Column stages (row_band == 0): stage s holds the tiles whose column panel
   // starts in [cols[s], cols[s+1]).  Row stages (row_band > 0, the streamed
@@ -1909,7 +1936,10 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
   // GPU with one trial group.
   static const bool no_pipe = std::getenv("PS_NO_PIPELINE") != nullptr;
   const long long ntiles = ps_tile_count(g.N, a->precision);
-  const bool pipelinable = !no_pipe && a->mode == PS_MODE_OVER_SAMPLES && k.shard_count == 1 &&
+  // sharded calls pipeline on the streamed (upper layout) path only: each
+  // shard then owns whole row bands and ships just those rows
+  const bool streamed = a->out_layout == PS_LAYOUT_UPPER && std::getenv("PS_PIPE_NO_STREAM") == nullptr;
+  const bool pipelinable = !no_pipe && a->mode == PS_MODE_OVER_SAMPLES && (k.shard_count == 1 || streamed) &&
                            a->stride_sample == 1 && a->stride_signal >= g.T &&
                            g.N >= 2048 && ntiles * g.B >= c->num_sms;
   if (pipelinable) {

@@ -159,3 +159,28 @@ def test_upper_coherence(mode):
 def test_bad_layout_rejected():
     with pytest.raises(ValueError):
         C.plv_family(np.zeros((4, 16), np.float32), layout="lower")
+
+
+def test_host_pipelined_upper_sharded_row_bands():
+    # sharded calls on the streamed host path: each shard owns whole row bands
+    # (dealt by work) and ships only those rows; the shards together give the
+    # unsharded upper triangle bit for bit, each entry from exactly one shard
+    rng = np.random.default_rng(88)
+    N, T = 3200, 160
+    x = rng.standard_normal((N, T)).astype(np.float32)
+    ref = C.plv_family(x, input_kind="real", layout="upper", metrics=("plv", "ciplv"))
+    P = 3
+    parts = [C.plv_family(x, input_kind="real", layout="upper", metrics=("plv", "ciplv"), shard=(r, P))
+             for r in range(P)]
+    for m in ("plv", "ciplv"):
+        owned = np.zeros((N, N), dtype=np.int32)
+        acc = np.zeros((N, N), dtype=np.float32)
+        for p in parts:
+            v = p[m].values
+            nz = np.any(v != 0, axis=1)  # rows this shard wrote
+            owned[nz] += 1
+            acc[nz] = v[nz]
+            assert p[m].meta["d2h_bytes"] < 0.7 * ref[m].meta["d2h_bytes"]
+        iu = np.triu_indices(N)
+        assert np.array_equal(acc[iu], ref[m].values[iu]), m
+        assert np.all(owned[np.arange(N - 1)] == 1), m  # every row (with an off-diagonal entry) from one shard
