@@ -330,29 +330,56 @@ def main():
         xin_np = xin.numpy()
         xin_view = np.transpose(xin_np, (1, 2, 0)) if not bands else np.transpose(xin_np, (0, 2, 3, 1))
         hout = {m: torch.zeros((B, N, N), dtype=odt, pin_memory=True).numpy() for m in ("plv", "iplv", "ciplv")}
+        gathered = world > 1 and R == 1 and B == 1
+        if gathered:
+            # N > 1, single trial: each rank copies in only its own row slice
+            # (its own host link) and one NCCL all-gather over NVLink assembles
+            # the input; each rank then computes and copies out its row bands
+            # (ps_plv_family_to_host, streamed)
+            r0, r1 = sharding.row_slice(N, rank, world)
+            loc = torch.from_numpy(np.ascontiguousarray(x_store[0, r0:r1])).pin_memory()
+            loc_rows = torch.view_as_real(loc) if loc.is_complex() else loc
+            in_bytes = loc.numel() * loc.element_size()
+
+        def e2e_step():
+            if gathered:
+                xg = sharding.all_gather_rows(loc_rows, N)
+                xg = torch.view_as_complex(xg) if loc.is_complex() else xg
+                return C.plv_family(xg, input_kind=kind, precision=args.precision, shard=shard, out=hout,
+                                    layout=layout)
+            return C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
+                                out=hout, layout=layout)
+
         for _ in range(1):
-            C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard, out=hout,
-                         layout=layout)
+            e2e_step()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            r_e = C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
-                               out=hout, layout=layout)
+            r_e = e2e_step()
         dt_e = (time.perf_counter() - t0) / args.steps
-        meta_e = next(iter(r_e.values())).meta
+        meta_e = dict(next(iter(r_e.values())).meta)
+        if gathered:
+            meta_e["h2d_bytes"] = in_bytes
         if world > 1:
             t = torch.tensor([dt_e], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt_e = float(t.item())
+            # whole-job link bytes: the sum over ranks
+            nb = torch.tensor([float(meta_e.get("h2d_bytes") or 0), float(meta_e.get("d2h_bytes") or 0)],
+                              device=dev, dtype=torch.float64)
+            dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+            meta_e["h2d_bytes"], meta_e["d2h_bytes"] = int(nb[0].item()), int(nb[1].item())
         # bytes the library actually moved over the host link (the pipelined
         # path ships one triangle's column blocks and mirrors on the host)
         e2e = {"value": work / dt_e, "unit": UNIT,
                "h2d_bytes_per_step": int(meta_e.get("h2d_bytes") or x_store.nbytes),
                "d2h_bytes_per_step": int(meta_e.get("d2h_bytes") or sum(v.nbytes for v in hout.values())),
                "output_bytes_per_step": int(sum(v.nbytes for v in hout.values())),
-               "ms_per_step": dt_e * 1e3, "api": "paper_1710_08037_b200.connectivity.plv_family(numpy pinned) "
-               "-> ps_plv_family_host (C ABI)"}
+               "ms_per_step": dt_e * 1e3,
+               "api": ("per-rank row slice (pinned) -> NCCL all-gather -> connectivity.plv_family(cuda input, numpy "
+                       "pinned outputs) -> ps_plv_family_to_host (C ABI), each rank its row bands") if gathered else
+                      "paper_1710_08037_b200.connectivity.plv_family(numpy pinned) -> ps_plv_family_host (C ABI)"}
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------
     cpu = None

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 5
+#define PS_ABI_VERSION 6
 
 typedef enum ps_status {
   PS_OK = 0,
@@ -194,6 +194,13 @@ ps_status ps_plv_family_staged(ps_ctx* ctx, const ps_plv_args* args, ps_plv_resu
  * host->device copy, compute, device->host copy, all inside the call.  This is
  * the entry point a host binding (ctypes / cgo / JNI) uses for plain arrays. */
 ps_status ps_plv_family_host(ps_ctx* ctx, const ps_plv_args* args, ps_plv_result* result);
+
+/* DEVICE input (valid in args->stream's order, e.g. assembled on every rank by
+ * an NCCL all-gather of per-rank host slices), HOST outputs: compute and
+ * device->host copy inside the call, the copy-out streamed while the Gram
+ * runs.  With PS_LAYOUT_UPPER and shard_count > 1 each shard owns whole row
+ * bands and writes only those rows of the host matrices (ABI v6). */
+ps_status ps_plv_family_to_host(ps_ctx* ctx, const ps_plv_args* args, ps_plv_result* result);
 
 /* Replaces signalprep.analytic_signal / bindings.py_analytic_signal
  * (SPEC.md:76-84, :530-537): out = x + i H{x}, Re(out) == x bit-exactly.

@@ -20,7 +20,7 @@ from . import errors
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
 if os.environ.get("PS_LIB_VARIANT"):  # A/B experiments: libphasesync_cuda.<variant>.so next to the default
     LIB_PATH = LIB_PATH.with_name(f"libphasesync_cuda.{os.environ['PS_LIB_VARIANT']}.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 LAYOUTS = {"full": 0, "upper": 1}
 
 # ps_status -> exception class (include/phasesync.h)
@@ -134,6 +134,7 @@ _SIGNATURES = {
     "ps_ctx_set_timing": ([ctypes.c_void_p, ctypes.c_int], ctypes.c_int),
     "ps_plv_family": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult)], ctypes.c_int),
     "ps_plv_family_host": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult)], ctypes.c_int),
+    "ps_plv_family_to_host": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult)], ctypes.c_int),
     "ps_plv_family_staged": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.POINTER(PlvResult), ctypes.c_int32,
                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "ps_analytic_signal": ([ctypes.c_void_p, ctypes.POINTER(PlvArgs), ctypes.c_void_p], ctypes.c_int),

@@ -68,7 +68,9 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
        'pool' (one Gram over all R*T observations).  SURVEY D1.
     shard: (index, count) output-tile sharding; entries owned by
        other shards are left as allocated (zeros when ``out`` is None).
-    out: optional preallocated outputs {metric: array} (same kind as x).
+    out: optional preallocated outputs {metric: array} (same kind as x; numpy
+       arrays for a CUDA x make the call copy the results out to the host,
+       streamed while the Gram runs -- ps_plv_family_to_host).
     stages: (stage_cols, ready_events) for a CUDA input that arrives in row
        chunks (ps_plv_family_staged): rows [cols[s], cols[s+1]) of every unit
        are valid once torch.cuda.Event ready_events[s] completes.
@@ -133,7 +135,29 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
         a.fir = ctypes.pointer(fs)
 
     outs = {}
-    if d.on_device:
+    # CUDA input with numpy output arrays: ps_plv_family_to_host (compute and a
+    # streamed copy-out into the host arrays inside the call)
+    host_out = d.on_device and out is not None and stages is None and all(
+        isinstance(out.get(m), np.ndarray) for m in metrics)
+    if host_out:
+        import torch
+
+        ndt = np.float64 if fp64 else np.float32
+        for m in metrics:
+            o = out[m]
+            if o.dtype != ndt or not o.flags.c_contiguous or o.size != slots * N * N:
+                raise ValueError(f"out[{m!r}] must be a C-contiguous {ndt.__name__} array with {slots * N * N} "
+                                 "elements")
+            outs[m] = o
+            setattr(a, "out_" + m, o.ctypes.data)
+        dev = torch.device("cuda", d.device)
+        with torch.cuda.device(dev):
+            a.stream = torch.cuda.current_stream(dev).cuda_stream
+            ctx = _native.context(d.device)
+            ctx.set_timing(timing)
+            res = _native.PlvResult()
+            _native.check(_native.lib().ps_plv_family_to_host(ctx.handle, ctypes.byref(a), ctypes.byref(res)))
+    elif d.on_device:
         import torch
 
         tdt = torch.float64 if fp64 else torch.float32

@@ -1111,8 +1111,11 @@ struct PipeTrace {
 //    rows, cols [i, N), is final when the band's tiles are emitted, and long
 //    contiguous host rows are what the copy engine moves fastest (55 GB/s
 //    against 35-45 GB/s for the 10-14 KB rows of column blocks).
+// dev_input: the input already is in device memory (ready in a->stream's
+// order, e.g. assembled by an NCCL all-gather): no copy-in, one stage, and the
+// output still streamed into the caller's host arrays (ps_plv_family_to_host).
 ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long span, long long esz,
-                         ps_plv_result* res) {
+                         ps_plv_result* res, bool dev_input = false) {
   const Geometry& g = k.g;
   static const long long w_env = [] {
     const char* s = std::getenv("PS_STAGE_W");  // experiment override (signals per stage)
@@ -1172,7 +1175,9 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   // cut points 0 = cols[0] < ... < cols[S] = N, every inner cut a multiple of
   // 256 counted from 0 (row / column panels never straddle a stage)
   std::vector<long long> cols;
-  if (stream_out) {
+  if (dev_input) {
+    cols.push_back(0);  // everything has arrived: one stage
+  } else if (stream_out) {
     std::vector<long long> cuts;
     long long x = g.N;
     for (size_t i = 0; x > 0; ++i) {
@@ -1195,7 +1200,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   c->launches = 0;
   bool copied = false;
   // device buffers: input span (same element layout as the host array), planes, outputs
-  PS_TRY(ensure(c->hin, (size_t)span * esz));
+  if (!dev_input) PS_TRY(ensure(c->hin, (size_t)span * esz));
   const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
   PS_TRY(ensure(c->planes, plane_bytes));
   const size_t oes = g.split ? 4 : 8;
@@ -1287,15 +1292,21 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     }
   }
   ps_plv_args d = *a;
-  d.input = c->hin.p;
+  void* din = dev_input ? const_cast<void*>(a->input) : c->hin.p;
+  d.input = din;
   const long long U = g.B * g.R;
   size_t h2d_bytes = 0;
+  if (dev_input) {  // the caller's stream order makes the input valid
+    cudaEvent_t ready = pool_event(c, 4 * (size_t)S + 3);
+    PS_CUDA(cudaEventRecord(ready, static_cast<cudaStream_t>(a->stream)));
+    PS_CUDA(cudaStreamWaitEvent(si, ready, 0));
+  }
   static const bool want_trace = std::getenv("PS_PIPE_TRACE") != nullptr;
   std::unique_ptr<PipeTrace> trace_holder(want_trace ? new PipeTrace(si) : nullptr);
   PipeTrace* trace = trace_holder.get();
   // ---- copy-in + normalise, per stage --------------------------------------
   for (int s = 0; s < S; ++s) {
-    for (long long u = 0; u < U; ++u) {
+    for (long long u = 0; u < U && !dev_input; ++u) {
       const long long b = u / g.R, t = u % g.R;
       const long long off = b * a->stride_band + t * a->stride_trial + lo(s) * a->stride_signal;
       const long long len = (hi(s) - 1 - lo(s)) * a->stride_signal + (g.T - 1) * a->stride_sample + 1;
@@ -1305,7 +1316,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     }
     if (trace) trace->rec(si, "h2d", s);
     for (long long u = 0; u < U; ++u)
-      PS_TRY(prepare_rows(c, &d, g, c->hin.p, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride,
+      PS_TRY(prepare_rows(c, &d, g, din, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride,
                           u * g.N + lo(s), u * g.N + hi(s), si, &copied));
     if (trace) trace->rec(si, "norm", s);
     PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), si));
@@ -1915,7 +1926,13 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
   return s;
 }
 
-ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+}  // extern "C"
+
+namespace {
+
+// Host-output calls: outputs land in the caller's host arrays.  dev_input:
+// the input is device memory (ready in a->stream's order) -- no copy-in.
+ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, bool dev_input) {
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   Call k;
   PS_TRY(validate(a, k.g));
@@ -1944,11 +1961,13 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
                            g.N >= 2048 && ntiles * g.B >= c->num_sms;
   if (pipelinable) {
     std::lock_guard<std::mutex> lock(c->mu);
-    return host_pipelined(c, a, k, span, esz, res);
+    return host_pipelined(c, a, k, span, esz, res, dev_input);
   }
   cudaStream_t st = static_cast<cudaStream_t>(a->stream);
-  PS_TRY(ensure(c->hin, (size_t)span * esz));
-  PS_CUDA(cudaMemcpyAsync(c->hin.p, a->input, (size_t)span * esz, cudaMemcpyHostToDevice, st));
+  if (!dev_input) {
+    PS_TRY(ensure(c->hin, (size_t)span * esz));
+    PS_CUDA(cudaMemcpyAsync(c->hin.p, a->input, (size_t)span * esz, cudaMemcpyHostToDevice, st));
+  }
   const bool pool = a->trial_reduce == PS_TRIALS_POOL;
   const long long slots = a->mode == PS_MODE_OVER_TRIALS ? g.B * g.T
                           : (a->trial_reduce == PS_TRIALS_NONE && !pool) ? g.B * g.R
@@ -1961,7 +1980,7 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
     if (((a->metrics >> m) & 1u) && houts[m]) ++nout;
   PS_TRY(ensure(c->hout, out_bytes * std::max(nout, 1)));
   ps_plv_args d = *a;
-  d.input = c->hin.p;
+  d.input = dev_input ? a->input : c->hin.p;
   void** douts[5] = {&d.out_plv, &d.out_iplv, &d.out_ciplv, &d.out_cre, &d.out_cim};
   int q = 0;
   for (int m = 0; m < 5; ++m) {
@@ -1979,10 +1998,22 @@ ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res
                               cudaMemcpyDeviceToHost, st));
   PS_CUDA(cudaStreamSynchronize(st));
   if (res) {
-    res->h2d_bytes = (int64_t)span * esz;
+    res->h2d_bytes = dev_input ? 0 : (int64_t)span * esz;
     res->d2h_bytes = (int64_t)out_bytes * q;
   }
   return PS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  return host_output_call(c, a, res, /*dev_input=*/false);
+}
+
+ps_status ps_plv_family_to_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  return host_output_call(c, a, res, /*dev_input=*/true);
 }
 
 ps_status ps_analytic_signal(ps_ctx* c, const ps_plv_args* a0, void* out) {

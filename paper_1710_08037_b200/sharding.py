@@ -91,6 +91,37 @@ def broadcast_input_staged(rows_view, cols, src: int = 0, group=None, stream=Non
     return events
 
 
+def row_slice(n_signals: int, rank: int, world: int) -> tuple:
+    """Rows [r0, r1) of the input a rank holds / copies in for
+    ``all_gather_rows`` (equal ceil(N / world) slices, the last one short)."""
+    per = -(-n_signals // world)
+    return min(rank * per, n_signals), min((rank + 1) * per, n_signals)
+
+
+def all_gather_rows(local_rows, n_signals: int, group=None, device=None):
+    """Assemble a single-trial input on every rank from per-rank row slices:
+    `local_rows` is this rank's rows ``row_slice(N, rank, world)`` -- a host
+    (pinned) or device tensor [rows, ...] -- copied in by this rank alone, then
+    one NCCL all-gather over NVLink gives every rank all N rows.  Returns the
+    device tensor [N, ...] (a view of the gathered buffer)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    per = -(-n_signals // world)
+    dev = device or (torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available()
+                     else torch.device("cpu"))
+    mine = torch.zeros((per,) + tuple(local_rows.shape[1:]), dtype=local_rows.dtype, device=dev)
+    if local_rows.shape[0]:
+        mine[: local_rows.shape[0]].copy_(local_rows, non_blocking=True)
+    full = torch.empty((per * world,) + tuple(local_rows.shape[1:]), dtype=local_rows.dtype, device=dev)
+    if dev.type == "cuda":
+        dist.all_gather_into_tensor(full, mine, group=group)
+    else:  # gloo (CPU tests)
+        dist.all_gather(list(full.chunk(world)), mine, group=group)
+    return full[:n_signals]
+
+
 def gather(outputs: dict, dst: int | None = 0, group=None) -> dict:
     """Assemble sharded outputs: reduce (dst given) or all-reduce (dst None)."""
     import torch.distributed as dist

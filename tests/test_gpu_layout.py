@@ -184,3 +184,65 @@ def test_host_pipelined_upper_sharded_row_bands():
         iu = np.triu_indices(N)
         assert np.array_equal(acc[iu], ref[m].values[iu]), m
         assert np.all(owned[np.arange(N - 1)] == 1), m  # every row (with an off-diagonal entry) from one shard
+
+
+@pytest.mark.parametrize("layout", ["upper", "full"])
+def test_device_input_host_outputs(layout):
+    # ps_plv_family_to_host: CUDA input, numpy outputs -- same values as the
+    # host path (streamed row bands for 'upper', column stages for 'full'),
+    # sharded calls write only their rows; small N takes the unpipelined path
+    import torch
+
+    rng = np.random.default_rng(89)
+    for N, T in ((3200, 160), (300, 200)):
+        x = rng.standard_normal((N, T)).astype(np.float32)
+        ref = C.plv_family(x, input_kind="real", layout=layout, metrics=("plv", "iplv", "ciplv"))
+        xd = torch.from_numpy(x).cuda()
+        outs = {m: np.zeros((1, N, N), np.float32) for m in ("plv", "iplv", "ciplv")}
+        got = C.plv_family(xd, input_kind="real", layout=layout, out=outs)
+        for m in outs:
+            assert isinstance(got[m].values, np.ndarray)
+            assert np.array_equal(got[m].values, ref[m].values), (N, layout, m)
+        assert got["plv"].meta["h2d_bytes"] == 0
+        if layout == "upper" and N >= 2048:
+            acc = {m: np.zeros((N, N), np.float32) for m in outs}
+            for r in range(2):
+                o = {m: np.zeros((1, N, N), np.float32) for m in outs}
+                C.plv_family(xd, input_kind="real", layout=layout, out=o, shard=(r, 2))
+                for m in o:
+                    rows = np.any(o[m][0] != 0, axis=1)
+                    acc[m][rows] = o[m][0][rows]
+            for m in outs:
+                assert np.array_equal(acc[m][:-1], ref[m].values[:-1]), m
+
+
+def test_all_gather_rows_nccl_single_rank():
+    # the multi-GPU host-input path of bench.py (per-rank row slice -> NCCL
+    # all-gather -> ps_plv_family_to_host) on a one-rank NCCL group
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1710_08037_b200 import sharding
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29561")
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(90)
+        N, T = 2600, 128
+        a = (rng.standard_normal((N, T)) + 1j * rng.standard_normal((N, T))).astype(np.complex64)
+        r0, r1 = sharding.row_slice(N, 0, 1)
+        loc = torch.view_as_real(torch.from_numpy(a[r0:r1]).pin_memory())
+        xg = torch.view_as_complex(sharding.all_gather_rows(loc, N))
+        outs = {m: np.zeros((1, N, N), np.float32) for m in ("plv", "iplv", "ciplv")}
+        got = C.plv_family(xg, input_kind="analytic", layout="upper", out=outs, shard=(0, 1))
+        ref = C.plv_family(a, input_kind="analytic", layout="upper")
+        for m in outs:
+            assert np.array_equal(got[m].values, ref[m].values), m
+    finally:
+        if own:
+            dist.destroy_process_group()

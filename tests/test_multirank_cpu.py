@@ -60,3 +60,33 @@ def test_two_rank_shard_and_gather(prec):
     for p in procs:
         p.join(timeout=60)
     assert sorted(res) == [(0, True), (1, True)]
+
+
+def _gather_worker(rank, world, port, N, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        full = np.random.default_rng(78).standard_normal((N, 64, 2)).astype(np.float32)
+        r0, r1 = sharding.row_slice(N, rank, world)
+        got = sharding.all_gather_rows(torch.from_numpy(full[r0:r1]), N, device=torch.device("cpu"))
+        q.put((rank, tuple(got.shape) == full.shape and np.array_equal(got.numpy(), full)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,N", [(2, 301), (3, 300), (3, 2)])
+def test_all_gather_rows_from_per_rank_slices(world, N):
+    # multi-GPU host input: each rank copies in only its row slice, one
+    # all-gather assembles the whole input on every rank (uneven and empty
+    # slices included)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, N, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert sorted(res) == [(r, True) for r in range(world)]
