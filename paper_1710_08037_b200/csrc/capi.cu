@@ -1197,6 +1197,10 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   auto hi = [&](int s) { return stream_out ? cols[S - s] : cols[s + 1]; };
   PS_TRY(ensure_pipeline(c, S));
   cudaStream_t si = c->s_in, sc = c->s_comp, sr = c->s_ref, so = c->s_out;
+  // a previous call that returned early on an error may still have work in
+  // flight on these streams (a kernel that would publish stale band flags):
+  // start from idle streams (free when the last call completed normally)
+  for (cudaStream_t q : {si, sc, sr, so}) PS_CUDA(cudaStreamSynchronize(q));
   c->launches = 0;
   bool copied = false;
   // device buffers: input span (same element layout as the host array), planes, outputs

@@ -1,9 +1,9 @@
 #!/bin/bash
-# streamed copy-out (row stages): band sizes (all stages / final stage)
+# row-stage schedule variants (first stage width), then the bench line and the reference arm
 cd /root/repo
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_layout.py -x -q > gpurun_out/gpu_layout.txt 2>&1; echo "exit $?" >> gpurun_out/gpu_layout.txt
-for bl in "4 4" "4 2" "4 1" "2 1" "6 2" "8 2"; do
-  set -- $bl
-  PS_SB_BAND=$1 PS_SB_BAND_LAST=$2 timeout 300 python tools/e2e_probe.py c5 2>/dev/null | tail -1 >> gpurun_out/e2e_sweep5.jsonl
+for sc in "" "512,1024,2048,3072,3584,3584,3584,2080,1024" "512,1536,2560,3584,3584,3584,2560,1536,512" "1024,2048,3072,4096,4096,3072,2048,512"; do
+  PS_STAGE_COLS="$sc" timeout 300 python tools/e2e_probe.py c5 2>/dev/null | tail -1 >> gpurun_out/e2e_sweep6.jsonl
 done
+timeout 900 python bench.py > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+timeout 900 python bench.py --impl reference > gpurun_out/bench_ref_c5.json 2> gpurun_out/bench_ref_c5.err
