@@ -1690,9 +1690,22 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   }
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[1], st));
   // ---- Gram + fused epilogue ------------------------------------------------
+  static const bool time_trace = std::getenv("PS_TIME_TRACE") != nullptr;  // diagnostics
+  const auto hp0 = std::chrono::steady_clock::now();
   PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
+  const auto hp1 = std::chrono::steady_clock::now();
+  if (time_trace && c->timing) PS_CUDA(cudaEventRecord(c->ev[4], st));
   PS_TRY(launch_stage(c, k, 0, st));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
+  if (time_trace && c->timing) {
+    PS_CUDA(cudaEventSynchronize(c->ev[2]));
+    float k_ms = 0.f, w_ms = 0.f;
+    PS_CUDA(cudaEventElapsedTime(&k_ms, c->ev[4], c->ev[2]));
+    PS_CUDA(cudaEventElapsedTime(&w_ms, c->ev[1], c->ev[2]));
+    std::fprintf(stderr, "[time] plan_host %.3f ms  gram_kernel %.3f ms  gram_window %.3f ms  G %d items %d\n",
+                 std::chrono::duration<double, std::milli>(hp1 - hp0).count(), k_ms, w_ms, k.G,
+                 k.stage_off.empty() ? 0 : k.stage_off.back());
+  }
   if (k.slot_mode == 2) {
     PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, (int)g.R, g.split ? 0 : 1, st,
                                     a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
