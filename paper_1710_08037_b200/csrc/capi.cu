@@ -11,6 +11,7 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1947,6 +1948,133 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
 
 namespace {
 
+// E2E host path for multi-trial trial-mean calls (B x R units of N rows each,
+// e.g. C2 / C4): pipelined over trials instead of signal stages.  The trial
+// groups (partial-sum slots of Rg trials) come from the device path's cost
+// model; a stage is a run of groups of one band holding ~384 MB of input.
+// Stage s+1's units cross the link (copy stream) while stage s's units are
+// normalised (prep stream) and stage s-1's Gram items accumulate their groups'
+// partial metric sums (compute stream).  The trial-group reduction, the FP64
+// refinement and the copy-out of the B small matrices per metric finish the
+// call, which then runs at the host link's rate.
+ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long span, long long esz,
+                              ps_plv_result* res, bool dev_input) {
+  const Geometry& g = k.g;
+  PS_TRY(ensure_pipeline(c, 1));
+  cudaStream_t si = c->s_in, sn = c->s_ref, sc = c->s_comp;
+  for (cudaStream_t q : {si, sc, sn, c->s_out}) PS_CUDA(cudaStreamSynchronize(q));
+  c->launches = 0;
+  bool copied = false;
+  if (!dev_input) PS_TRY(ensure(c->hin, (size_t)span * esz));
+  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  PS_TRY(ensure(c->planes, plane_bytes));
+  const size_t oes = g.split ? 4 : 8;
+  void* houts[5];
+  std::memcpy(houts, k.outs, sizeof(houts));
+  int nout = 0;
+  for (int m = 0; m < 5; ++m) nout += houts[m] ? 1 : 0;
+  const size_t out_bytes = (size_t)g.B * g.N * g.N * oes;
+  PS_TRY(ensure(c->hout, out_bytes * std::max(nout, 1)));
+  {
+    int q = 0;
+    for (int m = 0; m < 5; ++m) k.outs[m] = houts[m] ? static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes : nullptr;
+  }
+  if (dev_input) {  // the caller's stream order makes the input valid
+    cudaEvent_t ready = pool_event(c, 0);
+    PS_CUDA(cudaEventRecord(ready, static_cast<cudaStream_t>(a->stream)));
+    PS_CUDA(cudaStreamWaitEvent(si, ready, 0));
+  }
+  PS_TRY(prep_begin(c, a, g, si));
+  PS_TRY(reset_status(c, si));
+  PS_TRY(init_row_state(c, g, si));
+  PS_TRY(plan_call(c, a, k, {}, /*force_g1=*/false, si));
+  const int G = k.G, Rg = k.Rg;
+  const double unit_bytes = (double)g.N * (double)g.T * (double)esz;
+  const int gps = std::max(1, std::min(G, (int)std::lround(384.0 * (1 << 20) / (Rg * unit_bytes))));
+  // items run (band, group, tile): stage boundaries where the band or the
+  // group run changes
+  struct Stage {
+    long long b, t0, t1;
+  };
+  std::vector<Stage> stages;
+  {
+    std::vector<int> off(1, 0);
+    const std::vector<Item>& it = c->h_items;
+    for (size_t n = 0; n < it.size(); ++n) {
+      const bool start = n == 0 || it[n].b != it[n - 1].b || it[n].g / gps != it[n - 1].g / gps;
+      if (!start) continue;
+      if (n > 0) off.push_back((int)n);
+      const long long t0 = (long long)(it[n].g / gps) * gps * Rg;
+      stages.push_back(Stage{it[n].b, t0, std::min<long long>(g.R, t0 + (long long)gps * Rg)});
+    }
+    off.push_back((int)it.size());
+    k.stage_off = off;
+  }
+  const int S = (int)stages.size();
+  PS_TRY(ensure_pipeline(c, S));
+  const bool upper = a->out_layout == PS_LAYOUT_UPPER;
+  if (upper || k.slot_mode != 2)  // outputs copied whole: the lower triangle must read 0
+    PS_CUDA(cudaMemsetAsync(c->hout.p, 0, out_bytes * std::max(nout, 1), si));
+  ps_plv_args d = *a;
+  void* din = dev_input ? const_cast<void*>(a->input) : c->hin.p;
+  d.input = din;
+  size_t h2d_bytes = 0;
+  static const bool want_trace = std::getenv("PS_PIPE_TRACE") != nullptr;
+  std::unique_ptr<PipeTrace> trace_holder(want_trace ? new PipeTrace(si) : nullptr);
+  PipeTrace* trace = trace_holder.get();
+  for (int s = 0; s < S; ++s) {
+    const Stage& sg = stages[(size_t)s];
+    for (long long t = sg.t0; t < sg.t1 && !dev_input; ++t) {
+      const long long off = sg.b * a->stride_band + t * a->stride_trial;
+      const long long len = (g.N - 1) * a->stride_signal + (g.T - 1) * a->stride_sample + 1;
+      PS_CUDA(cudaMemcpyAsync(static_cast<char*>(c->hin.p) + off * esz, static_cast<const char*>(a->input) + off * esz,
+                              (size_t)len * esz, cudaMemcpyHostToDevice, si));
+      h2d_bytes += (size_t)len * esz;
+    }
+    if (trace) trace->rec(si, "h2d", s);
+    PS_CUDA(cudaEventRecord(pool_event(c, 3 * s + 1), si));
+    PS_CUDA(cudaStreamWaitEvent(sn, pool_event(c, 3 * s + 1), 0));
+    for (long long t = sg.t0; t < sg.t1; ++t) {
+      const long long u = sg.b * g.R + t;
+      PS_TRY(prepare_rows(c, &d, g, din, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride, u * g.N,
+                          (u + 1) * g.N, sn, &copied));
+    }
+    if (trace) trace->rec(sn, "norm", s);
+    PS_CUDA(cudaEventRecord(pool_event(c, 3 * s + 2), sn));
+    PS_CUDA(cudaStreamWaitEvent(sc, pool_event(c, 3 * s + 2), 0));
+    PS_TRY(launch_stage(c, k, s, sc));
+    if (trace) trace->rec(sc, "gram", s);
+  }
+  if (k.slot_mode == 2) {
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, (int)g.R, g.split ? 0 : 1, sc,
+                                upper ? g.N : 0));
+    for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
+  }
+  ps_status st = read_status(c, sc);
+  if (st == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, sc));
+  size_t d2h_bytes = 0;
+  for (int m = 0; m < 5 && st == PS_OK; ++m)
+    if (houts[m]) {
+      PS_CUDA(cudaMemcpyAsync(houts[m], k.outs[m], out_bytes, cudaMemcpyDeviceToHost, sc));
+      d2h_bytes += out_bytes;
+    }
+  if (trace) trace->rec(sc, "d2h", S - 1);
+  PS_CUDA(cudaStreamSynchronize(sc));
+  if (trace) trace->dump();
+  if (res) {
+    std::memset(res, 0, sizeof(*res));
+    res->n_observations = g.T;
+    res->n_masked_samples = (int64_t)c->h_status->n_masked;
+    res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->input_copied = copied ? 1 : 0;
+    res->n_kernel_launches = c->launches;
+    res->h2d_bytes = (int64_t)h2d_bytes;
+    res->d2h_bytes = (int64_t)d2h_bytes;
+  }
+  std::memcpy(k.outs, houts, sizeof(houts));
+  return st;
+}
+
 // Host-output calls: outputs land in the caller's host arrays.  dev_input:
 // the input is device memory (ready in a->stream's order) -- no copy-in.
 ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, bool dev_input) {
@@ -1976,6 +2104,18 @@ ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, 
   const bool pipelinable = !no_pipe && a->mode == PS_MODE_OVER_SAMPLES && (k.shard_count == 1 || streamed) &&
                            a->stride_sample == 1 && a->stride_signal >= g.T &&
                            g.N >= 2048 && ntiles * g.B >= c->num_sms;
+  // multi-trial trial means with a large input: pipelined over trial groups
+  static const long long unit_min = [] {
+    const char* e = std::getenv("PS_UNIT_PIPE_MIN_MB");  // threshold (MB of input)
+    return (e ? std::atoll(e) : 512LL) << 20;
+  }();
+  const bool unit_pipelinable = !no_pipe && a->mode == PS_MODE_OVER_SAMPLES && k.shard_count == 1 &&
+                                a->trial_reduce == PS_TRIALS_MEAN && g.R > 1 && a->stride_sample == 1 &&
+                                a->stride_signal >= g.T && span * esz >= unit_min;
+  if (unit_pipelinable) {
+    std::lock_guard<std::mutex> lock(c->mu);
+    return host_unit_pipelined(c, a, k, span, esz, res, dev_input);
+  }
   if (pipelinable) {
     std::lock_guard<std::mutex> lock(c->mu);
     return host_pipelined(c, a, k, span, esz, res, dev_input);

@@ -246,3 +246,35 @@ def test_all_gather_rows_nccl_single_rank():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("prec,dt,R", [("split", np.float32, 40), ("fp64", np.float64, 20)])
+def test_host_trial_group_pipeline(prec, dt, R):
+    # multi-trial trial means with >= 512 MB of host input (C2 / C4 shape):
+    # the host path pipelines copy-in + normalise of trial group g+1 with the
+    # Gram of group g; same values as the device path (up to the trial-group
+    # summation order) and as the oracle, upper layout with a zero lower triangle
+    import torch
+
+    rng = np.random.default_rng(91)
+    B, N, T = 2, 1024, 2048
+    x = rng.standard_normal((B, R, N, T)).astype(dt)  # trials-outer storage, unit sample stride
+    xv = np.transpose(x, (0, 2, 3, 1))                 # [B, N, T, R] view
+    assert x.nbytes >= 512 << 20
+    tol = 1e-5 if prec == "split" else 1e-12
+    for layout in ("full", "upper"):
+        host = C.plv_family(xv, input_kind="real", bands=True, precision=prec, layout=layout)
+        assert host["plv"].meta["h2d_bytes"] == x.nbytes
+        dev = C.plv_family(torch.from_numpy(x).cuda().permute(0, 2, 3, 1), input_kind="real", bands=True,
+                           precision=prec, layout=layout)
+        for m in ("plv", "iplv", "ciplv"):
+            h = host[m].values
+            d = dev[m].values.cpu().numpy()
+            assert np.max(np.abs(h - d)) <= (2e-6 if prec == "split" else 1e-13), (layout, m)
+            if layout == "upper":
+                il = np.tril_indices(N, -1)
+                assert not np.any(h[:, il[0], il[1]]), m
+    sub = np.ascontiguousarray(xv[1, :64]).astype(np.float64)
+    ref = O.plv_family(sub, input_kind="real")
+    for m in ("plv", "iplv", "ciplv"):
+        assert np.max(np.abs(host[m].values[1, :64, :64] - np.triu(ref[m]))) <= tol, m

@@ -17,17 +17,24 @@ cfg = sys.argv[1] if len(sys.argv) > 1 else "c5"
 layout = sys.argv[2] if len(sys.argv) > 2 else ("upper" if cfg == "c5" else "full")
 x = W.generate(cfg)
 N, T, R, B, dt, kind = W.CONFIGS[cfg]
-pin = torch.empty(x.shape[::-1][:0] + (R, N, T), dtype={"c64": torch.complex64, "f32": torch.float32,
-                                                          "f64": torch.float64}[dt], pin_memory=True).numpy()
-pin[...] = np.transpose(x, (2, 0, 1))
-xv = np.transpose(pin, (1, 2, 0))
-outs = {m: torch.zeros((1, N, N), dtype=torch.float32, pin_memory=True).numpy() for m in ("plv", "iplv", "ciplv")}
-res = C.plv_family(xv, input_kind=kind, out=outs, layout=layout)
+bands = x.ndim == 4
+tdt = {"c64": torch.complex64, "f32": torch.float32, "f64": torch.float64}[dt]
+if bands:  # [B, N, T, R] -> trials-outer storage [B, R, N, T]
+    pin = torch.empty((B, R, N, T), dtype=tdt, pin_memory=True).numpy()
+    pin[...] = np.transpose(x, (0, 3, 1, 2))
+    xv = np.transpose(pin, (0, 2, 3, 1))
+else:
+    pin = torch.empty((R, N, T), dtype=tdt, pin_memory=True).numpy()
+    pin[...] = np.transpose(x, (2, 0, 1))
+    xv = np.transpose(pin, (1, 2, 0))
+del x
+outs = {m: torch.zeros((B, N, N), dtype=torch.float32, pin_memory=True).numpy() for m in ("plv", "iplv", "ciplv")}
+res = C.plv_family(xv, input_kind=kind, out=outs, layout=layout, bands=bands)
 meta = {k: res["plv"].meta[k] for k in ("n_refined_pairs", "n_kernel_launches", "h2d_bytes", "d2h_bytes")}
 ts = []
-for _ in range(3):
+for _ in range(int(os.environ.get("E2E_REPS", "3"))):
     t0 = time.perf_counter()
-    C.plv_family(xv, input_kind=kind, out=outs, layout=layout)
+    C.plv_family(xv, input_kind=kind, out=outs, layout=layout, bands=bands)
     ts.append(time.perf_counter() - t0)
 print(json.dumps({"cfg": cfg, "layout": layout, "env": {k: v for k, v in os.environ.items() if k.startswith("PS_")},
                   "ms": [round(t * 1e3, 2) for t in ts],
