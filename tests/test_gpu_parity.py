@@ -450,6 +450,26 @@ def test_fused_hilbert_amplitude_floor_fixup():
     assert res["plv"].meta["n_masked_samples"] == int(m.sum())
 
 
+def test_hilbert_t65536_rows():
+    # fp32 real rows of T = 65536 (C3's length, cuFFT chain): odd row count,
+    # rows 1e6 apart in scale, an amplitude-floor fixup row.  (A zero stretch
+    # of T/5 at this length leaves H in the fp32 FFT noise floor inside it:
+    # 1.4e-5 PLV error through cuFFT, so the stretch here is shorter.)
+    rng = np.random.default_rng(65536)
+    T = 65536
+    x = rng.standard_normal((9, T)).astype(np.float32)
+    x[2] *= 1e6
+    x[3] *= 1e-6
+    x[5, 5000:9000] = 0.0
+    x = x[:, :, None]
+    for floor in (1e-6, 0.05):
+        ref = O.plv_family(x.astype(np.float64), input_kind="real", amp_floor=floor)
+        res = C.plv_family(x, input_kind="real", precision="split", amp_floor=floor)
+        check(res, ref, "split", f"four-step floor={floor}")
+        m = O.normalize_phasors(O.analytic_signal(x.astype(np.float64), axis=1), amp_floor=floor)[1]
+        assert res["plv"].meta["n_masked_samples"] == int(m.sum())
+
+
 def test_float32_trial_fastest_layout_copies():
     # reference layout [N, T, R] row-major: samples are strided -> packing copy
     rng = np.random.default_rng(5)
