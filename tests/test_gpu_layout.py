@@ -278,3 +278,16 @@ def test_host_trial_group_pipeline(prec, dt, R):
     ref = O.plv_family(sub, input_kind="real")
     for m in ("plv", "iplv", "ciplv"):
         assert np.max(np.abs(host[m].values[1, :64, :64] - np.triu(ref[m]))) <= tol, m
+
+
+def test_host_pipelined_upper_bands_and_trials():
+    # streamed row-band copy-out with several bands and a trial mean (one
+    # output slot per band): upper entries bit-identical to the full layout
+    rng = np.random.default_rng(92)
+    B, N, T, R = 2, 2304, 96, 3
+    x = rng.standard_normal((B, R, N, T)).astype(np.float32)
+    xv = np.transpose(x, (0, 2, 3, 1))  # [B, N, T, R], unit sample stride
+    full, upper = _both(xv, "host-stream-bands", input_kind="real", bands=True,
+                        metrics=("plv", "iplv", "ciplv"))
+    exact = 3 * B * N * (N + 1) // 2 * 4
+    assert upper["plv"].meta["d2h_bytes"] <= (1 + 256 / N) * exact
