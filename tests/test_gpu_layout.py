@@ -291,3 +291,39 @@ def test_host_pipelined_upper_bands_and_trials():
                         metrics=("plv", "iplv", "ciplv"))
     exact = 3 * B * N * (N + 1) // 2 * 4
     assert upper["plv"].meta["d2h_bytes"] <= (1 + 256 / N) * exact
+
+
+_UNIT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_1710_08037_b200 import connectivity as C
+rng = np.random.default_rng(93)
+worst = 0.0
+for B, R, N, T, prec, layout in ((2, 6, 300, 512, "split", "full"), (1, 7, 520, 256, "fp64", "upper"),
+                                 (3, 5, 129, 300, "split", "upper")):
+    x = rng.standard_normal((B, R, N, T)).astype(np.float32 if prec == "split" else np.float64)
+    xv = np.transpose(x, (0, 2, 3, 1))
+    host = C.plv_family(xv, input_kind="real", bands=True, precision=prec, layout=layout)
+    assert host["plv"].meta["h2d_bytes"] == x.nbytes
+    dev = C.plv_family(torch.from_numpy(x).cuda().permute(0, 2, 3, 1), input_kind="real", bands=True,
+                       precision=prec, layout=layout)
+    for m in ("plv", "iplv", "ciplv"):
+        worst = max(worst, float(np.max(np.abs(host[m].values - dev[m].values.cpu().numpy()))))
+print(worst)
+"""
+
+
+def test_host_trial_group_pipeline_small_shapes():
+    # the trial-group host pipeline forced onto small inputs (PS_UNIT_PIPE_MIN_MB=1,
+    # read once per process, hence the subprocess): uneven tile counts, prime
+    # trial counts, fp64 upper layout -- same values as the device path
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PS_UNIT_PIPE_MIN_MB="1")
+    out = subprocess.run([sys.executable, "-c", _UNIT_SCRIPT, root], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert float(out.stdout.strip().splitlines()[-1]) <= 2e-6

@@ -1,6 +1,7 @@
 """Small calls through every entry point, meant to run under
 `compute-sanitizer --tool memcheck` (and racecheck / synccheck) on the GPU box:
-device / host / pipelined / staged paths, split and fp64, real (fused T=4096,
+device / host / pipelined (column and streamed row stages) / staged /
+device-to-host paths, split and fp64, real (fused T=4096,
 cuFFT odd T, band-pass), analytic, phasor, time-resolved, coherence."""
 import os
 import sys
@@ -36,5 +37,15 @@ a = torch.from_numpy((rng.standard_normal((2600, 64)) + 1j * rng.standard_normal
 a = a.cuda()
 cols = sharding.stage_cols(2600, n_stages=3, min_width=512)
 C.plv_family(a, input_kind="analytic", stages=(cols, [None] * (len(cols) - 1)), shard=(1, 2))
+# streamed host path (upper layout, row stages, device-published band flags),
+# sharded, bands + trial mean, fp64 (event-released bands)
+C.plv_family(np.transpose(xb, (0, 2, 3, 1)), input_kind="real", bands=True, layout="upper")
+xs = rng.standard_normal((2304, 48)).astype(np.float32)
+C.plv_family(xs, input_kind="real", layout="upper", shard=(1, 2))
+C.plv_family(xs.astype(np.float64), input_kind="real", layout="upper", precision="fp64")
+# device input -> host outputs (ps_plv_family_to_host), streamed and not
+outs = {m: np.zeros((1, 2600, 2600), np.float32) for m in ("plv", "iplv", "ciplv")}
+C.plv_family(a, input_kind="analytic", layout="upper", out=outs)
+C.plv_family(a, input_kind="analytic", layout="full", out=outs)
 torch.cuda.synchronize()
 print("sanitize smoke done")
