@@ -423,14 +423,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               ptx::mma_f16_ss_warp<CG>(d_re, aRl, bRh, idesc_pos, 1u);
               ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIh, idesc_pos, 1u);
               ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIl, idesc_pos, 1u);
+#ifndef PS_EXPERIMENT_9MMA  // (timing experiment only: 9 of the 12 UMMAs, wrong values)
               ptx::mma_f16_ss_warp<CG>(d_re, aIl, bIh, idesc_pos, 1u);
+#endif
               // Im = Zi Zr' - Zr Zi'
               ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRh, idesc_pos, acc0);
               ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRl, idesc_pos, 1u);
+#ifndef PS_EXPERIMENT_9MMA
               ptx::mma_f16_ss_warp<CG>(d_im, aIl, bRh, idesc_pos, 1u);
+#endif
               ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIh, idesc_neg, 1u);
               ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIl, idesc_neg, 1u);
+#ifndef PS_EXPERIMENT_9MMA
               ptx::mma_f16_ss_warp<CG>(d_im, aRl, bIh, idesc_neg, 1u);
+#endif
             }
             ptx::mma_commit_warp<CG>(&empty[stage]);  // the group's smem slots free once these retire
             if (++stage == G::STAGES) {
