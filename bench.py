@@ -277,6 +277,7 @@ def main():
         info = r["plv"].meta
         gram_ms.append(info["ms_gram"])
         launches += int(info["n_kernel_launches"])
+    variant = int(info.get("gram_variant", 0))
     e1.record(stream)
     torch.cuda.synchronize()
     ms_total = e0.elapsed_time(e1)
@@ -300,8 +301,11 @@ def main():
     if not gram_avg > 0.0:
         gram_avg = ms_step
     achieved = algo_flops / (gram_avg / 1e3) / 1e12
-    passes = 1 if fp64 else 3
-    peak = pk["bf16_tflops"] / passes if not fp64 else FP64_DGEMM_TFLOPS
+    # tensor ceiling of the arithmetic actually run: 8 algorithmic flop per
+    # pair-sample against 24 fp16 tensor flop (3 passes x 4 real products) or
+    # 18 (3 passes x 3 products, Gauss form)
+    hw_flops = 18.0 if variant == 1 else 24.0
+    peak = pk["bf16_tflops"] * FLOPS_PER_PAIR_SAMPLE / hw_flops if not fp64 else FP64_DGEMM_TFLOPS
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gram_traffic.json")
     if os.path.exists(tpath):
@@ -317,8 +321,13 @@ def main():
                 if not fp64 else "gram_f64_kernel (DMMA)",
                 "algorithmic_flops_per_launch": algo_flops, "gram_ms_per_launch": gram_avg,
                 "gram_share_of_step": gram_avg / ms_step,
-                "peak_basis": (f"bf16_tflops {pk['bf16_tflops']} ({pk['source']}, burst) / 3 fp16 passes of the "
-                               "hi/lo split = algorithmic ceiling of the split scheme") if not fp64 else
+                "gram_variant": {0: "split fp16x3, 4 real products (12 UMMA / K step)",
+                                 1: "split fp16x3, Gauss 3-product form (9 UMMA / K step)",
+                                 2: "fp64 DMMA"}.get(variant, str(variant)),
+                "fp16_tensor_tflops_executed": achieved * hw_flops / FLOPS_PER_PAIR_SAMPLE if not fp64 else None,
+                "peak_basis": (f"bf16_tflops {pk['bf16_tflops']} ({pk['source']}, burst) x 8 algorithmic / "
+                               f"{hw_flops:g} fp16 tensor flop per pair-sample = algorithmic ceiling of the "
+                               "arithmetic run") if not fp64 else
                 f"cuBLAS DGEMM 8192^3 measured on a pool B200: {FP64_DGEMM_TFLOPS} TFLOP/s (tools/fp64_peak.py)",
                 "frac_of_bf16_peak": achieved / pk["bf16_tflops"]}
 

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 6
+#define PS_ABI_VERSION 7
 
 typedef enum ps_status {
   PS_OK = 0,
@@ -155,6 +155,11 @@ typedef struct ps_plv_result {
    * mirrors the rest on the host). */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
+  /* Gram arithmetic of the call (ABI v7): 0 = split fp16 x 3, four real
+   * products (12 UMMAs per K step); 1 = split fp16 x 3, three-product Gauss
+   * form (9 UMMAs); 2 = FP64 DMMA. */
+  int32_t gram_variant;
+  int32_t reserved;
 } ps_plv_result;
 
 /* ABI version check (PS_ABI_VERSION). */

@@ -20,7 +20,7 @@ from . import errors
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
 if os.environ.get("PS_LIB_VARIANT"):  # A/B experiments: libphasesync_cuda.<variant>.so next to the default
     LIB_PATH = LIB_PATH.with_name(f"libphasesync_cuda.{os.environ['PS_LIB_VARIANT']}.so")
-ABI_VERSION = 6
+ABI_VERSION = 7
 LAYOUTS = {"full": 0, "upper": 1}
 
 # ps_status -> exception class (include/phasesync.h)
@@ -119,6 +119,8 @@ class PlvResult(ctypes.Structure):
         ("ms_finish", ctypes.c_float),
         ("h2d_bytes", ctypes.c_int64),
         ("d2h_bytes", ctypes.c_int64),
+        ("gram_variant", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

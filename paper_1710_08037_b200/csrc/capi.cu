@@ -69,9 +69,13 @@ using PlanKey = std::tuple<int, long long, long long, int, int>;  // T, batch, i
 struct TmapKey {
   const void* base;
   long long T, N, U, pitch;
+  bool gauss;
   bool operator<(const TmapKey& o) const {
-    return std::tie(base, T, N, U, pitch) < std::tie(o.base, o.T, o.N, o.U, o.pitch);
+    return std::tie(base, T, N, U, pitch, gauss) < std::tie(o.base, o.T, o.N, o.U, o.pitch, o.gauss);
   }
+};
+struct Tmaps {
+  CUtensorMap a, b, b2;  // A panel, B panel (planes 0..), B panel planes 4..7 (Gauss)
 };
 
 }  // namespace
@@ -91,7 +95,7 @@ struct ps_ctx {
   std::vector<cudaEvent_t> tev;  // timing events of the staged path (2 per stage)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
-  std::map<TmapKey, std::pair<CUtensorMap, CUtensorMap>> tmaps;
+  std::map<TmapKey, Tmaps> tmaps;
   std::vector<Item> h_items;
   Item* h_items_pinned = nullptr;
   size_t h_items_cap = 0;
@@ -152,6 +156,11 @@ struct Geometry {
   int in_double;  // input scalar is double
   long long pitch;
   long long plane_stride;
+  // split Gram as the 3-product (Gauss) complex product: planes 4..7 hold
+  // S = Zr + Zi and D = Zr - Zi (hi / lo) next to {Re hi, Re lo, Im hi, Im lo}
+  bool gauss = false;
+  int nplanes() const { return split ? (gauss ? 8 : 4) : 2; }
+  size_t plane_bytes() const { return (size_t)nplanes() * plane_stride * (split ? 2 : 8); }
 };
 
 ps_status validate(const ps_plv_args* a, Geometry& g) {
@@ -544,6 +553,10 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
                              static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
     c->launches += 2;
   }
+  if (g.gauss && fmt == 0) {  // S = Zr + Zi, D = Zr - Zi planes of the Gauss Gram (after any masking)
+    PS_CUDA(launch_gauss_planes(out, plane_stride, row_lo * pitch, row_hi * pitch, st));
+    c->launches++;
+  }
   return PS_OK;
 }
 
@@ -621,10 +634,33 @@ struct Call {
   GramParams p;
   const CUtensorMap* ta = nullptr;
   const CUtensorMap* tb = nullptr;
+  const CUtensorMap* tb2 = nullptr;
   long long nn = 0;
   size_t oes = 4;
   long long slots = 1;  // output slots per metric
 };
+
+// The 3-product (Gauss) split Gram: 9 UMMAs per K step instead of 12
+// (gram_tc.cu), same 256 x 128 tiles, one accumulation buffer.  It pays where
+// the Gram dominates and rounds are long: complex (analytic / phasor) input
+// with >= 8192 samples per round (C5: Gram -7%, step -5%); with real input
+// or short trials the extra S / D plane pass outweighs it (measured C2-C4).
+// PS_GAUSS=1 forces it for every split over-samples call, PS_GAUSS=0 never.
+int gauss_mode() {
+  static const int m = [] {
+    const char* s = std::getenv("PS_GAUSS");
+    return s ? (std::atoi(s) != 0 ? 1 : 0) : -1;  // -1: automatic
+  }();
+  return m;
+}
+
+void decide_gauss(const ps_plv_args* a, Call& k) {
+  const bool eligible = k.g.split && a->mode == PS_MODE_OVER_SAMPLES;
+  const long long round_len = a->trial_reduce == PS_TRIALS_POOL ? k.g.T * k.g.R : k.g.T;
+  const bool automatic = a->input_kind != PS_INPUT_REAL && round_len >= 8192;
+  const int m = gauss_mode();
+  k.g.gauss = eligible && (m == 1 || (m == -1 && automatic));
+}
 
 int kc_blocks_default() {
   // TMEM accumulation chunk (drain period) in 32-sample K blocks; see gram_tc.cu
@@ -805,7 +841,9 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   p.plane_stride = g.plane_stride;
   p.status = c->d_status;
   p.illcond_tol = 4e-6f;  // 2.5x margin below the 1e-5 split-path tolerance
-  p.kc_blocks = kc_blocks_default();
+  // the Gauss Gram drains a single accumulation buffer: longer chunks (its
+  // error at 512 samples matches the 4-product Gram's at 128, accuracy probe)
+  p.kc_blocks = std::getenv("PS_KC_BLOCKS") || !g.gauss ? kc_blocks_default() : 16;
   p.upper_only = a->out_layout == PS_LAYOUT_UPPER ? 1 : 0;
   static const int dbg = [] {
     const char* s = std::getenv("PS_DEBUG_EPI");
@@ -834,35 +872,41 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   p.out_cre = kouts[3];
   p.out_cim = kouts[4];
   if (g.split) {
-    TmapKey key{c->planes.p, g.T, g.N, g.B * g.R, g.pitch};
+    TmapKey key{c->planes.p, g.T, g.N, g.B * g.R, g.pitch, g.gauss};
     auto it = c->tmaps.find(key);
     if (it == c->tmaps.end()) {
       auto enc = encode_fn();
       if (!enc) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
-      CUtensorMap ta, tb;
-      cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), 4};
+      Tmaps tm{};
+      cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), (cuuint64_t)g.nplanes()};
       cuuint64_t strides[3] = {(cuuint64_t)g.pitch * 2, (cuuint64_t)(g.N * g.pitch * 2),
                                (cuuint64_t)(g.plane_stride * 2)};
-      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, 4};  // 128 rows of the I panel per CTA
-      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)split_b_box_rows(), 1, 4};
+      // boxes: A = 128 rows x {4 planes | Gauss: 6 planes Zr, Zi, S}; B = the
+      // CTA's share of the J panel x {4 planes | Gauss: 2 planes Zr (+ b2: S, D)}
+      const cuuint32_t brows = (cuuint32_t)split_b_box_rows();
+      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, g.gauss ? 6u : 4u};
+      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, brows, 1, g.gauss ? 2u : 4u};
+      cuuint32_t boxB2[4] = {(cuuint32_t)kSplitBK, brows, 1, 4u};
       cuuint32_t estr[4] = {1, 1, 1, 1};
       const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
                                      : kSplitBK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
                                                       : CU_TENSOR_MAP_SWIZZLE_128B;
-      CUresult r1 = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxA, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      CUresult r2 = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, boxB, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+      auto encode = [&](CUtensorMap* m, cuuint32_t* box) {
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->planes.p, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      };
+      const CUresult r1 = encode(&tm.a, boxA), r2 = encode(&tm.b, boxB);
+      const CUresult r3 = g.gauss ? encode(&tm.b2, boxB2) : CUDA_SUCCESS;
+      if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS)
         return fail(PS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" +
-                                   std::to_string((int)r2));
+                                   std::to_string((int)r2) + "/" + std::to_string((int)r3));
       if (c->tmaps.size() > 64) c->tmaps.clear();
-      it = c->tmaps.emplace(key, std::make_pair(ta, tb)).first;
+      it = c->tmaps.emplace(key, tm).first;
     }
-    k.ta = &it->second.first;
-    k.tb = &it->second.second;
+    k.ta = &it->second.a;
+    k.tb = &it->second.b;
+    k.tb2 = g.gauss ? &it->second.b2 : nullptr;
   }
   return PS_OK;
 }
@@ -904,7 +948,7 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
     p.lock_lag = lk.second;
     p.lock_rounds = (int)rounds;
   }
-  if (k.g.split) PS_CUDA(launch_gram_split(k.ta, k.tb, p, grid, st));
+  if (k.g.split) PS_CUDA(launch_gram_split(k.ta, k.tb, k.tb2, k.g.gauss, p, grid, st));
   else PS_CUDA(launch_gram_f64(p, grid, st));
   c->launches++;
   return PS_OK;
@@ -1206,7 +1250,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   bool copied = false;
   // device buffers: input span (same element layout as the host array), planes, outputs
   if (!dev_input) PS_TRY(ensure(c->hin, (size_t)span * esz));
-  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  const size_t plane_bytes = g.plane_bytes();
   PS_TRY(ensure(c->planes, plane_bytes));
   const size_t oes = g.split ? 4 : 8;
   void* houts[5];
@@ -1558,6 +1602,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
+    res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
     res->h2d_bytes = (int64_t)h2d_bytes;
     res->d2h_bytes = (int64_t)d2h_bytes;
   }
@@ -1658,6 +1703,7 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   Call k;
   PS_TRY(validate(a, k.g));
   PS_TRY(setup_outputs(a, k));
+  decide_gauss(a, k);
   const Geometry& g = k.g;
   PS_CUDA(cudaSetDevice(c->device));
   cudaStream_t st = static_cast<cudaStream_t>(a->stream);
@@ -1665,7 +1711,7 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   bool copied = false;
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[0], st));
   // ---- phasor planes --------------------------------------------------------
-  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  const size_t plane_bytes = g.plane_bytes();
   PS_TRY(ensure(c->planes, plane_bytes));
   PS_TRY(reset_status(c, st));
   PS_TRY(prepare_phasors(c, a, g, a->input, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride, st, &copied));
@@ -1724,6 +1770,7 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
+    res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
     if (c->timing) {
       cudaEventElapsedTime(&res->ms_normalize, c->ev[0], c->ev[1]);
       cudaEventElapsedTime(&res->ms_gram, c->ev[1], c->ev[2]);
@@ -1823,7 +1870,7 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
   else
     PS_CUFFT(cufftExecR2C(fwd, (cufftReal*)c->xw.p, (cufftComplex*)c->spec.p));
   // ---- per-bin Gram operands (unit = (band, bin), K = R * S segments) ---------
-  const size_t plane_bytes = gt.split ? (size_t)4 * gt.plane_stride * 2 : (size_t)2 * gt.plane_stride * 8;
+  const size_t plane_bytes = gt.plane_bytes();
   PS_TRY(ensure(c->planes, plane_bytes));
   PS_TRY(ensure(c->maskcount, (size_t)gt.rows * sizeof(int)));
   PS_TRY(reset_status(c, st));
@@ -1859,6 +1906,7 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
     res->n_observations = K;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->n_kernel_launches = c->launches;
+    res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
     if (c->timing) {
       cudaEventElapsedTime(&res->ms_normalize, c->ev[0], c->ev[1]);
       cudaEventElapsedTime(&res->ms_gram, c->ev[1], c->ev[2]);
@@ -1875,6 +1923,7 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
   Call k;
   PS_TRY(validate(a, k.g));
   PS_TRY(setup_outputs(a, k));
+  decide_gauss(a, k);
   const Geometry& g = k.g;
   if (n_stages < 1 || !stage_cols) return fail(PS_E_INVALID, "n_stages must be >= 1 with stage_cols");
   if (a->mode != PS_MODE_OVER_SAMPLES) return fail(PS_E_UNSUPPORTED, "staged input supports mode over_samples only");
@@ -1889,7 +1938,7 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
   PS_TRY(ensure_pipeline(c, n_stages));
   c->launches = 0;
   bool copied = false;
-  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  const size_t plane_bytes = g.plane_bytes();
   PS_TRY(ensure(c->planes, plane_bytes));
   PS_TRY(prep_begin(c, a, g, st));  // Hilbert workspace sized once (no realloc mid-stage)
   PS_TRY(reset_status(c, st));
@@ -1930,6 +1979,7 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
+    res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
     if (c->timing) {
       PS_CUDA(cudaEventSynchronize(done));
       float tot = 0.f;
@@ -1966,7 +2016,7 @@ ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long lon
   c->launches = 0;
   bool copied = false;
   if (!dev_input) PS_TRY(ensure(c->hin, (size_t)span * esz));
-  const size_t plane_bytes = g.split ? (size_t)4 * g.plane_stride * 2 : (size_t)2 * g.plane_stride * 8;
+  const size_t plane_bytes = g.plane_bytes();
   PS_TRY(ensure(c->planes, plane_bytes));
   const size_t oes = g.split ? 4 : 8;
   void* houts[5];
@@ -2068,6 +2118,7 @@ ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long lon
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
+    res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
     res->h2d_bytes = (int64_t)h2d_bytes;
     res->d2h_bytes = (int64_t)d2h_bytes;
   }
@@ -2082,6 +2133,7 @@ ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, 
   Call k;
   PS_TRY(validate(a, k.g));
   PS_TRY(setup_outputs(a, k));
+  decide_gauss(a, k);
   const Geometry& g = k.g;
   PS_CUDA(cudaSetDevice(c->device));
   // span of the (possibly strided) host input, in elements

@@ -56,27 +56,44 @@ constexpr uint32_t TMEM_COLS = 512;
 constexpr uint32_t BUF_COLS = 2 * BN;          // Re + Im of one accumulation buffer
 constexpr int HALF = BN / (NEPI_WARPS / 4);    // columns per epilogue warp
 
-template <int CG>
+// GS = true: the 3-multiplication (Gauss) complex Gram.  With a = Zr_i,
+// b = Zi_i, c = Zr_j, d = Zi_j:  k1 = (a + b) c,  k2 = -a (c + d),
+// k3 = b (c - d);  Re = k1 - k3,  Im = k1 + k2 -- 9 split UMMAs per K step
+// instead of 12.  Planes 4..7 hold S = Zr + Zi and D = Zr - Zi (hi / lo);
+// A stages {Zr, Zi, S} (planes 0-5), B stages {Zr} (planes 0-1) and {S, D}
+// (planes 4-7).  The three accumulators of a 256 x 128 tile take 384 TMEM
+// columns, so there is one accumulation buffer (the MMA waits while the
+// epilogue drains a chunk, folding k1 - k3 and k1 + k2 into its Re / Im sums).
+template <int CG, bool GS = false>
 struct Geo {
-  static constexpr int BNC = BN / CG;                    // J-panel rows staged per CTA
+  static constexpr int BNT = BN;                         // tile columns (UMMA N)
+  static constexpr int H = BNT / (NEPI_WARPS / 4);       // columns per epilogue warp
+  static constexpr int NACC = GS ? 3 : 2;                // accumulators per buffer
+  static constexpr int NBUF = GS ? 1 : 2;                // accumulation buffers (ping-pong when 2)
+  static constexpr uint32_t BUF = NACC * BNT;            // TMEM columns per buffer
+  static constexpr int NPL = GS ? 6 : 4;                 // planes staged per operand
+  static constexpr int BNC = BNT / CG;                   // J-panel rows staged per CTA
   static constexpr int A_PLANE = BMC * BK * 2;
   static constexpr int B_PLANE = BNC * BK * 2;
-  static constexpr int A_BYTES = 4 * A_PLANE;
-  static constexpr int B_BYTES = 4 * B_PLANE;
+  static constexpr int A_BYTES = NPL * A_PLANE;
+  static constexpr int B_BYTES = NPL * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
-  static constexpr int STAGES = CG == 2 ? 4 : 3;
+  static constexpr int STAGES = GS ? 3 : (CG == 2 ? 4 : 3);
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr int UMMA_M = BMC * CG;
+  static_assert(NBUF * BUF <= TMEM_COLS, "the accumulation buffers must fit TMEM");
+  static_assert(H % 16 == 0, "epilogue loads 16 columns at a time");
 };
 
 static_assert(2 * BUF_COLS <= TMEM_COLS, "two Re+Im buffers must fit TMEM");
 static_assert(BK % 16 == 0 && BK * 2 <= 128, "BK must be a multiple of 16 within one swizzle row");
 static_assert(HALF % 16 == 0, "epilogue loads 16 columns at a time");
 
-__device__ __forceinline__ void add_chunk(float (&s)[HALF], uint32_t taddr) {
+template <int H>
+__device__ __forceinline__ void add_chunk(float (&s)[H], uint32_t taddr) {
   uint32_t v[16];
 #pragma unroll
-  for (int c = 0; c < HALF; c += 16) {
+  for (int c = 0; c < H; c += 16) {
     ptx::tmem_ld_32x32b_x16(taddr + c, v);
     ptx::tmem_wait_ld();
 #pragma unroll
@@ -84,9 +101,30 @@ __device__ __forceinline__ void add_chunk(float (&s)[HALF], uint32_t taddr) {
   }
 }
 
-__device__ __forceinline__ void store_sums(const float (&s)[HALF], uint32_t taddr) {
+// Gauss drain: Re += k1 - k3, Im += k1 + k2 (accumulators at +0, +n, +2n);
+// 4 columns per load keep the 2 x H register sums live without spilling
+template <int H>
+__device__ __forceinline__ void add_chunk_gauss(float (&re)[H], float (&im)[H], uint32_t taddr, uint32_t n) {
 #pragma unroll
-  for (int c = 0; c < HALF; c += 16) {
+  for (int c = 0; c < H; c += 4) {
+    uint32_t v1[4], v2[4], v3[4];
+    ptx::tmem_ld_32x32b_x4(taddr + c, v1);
+    ptx::tmem_ld_32x32b_x4(taddr + n + c, v2);
+    ptx::tmem_ld_32x32b_x4(taddr + 2 * n + c, v3);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float k1 = __uint_as_float(v1[k]);
+      re[c + k] += k1 - __uint_as_float(v3[k]);
+      im[c + k] += k1 + __uint_as_float(v2[k]);
+    }
+  }
+}
+
+template <int H>
+__device__ __forceinline__ void store_sums(const float (&s)[H], uint32_t taddr) {
+#pragma unroll
+  for (int c = 0; c < H; c += 16) {
     uint32_t v[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = __float_as_uint(s[c + k]);
@@ -96,6 +134,7 @@ __device__ __forceinline__ void store_sums(const float (&s)[HALF], uint32_t tadd
 
 // PLV-family epilogue of one finished round for row i and this warp's
 // HALF-column slice; sums are read back 4 columns at a time from TMEM.
+template <int BN, int HALF>
 __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, int r, int r0, int r1, uint32_t ta,
                                            int i, int h, bool any_masked) {
   const RoundInfo ri = round_info(p, w, r, r0, r1);
@@ -253,11 +292,12 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
 // covers all 256 rows.  CG = 1: item.g's high bit is unused; instead the host
 // doubles the items and the low bit of I (after << 1) selects the half -- see
 // launch_gram_split: for CG = 1 the host passes 128-row panel indices.
-template <int CG>
+template <int CG, bool GS>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gram_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                      const GramParams p) {
-  using G = Geo<CG>;
+                      const __grid_constant__ CUtensorMap tmB2, const GramParams p) {
+  using G = Geo<CG, GS>;
+  constexpr int BN = G::BNT;  // tile columns of this variant (shadows the 128-column default)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::STAGES * G::STAGE_BYTES);
@@ -285,6 +325,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     ptx::fence_mbar_init();
     ptx::tma_prefetch_desc(&tmA);
     ptx::tma_prefetch_desc(&tmB);
+    if (GS) ptx::tma_prefetch_desc(&tmB2);
   }
   if (warp == 1) {
     ptx::tmem_alloc_cg<CG>(tslot, TMEM_COLS);
@@ -357,11 +398,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               ptx::mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
               ptx::tma_load_4d(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
               ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
+              if (GS) ptx::tma_load_4d(sa + G::A_BYTES + 2 * G::B_PLANE, &tmB2, &full[stage], kb * BK, rowB, u, 4);
             } else {
               // rank 0's full barrier counts the bytes of both CTAs
               if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE_BYTES);
               ptx::tma_load_4d_cg2(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
               ptx::tma_load_4d_cg2(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
+              if (GS)
+                ptx::tma_load_4d_cg2(sa + G::A_BYTES + 2 * G::B_PLANE, &tmB2, &full[stage], kb * BK, rowB, u, 4);
             }
             if (++stage == G::STAGES) {
               stage = 0;
@@ -395,7 +439,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
             // __shfl_sync makes the operands provably warp-uniform, so ptxas
             // keeps them in uniform registers for UTCHMMA
-            const uint32_t d_re = __shfl_sync(0xffffffffu, tmem + (uint32_t)buf * BUF_COLS, 0);
+            const uint32_t d_re = __shfl_sync(0xffffffffu, tmem + (uint32_t)buf * G::BUF, 0);
             const uint32_t d_im = d_re + BN;
             ptx::mbar_wait(&full[stage], phase, tflag);
             ptx::tc_fence_after();
@@ -414,29 +458,49 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const uint64_t aIl = dA + ko + 3 * (G::A_PLANE >> 4);
               const uint64_t bRh = dB + ko + 0 * (G::B_PLANE >> 4);
               const uint64_t bRl = dB + ko + 1 * (G::B_PLANE >> 4);
-              const uint64_t bIh = dB + ko + 2 * (G::B_PLANE >> 4);
-              const uint64_t bIl = dB + ko + 3 * (G::B_PLANE >> 4);
+              const uint64_t bIh = dB + ko + 2 * (G::B_PLANE >> 4);  // GS: S hi
+              const uint64_t bIl = dB + ko + 3 * (G::B_PLANE >> 4);  // GS: S lo
               const uint32_t acc0 = (chunk_start && ks == 0) ? 0u : 1u;
-              // Re = Zr Zr' + Zi Zi'
-              ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRh, idesc_pos, acc0);
-              ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRl, idesc_pos, 1u);
-              ptx::mma_f16_ss_warp<CG>(d_re, aRl, bRh, idesc_pos, 1u);
-              ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIh, idesc_pos, 1u);
-              ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIl, idesc_pos, 1u);
+              if constexpr (GS) {
+                const uint64_t aSh = dA + ko + 4 * (G::A_PLANE >> 4);
+                const uint64_t aSl = dA + ko + 5 * (G::A_PLANE >> 4);
+                const uint64_t bDh = dB + ko + 4 * (G::B_PLANE >> 4);
+                const uint64_t bDl = dB + ko + 5 * (G::B_PLANE >> 4);
+                const uint32_t d_k3 = d_re + 2 * BN;
+                // k1 = S_i . Zr_j   (accumulator 0)
+                ptx::mma_f16_ss_warp<CG>(d_re, aSh, bRh, idesc_pos, acc0);
+                ptx::mma_f16_ss_warp<CG>(d_re, aSh, bRl, idesc_pos, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_re, aSl, bRh, idesc_pos, 1u);
+                // k2 = -Zr_i . S_j  (accumulator 1)
+                ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIh, idesc_neg, acc0);
+                ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIl, idesc_neg, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_im, aRl, bIh, idesc_neg, 1u);
+                // k3 = Zi_i . D_j   (accumulator 2)
+                ptx::mma_f16_ss_warp<CG>(d_k3, aIh, bDh, idesc_pos, acc0);
+                ptx::mma_f16_ss_warp<CG>(d_k3, aIh, bDl, idesc_pos, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_k3, aIl, bDh, idesc_pos, 1u);
+              } else {
+                // Re = Zr Zr' + Zi Zi'
+                ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRh, idesc_pos, acc0);
+                ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRl, idesc_pos, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_re, aRl, bRh, idesc_pos, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIh, idesc_pos, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_re, aIh, bIl, idesc_pos, 1u);
 #ifndef PS_EXPERIMENT_9MMA  // (timing experiment only: 9 of the 12 UMMAs, wrong values)
-              ptx::mma_f16_ss_warp<CG>(d_re, aIl, bIh, idesc_pos, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_re, aIl, bIh, idesc_pos, 1u);
 #endif
-              // Im = Zi Zr' - Zr Zi'
-              ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRh, idesc_pos, acc0);
-              ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRl, idesc_pos, 1u);
+                // Im = Zi Zr' - Zr Zi'
+                ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRh, idesc_pos, acc0);
+                ptx::mma_f16_ss_warp<CG>(d_im, aIh, bRl, idesc_pos, 1u);
 #ifndef PS_EXPERIMENT_9MMA
-              ptx::mma_f16_ss_warp<CG>(d_im, aIl, bRh, idesc_pos, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_im, aIl, bRh, idesc_pos, 1u);
 #endif
-              ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIh, idesc_neg, 1u);
-              ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIl, idesc_neg, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIh, idesc_neg, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_im, aRh, bIl, idesc_neg, 1u);
 #ifndef PS_EXPERIMENT_9MMA
-              ptx::mma_f16_ss_warp<CG>(d_im, aRl, bIh, idesc_neg, 1u);
+                ptx::mma_f16_ss_warp<CG>(d_im, aRl, bIh, idesc_neg, 1u);
 #endif
+              }
             }
             ptx::mma_commit_warp<CG>(&empty[stage]);  // the group's smem slots free once these retire
             if (++stage == G::STAGES) {
@@ -446,7 +510,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (chunk_end) {
               ptx::mma_commit_warp<CG>(&tfull[buf]);  // chunk partial complete -> epilogues
               uses[buf]++;
-              buf ^= 1;
+              if (G::NBUF == 2) buf ^= 1;
             }
           }
         }
@@ -461,9 +525,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     uint32_t uses[2] = {0u, 0u};
     int buf = 0;
     const bool any_masked = (p.status->flags & FLAG_ANY_MASKED) != 0;
-    float sre[HALF], sim[HALF];
+    constexpr int H = G::H;
+    // register sums of Re / Im (GS: folded from k1, k2, k3 at every drain)
+    float sre[H], sim[H];
 #pragma unroll
-    for (int k = 0; k < HALF; ++k) sre[k] = sim[k] = 0.0f;
+    for (int k = 0; k < H; ++k) sre[k] = sim[k] = 0.0f;
     for (int it = grp; it < p.n_items; it += ngrp) {
       const Item w = p.items[it];
       const int r0 = p.pool ? 0 : w.g * p.Rg;
@@ -473,27 +539,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int c = 0; c < nchunks; ++c) {
           ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
           ptx::tc_fence_after();
-          const uint32_t ta = tmem + lane_base + (uint32_t)buf * BUF_COLS + (uint32_t)(h * HALF);
+          const uint32_t ta = tmem + lane_base + (uint32_t)buf * G::BUF + (uint32_t)(h * H);
           // single-chunk rounds (short K: over_trials, coherence, T <= 128):
           // the chunk accumulator already is the round's sum (0 + x = x), so
           // it is emitted in place -- no drain / park round trip through TMEM
-          const bool direct = nchunks == 1 && !p.pool;
+          const bool direct = !GS && nchunks == 1 && !p.pool;
           if (!direct) {
-            add_chunk(sre, ta);
-            add_chunk(sim, ta + BN);
+            if constexpr (GS) {
+              add_chunk_gauss<H>(sre, sim, ta, BN);
+            } else {
+              add_chunk<H>(sre, ta);
+              add_chunk<H>(sim, ta + BN);
+            }
           }
           if (c == nchunks - 1 && (!p.pool || r == r1 - 1)) {
             // Round complete: park the fp32 sums back in this (still owned)
             // TMEM buffer and emit from there with a compact loop, so the
-            // 64 register sums are dead during the store-heavy epilogue.
+            // register sums are dead during the store-heavy epilogue.
             if (!direct) {
-              store_sums(sre, ta);
-              store_sums(sim, ta + BN);
+              store_sums<H>(sre, ta);
+              store_sums<H>(sim, ta + BN);
               ptx::tmem_wait_st();
             }
-            if (!(p.debug_flags & 1)) emit_round(p, w, r, r0, r1, ta, i, h, any_masked);
+            if (!(p.debug_flags & 1)) emit_round<BN, H>(p, w, r, r0, r1, ta, i, h, any_masked);
 #pragma unroll
-            for (int k = 0; k < HALF; ++k) sre[k] = sim[k] = 0.0f;  // sums dead across the emission
+            for (int k = 0; k < H; ++k) sre[k] = sim[k] = 0.0f;  // sums dead across the emission
           }
           ptx::tc_fence_before();
           __syncwarp();
@@ -502,7 +572,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             else ptx::mbar_arrive(&tempty[buf]);
           }
           uses[buf]++;
-          buf ^= 1;
+          if (G::NBUF == 2) buf ^= 1;
         }
       }
       if (p.sb_cnt) {  // item emitted by this warp: count it towards its output sub-block
@@ -528,11 +598,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-template <int CG>
-cudaError_t launch_cg(const void* tmapA, const void* tmapB, const GramParams& p, int groups, cudaStream_t st) {
-  using G = Geo<CG>;
+template <int CG, bool GS>
+cudaError_t launch_cg(const void* tmapA, const void* tmapB, const void* tmapB2, const GramParams& p, int groups,
+                      cudaStream_t st) {
+  using G = Geo<CG, GS>;
   cudaError_t e =
-      cudaFuncSetAttribute(gram_split_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
+      cudaFuncSetAttribute(gram_split_kernel<CG, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   if (p.n_items <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
@@ -547,8 +618,9 @@ cudaError_t launch_cg(const void* tmapA, const void* tmapB, const GramParams& p,
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gram_split_kernel<CG>, *static_cast<const CUtensorMap*>(tmapA),
-                            *static_cast<const CUtensorMap*>(tmapB), p);
+  return cudaLaunchKernelEx(&cfg, gram_split_kernel<CG, GS>, *static_cast<const CUtensorMap*>(tmapA),
+                            *static_cast<const CUtensorMap*>(tmapB),
+                            *static_cast<const CUtensorMap*>(tmapB2 ? tmapB2 : tmapB), p);
 }
 
 }  // namespace
@@ -567,10 +639,13 @@ int split_b_box_rows() { return BN / split_cta_group(); }
 
 int split_epi_arrivals() { return NEPI_WARPS * split_cta_group(); }
 
-cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p, int groups,
-                              cudaStream_t st) {
-  return split_cta_group() == 2 ? launch_cg<2>(tmapA, tmapB, p, groups, st)
-                                : launch_cg<1>(tmapA, tmapB, p, groups, st);
+cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const void* tmapB2, bool gauss,
+                              const GramParams& p, int groups, cudaStream_t st) {
+  if (gauss)
+    return split_cta_group() == 2 ? launch_cg<2, true>(tmapA, tmapB, tmapB2, p, groups, st)
+                                  : launch_cg<1, true>(tmapA, tmapB, tmapB2, p, groups, st);
+  return split_cta_group() == 2 ? launch_cg<2, false>(tmapA, tmapB, nullptr, p, groups, st)
+                                : launch_cg<1, false>(tmapA, tmapB, nullptr, p, groups, st);
 }
 
 }  // namespace ps

@@ -6,6 +6,7 @@
 // design decisions SPEC.md:120-125, per-pair effective T SPEC.md:260.
 // All of these are HBM-bound streaming kernels.
 #include <cuda_fp16.h>
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -1237,6 +1238,47 @@ cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long n
   hilbert_fused4096_kernel<<<grid, kFftThreads, kFftSmemBytes, st>>>(
       src, row0, nrows, static_cast<__half*>(out), pitch, plane_stride, rowstat, rowstat + rows_total,
       static_cast<float*>(const_cast<void*>(src.hbuf)), amp_floor, status);
+  return cudaGetLastError();
+}
+
+// Gauss-Gram operand planes: S = Zr + Zi and D = Zr - Zi from the split
+// planes {Re hi, Re lo, Im hi, Im lo} of the same samples, as hi / lo fp16
+// pairs in planes 4..7 (flat element range [e0, e1) of every plane, 8-aligned).
+__global__ void gauss_planes_kernel(__half* planes, long long ps, long long e0, long long e1) {
+  const long long n8 = (e1 - e0) / 8;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < n8; v += (long long)gridDim.x * blockDim.x) {
+    const long long e = e0 + 8 * v;
+    const uint4 rh = *reinterpret_cast<const uint4*>(planes + e);
+    const uint4 rl = *reinterpret_cast<const uint4*>(planes + ps + e);
+    const uint4 ih = *reinterpret_cast<const uint4*>(planes + 2 * ps + e);
+    const uint4 il = *reinterpret_cast<const uint4*>(planes + 3 * ps + e);
+    const __half* prh = reinterpret_cast<const __half*>(&rh);
+    const __half* prl = reinterpret_cast<const __half*>(&rl);
+    const __half* pih = reinterpret_cast<const __half*>(&ih);
+    const __half* pil = reinterpret_cast<const __half*>(&il);
+    __align__(16) __half sh[8], sl[8], dh[8], dl[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float zr = __half2float(prh[k]) + __half2float(prl[k]);
+      const float zi = __half2float(pih[k]) + __half2float(pil[k]);
+      const float S = zr + zi, D = zr - zi;
+      sh[k] = __float2half_rn(S);
+      sl[k] = __float2half_rn(S - __half2float(sh[k]));
+      dh[k] = __float2half_rn(D);
+      dl[k] = __float2half_rn(D - __half2float(dh[k]));
+    }
+    *reinterpret_cast<uint4*>(planes + 4 * ps + e) = *reinterpret_cast<const uint4*>(sh);
+    *reinterpret_cast<uint4*>(planes + 5 * ps + e) = *reinterpret_cast<const uint4*>(sl);
+    *reinterpret_cast<uint4*>(planes + 6 * ps + e) = *reinterpret_cast<const uint4*>(dh);
+    *reinterpret_cast<uint4*>(planes + 7 * ps + e) = *reinterpret_cast<const uint4*>(dl);
+  }
+}
+
+cudaError_t launch_gauss_planes(void* planes, long long plane_stride, long long e0, long long e1, cudaStream_t st) {
+  if (e1 <= e0) return cudaSuccess;
+  const long long n8 = (e1 - e0) / 8;
+  const unsigned grid = (unsigned)std::min<long long>((n8 + 255) / 256, 148LL * 16);
+  gauss_planes_kernel<<<grid, 256, 0, st>>>(static_cast<__half*>(planes), plane_stride, e0, e1);
   return cudaGetLastError();
 }
 

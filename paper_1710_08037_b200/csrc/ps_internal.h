@@ -158,8 +158,10 @@ cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void
 cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs,
                                 void* const* outs, long long elems_per_out, int R,
                                 int is_double, cudaStream_t st, long long upper_n);
-cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const GramParams& p,
-                              int grid, cudaStream_t st);
+cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const void* tmapB2, bool gauss,
+                              const GramParams& p, int grid, cudaStream_t st);
+// Gauss-Gram planes 4..7 (S, D hi / lo) from planes 0..3, flat elements [e0, e1)
+cudaError_t launch_gauss_planes(void* planes, long long plane_stride, long long e0, long long e1, cudaStream_t st);
 cudaError_t launch_gram_f64(const GramParams& p, int grid, cudaStream_t st);
 // Exact FP64 recomputation of queued ciPLV pairs.  groups[g]..groups[g+1]
 // index a run of entries (sorted by slot, i, j, u0) sharing one output

@@ -32,7 +32,7 @@ def test_struct_layout_matches_header():
     # ps_plv_args: 8 + 2*4 + 8*8 + 8 + 3*4 (+4 pad) + 5*8 + 2*4 + 8 + 2*4 + 8 (fir)
     assert ctypes.sizeof(_native.PlvArgs) == 8 + 8 + 64 + 8 + 16 + 40 + 8 + 8 + 8 + 8
     assert _native.PlvArgs.fir.offset == ctypes.sizeof(_native.PlvArgs) - 8
-    assert ctypes.sizeof(_native.PlvResult) == 3 * 8 + 2 * 4 + 4 * 4 + 2 * 8
+    assert ctypes.sizeof(_native.PlvResult) == 3 * 8 + 2 * 4 + 4 * 4 + 2 * 8 + 2 * 4
     assert ctypes.sizeof(_native.Fir) == 24
 
 
