@@ -553,7 +553,7 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
                              static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
     c->launches += 2;
   }
-  if (g.gauss && fmt == 0) {  // S = Zr + Zi, D = Zr - Zi planes of the Gauss Gram (after any masking)
+  if (g.gauss && fmt == 0 && !gauss_smem_convert()) {  // S = Zr + Zi, D = Zr - Zi planes of the Gauss Gram (after any masking)
     PS_CUDA(launch_gauss_planes(out, plane_stride, row_lo * pitch, row_hi * pitch, st));
     c->launches++;
   }
@@ -884,8 +884,10 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
       // boxes: A = 128 rows x {4 planes | Gauss: 6 planes Zr, Zi, S}; B = the
       // CTA's share of the J panel x {4 planes | Gauss: 2 planes Zr (+ b2: S, D)}
       const cuuint32_t brows = (cuuint32_t)split_b_box_rows();
-      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, g.gauss ? 6u : 4u};
-      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, brows, 1, g.gauss ? 2u : 4u};
+      // (Gauss with the smem S / D conversion streams the 4-plane boxes)
+      const bool gs_planes = g.gauss && !gauss_smem_convert();
+      cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, gs_planes ? 6u : 4u};
+      cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, brows, 1, gs_planes ? 2u : 4u};
       cuuint32_t boxB2[4] = {(cuuint32_t)kSplitBK, brows, 1, 4u};
       cuuint32_t estr[4] = {1, 1, 1, 1};
       const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
@@ -897,7 +899,7 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       };
       const CUresult r1 = encode(&tm.a, boxA), r2 = encode(&tm.b, boxB);
-      const CUresult r3 = g.gauss ? encode(&tm.b2, boxB2) : CUDA_SUCCESS;
+      const CUresult r3 = gs_planes ? encode(&tm.b2, boxB2) : CUDA_SUCCESS;
       if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS || r3 != CUDA_SUCCESS)
         return fail(PS_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r1) + "/" +
                                    std::to_string((int)r2) + "/" + std::to_string((int)r3));
@@ -906,7 +908,7 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     }
     k.ta = &it->second.a;
     k.tb = &it->second.b;
-    k.tb2 = g.gauss ? &it->second.b2 : nullptr;
+    k.tb2 = g.gauss && !gauss_smem_convert() ? &it->second.b2 : nullptr;
   }
   return PS_OK;
 }

@@ -64,6 +64,20 @@ constexpr int HALF = BN / (NEPI_WARPS / 4);    // columns per epilogue warp
 // (planes 4-7).  The three accumulators of a 256 x 128 tile take 384 TMEM
 // columns, so there is one accumulation buffer (the MMA waits while the
 // epilogue drains a chunk, folding k1 - k3 and k1 + k2 into its Re / Im sums).
+//
+// CV = true (Gauss only, PS_GAUSS_CONV=1; measured slower, kept as an
+// experiment): the S / D planes are not streamed.  TMA loads the
+// four split planes {Zr, Zi} hi / lo of A and B (4 of the 6 smem slots, the
+// same bytes per stage as the 4-product Gram) into each CTA's own full
+// barrier; the epilogue warps -- idle between chunk drains -- rebuild
+// S = Zr + Zi (A slots 4-5) and S, D (B slots 2-3, 4-5, over Zi) with the
+// arithmetic of gauss_planes_kernel (bit-identical operands), fence the
+// writes to the async proxy and arrive on rank 0's conv barrier, which the
+// MMA issuer waits on instead of full.  Bit-identical to CV = false
+// (tools/gauss_conv_check.py) but C5's Gram takes 88.5 ms against 52.3 ms:
+// the conversion adds ~80 KB of LSU shared-memory traffic per stage against
+// the 24 KB of TMA writes it saves, on an SM whose shared memory is already
+// busy feeding 18 UMMAs per stage (profiles/r01_gauss_conv.txt).
 template <int CG, bool GS = false>
 struct Geo {
   static constexpr int BNT = BN;                         // tile columns (UMMA N)
@@ -78,7 +92,9 @@ struct Geo {
   static constexpr int A_BYTES = NPL * A_PLANE;
   static constexpr int B_BYTES = NPL * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
-  static constexpr int STAGES = GS ? 3 : (CG == 2 ? 4 : 3);
+  // (GS, CG = 1: a 128-row J panel makes a 96 KB stage -- two fit the 227 KB)
+  static constexpr int STAGES = GS ? (CG == 2 ? 3 : 2) : (CG == 2 ? 4 : 3);
+  static_assert(STAGES * STAGE_BYTES + 1024 + 256 <= 227 * 1024, "stages must fit shared memory");
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr int UMMA_M = BMC * CG;
   static_assert(NBUF * BUF <= TMEM_COLS, "the accumulation buffers must fit TMEM");
@@ -118,6 +134,68 @@ __device__ __forceinline__ void add_chunk_gauss(float (&re)[H], float (&im)[H], 
       re[c + k] += k1 - __uint_as_float(v3[k]);
       im[c + k] += k1 + __uint_as_float(v2[k]);
     }
+  }
+}
+
+// S = Zr + Zi (and D = Zr - Zi) of 4 samples from their split hi / lo
+// halves, re-split to hi / lo -- the arithmetic of gauss_planes_kernel
+// (prep_kernels.cu), so the operands are bit-identical to the streamed planes
+template <bool WITH_D>
+__device__ __forceinline__ void gauss_split4(const uint2 rh, const uint2 rl, const uint2 ih, const uint2 il, uint2& sh,
+                                             uint2& sl, uint2& dh, uint2& dl) {
+  const __half* prh = reinterpret_cast<const __half*>(&rh);
+  const __half* prl = reinterpret_cast<const __half*>(&rl);
+  const __half* pih = reinterpret_cast<const __half*>(&ih);
+  const __half* pil = reinterpret_cast<const __half*>(&il);
+  __half* psh = reinterpret_cast<__half*>(&sh);
+  __half* psl = reinterpret_cast<__half*>(&sl);
+  __half* pdh = reinterpret_cast<__half*>(&dh);
+  __half* pdl = reinterpret_cast<__half*>(&dl);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float zr = __fadd_rn(__half2float(prh[k]), __half2float(prl[k]));
+    const float zi = __fadd_rn(__half2float(pih[k]), __half2float(pil[k]));
+    const float S = __fadd_rn(zr, zi);
+    psh[k] = __float2half_rn(S);
+    psl[k] = __float2half_rn(__fsub_rn(S, __half2float(psh[k])));
+    if (WITH_D) {
+      const float D = __fsub_rn(zr, zi);
+      pdh[k] = __float2half_rn(D);
+      pdl[k] = __float2half_rn(__fsub_rn(D, __half2float(pdh[k])));
+    }
+  }
+}
+
+// CV feed: form the S (A) and S, D (B) slots of one landed stage in place;
+// thread t of the 16 epilogue warps takes every 512th 8-byte position (the
+// swizzle is the same in every plane, so the element-wise map is offset-wise)
+template <class G>
+__device__ __forceinline__ void gauss_convert_stage(uint8_t* sa, int t) {
+  constexpr int NT = NEPI_WARPS * 32;
+#pragma unroll 1
+  for (int o = t * 8; o < G::A_PLANE; o += NT * 8) {
+    const uint2 rh = *reinterpret_cast<const uint2*>(sa + o);
+    const uint2 rl = *reinterpret_cast<const uint2*>(sa + G::A_PLANE + o);
+    const uint2 ih = *reinterpret_cast<const uint2*>(sa + 2 * G::A_PLANE + o);
+    const uint2 il = *reinterpret_cast<const uint2*>(sa + 3 * G::A_PLANE + o);
+    uint2 sh, sl, dh, dl;
+    gauss_split4<false>(rh, rl, ih, il, sh, sl, dh, dl);
+    *reinterpret_cast<uint2*>(sa + 4 * G::A_PLANE + o) = sh;
+    *reinterpret_cast<uint2*>(sa + 5 * G::A_PLANE + o) = sl;
+  }
+  uint8_t* sb = sa + G::A_BYTES;
+#pragma unroll 1
+  for (int o = t * 8; o < G::B_PLANE; o += NT * 8) {
+    const uint2 rh = *reinterpret_cast<const uint2*>(sb + o);
+    const uint2 rl = *reinterpret_cast<const uint2*>(sb + G::B_PLANE + o);
+    const uint2 ih = *reinterpret_cast<const uint2*>(sb + 2 * G::B_PLANE + o);
+    const uint2 il = *reinterpret_cast<const uint2*>(sb + 3 * G::B_PLANE + o);
+    uint2 sh, sl, dh, dl;
+    gauss_split4<true>(rh, rl, ih, il, sh, sl, dh, dl);
+    *reinterpret_cast<uint2*>(sb + 2 * G::B_PLANE + o) = sh;  // over Zi (read above)
+    *reinterpret_cast<uint2*>(sb + 3 * G::B_PLANE + o) = sl;
+    *reinterpret_cast<uint2*>(sb + 4 * G::B_PLANE + o) = dh;
+    *reinterpret_cast<uint2*>(sb + 5 * G::B_PLANE + o) = dl;
   }
 }
 
@@ -292,11 +370,14 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
 // covers all 256 rows.  CG = 1: item.g's high bit is unused; instead the host
 // doubles the items and the low bit of I (after << 1) selects the half -- see
 // launch_gram_split: for CG = 1 the host passes 128-row panel indices.
-template <int CG, bool GS>
+template <int CG, bool GS, bool CV>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gram_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmB2, const GramParams p) {
   using G = Geo<CG, GS>;
+  static_assert(!CV || GS, "smem S / D conversion is a Gauss-Gram feed");
+  // bytes TMA delivers per stage and CTA (CV: 4 planes of A and of B)
+  constexpr int LOAD_BYTES = CV ? 4 * (G::A_PLANE + G::B_PLANE) : G::STAGE_BYTES;
   constexpr int BN = G::BNT;  // tile columns of this variant (shadows the 128-column default)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -304,7 +385,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint64_t* empty = full + G::STAGES;
   uint64_t* tfull = empty + G::STAGES;  // [2]
   uint64_t* tempty = tfull + 2;         // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* conv = tempty + 2;          // [STAGES] (CV: operand slots complete, S / D formed)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(conv + G::STAGES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -317,6 +399,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int s = 0; s < G::STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&conv[s], CG * NEPI_WARPS);  // one arrival per epilogue warp of the group
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
@@ -394,7 +477,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             ++e;
             ptx::mbar_wait(&empty[stage], phase ^ 1u, tflag);
             uint8_t* sa = smem + stage * G::STAGE_BYTES;
-            if (CG == 1) {
+            if (CV) {
+              // each CTA counts its own 4 + 4 planes; its epilogue warps convert
+              ptx::mbar_arrive_expect_tx(&full[stage], LOAD_BYTES);
+              ptx::tma_load_4d(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
+              ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
+            } else if (CG == 1) {
               ptx::mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
               ptx::tma_load_4d(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
               ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
@@ -441,7 +529,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             // keeps them in uniform registers for UTCHMMA
             const uint32_t d_re = __shfl_sync(0xffffffffu, tmem + (uint32_t)buf * G::BUF, 0);
             const uint32_t d_im = d_re + BN;
-            ptx::mbar_wait(&full[stage], phase, tflag);
+            if (CV) ptx::mbar_wait_cluster(&conv[stage], phase);
+            else ptx::mbar_wait(&full[stage], phase, tflag);
             ptx::tc_fence_after();
             // descriptor of the stage's A tile; planes / K sub-steps are
             // constant offsets added to the 14-bit start-address field
@@ -524,6 +613,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     uint32_t uses[2] = {0u, 0u};
     int buf = 0;
+    int cst = 0;        // CV: stage / phase of the next stage to convert
+    uint32_t cph = 0u;
+    const int ct = (warp - 2) * 32 + lane;
     const bool any_masked = (p.status->flags & FLAG_ANY_MASKED) != 0;
     constexpr int H = G::H;
     // register sums of Re / Im (GS: folded from k1, k2, k3 at every drain)
@@ -537,6 +629,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int i = w.I * G::UMMA_M + (int)rank * BMC + il;
       for (int r = r0; r < r1; ++r) {
         for (int c = 0; c < nchunks; ++c) {
+          if constexpr (CV) {
+            // form S / D of this chunk's stages as they land (the MMA issuer
+            // waits on conv); the chunk's drain follows below
+            const int kb1 = min(nk, (c + 1) * kcb);
+            for (int kb = c * kcb; kb < kb1; ++kb) {
+              ptx::mbar_wait(&full[cst], cph, tflag);
+              gauss_convert_stage<G>(smem + cst * G::STAGE_BYTES, ct);
+              ptx::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) {
+                if (CG == 2) ptx::mbar_arrive_rank0_cluster(&conv[cst]);
+                else ptx::mbar_arrive(&conv[cst]);
+              }
+              if (++cst == G::STAGES) {
+                cst = 0;
+                cph ^= 1u;
+              }
+            }
+          }
           ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
           ptx::tc_fence_after();
           const uint32_t ta = tmem + lane_base + (uint32_t)buf * G::BUF + (uint32_t)(h * H);
@@ -598,12 +709,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-template <int CG, bool GS>
+template <int CG, bool GS, bool CV = false>
 cudaError_t launch_cg(const void* tmapA, const void* tmapB, const void* tmapB2, const GramParams& p, int groups,
                       cudaStream_t st) {
   using G = Geo<CG, GS>;
   cudaError_t e =
-      cudaFuncSetAttribute(gram_split_kernel<CG, GS>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
+      cudaFuncSetAttribute(gram_split_kernel<CG, GS, CV>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   if (p.n_items <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
@@ -618,12 +729,20 @@ cudaError_t launch_cg(const void* tmapA, const void* tmapB, const void* tmapB2, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gram_split_kernel<CG, GS>, *static_cast<const CUtensorMap*>(tmapA),
+  return cudaLaunchKernelEx(&cfg, gram_split_kernel<CG, GS, CV>, *static_cast<const CUtensorMap*>(tmapA),
                             *static_cast<const CUtensorMap*>(tmapB),
                             *static_cast<const CUtensorMap*>(tmapB2 ? tmapB2 : tmapB), p);
 }
 
 }  // namespace
+
+bool gauss_smem_convert() {
+  static const bool cv = [] {
+    const char* s = std::getenv("PS_GAUSS_CONV");
+    return s && std::atoi(s) != 0;
+  }();
+  return cv;
+}
 
 int split_cta_group() {
   static const int cg = [] {
@@ -641,6 +760,9 @@ int split_epi_arrivals() { return NEPI_WARPS * split_cta_group(); }
 
 cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const void* tmapB2, bool gauss,
                               const GramParams& p, int groups, cudaStream_t st) {
+  if (gauss && gauss_smem_convert())
+    return split_cta_group() == 2 ? launch_cg<2, true, true>(tmapA, tmapB, nullptr, p, groups, st)
+                                  : launch_cg<1, true, true>(tmapA, tmapB, nullptr, p, groups, st);
   if (gauss)
     return split_cta_group() == 2 ? launch_cg<2, true>(tmapA, tmapB, tmapB2, p, groups, st)
                                   : launch_cg<1, true>(tmapA, tmapB, tmapB2, p, groups, st);

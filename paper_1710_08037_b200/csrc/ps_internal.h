@@ -187,6 +187,11 @@ int split_cta_group();
 int split_panel_rows();   // rows of one execution panel (= UMMA M)
 int split_b_box_rows();   // J-panel rows staged per CTA
 int split_epi_arrivals(); // epilogue warps per CTA group (arrivals per item on GramParams::sb_cnt)
+// Gauss Gram operand feed: false (default) = TMA streams the precomputed
+// S / D planes 4..7 too; true (PS_GAUSS_CONV=1, experiment, slower) = TMA
+// streams the 4 split planes {Zr, Zi} hi / lo and the epilogue warps form
+// S / D in shared memory
+bool gauss_smem_convert();
 
 // tile geometry of the two Gram kernels (ownership / sharding granularity)
 constexpr int kSplitBM = 256;

@@ -89,6 +89,32 @@ constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 __device__ __forceinline__ void mbar_arrive_rank0(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerBitMask) : "memory");
 }
+// cluster-scope release arrive on rank 0's copy of `bar` (own CTA's when rank 0)
+__device__ __forceinline__ void mbar_arrive_rank0_cluster(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & kPeerBitMask)
+               : "memory");
+}
+// bounded cluster-scope acquire wait (arrivals from the peer CTA's threads)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  const long long t0 = clock64();
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 16000000000LL) asm volatile("trap;");
+  }
+}
+// generic-proxy smem writes -> visible to the async proxy (tcgen05.mma operands)
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
 // 2-CTA TMA: data lands in this CTA's smem, transaction bytes are counted on
 // rank 0's mbarrier.
 __device__ __forceinline__ void tma_load_4d_cg2(void* smem_dst, const void* tmap, uint64_t* bar, int c0, int c1,
