@@ -9,9 +9,14 @@ A step = one pass of the hot path over one batch of the synthetic workload
 real configs) -> upper-triangle Gram + fused PLV/iPLV/ciPLV epilogue, all
 three metrics written to HBM.  Default workload = config C5 (20k signals,
 BASELINE.json configs[4]): the config the metric's 1->8 GPU scaling target is
-quoted on; it fits one B200.  Multi-GPU (torchrun, one rank per GPU): input on
-rank 0, NCCL broadcast over NVLink inside the timed region, output tiles
-sharded across ranks (strong scaling, no gather).
+quoted on; it fits one B200.  Multi-GPU (one rank per GPU over NCCL; with
+--gpus N and no torchrun environment the script re-launches itself under
+torch.distributed.run): single-trial configs keep the input on rank 0 and
+broadcast it over NVLink inside the timed region, output tiles sharded across
+ranks (no gather); multi-trial configs (C2, C4) pre-place each rank's
+contiguous chunk of (band, trial) units and combine the per-rank trial sums
+with a fixed-order reduce-scatter (all-to-all + ordered sum) inside the timed
+region.
 
 Rank 0 prints ONE JSON line.  `--impl reference` times the reference's CPU
 algorithm (the NumPy restatement in oracle/, all host cores) on a bounded
@@ -37,7 +42,79 @@ from paper_1710_08037_b200 import workloads as W  # noqa: E402
 METRIC = "pair·samples/s for PLV+iPLV+ciPLV at 1/2/4/8 GPU; % tensor/HBM roofline"
 UNIT = "pair·samples/s"
 FLOPS_PER_PAIR_SAMPLE = 8  # complex MAC
-FP64_DGEMM_TFLOPS = 35.5   # FP64 roofline for --precision fp64 (tools/fp64_peak.py, K6)
+FP64_DGEMM_TFLOPS_FALLBACK = 35.5  # only if the live DGEMM probe fails (tools/fp64_peak.py, K6)
+
+
+def fp64_peak_tflops(dev):
+    """FP64 roofline measured live on this GPU (MEASURED_PEAKS.json has no
+    FP64 entry): best of 5 cuBLAS DGEMMs 8192^3 (2 N^3 flop), CUDA events."""
+    import torch
+
+    try:
+        n = 8192
+        a = torch.randn(n, n, dtype=torch.float64, device=dev)
+        b = torch.randn(n, n, dtype=torch.float64, device=dev)
+        torch.matmul(a, b)
+        torch.cuda.synchronize(dev)
+        best = None
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del a, b
+        return 2.0 * n ** 3 / (best / 1e3) / 1e12, "measured live: cuBLAS DGEMM 8192^3, best of 5 (this run)"
+    except Exception as exc:  # pragma: no cover - device dependent
+        return FP64_DGEMM_TFLOPS_FALLBACK, f"fallback {FP64_DGEMM_TFLOPS_FALLBACK} (probe failed: {exc})"
+
+
+def relaunch_under_torchrun(n: int) -> None:
+    """`bench.py --gpus N` without a torchrun environment: re-exec under
+    torch.distributed.run with N local ranks (one per GPU), 127.0.0.1
+    rendezvous and NCCL's communicator-init lines enabled.  Fails loudly when
+    fewer than N GPUs are visible (never silently runs fewer ranks)."""
+    import socket
+
+    if "--launch-selftest" not in sys.argv:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < n:
+            print(json.dumps({"error": f"--gpus {n} requested but only {have} CUDA device(s) are visible"}),
+                  flush=True)
+            sys.exit(3)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    argv = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execvpe(sys.executable, argv, env)
+
+
+def launch_selftest(args):
+    """CPU check of the launcher (gloo): every rank reports the world size it
+    sees; rank 0 prints the line a GPU run would carry n_gpus in."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.ones(1)
+    if world > 1:
+        dist.all_reduce(t)
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps({"launch_selftest": True, "n_gpus": world, "gpus_requested": args.gpus,
+                          "ranks_seen": int(t.item()), "nccl_debug": os.environ.get("NCCL_DEBUG")}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def finite(obj):
@@ -161,8 +238,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stage-bcast", dest="stage_bcast", action="store_false",
                     help="N>1: broadcast the whole input before computing instead of overlapping row chunks")
+    ap.add_argument("--launch-selftest", action="store_true", help="CPU/gloo check of the --gpus N launcher")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)  # does not return
+    if args.launch_selftest:
+        launch_selftest(args)
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -175,13 +258,17 @@ def main():
            "output_layout": layout + (" (i <= j of each [N][N] matrix, BASELINE configs[4])" if layout == "upper"
                                       else " (both triangles)"),
            "l2": "inputs larger than L2 (126 MB) every step",
-           "parallelism": f"output-tile shards x{world}" + (
-               (" + chunked NCCL broadcast of the input from rank 0, overlapped with compute" if R == 1 and B == 1
-                else " ((band, trial) units pre-placed on every rank)") if world > 1 else "")}
+           "parallelism": (f"output-tile shards x{world} + chunked NCCL broadcast of the input from rank 0, "
+                           "overlapped with compute" if R == 1 and B == 1 else
+                           f"(band, trial) unit shards x{world}: each rank holds and normalises only its "
+                           "contiguous chunk of units (pre-placed), per-rank trial sums, fixed-order "
+                           "reduce-scatter (NCCL all-to-all + ordered sum) of the trial mean, output rows "
+                           "sharded") if world > 1 else "single GPU"}
 
     if args.impl == "reference":
         if rank != 0:
             return
+        cfg["precision"] = "fp64 (the reference's CPU arithmetic: complex128 zgemm, SPEC.md:265)"
         os.environ.setdefault("OPENBLAS_NUM_THREADS", str(cores()))
         x = W.generate(args.config)
         if x.ndim == 4:
@@ -222,39 +309,59 @@ def main():
     # ---- workload: generated on the host (seeded), resident in HBM --------
     x_host = W.generate(args.config)
     if x_host.ndim == 3:
-        x_store = np.ascontiguousarray(np.transpose(x_host, (2, 0, 1)))        # [R, N, T]
+        x_store = np.ascontiguousarray(np.transpose(x_host, (2, 0, 1)))[None]  # [1, R, N, T]
     else:
         x_store = np.ascontiguousarray(np.transpose(x_host, (0, 3, 1, 2)))     # [B, R, N, T]
-    xd = torch.from_numpy(x_store).to(dev)
-    if world > 1 and rank != 0 and R == 1 and B == 1:
-        xd.zero_()  # single-trial configs: only rank 0 holds the input (broadcast in the timed region)
     bands = x_host.ndim == 4
-    xv = xd.permute(1, 2, 0) if not bands else xd.permute(0, 2, 3, 1)
-    shard = (rank, world)
     fp64 = args.precision == "fp64"
     odt = torch.float64 if fp64 else torch.float32
-    outs = {m: torch.zeros((B, N, N), dtype=odt, device=dev) for m in ("plv", "iplv", "ciplv")}
-    bcast_t = torch.view_as_real(xd) if xd.is_complex() else xd
+    metrics = ("plv", "iplv", "ciplv")
+    single = R == 1 and B == 1
+    units = world > 1 and not single  # (band, trial) unit sharding (C2, C4)
+    shard = (rank, world) if not units else (0, 1)
+
+    if units:
+        # each rank holds only its contiguous chunk of (band, trial) units,
+        # pre-placed on its GPU outside the timed region
+        frags_ix = sharding.unit_ranges(B, R, world, rank)
+        frags_dev = [(b, torch.from_numpy(np.ascontiguousarray(x_store[b, t0:t1])).to(dev).permute(1, 2, 0))
+                     for b, t0, t1 in frags_ix]
+        my_units = sum(t1 - t0 for _, t0, t1 in frags_ix)
+        parts = {m: torch.zeros((B, N, N), dtype=odt, device=dev) for m in metrics}
+        xd = None
+    else:
+        xd = torch.from_numpy(x_store).to(dev)                                  # [B, R, N, T]
+        if world > 1 and rank != 0:
+            xd.zero_()  # single-trial configs: only rank 0 holds the input (broadcast in the timed region)
+        xv = xd[0].permute(1, 2, 0) if not bands else xd.permute(0, 2, 3, 1)
+        outs = {m: torch.zeros((B, N, N), dtype=odt, device=dev) for m in metrics}
+        bcast_t = torch.view_as_real(xd) if xd.is_complex() else xd
 
     # N > 1, single-trial configs: the input lives on rank 0 and is broadcast
     # over NVLink in row chunks; each rank starts a chunk's normalisation and
     # the Gram tiles it unlocks as soon as it arrives (ps_plv_family_staged).
-    # Multi-trial configs: (band, trial) units are pre-placed on every rank
-    # and output tiles are sharded without a data exchange.
-    staged = world > 1 and R == 1 and B == 1 and args.stage_bcast
+    staged = world > 1 and single and args.stage_bcast
     cols = sharding.stage_cols(N, n_stages=8) if staged else None
     comm = torch.cuda.Stream() if staged else None
-    rows_view = bcast_t[0] if staged else None   # [N, T] (real) or [N, T, 2] (complex as float pairs)
+    rows_view = bcast_t[0, 0] if staged else None  # [N, T] (real) or [N, T, 2] (complex as float pairs)
 
     def step(timing=False):
+        """One pass of the hot path; returns (metas of the library calls)."""
+        if units:
+            _, metas = sharding.unit_partial_sums(frags_dev, B, N, input_kind=kind, precision=args.precision,
+                                                  metrics=metrics, layout=layout, out=parts, timing=timing)
+            sharding.reduce_trial_partials(parts, R)  # the exchange step: trial mean of this rank's row slice
+            return metas
         if staged:
             events = sharding.broadcast_input_staged(rows_view, cols, src=0, stream=comm)
-            return C.plv_family(xv, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
-                                out=outs, timing=timing, stages=(cols, events), layout=layout)
-        if world > 1 and R == 1 and B == 1:
+            r = C.plv_family(xv, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
+                             out=outs, timing=timing, stages=(cols, events), layout=layout)
+            return [r["plv"].meta]
+        if world > 1:
             sharding.broadcast_input(bcast_t, src=0)
-        return C.plv_family(xv, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
-                            out=outs, timing=timing, layout=layout)
+        r = C.plv_family(xv, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
+                         out=outs, timing=timing, layout=layout)
+        return [r["plv"].meta]
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -273,10 +380,12 @@ def main():
     gram_ms, launches = [], 0
     e0.record(stream)
     for _ in range(args.steps):
-        r = step(timing=True)
-        info = r["plv"].meta
-        gram_ms.append(info["ms_gram"])
-        launches += int(info["n_kernel_launches"])
+        metas = step(timing=True)
+        gram_ms.append(sum(float(mt["ms_gram"]) for mt in metas))
+        launches += sum(int(mt["n_kernel_launches"]) for mt in metas)
+        if units:
+            launches += len(metrics)  # ps_reduce_partials: one ordered-sum kernel per metric
+    info = metas[0]
     variant = int(info.get("gram_variant", 0))
     e1.record(stream)
     torch.cuda.synchronize()
@@ -292,20 +401,29 @@ def main():
 
     # ---- roofline of the dominant kernel (Gram + fused epilogue) ----------
     pk = peaks()
-    my_tiles = sum(1 for t in range(_native.tile_count(N, args.precision)) if t % world == rank)
-    frac_tiles = my_tiles / max(1, _native.tile_count(N, args.precision))
+    if units:
+        my_frac = my_units / (B * R)
+    else:
+        my_tiles = sum(1 for t in range(_native.tile_count(N, args.precision)) if t % world == rank)
+        my_frac = my_tiles / max(1, _native.tile_count(N, args.precision))
     gram_avg = float(np.mean(gram_ms)) if gram_ms else 0.0
-    algo_flops = FLOPS_PER_PAIR_SAMPLE * work * frac_tiles
+    algo_flops = FLOPS_PER_PAIR_SAMPLE * work * my_frac
     # (the library reports the Gram's CUDA-event time; without it, fall back
     # to the whole step so the JSON never carries inf / nan)
     if not gram_avg > 0.0:
         gram_avg = ms_step
     achieved = algo_flops / (gram_avg / 1e3) / 1e12
-    # tensor ceiling of the arithmetic actually run: 8 algorithmic flop per
-    # pair-sample against 24 fp16 tensor flop (3 passes x 4 real products) or
-    # 18 (3 passes x 3 products, Gauss form)
+    # SURVEY 8(d) denominator: bf16 burst peak / 3 split passes, i.e. 8
+    # algorithmic flop per pair-sample against 24 fp16 tensor flop (the
+    # 4-product split).  The Gauss form runs 18 tensor flop per pair-sample;
+    # its own (stricter) ceiling is reported as frac_of_variant_ceiling.
     hw_flops = 18.0 if variant == 1 else 24.0
-    peak = pk["bf16_tflops"] * FLOPS_PER_PAIR_SAMPLE / hw_flops if not fp64 else FP64_DGEMM_TFLOPS
+    if fp64:
+        peak, fp64_basis = fp64_peak_tflops(dev)
+        variant_peak = peak
+    else:
+        peak = pk["bf16_tflops"] * FLOPS_PER_PAIR_SAMPLE / 24.0
+        variant_peak = pk["bf16_tflops"] * FLOPS_PER_PAIR_SAMPLE / hw_flops
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gram_traffic.json")
     if os.path.exists(tpath):
@@ -325,51 +443,69 @@ def main():
                                  1: "split fp16x3, Gauss 3-product form (9 UMMA / K step)",
                                  2: "fp64 DMMA"}.get(variant, str(variant)),
                 "fp16_tensor_tflops_executed": achieved * hw_flops / FLOPS_PER_PAIR_SAMPLE if not fp64 else None,
-                "peak_basis": (f"bf16_tflops {pk['bf16_tflops']} ({pk['source']}, burst) x 8 algorithmic / "
-                               f"{hw_flops:g} fp16 tensor flop per pair-sample = algorithmic ceiling of the "
-                               "arithmetic run") if not fp64 else
-                f"cuBLAS DGEMM 8192^3 measured on a pool B200: {FP64_DGEMM_TFLOPS} TFLOP/s (tools/fp64_peak.py)",
-                "frac_of_bf16_peak": achieved / pk["bf16_tflops"]}
+                "peak_basis": (f"SURVEY 8(d): bf16_tflops {pk['bf16_tflops']} ({pk['source']}, burst) / 3 split "
+                               "passes (8 algorithmic / 24 fp16 tensor flop per pair-sample)") if not fp64 else
+                fp64_basis,
+                "variant_ceiling": variant_peak, "frac_of_variant_ceiling": achieved / variant_peak,
+                "frac_of_bf16_peak": achieved / pk["bf16_tflops"] if not fp64 else None}
 
     # ---- end to end through the public host API ----------------------------
     e2e = None
     if not args.no_e2e:
-        xin = torch.empty(x_store.shape, dtype=torch.from_numpy(x_store[:1]).dtype, pin_memory=True)
-        xin.numpy()[...] = x_store
-        xin_np = xin.numpy()
-        xin_view = np.transpose(xin_np, (1, 2, 0)) if not bands else np.transpose(xin_np, (0, 2, 3, 1))
-        hout = {m: torch.zeros((B, N, N), dtype=odt, pin_memory=True).numpy() for m in ("plv", "iplv", "ciplv")}
-        gathered = world > 1 and R == 1 and B == 1
-        if gathered:
-            # N > 1, single trial: each rank copies in only its own row slice
-            # (its own host link) and one NCCL all-gather over NVLink assembles
-            # the input; each rank then computes and copies out its row bands
+        hout = {m: torch.zeros((B, N, N), dtype=odt, pin_memory=True).numpy() for m in metrics}
+        if units:
+            # each rank copies only its units from pinned host memory over its
+            # own link, computes its trial sums, joins the fixed-order
+            # reduce-scatter and copies its rows of the trial mean back
+            frag_host = [(b, torch.from_numpy(np.ascontiguousarray(x_store[b, t0:t1])).pin_memory())
+                         for b, t0, t1 in frags_ix]
+            in_bytes = sum(h.numel() * h.element_size() for _, h in frag_host)
+            F = B * N
+            r0, r1 = sharding.row_slice(F, rank, world)
+            row_host = {m: torch.zeros((r1 - r0, N), dtype=odt, pin_memory=True) for m in metrics}
+            out_bytes = sum(v.numel() * v.element_size() for v in row_host.values())
+        elif world > 1:
+            # single trial: each rank copies in only its own row slice (its own
+            # host link) and one NCCL all-gather over NVLink assembles the
+            # input; each rank then computes and copies out its row bands
             # (ps_plv_family_to_host, streamed)
             r0, r1 = sharding.row_slice(N, rank, world)
-            loc = torch.from_numpy(np.ascontiguousarray(x_store[0, r0:r1])).pin_memory()
+            loc = torch.from_numpy(np.ascontiguousarray(x_store[0, 0, r0:r1])).pin_memory()
             loc_rows = torch.view_as_real(loc) if loc.is_complex() else loc
             in_bytes = loc.numel() * loc.element_size()
+        else:
+            xin = torch.empty(x_store.shape, dtype=torch.from_numpy(x_store[:1, :1, :1, :1]).dtype, pin_memory=True)
+            xin.numpy()[...] = x_store
+            xin_np = xin.numpy()
+            xin_view = np.transpose(xin_np[0], (1, 2, 0)) if not bands else np.transpose(xin_np, (0, 2, 3, 1))
 
         def e2e_step():
-            if gathered:
+            if units:
+                fr = [(b, h.to(dev, non_blocking=True).permute(1, 2, 0)) for b, h in frag_host]
+                _, metas_e = sharding.unit_partial_sums(fr, B, N, input_kind=kind, precision=args.precision,
+                                                        metrics=metrics, layout=layout, out=parts)
+                red = sharding.reduce_trial_partials(parts, R)
+                for m in metrics:
+                    row_host[m].copy_(red[m][0], non_blocking=True)
+                torch.cuda.synchronize()
+                return dict(metas_e[0], h2d_bytes=in_bytes, d2h_bytes=out_bytes)
+            if world > 1:
                 xg = sharding.all_gather_rows(loc_rows, N)
                 xg = torch.view_as_complex(xg) if loc.is_complex() else xg
-                return C.plv_family(xg, input_kind=kind, precision=args.precision, shard=shard, out=hout,
-                                    layout=layout)
-            return C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
-                                out=hout, layout=layout)
+                r = C.plv_family(xg, input_kind=kind, precision=args.precision, shard=shard, out=hout,
+                                 layout=layout)
+                return dict(next(iter(r.values())).meta, h2d_bytes=in_bytes)
+            r = C.plv_family(xin_view, input_kind=kind, precision=args.precision, bands=bands, shard=shard,
+                             out=hout, layout=layout)
+            return dict(next(iter(r.values())).meta)
 
-        for _ in range(1):
-            e2e_step()
+        e2e_step()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            r_e = e2e_step()
+            meta_e = e2e_step()
         dt_e = (time.perf_counter() - t0) / args.steps
-        meta_e = dict(next(iter(r_e.values())).meta)
-        if gathered:
-            meta_e["h2d_bytes"] = in_bytes
         if world > 1:
             t = torch.tensor([dt_e], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -379,15 +515,19 @@ def main():
                               device=dev, dtype=torch.float64)
             dist.all_reduce(nb, op=dist.ReduceOp.SUM)
             meta_e["h2d_bytes"], meta_e["d2h_bytes"] = int(nb[0].item()), int(nb[1].item())
-        # bytes the library actually moved over the host link (the pipelined
-        # path ships one triangle's column blocks and mirrors on the host)
+        # bytes the library actually moved over the host link
         e2e = {"value": work / dt_e, "unit": UNIT,
                "h2d_bytes_per_step": int(meta_e.get("h2d_bytes") or x_store.nbytes),
                "d2h_bytes_per_step": int(meta_e.get("d2h_bytes") or sum(v.nbytes for v in hout.values())),
                "output_bytes_per_step": int(sum(v.nbytes for v in hout.values())),
                "ms_per_step": dt_e * 1e3,
-               "api": ("per-rank row slice (pinned) -> NCCL all-gather -> connectivity.plv_family(cuda input, numpy "
-                       "pinned outputs) -> ps_plv_family_to_host (C ABI), each rank its row bands") if gathered else
+               "api": ("per-rank (band, trial) units (pinned) -> H2D -> sharding.unit_partial_sums "
+                       "(connectivity.plv_family trial_reduce='sum' -> ps_plv_family) -> "
+                       "sharding.reduce_trial_partials (NCCL all-to-all + ps_reduce_partials) -> D2H of the "
+                       "rank's rows of the trial mean") if units else
+                      ("per-rank row slice (pinned) -> NCCL all-gather -> connectivity.plv_family(cuda input, "
+                       "numpy pinned outputs) -> ps_plv_family_to_host (C ABI), each rank its row bands")
+                      if world > 1 else
                       "paper_1710_08037_b200.connectivity.plv_family(numpy pinned) -> ps_plv_family_host (C ABI)"}
 
     # ---- CPU baseline (rank 0, N=1 only) -----------------------------------

@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define PS_ABI_VERSION 7
+#define PS_ABI_VERSION 8
 
 typedef enum ps_status {
   PS_OK = 0,
@@ -61,7 +61,10 @@ typedef enum ps_precision {
 typedef enum ps_trial_reduce {
   PS_TRIALS_MEAN = 0,  /* mean over trials of per-trial metrics (default) */
   PS_TRIALS_NONE = 1,  /* one matrix per trial (PAPER.md:281-287 plv(:,:,t))        */
-  PS_TRIALS_POOL = 2   /* one Gram over all R*T observations                         */
+  PS_TRIALS_POOL = 2,  /* one Gram over all R*T observations                         */
+  PS_TRIALS_SUM = 3    /* sum over trials of per-trial metrics (ABI v8): the partial sums
+                          of a (band, trial)-sharded call, combined across ranks by
+                          ps_reduce_partials, which divides by the global trial count */
 } ps_trial_reduce;
 
 enum {
@@ -112,8 +115,13 @@ typedef struct ps_plv_args {
   void* out_cre;
   void* out_cim;
   /* Output-tile sharding across devices: this call computes
-   * only tiles t with t % shard_count == shard_index; other entries of the
-   * outputs are left untouched.  shard_count = 1 computes everything. */
+   * only tiles t with t % shard_count == shard_index; other entries of DEVICE
+   * outputs are left untouched.  The host-output entry points stage the
+   * outputs in device memory and copy whole matrices back, so there the
+   * entries owned by other shards are written as 0 (the shards' host
+   * matrices sum to the full result); with PS_LAYOUT_UPPER on the streamed
+   * host path a shard owns whole row bands and writes only those rows.
+   * shard_count = 1 computes everything. */
   int32_t shard_index;
   int32_t shard_count;
   void* stream;                /* cudaStream_t (NULL = legacy default stream) */
@@ -159,7 +167,12 @@ typedef struct ps_plv_result {
    * products (12 UMMAs per K step); 1 = split fp16 x 3, three-product Gauss
    * form (9 UMMAs); 2 = FP64 DMMA. */
   int32_t gram_variant;
-  int32_t reserved;
+  /* Split path (ABI v8): off-diagonal pairs whose |Re| rounds to 1 in fp32
+   * while |Im| > 4e-6 -- the ciPLV denominator 1 - Re^2 is below the split
+   * arithmetic's resolution there, so ciPLV (reported as 0) is indeterminate
+   * and the caller should use PS_PREC_FP64 for them (SPEC.md:259 singularity
+   * rule applies to |Re| >= 1 - 1e-12 only).  0 in FP64 mode. */
+  int32_t n_indeterminate_ciplv;
 } ps_plv_result;
 
 /* ABI version check (PS_ABI_VERSION). */
@@ -253,6 +266,32 @@ int64_t ps_welch_bins(int64_t window_len, double band_low, double band_high, int
  * the input precision, dense [n_bands][n_trials][n_signals][n_samples];
  * mask_out (optional, uint8, same dense layout) gets 1 where masked. */
 ps_status ps_normalize_phasors(ps_ctx* ctx, const ps_plv_args* args, void* out, uint8_t* mask_out);
+
+/* Combines the partial metric sums of a (band, trial)-sharded computation
+ * (PS_TRIALS_SUM) in a FIXED order ("deterministic tree order"):
+ *   out[e] = (parts[0][e] + parts[1][e] + ... + parts[n_parts-1][e]) / divisor
+ * summed left to right, part p at parts + p * part_stride elements; n elements.
+ * dtype PS_F32 or PS_F64; device pointers; out may not alias parts.  Used
+ * after an all-to-all that gives every rank the P partials of its output row
+ * slice (paper_1710_08037_b200/sharding.py reduce_trial_partials). */
+ps_status ps_reduce_partials(ps_ctx* ctx, const void* parts, int32_t n_parts, int64_t part_stride, int64_t n,
+                             double divisor, int32_t dtype, void* out, void* stream);
+
+/* Output-tile gather (SURVEY 8(e) "gathering the output only if the caller
+ * asks"): ps_shard_pack copies the upper-triangle tiles shard `shard_index` of
+ * `shard_count` owns (the rule of ps_pair_shard) out of a [N][N] matrix into
+ * a dense buffer of ps_shard_tiles() tiles x tile_rows x tile_cols elements
+ * (tile order = the library's enumeration); ps_shard_unpack writes the owned
+ * entries (i <= j) of such a buffer, received from shard `shard_index`, into a
+ * [N][N] matrix, plus the mirror (j, i) when `mirror` is 1 (negated when
+ * `mirror` is -1, the antisymmetric signed imaginary part).  dtype PS_F32 (split
+ * outputs) or PS_F64 (fp64 outputs); device pointers. */
+int64_t ps_shard_tiles(int64_t n_signals, int32_t precision, int32_t shard_count, int32_t shard_index,
+                       int32_t* tile_rows, int32_t* tile_cols);
+ps_status ps_shard_pack(ps_ctx* ctx, int64_t n_signals, int32_t precision, int32_t shard_count, int32_t shard_index,
+                        const void* matrix, void* packed, void* stream);
+ps_status ps_shard_unpack(ps_ctx* ctx, int64_t n_signals, int32_t precision, int32_t shard_count,
+                          int32_t shard_index, const void* packed, void* matrix, int32_t mirror, void* stream);
 
 /* Host-only helpers (no GPU needed): the output-tile sharding rule of
  * ps_plv_args.shard_index / shard_count.  ps_tile_count returns the number of

@@ -465,6 +465,72 @@ def plv_family(x, input_kind: str = "real", amp_floor: float = DEFAULT_AMP_FLOOR
     return plv_family_from_phasors(z, mask, trial_reduce, raw=raw)
 
 
+def _metrics_from_block(G: np.ndarray, C: np.ndarray, rows: np.ndarray, c0: int):
+    """_metrics_from_gram for the block rows x cols [c0, c0 + G.shape[1]):
+    same epilogue, diagonal rules where the
+    global column equals the row."""
+    if np.any(C <= 0):
+        raise EmptyEffectiveWindowError("all samples masked for some pair")
+    re = G.real / C
+    im = G.imag / C
+    plv = np.abs(G) / C
+    iplv = np.abs(im)
+    den = 1.0 - re * re
+    sing = np.abs(re) >= 1.0 - CIPLV_SINGULAR_EPS
+    ciplv = np.where(sing, 0.0, np.abs(im) / np.sqrt(np.where(sing, 1.0, den)))
+    r = np.nonzero((rows >= c0) & (rows < c0 + G.shape[1]))[0]
+    plv[r, rows[r] - c0] = 1.0
+    iplv[r, rows[r] - c0] = 0.0
+    ciplv[r, rows[r] - c0] = 0.0
+    return plv, iplv, ciplv
+
+
+def plv_family_rows(x, rows, input_kind: str = "real", amp_floor: float = DEFAULT_AMP_FLOOR,
+                    trial_reduce: str = "mean", col_block: int | None = None):
+    """Rows ``rows`` (all columns) of the plv_family matrices -- the oracle at
+    full config size for a row subset: every signal is normalised (row-local
+    work: analytic signal, median floor) in column blocks of
+    ``col_block`` signals, and G[rows, block] = z_rows z_block^H per trial in
+    complex128 (SPEC.md:265, PAPER.md:286).  x: [N, T, R].  trial_reduce
+    'mean' (default) or 'none' ([len(rows), N, R]).  Returns dict of
+    [len(rows), N] float64 arrays."""
+    x = np.asarray(x)
+    if x.ndim == 2:
+        x = x[:, :, None]
+    N, T, R = x.shape
+    rows = np.asarray(rows, dtype=np.int64)
+    if col_block is None:  # ~1 GB of complex128 phasors per column block
+        col_block = max(64, (1 << 26) // (T * R))
+
+    def prep(sel):
+        xs = x[sel]
+        if input_kind == "real":
+            return normalize_phasors(analytic_signal(xs), amp_floor)
+        if input_kind == "analytic":
+            return normalize_phasors(xs, amp_floor)
+        return phasors_from_unit(xs)
+
+    zr, mr = prep(rows)
+    acc = {k: np.zeros((len(rows), N, R if trial_reduce == "none" else 1)) for k in ("plv", "iplv", "ciplv")}
+    for c0 in range(0, N, col_block):
+        c1 = min(N, c0 + col_block)
+        zc, mc = prep(slice(c0, c1))
+        for t in range(R):
+            G = np.ascontiguousarray(zr[:, :, t]) @ np.ascontiguousarray(zc[:, :, t]).conj().T
+            if np.any(mr[:, :, t]) or np.any(mc[:, :, t]):
+                C = (~mr[:, :, t]).astype(np.float64) @ (~mc[:, :, t]).astype(np.float64).T
+            else:
+                C = np.full(G.shape, float(T))
+            p, i, c = _metrics_from_block(G, C, rows, c0)
+            k = t if trial_reduce == "none" else 0
+            acc["plv"][:, c0:c1, k] += p
+            acc["iplv"][:, c0:c1, k] += i
+            acc["ciplv"][:, c0:c1, k] += c
+    if trial_reduce == "none":
+        return acc
+    return {k: v[:, :, 0] / R for k, v in acc.items()}
+
+
 def plv_matrix(phasors, mode: str = "over_samples", trial_reduce: str = "mean"):
     """(1/T)|z_i . z_j^H| via one complex product per trial
     (mode 'over_samples', Eq 7) or per sample over trials (mode 'over_trials',

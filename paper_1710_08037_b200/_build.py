@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libphasesync_cuda.so"
-SOURCES = ["capi.cu", "prep_kernels.cu", "gram_tc.cu", "gram_f64.cu", "refine.cu"]
+SOURCES = ["capi.cu", "prep_kernels.cu", "gram_tc.cu", "gram_f64.cu", "refine.cu", "shard_kernels.cu"]
 HEADERS = ["ps_internal.h", "ptx.cuh", "epilogue.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -20,7 +20,7 @@ from . import errors
 LIB_PATH = Path(__file__).resolve().parent / "libphasesync_cuda.so"
 if os.environ.get("PS_LIB_VARIANT"):  # A/B experiments: libphasesync_cuda.<variant>.so next to the default
     LIB_PATH = LIB_PATH.with_name(f"libphasesync_cuda.{os.environ['PS_LIB_VARIANT']}.so")
-ABI_VERSION = 7
+ABI_VERSION = 8
 LAYOUTS = {"full": 0, "upper": 1}
 
 # ps_status -> exception class (include/phasesync.h)
@@ -43,7 +43,7 @@ STATUS_EXC = {
 DTYPES = {"f32": 0, "f64": 1, "c64": 2, "c128": 3}
 INPUT_KINDS = {"real": 0, "analytic": 1, "phasor": 2}
 PRECISIONS = {"split": 0, "f16x3": 0, "fp64": 1}
-TRIAL_REDUCE = {"mean": 0, "none": 1, "pool": 2}
+TRIAL_REDUCE = {"mean": 0, "none": 1, "pool": 2, "sum": 3}
 METRIC_BITS = {"plv": 1, "iplv": 2, "ciplv": 4, "cre": 8, "cim": 16}
 METRIC_ORDER = ("plv", "iplv", "ciplv", "cre", "cim")
 
@@ -120,7 +120,7 @@ class PlvResult(ctypes.Structure):
         ("h2d_bytes", ctypes.c_int64),
         ("d2h_bytes", ctypes.c_int64),
         ("gram_variant", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("n_indeterminate_ciplv", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:
@@ -150,6 +150,14 @@ _SIGNATURES = {
     "ps_pair_shard": ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64],
                       ctypes.c_int32),
     "ps_tile_count": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_int64),
+    "ps_reduce_partials": ([ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
+                            ctypes.c_double, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "ps_shard_tiles": ([ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                        ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)], ctypes.c_int64),
+    "ps_shard_pack": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p], ctypes.c_int),
+    "ps_shard_unpack": ([ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_void_p], ctypes.c_int),
 }
 
 _lib = None
@@ -246,3 +254,12 @@ def pair_shard(n_signals: int, precision: str, shard_count: int, i: int, j: int)
 
 def tile_count(n_signals: int, precision: str) -> int:
     return int(lib().ps_tile_count(n_signals, PRECISIONS[precision]))
+
+
+def shard_tiles(n_signals: int, precision: str, shard_count: int, shard_index: int) -> tuple:
+    """(number of tiles shard `shard_index` owns, tile rows, tile cols) -- the
+    packed-buffer geometry of ps_shard_pack (host logic, CPU-callable)."""
+    r, c = ctypes.c_int32(), ctypes.c_int32()
+    n = lib().ps_shard_tiles(n_signals, PRECISIONS[precision], shard_count, shard_index, ctypes.byref(r),
+                             ctypes.byref(c))
+    return int(n), int(r.value), int(c.value)

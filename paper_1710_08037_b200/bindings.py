@@ -2,6 +2,7 @@
 
   py_analytic_signal(real array) -> complex array
   py_plv / py_iplv / py_ciplv(arrays, config) -> matrix SPEC.md:538-544
+  py_coherence(arrays, config) -> matrix / spectra     SPEC.md:538-544 (Eq 12)
 
 No numerical logic lives here: every call delegates to the same
 core functions (connectivity / signalprep), so binding and core agree
@@ -60,3 +61,35 @@ def py_plv_family(arrays, config=None, metrics=("plv", "iplv", "ciplv")):
                                   amp_floor=cfg["amp_floor"], trial_reduce=cfg["trial_reduce"],
                                   precision=cfg["precision"])
     return {m: r.values for m, r in res.items()}
+
+
+_COH_DEFAULTS = {"window_len": 400, "overlap": 200, "band": None, "mode": "max", "metric": "coh",
+                 "precision": "split"}
+
+
+def py_coherence(arrays, config=None):
+    """SPEC.md:538-544 (Eq 12): Welch coherence for all
+    pairs, delegating to connectivity.coherence_matrix.  config keys:
+    window_len / overlap (WelchConfig; defaults 400 / 200 as
+    in Fig 2), band = (low, high) in radians per sample, mode 'max' / 'mean'
+    (band_coherence) -> [N, N]; band None -> the per-bin
+    spectra over [0, pi] -> [N, N, n_bins] (coherence_welch, SPEC.md:213-220);
+    metric 'coh' (|C|) or 'icoh' (imaginary coherency, SPEC.md:240-246);
+    precision 'split' / 'fp64'.  Same arguments as `phasesync connectivity
+    --metric coh_max|coh_mean`, so the two agree bit-exactly."""
+    import numpy as np
+
+    cfg = dict(_COH_DEFAULTS)
+    if config:
+        unknown = set(config) - set(_COH_DEFAULTS)
+        if unknown:
+            raise ValueError(f"unknown config keys {sorted(unknown)}; allowed {sorted(_COH_DEFAULTS)}")
+        cfg.update(config)
+    wc = connectivity.WelchConfig(int(cfg["window_len"]), int(cfg["overlap"]))
+    if cfg["band"] is None:
+        band, mode = (0.0, float(np.pi)), "none"
+    else:
+        band, mode = tuple(cfg["band"]), cfg["mode"]
+    res = connectivity.coherence_matrix(arrays, wc, band, mode=mode, metrics=(cfg["metric"],),
+                                        precision=cfg["precision"])
+    return res[cfg["metric"]].values

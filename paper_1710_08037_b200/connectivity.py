@@ -64,8 +64,10 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
        'phasor' (unit phasors, zeros = masked); default from the dtype.
     precision: 'split' (tcgen05 fp16x3, fp32 outputs, |err| <= 1e-5) or 'fp64'
        (DMMA, fp64 outputs, |err| <= 1e-12).
-    trial_reduce: 'mean' (mean of per-trial metrics), 'none' (per trial), or
-       'pool' (one Gram over all R*T observations).  SURVEY D1.
+    trial_reduce: 'mean' (mean of per-trial metrics), 'none' (per trial),
+       'pool' (one Gram over all R*T observations) -- SURVEY D1 -- or 'sum'
+       (sum of per-trial metrics: the partial sums of a (band, trial)-sharded
+       call, combined by sharding.reduce_trial_partials).
     shard: (index, count) output-tile sharding; entries owned by
        other shards are left as allocated (zeros when ``out`` is None).
     out: optional preallocated outputs {metric: array} (same kind as x; numpy
@@ -202,6 +204,12 @@ def plv_family(x, *, input_kind: str | None = None, metrics: Iterable[str] = ("p
         res = _native.PlvResult()
         _native.check(_native.lib().ps_plv_family_host(ctx.handle, ctypes.byref(a), ctypes.byref(res)))
     info = res.as_dict()
+    if info.get("n_indeterminate_ciplv") and "ciplv" in metrics:
+        import warnings
+
+        warnings.warn(f"{info['n_indeterminate_ciplv']} ciPLV pair(s) have |Re| within fp32 resolution of 1 and "
+                      "|Im| > 4e-6: their ciPLV is indeterminate in split precision (reported 0); use "
+                      "precision='fp64' for them (SPEC.md:259)", errors.CiplvIndeterminateWarning, stacklevel=2)
     info["input_copied"] = bool(info["input_copied"]) or d.copied
     info["precision"] = precision
     info["trial_reduce"] = trial_reduce

@@ -92,6 +92,7 @@ struct ps_ctx {
   Buf lockbuf;             // Gram producer lockstep counters (one launch at a time per ctx)
   Buf hscale;              // per-row factors restoring H after scaled packing (odd T)
   Buf sortws;              // device-side ordering of the ciPLV refinement queue
+  Buf shardtiles;          // (I, J) of the tiles one shard owns (ps_shard_pack / unpack)
   std::vector<cudaEvent_t> tev;  // timing events of the staged path (2 per stage)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
@@ -179,7 +180,7 @@ ps_status validate(const ps_plv_args* a, Geometry& g) {
   if (a->input_kind < 0 || a->input_kind > 2) return fail(PS_E_INVALID, "unknown input_kind");
   if (a->precision != PS_PREC_SPLIT_F16X3 && a->precision != PS_PREC_FP64)
     return fail(PS_E_INVALID, "unknown precision");
-  if (a->trial_reduce < 0 || a->trial_reduce > 2) return fail(PS_E_INVALID, "unknown trial_reduce");
+  if (a->trial_reduce < 0 || a->trial_reduce > 3) return fail(PS_E_INVALID, "unknown trial_reduce");
   if (a->mode != PS_MODE_OVER_SAMPLES && a->mode != PS_MODE_OVER_TRIALS) return fail(PS_E_INVALID, "unknown mode");
   if (a->out_layout != PS_LAYOUT_FULL && a->out_layout != PS_LAYOUT_UPPER)
     return fail(PS_E_INVALID, "unknown out_layout");
@@ -630,6 +631,9 @@ struct Call {
   int shard_count = 1, shard_index = 0;
   bool pool = false;
   int G = 1, slot_mode = 1, mean_div = 1, Rg = 1;
+  // divisor of the trial-group reduction: R (trial mean) or 1 (PS_TRIALS_SUM)
+  int reduce_div = 1;
+  bool trial_sum = false;
   std::vector<int> stage_off;  // item offsets of the stages (size n_stages + 1)
   GramParams p;
   const CUtensorMap* ta = nullptr;
@@ -781,7 +785,9 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     }();
     if (g_env > 0 && k.shard_count == 1 && !force_g1) k.G = std::min<int>(g_env, (int)g.R);
     k.slot_mode = k.G == 1 ? 1 : 2;
-    k.mean_div = k.G == 1 ? (int)g.R : 1;
+    k.trial_sum = a->trial_reduce == PS_TRIALS_SUM;
+    k.mean_div = (k.G == 1 && !k.trial_sum) ? (int)g.R : 1;
+    k.reduce_div = k.trial_sum ? 1 : (int)g.R;
   }
   k.Rg = (int)((g.R + k.G - 1) / k.G);
   k.slots = (a->trial_reduce == PS_TRIALS_NONE && !k.pool) ? g.B * g.R : g.B;
@@ -843,7 +849,16 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   p.illcond_tol = 4e-6f;  // 2.5x margin below the 1e-5 split-path tolerance
   // the Gauss Gram drains a single accumulation buffer: longer chunks (its
   // error at 512 samples matches the 4-product Gram's at 128, accuracy probe)
-  p.kc_blocks = std::getenv("PS_KC_BLOCKS") || !g.gauss ? kc_blocks_default() : 16;
+  // PS_KC_BLOCKS (experiments) is capped at the longest chunk whose measured
+  // error stays inside the 1e-5 split budget (profiles/r01_accuracy_probe_kc,
+  // r02_accuracy_probe_gauss_kc: 4-product kc 4 = 128 samples, Gauss kc 16 =
+  // 512 samples); PS_KC_UNSAFE=1 lifts the cap for accuracy probes only
+  {
+    const int kc_max = g.gauss ? 16 : 4;
+    static const bool unsafe = std::getenv("PS_KC_UNSAFE") != nullptr;
+    const int want = std::getenv("PS_KC_BLOCKS") ? kc_blocks_default() : kc_max;
+    p.kc_blocks = unsafe ? want : std::min(want, kc_max);
+  }
   p.upper_only = a->out_layout == PS_LAYOUT_UPPER ? 1 : 0;
   static const int dbg = [] {
     const char* s = std::getenv("PS_DEBUG_EPI");
@@ -989,7 +1004,7 @@ ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long 
       pr.out_ciplv = k.outs[2];
       PS_CUDA(launch_refine_sorted(pr, static_cast<RefineEntry*>(c->refine.p) + lo, n, k.slot_mode == 2 ? k.G : 1, ib,
                                    c->sortws.p, c->sortws.n, d_ent, d_exact, d_grp, single_round ? 1 : 0,
-                                   (int)k.g.R, st));
+                                   k.trial_sum ? -(int)k.g.R : (int)k.g.R, st));
       c->launches += 8;
       PS_CUDA(cudaStreamSynchronize(st));
       return PS_OK;
@@ -1020,8 +1035,8 @@ ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long 
   PS_CUDA(cudaMemcpyAsync(d_grp, groups.data(), groups.size() * sizeof(int), cudaMemcpyHostToDevice, st));
   GramParams pr = k.p;
   pr.out_ciplv = k.outs[2];
-  PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, (int)ent.size(), d_exact, single_round ? 1 : 0, (int)k.g.R,
-                        st));
+  PS_CUDA(launch_refine(pr, d_ent, d_grp, n_groups, (int)ent.size(), d_exact, single_round ? 1 : 0,
+                        k.trial_sum ? -(int)k.g.R : (int)k.g.R, st));
   c->launches += 2;
   // host vectors must outlive the async copies
   PS_CUDA(cudaStreamSynchronize(st));
@@ -1602,6 +1617,7 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     res->n_observations = k.pool ? g.T * g.R : g.T;
     res->n_masked_samples = (int64_t)c->h_status->n_masked;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->n_indeterminate_ciplv = (int32_t)std::min<unsigned long long>(c->h_status->n_indeterminate, INT32_MAX);
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
     res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
@@ -1646,6 +1662,81 @@ int32_t ps_pair_shard(int64_t n_signals, int32_t precision, int32_t shard_count,
   return (int32_t)(t % shard_count);
 }
 
+// Tiles shard `s` of `P` owns, in the library's enumeration order (the rule
+// of ps_pair_shard: tile t belongs to shard t % P).
+static void shard_tile_list(int64_t N, int32_t precision, int32_t P, int32_t s, std::vector<int2>& out, int* bm,
+                            int* bn) {
+  const bool split = precision == PS_PREC_SPLIT_F16X3;
+  *bm = split ? kSplitBM : kF64BM;
+  *bn = split ? kSplitBN : kF64BN;
+  std::vector<std::pair<int, int>> tiles;
+  build_tiles(N, *bm, *bn, tiles);
+  out.clear();
+  if (P < 1) P = 1;
+  for (size_t t = 0; t < tiles.size(); ++t)
+    if ((int)(t % P) == s) out.push_back(make_int2(tiles[t].first, tiles[t].second));
+}
+
+int64_t ps_shard_tiles(int64_t n_signals, int32_t precision, int32_t shard_count, int32_t shard_index,
+                       int32_t* tile_rows, int32_t* tile_cols) {
+  if (n_signals < 1 || shard_count < 1 || shard_index < 0 || shard_index >= shard_count) return -1;
+  std::vector<int2> v;
+  int bm, bn;
+  shard_tile_list(n_signals, precision, shard_count, shard_index, v, &bm, &bn);
+  if (tile_rows) *tile_rows = bm;
+  if (tile_cols) *tile_cols = bn;
+  return (int64_t)v.size();
+}
+
+static ps_status shard_move(ps_ctx* c, int64_t N, int32_t precision, int32_t P, int32_t s, const void* src, void* dst,
+                            bool pack, int32_t mirror, void* stream) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  if (!src || !dst) return fail(PS_E_INVALID, "NULL buffer");
+  if (N < 1 || P < 1 || s < 0 || s >= P) return fail(PS_E_INVALID, "bad n_signals / shard arguments");
+  if (precision != PS_PREC_SPLIT_F16X3 && precision != PS_PREC_FP64) return fail(PS_E_INVALID, "unknown precision");
+  std::lock_guard<std::mutex> lock(c->mu);
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  std::vector<int2> v;
+  int bm, bn;
+  shard_tile_list(N, precision, P, s, v, &bm, &bn);
+  if (v.empty()) return PS_OK;
+  PS_TRY(ensure(c->shardtiles, v.size() * sizeof(int2)));
+  // stream-ordered upload (pageable source: the copy completes before the
+  // call returns, so the host vector may go out of scope)
+  PS_CUDA(cudaMemcpyAsync(c->shardtiles.p, v.data(), v.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+  const int dbl = precision == PS_PREC_FP64 ? 1 : 0;
+  if (pack) PS_CUDA(launch_shard_pack(src, N, c->shardtiles.p, (int)v.size(), bm, bn, dbl, dst, st));
+  else PS_CUDA(launch_shard_unpack(src, N, c->shardtiles.p, (int)v.size(), bm, bn, dbl, dst, mirror, st));
+  // the tile table is reused by the next call on any stream
+  PS_CUDA(cudaStreamSynchronize(st));
+  return PS_OK;
+}
+
+ps_status ps_shard_pack(ps_ctx* c, int64_t n_signals, int32_t precision, int32_t shard_count, int32_t shard_index,
+                        const void* matrix, void* packed, void* stream) {
+  return shard_move(c, n_signals, precision, shard_count, shard_index, matrix, packed, true, 0, stream);
+}
+
+ps_status ps_shard_unpack(ps_ctx* c, int64_t n_signals, int32_t precision, int32_t shard_count, int32_t shard_index,
+                          const void* packed, void* matrix, int32_t mirror, void* stream) {
+  return shard_move(c, n_signals, precision, shard_count, shard_index, packed, matrix, false, mirror, stream);
+}
+
+ps_status ps_reduce_partials(ps_ctx* c, const void* parts, int32_t n_parts, int64_t part_stride, int64_t n,
+                             double divisor, int32_t dtype, void* out, void* stream) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  if (!parts || !out) return fail(PS_E_INVALID, "NULL buffer");
+  if (n_parts < 1 || n < 0 || part_stride < n) return fail(PS_E_INVALID, "need n_parts >= 1 and part_stride >= n");
+  if (dtype != PS_F32 && dtype != PS_F64) return fail(PS_E_INVALID, "dtype must be PS_F32 or PS_F64");
+  if (!(divisor != 0.0)) return fail(PS_E_INVALID, "divisor must be non-zero");
+  std::lock_guard<std::mutex> lock(c->mu);
+  PS_CUDA(cudaSetDevice(c->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  PS_CUDA(launch_reduce_partials(parts, n_parts, part_stride, n, divisor, dtype == PS_F64 ? 1 : 0, out, st));
+  return PS_OK;
+}
+
 const char* ps_last_error(void) { return g_last_error.c_str(); }
 
 ps_status ps_ctx_create(int device, ps_ctx** out) {
@@ -1677,7 +1768,8 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (auto& kv : c->plans) cufftDestroy(kv.second);
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
-                 &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale, &c->sortws, &c->sbinfo, &c->rpick})
+                 &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale, &c->sortws, &c->sbinfo, &c->rpick,
+                 &c->shardtiles})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1699,9 +1791,13 @@ ps_status ps_ctx_set_timing(ps_ctx* c, int enable) {
   return PS_OK;
 }
 
-ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
-  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
-  std::lock_guard<std::mutex> lock(c->mu);
+}  // extern "C"
+
+namespace {
+
+// ps_plv_family with c->mu already held by the caller (the host-output entry
+// points hold it across their staging-buffer use, copy-in and copy-out).
+ps_status plv_family_locked(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   Call k;
   PS_TRY(validate(a, k.g));
   PS_TRY(setup_outputs(a, k));
@@ -1743,7 +1839,9 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
   const auto hp0 = std::chrono::steady_clock::now();
   PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
   const auto hp1 = std::chrono::steady_clock::now();
-  if (time_trace && c->timing) PS_CUDA(cudaEventRecord(c->ev[4], st));
+  // the Gram window opens after the host-side planning (ms_gram = kernel time
+  // + the item-table upload, never host planning time)
+  if (c->timing) PS_CUDA(cudaEventRecord(c->ev[4], st));
   PS_TRY(launch_stage(c, k, 0, st));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
   if (time_trace && c->timing) {
@@ -1756,7 +1854,7 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
                  k.stage_off.empty() ? 0 : k.stage_off.back());
   }
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, (int)g.R, g.split ? 0 : 1, st,
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, k.reduce_div, g.split ? 0 : 1, st,
                                     a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
@@ -1770,16 +1868,27 @@ ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
     res->n_observations = k.pool ? g.T * g.R : g.T;
     res->n_masked_samples = (int64_t)c->h_status->n_masked;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->n_indeterminate_ciplv = (int32_t)std::min<unsigned long long>(c->h_status->n_indeterminate, INT32_MAX);
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
     res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
     if (c->timing) {
       cudaEventElapsedTime(&res->ms_normalize, c->ev[0], c->ev[1]);
-      cudaEventElapsedTime(&res->ms_gram, c->ev[1], c->ev[2]);
+      cudaEventElapsedTime(&res->ms_gram, c->ev[4], c->ev[2]);
       cudaEventElapsedTime(&res->ms_finish, c->ev[2], c->ev[3]);
     }
   }
   return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  std::lock_guard<std::mutex> lock(c->mu);
+  return plv_family_locked(c, a, res);
 }
 
 int64_t ps_welch_bins(int64_t W, double lo, double hi, int64_t* first_bin) {
@@ -1885,7 +1994,7 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
   PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
   PS_TRY(launch_stage(c, k, 0, st));
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, gt.B * k.nn, (int)gt.R, gt.split ? 0 : 1, st,
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, gt.B * k.nn, k.reduce_div, gt.split ? 0 : 1, st,
                                     a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
@@ -1907,6 +2016,7 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
     std::memset(res, 0, sizeof(*res));
     res->n_observations = K;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->n_indeterminate_ciplv = (int32_t)std::min<unsigned long long>(c->h_status->n_indeterminate, INT32_MAX);
     res->n_kernel_launches = c->launches;
     res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
     if (c->timing) {
@@ -1979,6 +2089,7 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
     res->n_observations = k.pool ? g.T * g.R : g.T;
     res->n_masked_samples = (int64_t)c->h_status->n_masked;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->n_indeterminate_ciplv = (int32_t)std::min<unsigned long long>(c->h_status->n_indeterminate, INT32_MAX);
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
     res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
@@ -2098,7 +2209,7 @@ ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long lon
     if (trace) trace->rec(sc, "gram", s);
   }
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, (int)g.R, g.split ? 0 : 1, sc,
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, k.reduce_div, g.split ? 0 : 1, sc,
                                 upper ? g.N : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
@@ -2118,6 +2229,7 @@ ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long lon
     res->n_observations = g.T;
     res->n_masked_samples = (int64_t)c->h_status->n_masked;
     res->n_refined_pairs = (int64_t)c->h_status->n_illcond;
+    res->n_indeterminate_ciplv = (int32_t)std::min<unsigned long long>(c->h_status->n_indeterminate, INT32_MAX);
     res->input_copied = copied ? 1 : 0;
     res->n_kernel_launches = c->launches;
     res->gram_variant = k.g.split ? (k.g.gauss ? 1 : 0) : 2;
@@ -2132,6 +2244,10 @@ ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long lon
 // the input is device memory (ready in a->stream's order) -- no copy-in.
 ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, bool dev_input) {
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
+  // c->hin / c->hout are per-context staging buffers: the lock covers their
+  // sizing, the copy-in, the compute and the copy-out (concurrent callers on
+  // one context serialise instead of sharing the buffers)
+  std::lock_guard<std::mutex> lock(c->mu);
   Call k;
   PS_TRY(validate(a, k.g));
   PS_TRY(setup_outputs(a, k));
@@ -2164,16 +2280,11 @@ ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, 
     return (e ? std::atoll(e) : 512LL) << 20;
   }();
   const bool unit_pipelinable = !no_pipe && a->mode == PS_MODE_OVER_SAMPLES && k.shard_count == 1 &&
-                                a->trial_reduce == PS_TRIALS_MEAN && g.R > 1 && a->stride_sample == 1 &&
+                                (a->trial_reduce == PS_TRIALS_MEAN || a->trial_reduce == PS_TRIALS_SUM) && g.R > 1 &&
+                                a->stride_sample == 1 &&
                                 a->stride_signal >= g.T && span * esz >= unit_min;
-  if (unit_pipelinable) {
-    std::lock_guard<std::mutex> lock(c->mu);
-    return host_unit_pipelined(c, a, k, span, esz, res, dev_input);
-  }
-  if (pipelinable) {
-    std::lock_guard<std::mutex> lock(c->mu);
-    return host_pipelined(c, a, k, span, esz, res, dev_input);
-  }
+  if (unit_pipelinable) return host_unit_pipelined(c, a, k, span, esz, res, dev_input);
+  if (pipelinable) return host_pipelined(c, a, k, span, esz, res, dev_input);
   cudaStream_t st = static_cast<cudaStream_t>(a->stream);
   if (!dev_input) {
     PS_TRY(ensure(c->hin, (size_t)span * esz));
@@ -2198,9 +2309,12 @@ ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, 
     if (((a->metrics >> m) & 1u) && houts[m]) *douts[m] = static_cast<char*>(c->hout.p) + (size_t)(q++) * out_bytes;
     else *douts[m] = nullptr;
   }
-  if (a->out_layout == PS_LAYOUT_UPPER)  // the full-matrix copy-out carries the lower triangle: 0, not stale
-    PS_CUDA(cudaMemsetAsync(c->hout.p, 0, out_bytes * q, st));
-  ps_status s = ps_plv_family(c, &d, res);
+  // the whole-matrix copy-out carries the entries this call does not write --
+  // the lower triangle (upper layout) or other shards' tiles (sharded call):
+  // they must arrive as 0, never as a previous call's values in the reused
+  // staging buffer
+  if (a->out_layout == PS_LAYOUT_UPPER || k.shard_count > 1) PS_CUDA(cudaMemsetAsync(c->hout.p, 0, out_bytes * q, st));
+  ps_status s = plv_family_locked(c, &d, res);
   if (s != PS_OK) return s;
   q = 0;
   for (int m = 0; m < 5; ++m)

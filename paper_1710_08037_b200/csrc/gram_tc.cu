@@ -219,6 +219,10 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
   const long long Tobs = (long long)p.T * ri.nu;
   const float inv_t = 1.0f / static_cast<float>(Tobs);
   unsigned illc = 0;
+  // |Re| rounded to 1 in fp32 with a clearly non-zero Im: the ciPLV
+  // denominator is below the split arithmetic's resolution (reported 0,
+  // counted so the caller knows to use fp64; ps_plv_result.n_indeterminate_ciplv)
+  unsigned nind = 0;
   // Interior warp block: all 32 rows of this warp lie strictly above all
   // HALF columns of its slice and inside the matrix -- no per-pair diagonal /
   // bounds / mask logic (every tile off the diagonal band takes this path).
@@ -232,6 +236,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
     auto illcond = [&](const PairMetrics<float>& m, int j) {
       const float are = fabsf(m.cre);
       const float d = (1.0f - are) * (1.0f + are);
+      if (d <= 0.0f && m.iplv > p.illcond_tol) ++nind;
       if (d > 0.0f && m.iplv * are + d > kt * d * d * rsqrtf(d)) {
         ++illc;
         if (p.refine) {
@@ -269,6 +274,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
         emit8_first(p, ri.slot, i, j0, m8, ri.last);
       }
       if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+      if (nind) atomicAdd(&p.status->n_indeterminate, (unsigned long long)nind);
       return;
     }
 #pragma unroll 1
@@ -284,6 +290,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
         m4[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_t);
         const float are = fabsf(m4[e].cre);
         const float d = (1.0f - are) * (1.0f + are);
+        if (d <= 0.0f && m4[e].iplv > p.illcond_tol) ++nind;
         if (d > 0.0f && m4[e].iplv * are + d > kt * d * d * rsqrtf(d)) {
           ++illc;
           if (p.refine) {
@@ -304,6 +311,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
       emit4_all(p, ri.slot, i, j0, m4, ri.first, ri.last);
     }
     if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+    if (nind) atomicAdd(&p.status->n_indeterminate, (unsigned long long)nind);
     return;
   }
 #pragma unroll 1
@@ -337,6 +345,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
         m = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), it_);
         const float are = fabsf(m.cre);
         const float d = (1.0f - are) * (1.0f + are);
+        if (d <= 0.0f && m.iplv > p.illcond_tol) ++nind;
         // predicted ciPLV error for a ~1e-6 error in Re / Im: queue the pair
         // for exact FP64 recomputation (refine kernel) when it exceeds tol
         if (d > 0.0f && 1e-6f * (fabsf(m.cim) * are / d + 1.0f) > p.illcond_tol * sqrtf(d)) {
@@ -361,6 +370,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
     if (vec) emit4_all(p, ri.slot, i, j0, m4, ri.first, ri.last);
   }
   if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+  if (nind) atomicAdd(&p.status->n_indeterminate, (unsigned long long)nind);
 }
 
 // 576 threads = 18 warps, one CTA per SM; with 5 warps on some SM sub-partition

@@ -26,7 +26,8 @@ struct DevStatus {
   int n_fix_rows;            // rows that needed the exact-median path
   unsigned long long n_masked;
   unsigned long long n_illcond;   // ciPLV pairs flagged ill-conditioned
-  int pad[10];
+  unsigned long long n_indeterminate;  // split: |Re| rounds to 1 with |Im| > tol (ciPLV reported 0)
+  int pad[8];
 };
 
 // Where the (possibly strided) source samples of row r live.
@@ -180,6 +181,14 @@ cudaError_t launch_refine_pick(const RefineEntry* entries, int n, const float* o
 cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, void* ws,
                                  size_t ws_bytes, RefineEntry* sorted, double* exact, int* groups, int overwrite,
                                  int div, cudaStream_t st);
+
+// multi-GPU combine / gather (shard_kernels.cu)
+cudaError_t launch_reduce_partials(const void* parts, int P, long long stride, long long n, double div, int is_double,
+                                   void* out, cudaStream_t st);
+cudaError_t launch_shard_pack(const void* M, long long N, const void* tiles, int n_tiles, int bm, int bn, int is_double,
+                              void* packed, cudaStream_t st);
+cudaError_t launch_shard_unpack(const void* packed, long long N, const void* tiles, int n_tiles, int bm, int bn,
+                                int is_double, void* M, int mirror, cudaStream_t st);
 
 // split Gram variant: 2 = CTA pair (cta_group::2, 256-row panels), 1 = single
 // CTA (128-row panels).  PS_CTA_GROUP=1 selects the latter.

@@ -95,10 +95,13 @@ __global__ void refine_apply_kernel(const GramParams p, const RefineEntry* __res
   float* o = static_cast<float*>(p.out_ciplv) + (long long)e0.slot * p.N * p.N;
   const long long a = (long long)e0.i * p.N + e0.j, b = (long long)e0.j * p.N + e0.i;
   // every round of the slot refined: take the exact mean outright (keeps
-  // exact zeros of the singularity rule exact); otherwise correct the mean
+  // exact zeros of the singularity rule exact); otherwise correct the mean.
+  // div = R rounds per slot (trial mean: / R); div = -R: trial SUM (no division)
+  const int nr = div < 0 ? -div : div;
+  const double dv = div < 0 ? 1.0 : (double)div;
   const float v = overwrite ? (float)exact[k1 - 1]
-                  : (k1 - k0 == div) ? (float)(sum / (double)div)
-                                     : (float)((double)o[a] + corr / (double)div);
+                  : (k1 - k0 == nr) ? (float)(sum / dv)
+                                    : (float)((double)o[a] + corr / dv);
   o[a] = v;
   if (!p.upper_only) o[b] = v;
 }

@@ -122,8 +122,11 @@ def all_gather_rows(local_rows, n_signals: int, group=None, device=None):
     return full[:n_signals]
 
 
-def gather(outputs: dict, dst: int | None = 0, group=None) -> dict:
-    """Assemble sharded outputs: reduce (dst given) or all-reduce (dst None)."""
+def gather_dense(outputs: dict, dst: int | None = 0, group=None) -> dict:
+    """Assemble sharded outputs by a dense SUM reduce (dst given) / all-reduce
+    (dst None) of the zero-filled shards -- exact (each entry has one writer)
+    but every rank pushes whole N x N matrices; ``gather`` moves only the tiles
+    each rank owns.  Kept for callers whose outputs are not tile-sharded."""
     import torch.distributed as dist
 
     for v in outputs.values():
@@ -133,3 +136,184 @@ def gather(outputs: dict, dst: int | None = 0, group=None) -> dict:
         else:
             dist.reduce(t, dst=dst, op=dist.ReduceOp.SUM, group=group)
     return outputs
+
+
+def _native_pack(mat, n_signals, precision, world, rank, packed):
+    import torch
+
+    from . import _native
+
+    ctx = _native.context(mat.device.index)
+    with torch.cuda.device(mat.device):
+        st = torch.cuda.current_stream(mat.device).cuda_stream
+        _native.check(_native.lib().ps_shard_pack(ctx.handle, n_signals, _native.PRECISIONS[precision], world, rank,
+                                                  mat.data_ptr(), packed.data_ptr(), st))
+
+
+def _native_unpack(packed, n_signals, precision, world, shard, mat, mirror):
+    import torch
+
+    from . import _native
+
+    ctx = _native.context(mat.device.index)
+    with torch.cuda.device(mat.device):
+        st = torch.cuda.current_stream(mat.device).cuda_stream
+        _native.check(_native.lib().ps_shard_unpack(ctx.handle, n_signals, _native.PRECISIONS[precision], world,
+                                                    shard, packed.data_ptr(), mat.data_ptr(), int(mirror), st))
+
+
+def gather(outputs: dict, n_signals: int, precision: str = "split", layout: str = "full", group=None,
+           packer=None, unpacker=None, tile_counts=None) -> dict:
+    """All-gather of owned output tiles ("gathering the output
+    only if the caller asks for it").  Each rank packs the upper-triangle
+    tiles it owns (ps_shard_pack, the ps_pair_shard rule) of every [N][N]
+    slot of every metric into one dense buffer, one NCCL all-gather moves
+    1/P of the output per rank, and every rank unpacks the other ranks'
+    tiles (ps_shard_unpack: owned entries i <= j, plus the mirror for the full
+    layout -- negated for the antisymmetric 'cim').  ``outputs``: {metric:
+    CUDA tensor [..., N, N] or ConnectivityMatrix}, filled in place.
+    packer / unpacker / tile_counts: injectable for the CPU (gloo) tests of
+    the exchange; the product path uses the library's kernels."""
+    import torch
+    import torch.distributed as dist
+
+    from . import _native
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if world == 1:
+        return outputs
+    packer = packer or _native_pack
+    unpacker = unpacker or _native_unpack
+    if tile_counts is None:
+        geo = [_native.shard_tiles(n_signals, precision, world, s) for s in range(world)]
+        counts = [g[0] for g in geo]
+        te = geo[0][1] * geo[0][2]
+    else:
+        counts, te = tile_counts
+    per = max(counts) * te
+    for name, v in outputs.items():
+        t = v.values if hasattr(v, "values") and not hasattr(v, "dtype") else v
+        mats = t.reshape(-1, n_signals, n_signals)
+        mirror = 0 if layout == "upper" else (-1 if name == "cim" else 1)
+        for slot in range(mats.shape[0]):
+            mat = mats[slot]
+            mine = torch.zeros(per, dtype=mat.dtype, device=mat.device)
+            packer(mat, n_signals, precision, world, rank, mine)
+            allp = torch.empty(world * per, dtype=mat.dtype, device=mat.device)
+            if mat.is_cuda:
+                dist.all_gather_into_tensor(allp, mine, group=group)
+            else:  # gloo (CPU tests)
+                dist.all_gather(list(allp.chunk(world)), mine, group=group)
+            for s in range(world):
+                if s != rank:
+                    unpacker(allp[s * per:(s + 1) * per], n_signals, precision, world, s, mat, mirror)
+    return outputs
+
+
+# ---------------------------------------------------------------------------
+# (band, trial) unit sharding for multi-trial configs (C2, C4; SURVEY 8(e))
+# ---------------------------------------------------------------------------
+def unit_ranges(n_bands: int, n_trials: int, world: int, rank: int) -> list:
+    """This rank's contiguous chunk of the flattened (band, trial) unit list
+    (units u = b * R + t; chunk sizes differ by at most one) as
+    [(band, t0, t1), ...] -- at most one fragment per band.  SPEC.md:128:
+    per-trial work is independent."""
+    U = n_bands * n_trials
+    u0, u1 = U * rank // world, U * (rank + 1) // world
+    out = []
+    u = u0
+    while u < u1:
+        b, t0 = divmod(u, n_trials)
+        t1 = min(n_trials, t0 + (u1 - u))
+        out.append((b, t0, t1))
+        u += t1 - t0
+    return out
+
+
+def unit_partial_sums(fragments, n_bands: int, n_signals: int, *, input_kind: str = "real",
+                      precision: str = "split", metrics=("plv", "iplv", "ciplv"), layout: str = "full",
+                      out: dict | None = None, timing: bool = False) -> tuple:
+    """Per-band sums over this rank's trials of the per-trial metrics
+    (trial_reduce='sum'): ``fragments`` = [(band, x)] with x this rank's
+    trials of that band as a CUDA [N, T, r] array (e.g. a view of its
+    pre-placed [r, N, T] units).  Returns ({metric: [B, N, N] tensor, zero for
+    bands this rank holds no trial of}, [meta of each call])."""
+    import torch
+
+    from . import connectivity as C
+
+    fp64 = precision == "fp64"
+    dev = None
+    for _, xf in fragments:
+        dev = xf.device
+        break
+    if dev is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    tdt = torch.float64 if fp64 else torch.float32
+    parts = out if out is not None else {
+        m: torch.zeros((n_bands, n_signals, n_signals), dtype=tdt, device=dev) for m in metrics}
+    if out is not None:
+        for m in metrics:
+            parts[m].zero_()
+    metas = []
+    for b, xf in fragments:
+        res = C.plv_family(xf, input_kind=input_kind, metrics=metrics, precision=precision, trial_reduce="sum",
+                           out={m: parts[m][b:b + 1] for m in metrics}, layout=layout, timing=timing)
+        metas.append(next(iter(res.values())).meta)
+    return parts, metas
+
+
+def _native_reduce(parts, n_parts, stride, n, divisor, out):
+    import torch
+
+    from . import _native
+
+    ctx = _native.context(out.device.index)
+    with torch.cuda.device(out.device):
+        st = torch.cuda.current_stream(out.device).cuda_stream
+        dt = _native.DTYPES["f64"] if out.dtype == torch.float64 else _native.DTYPES["f32"]
+        _native.check(_native.lib().ps_reduce_partials(ctx.handle, parts.data_ptr(), n_parts, stride, n,
+                                                       float(divisor), dt, out.data_ptr(), st))
+
+
+def reduce_trial_partials(parts: dict, n_trials: int, group=None, gather_all: bool = False, reducer=None) -> dict:
+    """Combine the ranks' per-band trial sums into the trial mean, in a fixed
+    rank order.  The [B, N, N] slots are read as B*N flat rows
+    split into ``row_slice`` chunks; one all-to-all hands rank s the P
+    partials of its row chunk, and ps_reduce_partials sums them left to right
+    (rank 0 first) and divides by the global trial count: a deterministic
+    reduce-scatter.  Returns {metric: (rows [r0, r1) of the flat [B*N, N]
+    result, (r0, r1))}; with gather_all=True the full [B, N, N] mean on every
+    rank instead (one more all-gather).  ``reducer`` is injectable for the
+    CPU (gloo) tests; the product path uses the library's kernel."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    reducer = reducer or _native_reduce
+    out = {}
+    for m, t in parts.items():
+        B, N = t.shape[0], t.shape[-1]
+        F = B * N
+        flat = t.reshape(F, N)
+        sl = [row_slice(F, s, world) for s in range(world)]
+        r0, r1 = sl[rank]
+        mine = r1 - r0
+        if world == 1:
+            recv = flat.contiguous().reshape(-1)
+        else:
+            recv = torch.empty(world * mine * N, dtype=t.dtype, device=t.device)
+            dist.all_to_all_single(recv, flat.contiguous().reshape(-1), output_split_sizes=[mine * N] * world,
+                                   input_split_sizes=[(b - a) * N for a, b in sl], group=group)
+        res = torch.empty(mine * N, dtype=t.dtype, device=t.device)
+        if mine:
+            reducer(recv, world, mine * N, mine * N, float(n_trials), res)
+        rows = res.reshape(mine, N)
+        if gather_all:
+            full = all_gather_rows(rows, F, group=group, device=t.device)
+            out[m] = full.reshape(B, N, N)
+        else:
+            out[m] = (rows, (r0, r1))
+    return out

@@ -627,42 +627,7 @@ def props(res, N):
     assert np.all(dg == 1.0)
 
 
-@pytest.mark.parametrize("cfg", ["c3", "c5", "c2"])
-def test_full_size_configs_subset_parity(cfg):
-    import torch
-
-    N, T, R, B, dt, kind = W.CONFIGS[cfg]
-    x = W.generate(cfg)
-    xd = torch.from_numpy(np.ascontiguousarray(np.transpose(x, (2, 0, 1)))).cuda()  # [R, N, T]
-    xd = xd.permute(1, 2, 0)                                                         # [N, T, R] view
-    res = C.plv_family(xd, input_kind=kind, precision="split")
-    host = {m: res[m].values.cpu().numpy() for m in METRICS}
-    hres = {m: C.ConnectivityMatrix(values=host[m], metric=m, n_observations=T) for m in METRICS}
-    props(hres, N)
-    idx = np.sort(np.random.default_rng(1).choice(N, size=min(N, 160), replace=False))
-    errs = subset_check(x, hres, idx, kind, "split", f"{cfg}-full")
-    for m, e in errs.items():
-        assert e <= TOL["split"], (cfg, m, e)
-
-
-def test_full_size_c4_band_subset_parity():
-    # one C4 band at full size (2500 x 4096 x 60 trials, fp32 real, trial mean):
-    # the fused T = 4096 Hilbert kernel + the trial-group Gram, checked on a
-    # random signal subset against the oracle over all 60 trials
-    import torch
-
-    N, T, R, B, dt, kind = W.CONFIGS["c4"]
-    x = W.c4(bands=W.C4_BANDS[1:2])                      # [1, N, T, R] view of [1, R, N, T]
-    store = np.ascontiguousarray(np.transpose(x, (0, 3, 1, 2)))
-    xd = torch.from_numpy(store).cuda().permute(0, 2, 3, 1)
-    res = C.plv_family(xd, input_kind="real", precision="split", bands=True)
-    host = {m: res[m].values[0].cpu().numpy() for m in METRICS}
-    hres = {m: C.ConnectivityMatrix(values=host[m], metric=m, n_observations=T) for m in METRICS}
-    props(hres, N)
-    idx = np.sort(np.random.default_rng(2).choice(N, size=96, replace=False))
-    errs = subset_check(x[0], hres, idx, "real", "split", "c4-band-full")
-    for m, e in errs.items():
-        assert e <= TOL["split"], ("c4", m, e)
+# full-size configs: tests/test_gpu_scale_parity.py (structured row subsets, both precisions)
 
 
 # ------------------------------------------------------------ CLI (acceptance #9)

@@ -26,7 +26,8 @@ def one(case):
         x, kind = W.c2(n_signals=300, n_samples=10000, n_trials=4, n_coupled=30), "real"
     ref = O.plv_family(x, input_kind=kind)
     res = C.plv_family(x, input_kind=kind, precision="split")
-    out = {"case": case, "kc_blocks": os.environ.get("PS_KC_BLOCKS", "4")}
+    out = {"case": case, "kc_blocks": os.environ.get("PS_KC_BLOCKS", "4"), "gauss": os.environ.get("PS_GAUSS"),
+           "gram_variant": int(res["plv"].meta["gram_variant"])}
     for m in ("plv", "iplv", "ciplv"):
         d = np.asarray(res[m].values, dtype=np.float64) - ref[m]
         out[m] = float(np.max(np.abs(d)))
@@ -39,7 +40,12 @@ if __name__ == "__main__":
     if len(sys.argv) > 2:
         one(sys.argv[2])
         sys.exit(0)
+    # `accuracy_probe.py gauss`: the Gauss 3-product Gram (PS_GAUSS=1) around
+    # its default chunk (kc 16 = 512 samples); otherwise the 4-product Gram
+    gauss = len(sys.argv) > 1 and sys.argv[1] == "gauss"
+    kcs = ("4", "8", "16", "32") if gauss else ("1", "2", "4", "8", "100000")
     for case in ("c1", "c5s", "c3s", "c2s"):
-        for kc in ("1", "2", "4", "8", "100000"):
-            env = dict(os.environ, PS_KC_BLOCKS=kc)
+        for kc in kcs:
+            # PS_KC_UNSAFE: the library caps PS_KC_BLOCKS at the validated chunk otherwise
+            env = dict(os.environ, PS_KC_BLOCKS=kc, PS_KC_UNSAFE="1", PS_GAUSS="1" if gauss else "0")
             subprocess.run([sys.executable, __file__, "one", case], env=env, check=False)
