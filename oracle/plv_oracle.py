@@ -373,6 +373,9 @@ def _metrics_from_gram(G: np.ndarray, C: np.ndarray):
     den = 1.0 - re * re
     sing = np.abs(re) >= 1.0 - CIPLV_SINGULAR_EPS
     ciplv = np.where(sing, 0.0, np.abs(im) / np.sqrt(np.where(sing, 1.0, den)))
+    # |Im|^2 <= 1 - Re^2 (Cauchy-Schwarz): rounding near the singularity can
+    # push the quotient past 1; keep the output bound [0, 1]
+    ciplv = np.minimum(ciplv, 1.0)
     n = G.shape[0]
     d = np.arange(n)
     plv[d, d] = 1.0
@@ -477,7 +480,7 @@ def _metrics_from_block(G: np.ndarray, C: np.ndarray, rows: np.ndarray, c0: int)
     iplv = np.abs(im)
     den = 1.0 - re * re
     sing = np.abs(re) >= 1.0 - CIPLV_SINGULAR_EPS
-    ciplv = np.where(sing, 0.0, np.abs(im) / np.sqrt(np.where(sing, 1.0, den)))
+    ciplv = np.minimum(np.where(sing, 0.0, np.abs(im) / np.sqrt(np.where(sing, 1.0, den))), 1.0)
     r = np.nonzero((rows >= c0) & (rows < c0 + G.shape[1]))[0]
     plv[r, rows[r] - c0] = 1.0
     iplv[r, rows[r] - c0] = 0.0

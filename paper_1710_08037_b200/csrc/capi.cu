@@ -478,6 +478,14 @@ ps_status reset_status(ps_ctx* c, cudaStream_t st) {
   return PS_OK;
 }
 
+// Re-read the device status after the FP64 refinement (its kernels add to
+// the indeterminate-ciPLV count); the flags were checked before it ran.
+ps_status refresh_status(ps_ctx* c, cudaStream_t st) {
+  PS_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  PS_CUDA(cudaStreamSynchronize(st));
+  return PS_OK;
+}
+
 ps_status read_status(ps_ctx* c, cudaStream_t st) {
   PS_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
   PS_CUDA(cudaStreamSynchronize(st));
@@ -1860,7 +1868,10 @@ ps_status plv_family_locked(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res)
   }
   ps_status s = read_status(c, st);
   // ---- exact FP64 refinement of ill-conditioned ciPLV pairs (split path) ----
-  if (s == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+  if (s == PS_OK && c->h_status->n_illcond) {
+    PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+    PS_TRY(refresh_status(c, st));
+  }
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[3], st));
   if (c->timing) PS_CUDA(cudaEventSynchronize(c->ev[3]));
   if (res) {
@@ -2000,7 +2011,10 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
   }
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
   ps_status s = read_status(c, st);
-  if (s == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+  if (s == PS_OK && c->h_status->n_illcond) {
+    PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+    PS_TRY(refresh_status(c, st));
+  }
   if (s == PS_OK && w->reduce == PS_BAND_MAX) {
     for (int m = 0; m < 5; ++m)
       if (k.outs[m]) {
@@ -2083,7 +2097,10 @@ ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* r
   PS_CUDA(cudaEventRecord(done, c->s_comp));
   PS_CUDA(cudaStreamWaitEvent(st, done, 0));
   ps_status s = read_status(c, st);
-  if (s == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+  if (s == PS_OK && c->h_status->n_illcond) {
+    PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, st));
+    PS_TRY(refresh_status(c, st));
+  }
   if (res) {
     std::memset(res, 0, sizeof(*res));
     res->n_observations = k.pool ? g.T * g.R : g.T;
@@ -2214,7 +2231,10 @@ ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long lon
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
   ps_status st = read_status(c, sc);
-  if (st == PS_OK) PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, sc));
+  if (st == PS_OK && c->h_status->n_illcond) {
+    PS_TRY(refine_range(c, k, 0, c->h_status->n_illcond, sc));
+    PS_TRY(refresh_status(c, sc));
+  }
   size_t d2h_bytes = 0;
   for (int m = 0; m < 5 && st == PS_OK; ++m)
     if (houts[m]) {

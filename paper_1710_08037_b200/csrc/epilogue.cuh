@@ -42,6 +42,9 @@ __device__ __forceinline__ PairMetrics<S> pair_metrics(S gre, S gim, S inv_t) {
   } else {
     plv = sqrt(cre * cre + cim * cim);
     ci = (are >= S(1) - S(1e-12)) ? S(0) : aim / sqrt(S(1) - cre * cre);
+    // |Im|^2 <= 1 - Re^2 (Cauchy-Schwarz); near the singularity rounding can
+    // still push the quotient past 1 -- keep the SPEC.md:150 bound
+    ci = ci > S(1) ? S(1) : ci;
   }
   m.plv = plv;
   m.iplv = aim;

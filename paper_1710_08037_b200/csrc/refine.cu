@@ -76,6 +76,15 @@ __global__ void refine_exact_kernel(const GramParams p, const RefineEntry* __res
     const double inv = te > 0 ? 1.0 / (double)te : 0.0;
     const PairMetrics<double> m = pair_metrics<double, false>(gre, gim, inv);
     exact[w] = m.ciplv > 1.0 ? 1.0 : m.ciplv;
+    // The planes hold z to 2^-24 per component, so even this FP64 sum carries
+    // ~3 * 2^-24 * sqrt(2 / T) in Re and Im (rounding errors averaged over T).
+    // ciPLV amplifies an error e in Re by ciPLV |Re| / (1 - Re^2) and one in Im
+    // by 1 / sqrt(1 - Re^2): when that exceeds the 1e-5 budget the value is
+    // indeterminate in split precision -- counted, so the caller is told to
+    // use fp64 (ps_plv_result.n_indeterminate_ciplv)
+    const double are = fabs(m.cre), d = 1.0 - m.cre * m.cre;
+    const double dz = 3.0 * 5.9604644775390625e-8 * sqrt(2.0 / (double)(te > 0 ? te : 1));
+    if (d > 0.0 && m.ciplv * are * dz / d + dz / sqrt(d) > 1e-5) atomicAdd(&p.status->n_indeterminate, 1ull);
   }
 }
 
