@@ -93,6 +93,7 @@ struct ps_ctx {
   Buf hscale;              // per-row factors restoring H after scaled packing (odd T)
   Buf sortws;              // device-side ordering of the ciPLV refinement queue
   Buf shardtiles;          // (I, J) of the tiles one shard owns (ps_shard_pack / unpack)
+  Buf ind, cntws, cntitems;  // K7: unmasked-indicator plane, per-pair counts, count-pass items
   std::vector<cudaEvent_t> tev;  // timing events of the staged path (2 per stage)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
@@ -650,6 +651,7 @@ struct Call {
   long long nn = 0;
   size_t oes = 4;
   long long slots = 1;  // output slots per metric
+  std::vector<std::pair<int, int>> mine;  // ownership tiles of this call (plan_call)
 };
 
 // The 3-product (Gauss) split Gram: 9 UMMAs per K step instead of 12
@@ -742,6 +744,7 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     for (size_t t = 0; t < tiles.size(); ++t)
       if ((int)(t % k.shard_count) == k.shard_index) mine.push_back(tiles[t]);
   }
+  k.mine = mine;
   const int n_stages = cols.empty() ? 1 : (int)cols.size() - 1;
   // Column stages (row_band == 0): stage s holds the tiles whose column panel
   // starts in [cols[s], cols[s+1]).  Row stages (row_band > 0, the streamed
@@ -934,6 +937,98 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     k.tb2 = g.gauss && !gauss_smem_convert() ? &it->second.b2 : nullptr;
   }
   return PS_OK;
+}
+
+// K7 mask-count Gram (SPEC.md:260 per-pair effective T): when the
+// normalisation masked any sample, T_ij = sum_t u_i(t) u_j(t) for every pair
+// of the call's tiles comes from one tcgen05 product of the 0/1 indicator
+// planes (gram_tc.cu, MK variant) -- exact -- and the metric epilogues read it
+// (interior fast path kept) instead of scanning both rows' planes.  Runs after
+// plan_call, before the Gram; the host reads the mask flag first (one short
+// synchronisation; the pipelined host paths keep the plane scan).
+ps_status mask_count_pass(ps_ctx* c, Call& k, cudaStream_t st) {
+  const Geometry& g = k.g;
+  const long long ip = round_up(g.T, 8);
+  PS_TRY(ensure(c->ind, (size_t)g.rows * ip * 2));
+  PS_CUDA(launch_indicator_plane(c->planes.p, g.plane_stride, g.split ? 1 : 0, g.rows, (int)g.pitch, (int)g.T,
+                                 c->ind.p, (int)ip, st));
+  c->launches++;
+  const long long cslots = k.pool ? g.B : g.B * g.R;
+  PS_TRY(ensure(c->cntws, (size_t)cslots * g.N * g.N * sizeof(int)));
+  // count tiles: the split geometry's ownership tiles (fp64 calls: all of them)
+  std::vector<std::pair<int, int>> tiles;
+  if (g.split) tiles = k.mine;
+  else build_tiles(g.N, kSplitBM, kSplitBN, tiles);
+  const int exec_rows = split_panel_rows();
+  const int sub = kSplitBM / exec_rows;
+  const int units = k.pool ? 1 : (int)g.R;
+  std::vector<Item> items;
+  for (int b = 0; b < g.B; ++b)
+    for (int gi = 0; gi < units; ++gi)
+      for (const auto& t : tiles)
+        for (int hs = 0; hs < sub; ++hs) {
+          const int I = t.first * sub + hs;
+          const long long jmax = std::min<long long>((long long)t.second * kSplitBN + kSplitBN, g.N) - 1;
+          if ((long long)I * exec_rows > jmax || (long long)I * exec_rows >= g.N) continue;
+          items.push_back(Item{b, gi, I, t.second});
+        }
+  if (items.empty()) return PS_OK;
+  PS_TRY(ensure(c->cntitems, items.size() * sizeof(Item)));
+  // pageable source: staged before the call returns
+  PS_CUDA(cudaMemcpyAsync(c->cntitems.p, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice, st));
+  GramParams pc;
+  std::memset(&pc, 0, sizeof(pc));
+  pc.N = (int)g.N;
+  pc.T = (int)g.T;
+  pc.R = (int)g.R;
+  pc.B = (int)g.B;
+  pc.Tp = (int)ip;
+  pc.rows = (int)g.rows;
+  pc.Rg = 1;
+  pc.G = units;
+  pc.pool = k.pool ? 1 : 0;
+  pc.items = static_cast<const Item*>(c->cntitems.p);
+  pc.n_items = (int)items.size();
+  pc.status = c->d_status;
+  pc.kc_blocks = 64;  // drains are exact for integer counts: long chunks
+  pc.cnt = static_cast<int*>(c->cntws.p);
+  auto enc = encode_fn();
+  if (!enc) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  CUtensorMap ta, tb;
+  cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), 1};
+  cuuint64_t strides[3] = {(cuuint64_t)ip * 2, (cuuint64_t)(g.N * ip * 2), (cuuint64_t)(g.rows * ip * 2)};
+  cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, 1};
+  cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)split_b_box_rows(), 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
+                                 : kSplitBK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                  : CU_TENSOR_MAP_SWIZZLE_128B;
+  const CUresult r1 = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->ind.p, dims, strides, boxA, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r2 = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->ind.p, dims, strides, boxB, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
+    return fail(PS_E_CUDA, "cuTensorMapEncodeTiled (indicator plane) failed");
+  const int grid = std::min(pc.n_items, c->num_sms / split_cta_group());
+  PS_CUDA(launch_gram_count(&ta, &tb, pc, grid, st));
+  c->launches++;
+  k.p.cnt = pc.cnt;
+  return PS_OK;
+}
+
+// Did the normalisation mask any sample?  (reads the device flag; syncs `st`)
+ps_status any_masked(ps_ctx* c, cudaStream_t st, bool* out) {
+  PS_CUDA(cudaMemcpyAsync(c->h_status, c->d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, st));
+  PS_CUDA(cudaStreamSynchronize(st));
+  *out = (c->h_status->flags & FLAG_ANY_MASKED) != 0;
+  return PS_OK;
+}
+
+static bool k7_enabled() {
+  static const bool on = std::getenv("PS_NO_K7") == nullptr;  // PS_NO_K7=1: plane scan (A/B experiments)
+  return on;
 }
 
 ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
@@ -1777,7 +1872,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
                  &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale, &c->sortws, &c->sbinfo, &c->rpick,
-                 &c->shardtiles})
+                 &c->shardtiles, &c->ind, &c->cntws, &c->cntitems})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -1848,8 +1943,14 @@ ps_status plv_family_locked(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res)
   PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
   const auto hp1 = std::chrono::steady_clock::now();
   // the Gram window opens after the host-side planning (ms_gram = kernel time
-  // + the item-table upload, never host planning time)
+  // + the item-table upload + the K7 count pass when samples are masked,
+  // never host planning time)
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[4], st));
+  if (k7_enabled()) {
+    bool masked = false;
+    PS_TRY(any_masked(c, st, &masked));
+    if (masked) PS_TRY(mask_count_pass(c, k, st));
+  }
   PS_TRY(launch_stage(c, k, 0, st));
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
   if (time_trace && c->timing) {

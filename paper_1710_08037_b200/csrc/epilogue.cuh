@@ -97,6 +97,11 @@ __device__ __noinline__ int masked_overlap(const void* planes, long long plane_s
 // fixup kernel reported masked samples.
 template <bool SPLIT>
 __device__ __forceinline__ long long effective_T(const GramParams& p, int u0, int nu, int i, int j) {
+  if (p.cnt) {  // K7 count Gram ran: one load (pool: the band's slot already sums its units)
+    const long long cs = p.pool ? (long long)(u0 / p.R) : (long long)u0;
+    const int a = i < j ? i : j, b = i < j ? j : i;
+    return p.cnt[cs * (long long)p.N * p.N + (long long)a * p.N + b];
+  }
   long long tot = 0;
   for (int u = u0; u < u0 + nu; ++u) {
     const long long ri = (long long)u * p.N + i, rj = (long long)u * p.N + j;

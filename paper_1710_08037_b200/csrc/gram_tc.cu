@@ -78,14 +78,20 @@ constexpr int HALF = BN / (NEPI_WARPS / 4);    // columns per epilogue warp
 // the conversion adds ~80 KB of LSU shared-memory traffic per stage against
 // the 24 KB of TMA writes it saves, on an SM whose shared memory is already
 // busy feeding 18 UMMAs per stage (profiles/r01_gauss_conv.txt).
-template <int CG, bool GS = false>
+// MK = true: the mask-count Gram (K7).  One fp16 plane per
+// operand holds the unmasked indicator u(t) in {0, 1}; one UMMA per K step
+// accumulates T_ij = sum_t u_i(t) u_j(t) -- exact in fp32 for T < 2^24 (every
+// partial sum is an integer below 2^24, so the accumulate never rounds) --
+// and the epilogue stores the per-pair counts (int32) the metric epilogue of
+// the main Gram then reads instead of scanning the planes.
+template <int CG, bool GS = false, bool MK = false>
 struct Geo {
   static constexpr int BNT = BN;                         // tile columns (UMMA N)
   static constexpr int H = BNT / (NEPI_WARPS / 4);       // columns per epilogue warp
-  static constexpr int NACC = GS ? 3 : 2;                // accumulators per buffer
+  static constexpr int NACC = GS ? 3 : (MK ? 1 : 2);     // accumulators per buffer
   static constexpr int NBUF = GS ? 1 : 2;                // accumulation buffers (ping-pong when 2)
   static constexpr uint32_t BUF = NACC * BNT;            // TMEM columns per buffer
-  static constexpr int NPL = GS ? 6 : 4;                 // planes staged per operand
+  static constexpr int NPL = GS ? 6 : (MK ? 1 : 4);      // planes staged per operand
   static constexpr int BNC = BNT / CG;                   // J-panel rows staged per CTA
   static constexpr int A_PLANE = BMC * BK * 2;
   static constexpr int B_PLANE = BNC * BK * 2;
@@ -93,7 +99,7 @@ struct Geo {
   static constexpr int B_BYTES = NPL * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
   // (GS, CG = 1: a 128-row J panel makes a 96 KB stage -- two fit the 227 KB)
-  static constexpr int STAGES = GS ? (CG == 2 ? 3 : 2) : (CG == 2 ? 4 : 3);
+  static constexpr int STAGES = MK ? 8 : GS ? (CG == 2 ? 3 : 2) : (CG == 2 ? 4 : 3);
   static_assert(STAGES * STAGE_BYTES + 1024 + 256 <= 227 * 1024, "stages must fit shared memory");
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr int UMMA_M = BMC * CG;
@@ -228,7 +234,18 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
   // bounds / mask logic (every tile off the diagonal band takes this path).
   const int lane = threadIdx.x & 31;
   const int ib = i - lane, jb = w.J * BN + h * HALF;
-  const bool interior = !any_masked && (p.N & 3) == 0 && ib + 31 < jb && jb + HALF <= p.N;
+  // (masked samples: the interior path stays when the K7 count Gram supplied
+  // per-pair counts -- one int load per pair instead of the plane scan)
+  const bool interior = (!any_masked || p.cnt) && (p.N & 3) == 0 && ib + 31 < jb && jb + HALF <= p.N;
+  auto inv_at = [&](int j) -> float {
+    if (!any_masked) return inv_t;
+    const long long te = effective_T<true>(p, ri.u0, ri.nu, i, j);
+    if (te <= 0) {
+      atomicOr(&p.status->flags, FLAG_EMPTY_WINDOW);
+      return 0.0f;
+    }
+    return 1.0f / static_cast<float>(te);
+  };
   if (interior) {
     // ill-conditioning test of the general path, 1e-6 (|cim| are / d + 1) >
     // tol sqrt(d), multiplied through by d / 1e-6 (d > 0): no division
@@ -268,7 +285,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
         PairMetrics<float> m8[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          m8[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_t);
+          m8[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(j0 + e));
           illcond(m8[e], j0 + e);
         }
         emit8_first(p, ri.slot, i, j0, m8, ri.last);
@@ -287,7 +304,7 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
       PairMetrics<float> m4[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        m4[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_t);
+        m4[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(j0 + e));
         const float are = fabsf(m4[e].cre);
         const float d = (1.0f - are) * (1.0f + are);
         if (d <= 0.0f && m4[e].iplv > p.illcond_tol) ++nind;
@@ -380,11 +397,12 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
 // covers all 256 rows.  CG = 1: item.g's high bit is unused; instead the host
 // doubles the items and the low bit of I (after << 1) selects the half -- see
 // launch_gram_split: for CG = 1 the host passes 128-row panel indices.
-template <int CG, bool GS, bool CV>
+template <int CG, bool GS, bool CV, bool MK = false>
 __global__ void __launch_bounds__(NTHREADS, 1)
     gram_split_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const __grid_constant__ CUtensorMap tmB2, const GramParams p) {
-  using G = Geo<CG, GS>;
+  using G = Geo<CG, GS, MK>;
+  static_assert(!(MK && (GS || CV)), "the mask-count Gram is its own variant");
   static_assert(!CV || GS, "smem S / D conversion is a Gauss-Gram feed");
   // bytes TMA delivers per stage and CTA (CV: 4 planes of A and of B)
   constexpr int LOAD_BYTES = CV ? 4 * (G::A_PLANE + G::B_PLANE) : G::STAGE_BYTES;
@@ -560,7 +578,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const uint64_t bIh = dB + ko + 2 * (G::B_PLANE >> 4);  // GS: S hi
               const uint64_t bIl = dB + ko + 3 * (G::B_PLANE >> 4);  // GS: S lo
               const uint32_t acc0 = (chunk_start && ks == 0) ? 0u : 1u;
-              if constexpr (GS) {
+              if constexpr (MK) {
+                // T_ij += u_i . u_j  (plane 0 of each operand: the unmasked indicator)
+                ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRh, idesc_pos, acc0);
+              } else if constexpr (GS) {
                 const uint64_t aSh = dA + ko + 4 * (G::A_PLANE >> 4);
                 const uint64_t aSl = dA + ko + 5 * (G::A_PLANE >> 4);
                 const uint64_t bDh = dB + ko + 4 * (G::B_PLANE >> 4);
@@ -664,16 +685,38 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           // single-chunk rounds (short K: over_trials, coherence, T <= 128):
           // the chunk accumulator already is the round's sum (0 + x = x), so
           // it is emitted in place -- no drain / park round trip through TMEM
-          const bool direct = !GS && nchunks == 1 && !p.pool;
+          const bool direct = !GS && !MK && nchunks == 1 && !p.pool;
           if (!direct) {
             if constexpr (GS) {
               add_chunk_gauss<H>(sre, sim, ta, BN);
+            } else if constexpr (MK) {
+              add_chunk<H>(sre, ta);
             } else {
               add_chunk<H>(sre, ta);
               add_chunk<H>(sim, ta + BN);
             }
           }
-          if (c == nchunks - 1 && (!p.pool || r == r1 - 1)) {
+          if (MK && c == nchunks - 1 && (!p.pool || r == r1 - 1)) {
+            // per-pair observation counts of this round's unit (pool: of the
+            // band) -> p.cnt[slot][i][j], every in-bounds pair of the tile
+            if (i < p.N) {
+              const long long cs = p.pool ? (long long)w.b : (long long)w.b * p.R + r;
+              int* dst = p.cnt + cs * (long long)p.N * p.N + (long long)i * p.N;
+              const int jb = w.J * BN + h * H;
+              if ((p.N & 3) == 0 && jb + H <= p.N) {
+#pragma unroll
+                for (int k = 0; k < H; k += 4)
+                  *reinterpret_cast<int4*>(dst + jb + k) =
+                      make_int4((int)sre[k], (int)sre[k + 1], (int)sre[k + 2], (int)sre[k + 3]);
+              } else {
+#pragma unroll
+                for (int k = 0; k < H; ++k)
+                  if (jb + k < p.N) dst[jb + k] = (int)sre[k];
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < H; ++k) sre[k] = 0.0f;
+          } else if (!MK && c == nchunks - 1 && (!p.pool || r == r1 - 1)) {
             // Round complete: park the fp32 sums back in this (still owned)
             // TMEM buffer and emit from there with a compact loop, so the
             // register sums are dead during the store-heavy epilogue.
@@ -719,12 +762,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
 }
 
-template <int CG, bool GS, bool CV = false>
+template <int CG, bool GS, bool CV = false, bool MK = false>
 cudaError_t launch_cg(const void* tmapA, const void* tmapB, const void* tmapB2, const GramParams& p, int groups,
                       cudaStream_t st) {
-  using G = Geo<CG, GS>;
-  cudaError_t e =
-      cudaFuncSetAttribute(gram_split_kernel<CG, GS, CV>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES);
+  using G = Geo<CG, GS, MK>;
+  cudaError_t e = cudaFuncSetAttribute(gram_split_kernel<CG, GS, CV, MK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       G::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   if (p.n_items <= 0) return cudaSuccess;
   cudaLaunchConfig_t cfg = {};
@@ -739,7 +782,7 @@ cudaError_t launch_cg(const void* tmapA, const void* tmapB, const void* tmapB2, 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gram_split_kernel<CG, GS, CV>, *static_cast<const CUtensorMap*>(tmapA),
+  return cudaLaunchKernelEx(&cfg, gram_split_kernel<CG, GS, CV, MK>, *static_cast<const CUtensorMap*>(tmapA),
                             *static_cast<const CUtensorMap*>(tmapB),
                             *static_cast<const CUtensorMap*>(tmapB2 ? tmapB2 : tmapB), p);
 }
@@ -778,6 +821,11 @@ cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const void* 
                                   : launch_cg<1, true>(tmapA, tmapB, tmapB2, p, groups, st);
   return split_cta_group() == 2 ? launch_cg<2, false>(tmapA, tmapB, nullptr, p, groups, st)
                                 : launch_cg<1, false>(tmapA, tmapB, nullptr, p, groups, st);
+}
+
+cudaError_t launch_gram_count(const void* tmapA, const void* tmapB, const GramParams& p, int groups, cudaStream_t st) {
+  return split_cta_group() == 2 ? launch_cg<2, false, false, true>(tmapA, tmapB, nullptr, p, groups, st)
+                                : launch_cg<1, false, false, true>(tmapA, tmapB, nullptr, p, groups, st);
 }
 
 }  // namespace ps

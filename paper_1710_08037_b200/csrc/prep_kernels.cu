@@ -1420,6 +1420,47 @@ cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void
   return cudaGetLastError();
 }
 
+// K7 operand: u(t) = 1 where a sample is unmasked (masked samples are exactly
+// 0 in every plane; an unmasked unit phasor never has both hi parts 0), 0 where
+// masked or in the row padding.  One thread per 8-sample chunk, 16-byte store.
+__device__ __forceinline__ bool is_zero_el(__half v) { return __half2float(v) == 0.0f; }
+__device__ __forceinline__ bool is_zero_el(double v) { return v == 0.0; }
+
+template <typename E, int IM_PLANE>
+__global__ void indicator_plane_kernel(const E* __restrict__ planes, long long ps, long long rows, int Tp, int T,
+                                       __half* __restrict__ ind, int ip) {
+  const long long cpr = ip / 8;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cpr;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / cpr;
+    const int t0 = (int)(e % cpr) * 8;
+    __align__(16) __half v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int t = t0 + k;
+      bool u = false;
+      if (t < T) {
+        const long long idx = r * Tp + t;
+        u = !(is_zero_el(planes[idx]) && is_zero_el(planes[IM_PLANE * ps + idx]));
+      }
+      v[k] = __float2half_rn(u ? 1.0f : 0.0f);
+    }
+    *reinterpret_cast<uint4*>(ind + r * ip + t0) = *reinterpret_cast<const uint4*>(v);
+  }
+}
+
+cudaError_t launch_indicator_plane(const void* planes, long long plane_stride, int split, long long rows, int Tp,
+                                   int T, void* ind, int ind_pitch, cudaStream_t st) {
+  const int g = grid_for(rows * (ind_pitch / 8), 256);
+  if (split)
+    indicator_plane_kernel<__half, 2><<<g, 256, 0, st>>>((const __half*)planes, plane_stride, rows, Tp, T,
+                                                          (__half*)ind, ind_pitch);
+  else
+    indicator_plane_kernel<double, 1><<<g, 256, 0, st>>>((const double*)planes, plane_stride, rows, Tp, T,
+                                                          (__half*)ind, ind_pitch);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs, void* const* outs,
                                 long long elems_per_out, int R, int is_double, cudaStream_t st, long long upper_n) {
   // ws holds n_outputs consecutive blocks of [B][G][slot_elems]

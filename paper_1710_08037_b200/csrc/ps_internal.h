@@ -103,6 +103,11 @@ struct GramParams {
   const int* item_sb;
   const int* sb_need;
   volatile int* sb_flag;
+  // Per-pair observation counts (K7 mask-count Gram): written by
+  // the count kernel ([slots][N][N] int32, slot = b*R + r, or b for pool),
+  // read by the metric epilogues in place of the plane scan when samples are
+  // masked.  nullptr: no count pass ran.
+  int* cnt;
 };
 
 // ---- launchers (return cudaError_t) --------------------------------------
@@ -159,6 +164,12 @@ cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void
 cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs,
                                 void* const* outs, long long elems_per_out, int R,
                                 int is_double, cudaStream_t st, long long upper_n);
+// K7: per-pair observation counts from the unmasked-indicator plane (same
+// items / tiles / cluster layout as the split Gram; p.cnt receives the counts)
+cudaError_t launch_gram_count(const void* tmapA, const void* tmapB, const GramParams& p, int groups, cudaStream_t st);
+// unmasked indicator u(t) (fp16 0 / 1, padding 0) of every plane row
+cudaError_t launch_indicator_plane(const void* planes, long long plane_stride, int split, long long rows, int Tp,
+                                   int T, void* ind, int ind_pitch, cudaStream_t st);
 cudaError_t launch_gram_split(const void* tmapA, const void* tmapB, const void* tmapB2, bool gauss,
                               const GramParams& p, int grid, cudaStream_t st);
 // Gauss-Gram planes 4..7 (S, D hi / lo) from planes 0..3, flat elements [e0, e1)

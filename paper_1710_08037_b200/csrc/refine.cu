@@ -84,7 +84,10 @@ __global__ void refine_exact_kernel(const GramParams p, const RefineEntry* __res
     // use fp64 (ps_plv_result.n_indeterminate_ciplv)
     const double are = fabs(m.cre), d = 1.0 - m.cre * m.cre;
     const double dz = 3.0 * 5.9604644775390625e-8 * sqrt(2.0 / (double)(te > 0 ? te : 1));
-    if (d > 0.0 && m.ciplv * are * dz / d + dz / sqrt(d) > 1e-5) atomicAdd(&p.status->n_indeterminate, 1ull);
+    // (Im exactly 0 from the planes: identical rows, whose plane errors cancel
+    // in Im exactly as well -- ciPLV = 0 is exact there)
+    const double e_im = m.cim != 0.0 ? dz / sqrt(d > 0.0 ? d : 1.0) : 0.0;
+    if (d > 0.0 && m.ciplv * are * dz / d + e_im > 1e-5) atomicAdd(&p.status->n_indeterminate, 1ull);
   }
 }
 
