@@ -83,6 +83,7 @@ struct Tmaps {
 struct ps_ctx {
   int device = 0;
   int num_sms = 148;
+  size_t total_mem = 0;  // device memory (cudaDeviceProp.totalGlobalMem)
   bool timing = false;
   std::mutex mu;
   std::map<PlanKey, cufftHandle> plans;
@@ -785,10 +786,13 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     // items per group = tiles in 128-row halves for the single-CTA variant
     const int slots = c->num_sms / (g.split ? split_cta_group() : 1);
     const long long per_group = (long long)mine.size() * g.B * (g.split ? kSplitBM / split_panel_rows() : 1);
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
+    // partial-sum workspace budget from the device's total memory (fixed per
+    // device: the trial-group choice -- and with it the summation order --
+    // does not depend on what else happens to be allocated, and no
+    // cudaMemGetInfo on the call path: it can stall for tens of ms while
+    // another process queries the driver, e.g. nvidia-smi)
     const size_t ws_per_group = (size_t)g.B * g.N * g.N * (g.split ? 4 : 8) * 5;  // worst case: 5 metrics
-    const size_t ws_budget = std::min<size_t>(free_b / 4, (size_t)24 << 30);
+    const size_t ws_budget = std::min<size_t>(c->total_mem / 6, (size_t)24 << 30);
     k.G = (k.shard_count > 1 || force_g1) ? 1 : choose_groups(per_group, (int)g.R, slots, ws_per_group, ws_budget);
     static const int g_env = [] {
       const char* s = std::getenv("PS_GROUPS");  // experiment override
@@ -948,8 +952,8 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
 // synchronisation; the pipelined host paths keep the plane scan).
 ps_status mask_count_pass(ps_ctx* c, Call& k, cudaStream_t st) {
   const Geometry& g = k.g;
-  const long long ip = round_up(g.T, 8);
-  PS_TRY(ensure(c->ind, (size_t)g.rows * ip * 2));
+  const long long ip = round_up(g.T, 16);  // E4M3 bytes, 16-byte rows for TMA
+  PS_TRY(ensure(c->ind, (size_t)g.rows * ip));
   PS_CUDA(launch_indicator_plane(c->planes.p, g.plane_stride, g.split ? 1 : 0, g.rows, (int)g.pitch, (int)g.T,
                                  c->ind.p, (int)ip, st));
   c->launches++;
@@ -990,25 +994,24 @@ ps_status mask_count_pass(ps_ctx* c, Call& k, cudaStream_t st) {
   pc.items = static_cast<const Item*>(c->cntitems.p);
   pc.n_items = (int)items.size();
   pc.status = c->d_status;
-  pc.kc_blocks = 64;  // drains are exact for integer counts: long chunks
+  pc.kc_blocks = 16;  // 16 x 128-sample stages per drain (exact for integer counts)
   pc.cnt = static_cast<int*>(c->cntws.p);
   auto enc = encode_fn();
   if (!enc) return fail(PS_E_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
   CUtensorMap ta, tb;
   cuuint64_t dims[4] = {(cuuint64_t)g.T, (cuuint64_t)g.N, (cuuint64_t)(g.B * g.R), 1};
-  cuuint64_t strides[3] = {(cuuint64_t)ip * 2, (cuuint64_t)(g.N * ip * 2), (cuuint64_t)(g.rows * ip * 2)};
-  cuuint32_t boxA[4] = {(cuuint32_t)kSplitBK, 128u, 1, 1};
-  cuuint32_t boxB[4] = {(cuuint32_t)kSplitBK, (cuuint32_t)split_b_box_rows(), 1, 1};
+  cuuint64_t strides[3] = {(cuuint64_t)ip, (cuuint64_t)(g.N * ip), (cuuint64_t)(g.rows * ip)};
+  // 128 one-byte samples per stage row: the 128B swizzle of the MK kernel
+  cuuint32_t boxA[4] = {(cuuint32_t)(4 * kSplitBK), 128u, 1, 1};
+  cuuint32_t boxB[4] = {(cuuint32_t)(4 * kSplitBK), (cuuint32_t)split_b_box_rows(), 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUtensorMapSwizzle swz = kSplitBK == 16   ? CU_TENSOR_MAP_SWIZZLE_32B
-                                 : kSplitBK == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                  : CU_TENSOR_MAP_SWIZZLE_128B;
-  const CUresult r1 = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->ind.p, dims, strides, boxA, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  const CUresult r2 = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, c->ind.p, dims, strides, boxB, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  static_assert(kSplitBK == 32, "the fp8 count operand rows are 128 bytes (4 x kSplitBK samples)");
+  const CUresult r1 = enc(&ta, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, c->ind.p, dims, strides, boxA, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const CUresult r2 = enc(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, c->ind.p, dims, strides, boxB, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r1 != CUDA_SUCCESS || r2 != CUDA_SUCCESS)
     return fail(PS_E_CUDA, "cuTensorMapEncodeTiled (indicator plane) failed");
   const int grid = std::min(pc.n_items, c->num_sms / split_cta_group());
@@ -1855,6 +1858,7 @@ ps_status ps_ctx_create(int device, ps_ctx** out) {
   ps_ctx* c = new ps_ctx();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  c->total_mem = prop.totalGlobalMem;
   if (cudaMalloc(&c->d_status, sizeof(DevStatus)) != cudaSuccess ||
       cudaMallocHost(&c->h_status, sizeof(DevStatus)) != cudaSuccess) {
     delete c;

@@ -78,12 +78,16 @@ constexpr int HALF = BN / (NEPI_WARPS / 4);    // columns per epilogue warp
 // the conversion adds ~80 KB of LSU shared-memory traffic per stage against
 // the 24 KB of TMA writes it saves, on an SM whose shared memory is already
 // busy feeding 18 UMMAs per stage (profiles/r01_gauss_conv.txt).
-// MK = true: the mask-count Gram (K7).  One fp16 plane per
-// operand holds the unmasked indicator u(t) in {0, 1}; one UMMA per K step
-// accumulates T_ij = sum_t u_i(t) u_j(t) -- exact in fp32 for T < 2^24 (every
-// partial sum is an integer below 2^24, so the accumulate never rounds) --
-// and the epilogue stores the per-pair counts (int32) the metric epilogue of
-// the main Gram then reads instead of scanning the planes.
+// MK = true: the mask-count Gram (K7).  One E4M3 (fp8) plane per
+// operand holds the unmasked indicator u(t) in {0, 1} (1 byte per sample);
+// one kind::f8f6f4 UMMA (K = 32) per 32-sample stage accumulates
+// T_ij = sum_t u_i(t) u_j(t) -- exact in fp32 for T < 2^24 (every partial sum
+// is an integer below 2^24, so the accumulate never rounds) -- and the
+// epilogue stores the per-pair counts (int32) the metric epilogue of the main
+// Gram then reads instead of scanning the planes.  A stage holds 128 samples
+// (128-byte operand rows, the 128B swizzle, 1024-byte 8-row groups; four K =
+// 32 UMMAs per stage): TMA moves whole 128-byte row segments, 4x fewer row
+// requests per sample than 32-sample stages.
 template <int CG, bool GS = false, bool MK = false>
 struct Geo {
   static constexpr int BNT = BN;                         // tile columns (UMMA N)
@@ -93,13 +97,15 @@ struct Geo {
   static constexpr uint32_t BUF = NACC * BNT;            // TMEM columns per buffer
   static constexpr int NPL = GS ? 6 : (MK ? 1 : 4);      // planes staged per operand
   static constexpr int BNC = BNT / CG;                   // J-panel rows staged per CTA
-  static constexpr int A_PLANE = BMC * BK * 2;
-  static constexpr int B_PLANE = BNC * BK * 2;
+  static constexpr int ES = MK ? 1 : 2;                  // operand bytes per sample
+  static constexpr int KB = MK ? 4 * BK : BK;            // samples per pipeline stage
+  static constexpr int A_PLANE = BMC * KB * ES;
+  static constexpr int B_PLANE = BNC * KB * ES;
   static constexpr int A_BYTES = NPL * A_PLANE;
   static constexpr int B_BYTES = NPL * B_PLANE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;  // per CTA
   // (GS, CG = 1: a 128-row J panel makes a 96 KB stage -- two fit the 227 KB)
-  static constexpr int STAGES = MK ? 8 : GS ? (CG == 2 ? 3 : 2) : (CG == 2 ? 4 : 3);
+  static constexpr int STAGES = MK ? 6 : GS ? (CG == 2 ? 3 : 2) : (CG == 2 ? 4 : 3);
   static_assert(STAGES * STAGE_BYTES + 1024 + 256 <= 227 * 1024, "stages must fit shared memory");
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
   static constexpr int UMMA_M = BMC * CG;
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  const int nk = (p.T + BK - 1) / BK;
+  const int nk = (p.T + G::KB - 1) / G::KB;
   const int kcb = p.kc_blocks;
   const int nchunks = (nk + kcb - 1) / kcb;
 
@@ -508,20 +514,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (CV) {
               // each CTA counts its own 4 + 4 planes; its epilogue warps convert
               ptx::mbar_arrive_expect_tx(&full[stage], LOAD_BYTES);
-              ptx::tma_load_4d(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
-              ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
+              ptx::tma_load_4d(sa, &tmA, &full[stage], kb * G::KB, rowA, u, 0);
+              ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * G::KB, rowB, u, 0);
             } else if (CG == 1) {
               ptx::mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
-              ptx::tma_load_4d(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
-              ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
-              if (GS) ptx::tma_load_4d(sa + G::A_BYTES + 2 * G::B_PLANE, &tmB2, &full[stage], kb * BK, rowB, u, 4);
+              ptx::tma_load_4d(sa, &tmA, &full[stage], kb * G::KB, rowA, u, 0);
+              ptx::tma_load_4d(sa + G::A_BYTES, &tmB, &full[stage], kb * G::KB, rowB, u, 0);
+              if (GS) ptx::tma_load_4d(sa + G::A_BYTES + 2 * G::B_PLANE, &tmB2, &full[stage], kb * G::KB, rowB, u, 4);
             } else {
               // rank 0's full barrier counts the bytes of both CTAs
               if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * G::STAGE_BYTES);
-              ptx::tma_load_4d_cg2(sa, &tmA, &full[stage], kb * BK, rowA, u, 0);
-              ptx::tma_load_4d_cg2(sa + G::A_BYTES, &tmB, &full[stage], kb * BK, rowB, u, 0);
+              ptx::tma_load_4d_cg2(sa, &tmA, &full[stage], kb * G::KB, rowA, u, 0);
+              ptx::tma_load_4d_cg2(sa + G::A_BYTES, &tmB, &full[stage], kb * G::KB, rowB, u, 0);
               if (GS)
-                ptx::tma_load_4d_cg2(sa + G::A_BYTES + 2 * G::B_PLANE, &tmB2, &full[stage], kb * BK, rowB, u, 4);
+                ptx::tma_load_4d_cg2(sa + G::A_BYTES + 2 * G::B_PLANE, &tmB2, &full[stage], kb * G::KB, rowB, u, 4);
             }
             if (++stage == G::STAGES) {
               stage = 0;
@@ -579,8 +585,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               const uint64_t bIl = dB + ko + 3 * (G::B_PLANE >> 4);  // GS: S lo
               const uint32_t acc0 = (chunk_start && ks == 0) ? 0u : 1u;
               if constexpr (MK) {
-                // T_ij += u_i . u_j  (plane 0 of each operand: the unmasked indicator)
-                ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRh, idesc_pos, acc0);
+                // T_ij += u_i . u_j over the stage's 128 samples: four fp8
+                // UMMAs (K = 32), each 32 bytes further along the swizzled rows
+                if (ks == 0) {
+                  const uint64_t a8 = ptx::make_smem_desc(sa_u, 8u * G::KB, 2u);  // 128B swizzle
+                  const uint64_t b8 = a8 + (uint64_t)(G::A_BYTES >> 4);
+#pragma unroll
+                  for (int k8 = 0; k8 < G::KB / 32; ++k8)
+                    ptx::mma_f8_ss_warp<CG>(d_re, a8 + 2 * k8, b8 + 2 * k8, idesc_pos, (chunk_start && k8 == 0) ? 0u : 1u);
+                }
               } else if constexpr (GS) {
                 const uint64_t aSh = dA + ko + 4 * (G::A_PLANE >> 4);
                 const uint64_t aSl = dA + ko + 5 * (G::A_PLANE >> 4);

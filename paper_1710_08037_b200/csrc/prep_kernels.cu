@@ -646,10 +646,13 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(SrcDesc src, long lo
       }
       return prefix;
     };
+    // PhasorEpochs (KIND 2, plv_matrix input): masked
+    // samples are the exact zeros -- no amplitude floor, no
+    // median (the oracle's phasors_from_unit); the selection is skipped
     const long long k1 = (T % 2 == 0) ? (T / 2 - 1) : (T / 2);
-    const unsigned long long v1 = select_kth(k1);
+    const unsigned long long v1 = KIND == 2 ? 0ull : select_kth(k1);
     unsigned long long v2 = v1;
-    if (T % 2 == 0) {
+    if (KIND != 2 && T % 2 == 0) {
       // count of keys <= v1 and the smallest key > v1
       unsigned long long mgt = ~0ull;
       long long cle = 0;
@@ -683,7 +686,7 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(SrcDesc src, long lo
       __syncthreads();
     }
     const double median = 0.5 * (val_of(v1) + val_of(v2));
-    const double thr = amp_floor * median;
+    const double thr = KIND == 2 ? 0.0 : amp_floor * median;
     // ---- masking pass ---------------------------------------------------
     long long cnt = 0;
     const long long obase = (FMT == OUT_COMPLEX ? rl : r) * pitch;
@@ -708,6 +711,41 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(SrcDesc src, long lo
       if (cnt == T) atomicOr(&st->flags, FLAG_ALL_MASKED);
     }
     __syncthreads();
+  }
+}
+
+// PhasorEpochs (KIND 2): masked samples are the exact zeros, which the
+// normaliser already wrote as z = 0; rows whose minimum |z| is 0 only need
+// their zeros counted.  One warp per row, coalesced along samples (the
+// general fixup's block-per-row median machinery is not needed).
+template <typename IT>
+__global__ void phasor_zero_count_kernel(SrcDesc src, long long row0, long long nrows,
+                                         const unsigned long long* rowmin, int* maskcount, DevStatus* st) {
+  const int lane = threadIdx.x & 31;
+  const long long wpb = blockDim.x >> 5;
+  const long long T = src.T;
+  for (long long rl = (long long)blockIdx.x * wpb + (threadIdx.x >> 5); rl < nrows; rl += (long long)gridDim.x * wpb) {
+    const long long r = row0 + rl;
+    if (val_of(rowmin[r]) != 0.0) {
+      if (lane == 0) maskcount[r] = 0;
+      continue;
+    }
+    const long long roff = row_offset(src, r);
+    long long cnt = 0;
+    for (long long t = lane; t < T; t += 32) {
+      const IT* q = static_cast<const IT*>(src.ptr) + 2 * (roff + t * src.s_samp);
+      cnt += (q[0] == IT(0) && q[1] == IT(0)) ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) {
+      maskcount[r] = static_cast<int>(cnt);
+      atomicAdd(&st->n_fix_rows, 1);
+      if (cnt > 0) {
+        atomicOr(&st->flags, FLAG_ANY_MASKED);
+        atomicAdd(&st->n_masked, static_cast<unsigned long long>(cnt));
+      }
+      if (cnt == T) atomicOr(&st->flags, FLAG_ALL_MASKED);
+    }
   }
 }
 
@@ -1377,6 +1415,14 @@ cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows
   const unsigned grid = static_cast<unsigned>(nrows < 148 * 8 ? nrows : 148 * 8);
   const unsigned long long* rowmin = rowstat;
   const unsigned long long* rowmax = rowstat + rows_total;
+  if (src.kind == 2) {  // phasors: count the exact zeros (no median)
+    const unsigned g = static_cast<unsigned>(std::min<long long>((nrows + 7) / 8, 148LL * 16));
+    if (src.is_double)
+      phasor_zero_count_kernel<double><<<g, 256, 0, st>>>(src, row0, nrows, rowmin, maskcount, status);
+    else
+      phasor_zero_count_kernel<float><<<g, 256, 0, st>>>(src, row0, nrows, rowmin, maskcount, status);
+    return cudaGetLastError();
+  }
   if (src.kind == 0) {
     if (fmt == OUT_SPLIT) PS_FIX_DISPATCH(0, OUT_SPLIT);
     else if (fmt == OUT_F64) PS_FIX_DISPATCH(0, OUT_F64);
@@ -1422,28 +1468,29 @@ cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void
 
 // K7 operand: u(t) = 1 where a sample is unmasked (masked samples are exactly
 // 0 in every plane; an unmasked unit phasor never has both hi parts 0), 0 where
-// masked or in the row padding.  One thread per 8-sample chunk, 16-byte store.
+// masked or in the row padding -- as E4M3 bytes (1.0 = 0x38).  One thread per
+// 16-sample chunk, 16-byte store.
 __device__ __forceinline__ bool is_zero_el(__half v) { return __half2float(v) == 0.0f; }
 __device__ __forceinline__ bool is_zero_el(double v) { return v == 0.0; }
 
 template <typename E, int IM_PLANE>
 __global__ void indicator_plane_kernel(const E* __restrict__ planes, long long ps, long long rows, int Tp, int T,
-                                       __half* __restrict__ ind, int ip) {
-  const long long cpr = ip / 8;
+                                       uint8_t* __restrict__ ind, int ip) {
+  const long long cpr = ip / 16;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < rows * cpr;
        e += (long long)gridDim.x * blockDim.x) {
     const long long r = e / cpr;
-    const int t0 = (int)(e % cpr) * 8;
-    __align__(16) __half v[8];
+    const int t0 = (int)(e % cpr) * 16;
+    __align__(16) uint8_t v[16];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < 16; ++k) {
       const int t = t0 + k;
       bool u = false;
       if (t < T) {
         const long long idx = r * Tp + t;
         u = !(is_zero_el(planes[idx]) && is_zero_el(planes[IM_PLANE * ps + idx]));
       }
-      v[k] = __float2half_rn(u ? 1.0f : 0.0f);
+      v[k] = u ? 0x38 : 0x00;  // E4M3 1.0 / 0.0
     }
     *reinterpret_cast<uint4*>(ind + r * ip + t0) = *reinterpret_cast<const uint4*>(v);
   }
@@ -1451,13 +1498,13 @@ __global__ void indicator_plane_kernel(const E* __restrict__ planes, long long p
 
 cudaError_t launch_indicator_plane(const void* planes, long long plane_stride, int split, long long rows, int Tp,
                                    int T, void* ind, int ind_pitch, cudaStream_t st) {
-  const int g = grid_for(rows * (ind_pitch / 8), 256);
+  const int g = grid_for(rows * (ind_pitch / 16), 256);
   if (split)
     indicator_plane_kernel<__half, 2><<<g, 256, 0, st>>>((const __half*)planes, plane_stride, rows, Tp, T,
-                                                          (__half*)ind, ind_pitch);
+                                                          (uint8_t*)ind, ind_pitch);
   else
     indicator_plane_kernel<double, 1><<<g, 256, 0, st>>>((const double*)planes, plane_stride, rows, Tp, T,
-                                                          (__half*)ind, ind_pitch);
+                                                          (uint8_t*)ind, ind_pitch);
   return cudaGetLastError();
 }
 
