@@ -95,6 +95,7 @@ struct ps_ctx {
   Buf sortws;              // device-side ordering of the ciPLV refinement queue
   Buf shardtiles;          // (I, J) of the tiles one shard owns (ps_shard_pack / unpack)
   Buf ind, cntws, cntitems;  // K7: unmasked-indicator plane, per-pair counts, count-pass items
+  Buf profbuf;               // PS_GRAM_PROF counters
   std::vector<cudaEvent_t> tev;  // timing events of the staged path (2 per stage)
   DevStatus* d_status = nullptr;
   DevStatus* h_status = nullptr;  // pinned
@@ -231,6 +232,7 @@ SrcDesc make_src(const ps_plv_args* a, const Geometry& g, const void* ptr) {
   s.h_row0 = 0;
   s.h_ld = g.T;
   s.h_scale = nullptr;
+  s.gauss_planes = 0;
   return s;
 }
 
@@ -526,6 +528,11 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
   };
   const long long rc = a->input_kind == PS_INPUT_REAL ? prep_chunk_rows(a, g) : (row_hi - row_lo);
   const bool bandpass = a->input_kind == PS_INPUT_REAL && a->fir;
+  // Gauss Gram: the vectorised normaliser writes the S / D planes in the same
+  // pass; any chunk that took another route gets them from gauss_planes_kernel
+  const bool want_gauss = g.gauss && fmt == 0 && !gauss_smem_convert();
+  src.gauss_planes = want_gauss ? 1 : 0;
+  bool gauss_all = true;
   const bool fused = a->input_kind == PS_INPUT_REAL && !bandpass && hilbert_fused_enabled() &&
                      hilbert_fused_supported(src, fmt, g.cdouble ? 1 : 0, (int)pitch);
   for (long long row0 = row_lo; row0 < row_hi; row0 += rc) {
@@ -533,8 +540,10 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
     if (bandpass) {  // Hf was computed by prep_begin for this call
       SrcDesc fs;
       PS_TRY(bandpass_chunk(c, a, g, src, row0, nr, true, st, &fs));
+      int gd = 0;
       PS_CUDA(launch_normalize_fmt(fs, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
-                                   c->d_status, st));
+                                   c->d_status, st, &gd));
+      gauss_all = gauss_all && gd;
       PS_CUDA(launch_fixup_fmt(fs, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
                                static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
       c->launches += 2;
@@ -548,6 +557,7 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
       src.h_row0 = row0;
       PS_CUDA(launch_hilbert_fused(src, row0, nr, out, (int)pitch, plane_stride, rs, g.rows, a->amp_floor,
                                    c->d_status, st));
+      gauss_all = false;
       PS_CUDA(launch_fixup_fmt(src, row0, nr, out, fmt, 0, (int)pitch, plane_stride, rs, g.rows,
                                static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
       c->launches += 2;
@@ -558,13 +568,15 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
       src.hbuf = c->hbuf.p;
       src.h_row0 = row0;
     }
+    int gd = 0;
     PS_CUDA(launch_normalize_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
-                                 c->d_status, st));
+                                 c->d_status, st, &gd));
+    gauss_all = gauss_all && gd;
     PS_CUDA(launch_fixup_fmt(src, row0, nr, out_at(row0), fmt, g.cdouble, (int)pitch, plane_stride, rs, g.rows,
                              static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
     c->launches += 2;
   }
-  if (g.gauss && fmt == 0 && !gauss_smem_convert()) {  // S = Zr + Zi, D = Zr - Zi planes of the Gauss Gram (after any masking)
+  if (want_gauss && !gauss_all) {  // S = Zr + Zi, D = Zr - Zi planes of the Gauss Gram (after any masking)
     PS_CUDA(launch_gauss_planes(out, plane_stride, row_lo * pitch, row_hi * pitch, st));
     c->launches++;
   }
@@ -686,14 +698,49 @@ int kc_blocks_default() {
   return kcb;
 }
 
-// Supertile edge (in ownership tiles) of the item raster order within a stage.
-int raster_tiles() {
-  static const int S = [] {
+// Supertile of the item raster order within a stage: SI row panels x SJ
+// column panels, and the order inside it (0: J-major, 1: I-major).  The 74
+// items in flight at a time share their operand panels through L2; what a
+// wave fetches from DRAM is (rows of its A panels + rows of its B panels) x
+// T, so the raster shapes a wave to cover few 256-row A panels and more
+// 128-row B panels.  PS_RASTER="SI[,SJ[,order]]" (experiments).
+struct Raster {
+  int si = 12, sj = 12, order = 0;
+};
+// Defaults per Gram variant: the Gauss Gram streams 8 planes (16 B per row
+// sample), so a wave's DRAM traffic is twice the 4-product's: it takes 8 row
+// panels x 12 column panels, I-major (a wave of 74 items spans ~6 A panels and
+// ~12 B panels; C5 Gram 53.1 -> 50.2 ms), the 4-product keeps the square
+// 12 x 12 J-major raster (C3 13.7 ms against 14.7 with the Gauss shape;
+// profiles/r02_raster_lockstep.txt, r02_sweep_variants.txt)
+Raster raster_shape(bool gauss) {
+  static const bool has_env = std::getenv("PS_RASTER") != nullptr;
+  if (!has_env) {
+    Raster d;
+    if (gauss) {
+      d.si = 8;
+      d.sj = 12;
+      d.order = 1;
+    }
+    return d;
+  }
+  static const Raster r = [] {
+    Raster x;
     const char* s = std::getenv("PS_RASTER");
-    return s ? std::max(1, std::atoi(s)) : 12;
+    if (s) {
+      x.si = x.sj = std::max(1, std::atoi(s));
+      const char* c = std::strchr(s, ',');
+      if (c) {
+        x.sj = std::max(1, std::atoi(c + 1));
+        c = std::strchr(c + 1, ',');
+        if (c) x.order = std::atoi(c + 1) != 0 ? 1 : 0;
+      }
+    }
+    return x;
   }();
-  return S;
+  return r;
 }
+int raster_tiles() { return raster_shape(false).si; }
 
 // Row panels per streamed output band in the final row stage.
 int row_band_last(int row_band) {
@@ -767,12 +814,17 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
   // is one output block of full upper rows); the in-flight window (~74
   // consecutive items: ~74/S column panels x S row panels) stays L2-sized.
   // Column stages: S x S supertile raster.
+  const Raster rs = raster_shape(g.gauss);
   std::stable_sort(mine.begin(), mine.end(), [&](const std::pair<int, int>& x, const std::pair<int, int>& y) {
     const int sx = stage_of(x), sy = stage_of(y);
-    const int bx = row_band > 0 ? band_of(sx) : S, by = row_band > 0 ? band_of(sy) : S;
-    const int xs = row_band > 0 ? 0 : x.second / S, ys = row_band > 0 ? 0 : y.second / S;
-    return std::make_tuple(sx, xs, x.first / bx, x.second, x.first) <
-           std::make_tuple(sy, ys, y.first / by, y.second, y.first);
+    if (row_band > 0) {
+      const int bx = band_of(sx), by = band_of(sy);
+      return std::make_tuple(sx, x.first / bx, x.second, x.first) < std::make_tuple(sy, y.first / by, y.second, y.first);
+    }
+    const int ix = rs.order ? x.first : x.second, jx = rs.order ? x.second : x.first;
+    const int iy = rs.order ? y.first : y.second, jy = rs.order ? y.second : y.first;
+    return std::make_tuple(sx, x.second / rs.sj, x.first / rs.si, ix, jx) <
+           std::make_tuple(sy, y.second / rs.sj, y.first / rs.si, iy, jy);
   });
   k.pool = a->trial_reduce == PS_TRIALS_POOL;
   if (k.pool || g.R == 1) {
@@ -1045,9 +1097,11 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
   const int grid = std::min(p.n_items, c->num_sms / cta_per_group);
   // producer lockstep (GramParams::lock_cnt): needs the same number of K
   // blocks in every item; PS_LOCKSTEP="group,lag" in K blocks ("0" = off)
-  static const std::pair<int, int> lk = [] {
+  // (group, lag) in K blocks: the Gauss Gram's 8-plane working set takes the
+  // tighter window (16, 2); the 4-product (32, 2) (profiles/r02_raster_lockstep.txt)
+  static const std::pair<int, int> lk_env = [] {
     const char* s = std::getenv("PS_LOCKSTEP");
-    int g = 32, l = 2;
+    int g = -1, l = 2;
     if (s) {
       g = std::atoi(s);
       const char* comma = std::strchr(s, ',');
@@ -1055,6 +1109,7 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
     }
     return std::make_pair(g, l);
   }();
+  const std::pair<int, int> lk = lk_env.first >= 0 ? lk_env : std::make_pair(k.g.gauss ? 16 : 32, 2);
   p.lock_cnt = nullptr;
   const bool uniform = k.pool || (k.g.R % k.Rg) == 0;
   if (k.g.split && lk.first > 0 && uniform) {
@@ -1071,9 +1126,31 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
     p.lock_lag = lk.second;
     p.lock_rounds = (int)rounds;
   }
+  static const bool prof = std::getenv("PS_GRAM_PROF") != nullptr;  // diagnostics: pipeline wait cycles
+  if (prof && k.g.split) {
+    PS_TRY(ensure(c->profbuf, 8 * sizeof(unsigned long long)));
+    PS_CUDA(cudaMemsetAsync(c->profbuf.p, 0, 8 * sizeof(unsigned long long), st));
+    p.prof = static_cast<unsigned long long*>(c->profbuf.p);
+  }
+  static const int pf = [] {
+    const char* e = std::getenv("PS_PREFETCH");  // L2 prefetch distance (K blocks); 0 = off
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  p.prefetch_blocks = pf;
   if (k.g.split) PS_CUDA(launch_gram_split(k.ta, k.tb, k.tb2, k.g.gauss, p, grid, st));
   else PS_CUDA(launch_gram_f64(p, grid, st));
   c->launches++;
+  if (p.prof) {
+    unsigned long long h[8];
+    PS_CUDA(cudaMemcpyAsync(h, p.prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+    PS_CUDA(cudaStreamSynchronize(st));
+    const double mt = (double)std::max<unsigned long long>(h[2], 1), pt = (double)std::max<unsigned long long>(h[4], 1);
+    std::fprintf(stderr,
+                 "[gram-prof] variant %s items %d grid %d: MMA issuer blocked on operands %.1f%%, on TMEM buffers "
+                 "%.1f%%; producer blocked on free stages %.1f%%\n",
+                 k.g.gauss ? "gauss" : "4prod", p.n_items, grid, 100.0 * h[0] / mt, 100.0 * h[1] / mt,
+                 100.0 * h[3] / pt);
+  }
   return PS_OK;
 }
 
@@ -1876,7 +1953,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (Buf* b : {&c->xw, &c->spec, &c->hbuf, &c->planes, &c->rowstat, &c->maskcount, &c->items, &c->gws, &c->hin,
                  &c->hout, &c->refine, &c->refine_sorted, &c->planes_t, &c->maskcount_t, &c->fir_taps,
                  &c->fir_spec, &c->cohws, &c->lockbuf, &c->hscale, &c->sortws, &c->sbinfo, &c->rpick,
-                 &c->shardtiles, &c->ind, &c->cntws, &c->cntitems})
+                 &c->shardtiles, &c->ind, &c->cntws, &c->cntitems, &c->profbuf})
     if (b->p) cudaFree(b->p);
   if (c->d_status) cudaFree(c->d_status);
   if (c->h_status) cudaFreeHost(c->h_status);

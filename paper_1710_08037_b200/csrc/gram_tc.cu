@@ -463,6 +463,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      long long w_empty = 0;
+      const long long p_t0 = clock64();
       // lockstep bookkeeping (see GramParams::lock_cnt)
       const bool lock = p.lock_cnt != nullptr;
       const long long S = p.lock_group;
@@ -509,9 +511,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
             ++e;
-            ptx::mbar_wait(&empty[stage], phase ^ 1u, tflag);
+            if (p.prof) ptx::mbar_wait_prof(&empty[stage], phase ^ 1u, &w_empty);
+            else ptx::mbar_wait(&empty[stage], phase ^ 1u, tflag);
             uint8_t* sa = smem + stage * G::STAGE_BYTES;
-            if (CV) {
+            if (p.debug_flags & 64) {
+              // experiment (PS_DEBUG_EPI=64): no operand loads at all -- the
+              // stage is released without TMA, so the kernel times the MMA /
+              // epilogue pipeline alone (values meaningless)
+              if (CG == 1 || rank == 0) ptx::mbar_arrive(&full[stage]);
+            } else if (CV) {
               // each CTA counts its own 4 + 4 planes; its epilogue warps convert
               ptx::mbar_arrive_expect_tx(&full[stage], LOAD_BYTES);
               ptx::tma_load_4d(sa, &tmA, &full[stage], kb * G::KB, rowA, u, 0);
@@ -529,6 +537,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               if (GS)
                 ptx::tma_load_4d_cg2(sa + G::A_BYTES + 2 * G::B_PLANE, &tmB2, &full[stage], kb * G::KB, rowB, u, 4);
             }
+            if (p.prefetch_blocks > 0 && !(p.debug_flags & 64)) {
+              const int kp = kb + p.prefetch_blocks;
+              if (kp < nk) {
+                ptx::tma_prefetch_4d(&tmA, kp * G::KB, rowA, u, 0);
+                ptx::tma_prefetch_4d(&tmB, kp * G::KB, rowB, u, 0);
+                if (GS && !CV) ptx::tma_prefetch_4d(&tmB2, kp * G::KB, rowB, u, 4);
+              }
+            }
             if (++stage == G::STAGES) {
               stage = 0;
               phase ^= 1u;
@@ -537,6 +553,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
       if (lock && e > 0) atomicAdd(&p.lock_cnt[(e - 1) / S], 1);  // last (possibly partial) group
+      if (p.prof) {
+        atomicAdd(&p.prof[3], (unsigned long long)w_empty);
+        atomicAdd(&p.prof[4], (unsigned long long)(clock64() - p_t0));
+      }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (rank 0) =====================
@@ -547,6 +567,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t phase = 0;
       uint32_t uses[2] = {0u, 0u};
       int buf = 0;
+      long long w_full = 0, w_tempty = 0;
+      const long long m_t0 = clock64();
       for (int it = grp; it < p.n_items; it += ngrp) {
         const Item w = p.items[it];
         const int r0 = p.pool ? 0 : w.g * p.Rg;
@@ -556,7 +578,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const bool chunk_start = (kb % kcb) == 0;
             const bool chunk_end = (kb % kcb) == kcb - 1 || kb == nk - 1;
             if (chunk_start) {
-              ptx::mbar_wait(&tempty[buf], (uses[buf] & 1u) ^ 1u, tflag);
+              if (p.prof) ptx::mbar_wait_prof(&tempty[buf], (uses[buf] & 1u) ^ 1u, &w_tempty);
+              else ptx::mbar_wait(&tempty[buf], (uses[buf] & 1u) ^ 1u, tflag);
               ptx::tc_fence_after();
             }
             // __shfl_sync makes the operands provably warp-uniform, so ptxas
@@ -564,6 +587,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             const uint32_t d_re = __shfl_sync(0xffffffffu, tmem + (uint32_t)buf * G::BUF, 0);
             const uint32_t d_im = d_re + BN;
             if (CV) ptx::mbar_wait_cluster(&conv[stage], phase);
+            else if (p.prof) ptx::mbar_wait_prof(&full[stage], phase, &w_full);
             else ptx::mbar_wait(&full[stage], phase, tflag);
             ptx::tc_fence_after();
             // descriptor of the stage's A tile; planes / K sub-steps are
@@ -647,6 +671,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             }
           }
         }
+      }
+      if (p.prof && lane == 0) {
+        atomicAdd(&p.prof[0], (unsigned long long)w_full);
+        atomicAdd(&p.prof[1], (unsigned long long)w_tempty);
+        atomicAdd(&p.prof[2], (unsigned long long)(clock64() - m_t0));
       }
     }
   } else {

@@ -233,11 +233,31 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
       *reinterpret_cast<uint2*>(o + ps) = make_uint2(pack_half2(rlo[0], rlo[1]), pack_half2(rlo[2], rlo[3]));
       *reinterpret_cast<uint2*>(o + 2 * ps) = make_uint2(pack_half2(ih[0], ih[1]), pack_half2(ih[2], ih[3]));
       *reinterpret_cast<uint2*>(o + 3 * ps) = make_uint2(pack_half2(ilo[0], ilo[1]), pack_half2(ilo[2], ilo[3]));
+      if (src.gauss_planes) {
+        // Gauss-Gram operands S = Zr + Zi, D = Zr - Zi from the rounded split
+        // values -- the arithmetic of gauss_planes_kernel, fused here so the
+        // planes are not read back (16 B / sample saved)
+        __half sh[4], sl[4], dh[4], dl[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float zr = __half2float(rh[k]) + __half2float(rlo[k]);
+          const float zi = __half2float(ih[k]) + __half2float(ilo[k]);
+          const float S = zr + zi, D = zr - zi;
+          sh[k] = __float2half_rn(S);
+          sl[k] = __float2half_rn(S - __half2float(sh[k]));
+          dh[k] = __float2half_rn(D);
+          dl[k] = __float2half_rn(D - __half2float(dh[k]));
+        }
+        *reinterpret_cast<uint2*>(o + 4 * ps) = make_uint2(pack_half2(sh[0], sh[1]), pack_half2(sh[2], sh[3]));
+        *reinterpret_cast<uint2*>(o + 5 * ps) = make_uint2(pack_half2(sl[0], sl[1]), pack_half2(sl[2], sl[3]));
+        *reinterpret_cast<uint2*>(o + 6 * ps) = make_uint2(pack_half2(dh[0], dh[1]), pack_half2(dh[2], dh[3]));
+        *reinterpret_cast<uint2*>(o + 7 * ps) = make_uint2(pack_half2(dl[0], dl[1]), pack_half2(dl[2], dl[3]));
+      }
     } else if (t0 < pitch) {  // T % 4 == 0: the pitch pad is one 4-sample group
       __half* o = out + obase + t0;
       const uint2 z = make_uint2(0u, 0u);
-#pragma unroll
-      for (int pl = 0; pl < 4; ++pl) *reinterpret_cast<uint2*>(o + pl * ps) = z;
+      const int np = src.gauss_planes ? 8 : 4;
+      for (int pl = 0; pl < np; ++pl) *reinterpret_cast<uint2*>(o + pl * ps) = z;
     }
   }
   __shared__ float smin[kNormThreads / 32], smax[kNormThreads / 32];
@@ -694,6 +714,11 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(SrcDesc src, long lo
       const double a = row_amp<IT, S, KIND>(src, roff, r, t);
       if (a < thr || a == 0.0) {
         zero_z<S, FMT>(out, plane_stride, obase + t);
+        if (FMT == OUT_SPLIT && src.gauss_planes) {  // S, D planes written by the normaliser
+          __half* hp = static_cast<__half*>(out);
+#pragma unroll
+          for (int pl = 4; pl < 8; ++pl) hp[pl * plane_stride + obase + t] = __float2half_rn(0.0f);
+        }
         ++cnt;
       }
     }
@@ -1339,7 +1364,8 @@ cudaError_t launch_gauss_planes(void* planes, long long plane_stride, long long 
 
 cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
                                  int cdouble, int pitch, long long plane_stride, unsigned long long* rowstat,
-                                 long long rows_total, DevStatus* status, cudaStream_t st) {
+                                 long long rows_total, DevStatus* status, cudaStream_t st, int* gauss_done) {
+  if (gauss_done) *gauss_done = 0;
   // vectorised fast path: fp32 source, split planes, contiguous 16B-aligned rows
   {
     const bool aligned_base = (reinterpret_cast<uintptr_t>(src.ptr) & 15u) == 0 &&
@@ -1357,6 +1383,7 @@ cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long n
       __half* o = static_cast<__half*>(out);
       unsigned long long* rmin = rowstat;
       unsigned long long* rmax = rowstat + rows_total;
+      if (gauss_done) *gauss_done = src.gauss_planes ? 1 : 0;
       if (src.kind == 0)
         normalize_vec_kernel<0><<<(unsigned)vblk, kNormThreads, 0, st>>>(src, row0, vchunks, o, pitch, plane_stride,
                                                                          rmin, rmax, status);

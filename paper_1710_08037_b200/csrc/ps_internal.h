@@ -41,6 +41,8 @@ struct SrcDesc {
   long long h_row0;          // first row held in hbuf
   long long h_ld;            // hbuf row stride (elements; T unless band-pass padded)
   const void* h_scale;       // per-row factor on hbuf values ([rows_in_chunk], hbuf type), nullptr = 1
+  int gauss_planes;          // split output for the Gauss Gram: planes 4..7 (S, D hi / lo) are
+                             // written by the vectorised normaliser and zeroed by the fixup
 };
 
 // An ill-conditioned ciPLV value of the split path queued for exact FP64
@@ -108,6 +110,16 @@ struct GramParams {
   // read by the metric epilogues in place of the plane scan when samples are
   // masked.  nullptr: no count pass ran.
   int* cnt;
+  // PS_GRAM_PROF=1 (diagnostics): cycles the pipeline roles spent blocked,
+  // summed over CTAs: [0] MMA issuer on operand stages (full), [1] MMA issuer
+  // on accumulation buffers (tempty), [2] MMA issuer total, [3] producer on
+  // free stages (empty), [4] producer total.  nullptr: off.
+  unsigned long long* prof;
+  // split kernel producer: L2 prefetch distance in K blocks (0 = off); the
+  // operand slices of block kb + prefetch_blocks are pulled into L2 while
+  // block kb is loaded into shared memory (hides DRAM latency the few
+  // shared-memory stages cannot)
+  int prefetch_blocks;
 };
 
 // ---- launchers (return cudaError_t) --------------------------------------
@@ -123,9 +135,11 @@ cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_d
                                     cudaStream_t st);
 // fmt: 0 split fp16 planes, 1 f64 planes, 2 complex interleaved (compute type)
 // cdouble: compute in double although the source is float
+// *gauss_done (optional) = 1 when the Gauss planes 4..7 were written too
+// (vectorised path with src.gauss_planes), else 0
 cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
                                  int cdouble, int pitch, long long plane_stride, unsigned long long* rowstat,
-                                 long long rows_total, DevStatus* status, cudaStream_t st);
+                                 long long rows_total, DevStatus* status, cudaStream_t st, int* gauss_done = nullptr);
 cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
                              int cdouble, int pitch, long long plane_stride, const unsigned long long* rowstat,
                              long long rows_total, int* maskcount, double amp_floor, DevStatus* status,

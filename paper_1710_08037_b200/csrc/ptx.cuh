@@ -55,6 +55,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, int* /
   }
 }
 
+// mbar_wait that adds the cycles it spent blocked to *acc (profiling builds of
+// the pipeline: PS_GRAM_PROF)
+__device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, long long* acc) {
+  const uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try_wait(a, parity)) {
+    if (clock64() - t0 > 16000000000LL) asm volatile("trap;");
+  }
+  *acc += clock64() - t0;
+}
+
 // ---- TMA ------------------------------------------------------------------
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
@@ -64,6 +76,14 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 
 __device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+// L2 prefetch of a TMA box (no shared memory, no barrier): pulls the operand
+// slice a later tma_load_4d will read from DRAM into L2 ahead of time
+__device__ __forceinline__ void tma_prefetch_4d(const void* tmap, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 __device__ __forceinline__ void tma_load_4d(void* smem_dst, const void* tmap, uint64_t* bar, int c0,
                                             int c1, int c2, int c3) {

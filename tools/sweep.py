@@ -49,13 +49,14 @@ def child(cfg, steps=3):
 
 if __name__ == "__main__":
     if sys.argv[1] == "--child":
-        child(sys.argv[2])
+        child(sys.argv[2], steps=int(os.environ.get("SWEEP_STEPS", "3")))
         sys.exit(0)
     cfg = sys.argv[1]
     axes = []
     for a in sys.argv[2:]:
-        k, vs = a.split("=")
-        axes.append([(k, v) for v in vs.split(",")])
+        k, vs = a.split("=", 1)
+        sep = ";" if ";" in vs else ","  # values with commas (PS_LOCKSTEP=32,2;16,1)
+        axes.append([(k, v) for v in vs.split(sep)])
     for combo in itertools.product(*axes) if axes else [()]:
         env = dict(os.environ)
         env.update(dict(combo))
