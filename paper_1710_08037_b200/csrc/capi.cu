@@ -684,7 +684,13 @@ int gauss_mode() {
 void decide_gauss(const ps_plv_args* a, Call& k) {
   const bool eligible = k.g.split && a->mode == PS_MODE_OVER_SAMPLES;
   const long long round_len = a->trial_reduce == PS_TRIALS_POOL ? k.g.T * k.g.R : k.g.T;
-  const bool automatic = a->input_kind != PS_INPUT_REAL && round_len >= 8192;
+  // complex input: rounds >= 8192 samples (C5).  Real input, whose S / D
+  // planes now come out of the normaliser at 8 B / sample more writes: where
+  // the Gram dominates the normalisation by enough -- N >= 2048 signals and
+  // rounds >= 8192 (C3: step 17.7 -> 16.7 ms; C2, N = 1200: 6.3 -> 6.5 ms, not
+  // taken; profiles/r02_gauss_real_input.txt)
+  const bool automatic =
+      round_len >= 8192 && (a->input_kind != PS_INPUT_REAL || (k.g.N >= 2048 && !a->fir));
   const int m = gauss_mode();
   k.g.gauss = eligible && (m == 1 || (m == -1 && automatic));
 }
