@@ -232,3 +232,50 @@ def normalize_phasors(a, amp_floor: float = 1e-6) -> PhasorEpochs:
     if host:
         z, m = z.cpu().numpy(), m.cpu().numpy()
     return PhasorEpochs(data=z, mask=m)
+
+
+def instantaneous_phase(a):
+    """the angle of every complex sample, in (-pi, pi]; the
+    phase of 0 is defined as 0.  Elementwise on the input's own
+    device (torch for CUDA tensors, numpy for host arrays); accepts
+    AnalyticEpochs / PhasorEpochs or a complex array of any shape."""
+    import torch
+
+    src = _unwrap(a)
+    if isinstance(src, torch.Tensor):
+        ph = torch.angle(src)
+        return torch.where(ph == -math.pi, torch.full_like(ph, math.pi), ph)
+    ph = np.angle(np.asarray(src))
+    return np.where(ph == -np.pi, np.pi, ph)
+
+
+def downsample(x, factor: int, alias_tol: float = 0.01):
+    """SPEC.md:103-111: keep every factor-th sample (axis 1 of [N, T(, R)]);
+    RealEpochs.fs is divided by factor.  FactorTooLargeError when fewer than 2
+    samples would remain.  The caller guarantees band limitation below
+    pi / factor; an AliasingWarning is raised when more than `alias_tol` of the
+    (mean-removed) periodogram power lies above it."""
+    import torch
+
+    factor = int(factor)
+    if factor < 1:
+        raise ValueError("factor must be a positive integer")
+    src = _unwrap(x)
+    T = int(src.shape[1])
+    n_out = (T + factor - 1) // factor
+    if n_out < 2:
+        raise errors.FactorTooLargeError(f"downsampling {T} samples by {factor} leaves {n_out} < 2")
+    if factor > 1:
+        t = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.asarray(src))
+        v = t.movedim(1, -1).to(torch.float64)
+        p = torch.fft.rfft(v - v.mean(dim=-1, keepdim=True), dim=-1).abs().square().sum(
+            dim=tuple(range(v.dim() - 1)))
+        k_cut = T / (2.0 * factor)  # bin of pi / factor rad/sample
+        tot = float(p.sum())
+        if tot > 0.0 and float(p[int(math.floor(k_cut)) + 1:].sum()) > alias_tol * tot:
+            warnings.warn(f"signal has power above pi/{factor} rad/sample: downsampling aliases it",
+                          errors.AliasingWarning, stacklevel=2)
+    res = src[:, ::factor]
+    if isinstance(x, RealEpochs):
+        return RealEpochs(data=res, fs=None if x.fs is None else x.fs / factor)
+    return res
