@@ -555,9 +555,10 @@ ps_status prepare_rows(ps_ctx* c, const ps_plv_args* a, const Geometry& g, const
       PS_TRY(ensure(c->hbuf, (size_t)nr * g.T * sizeof(float)));
       src.hbuf = c->hbuf.p;
       src.h_row0 = row0;
+      int gd = 0;
       PS_CUDA(launch_hilbert_fused(src, row0, nr, out, (int)pitch, plane_stride, rs, g.rows, a->amp_floor,
-                                   c->d_status, st));
-      gauss_all = false;
+                                   c->d_status, st, &gd));
+      gauss_all = gauss_all && gd;
       PS_CUDA(launch_fixup_fmt(src, row0, nr, out, fmt, 0, (int)pitch, plane_stride, rs, g.rows,
                                static_cast<int*>(c->maskcount.p), a->amp_floor, c->d_status, st));
       c->launches += 2;
@@ -1153,9 +1154,11 @@ ps_status launch_stage(ps_ctx* c, Call& k, int s, cudaStream_t st) {
     const double mt = (double)std::max<unsigned long long>(h[2], 1), pt = (double)std::max<unsigned long long>(h[4], 1);
     std::fprintf(stderr,
                  "[gram-prof] variant %s items %d grid %d: MMA issuer blocked on operands %.1f%%, on TMEM buffers "
-                 "%.1f%%; producer blocked on free stages %.1f%%\n",
+                 "%.1f%%; producer blocked on free stages %.1f%%; epilogue warps blocked on accumulators %.1f%%, "
+                 "emitting %.1f%%\n",
                  k.g.gauss ? "gauss" : "4prod", p.n_items, grid, 100.0 * h[0] / mt, 100.0 * h[1] / mt,
-                 100.0 * h[3] / pt);
+                 100.0 * h[3] / pt, 100.0 * h[5] / std::max<unsigned long long>(h[7], 1),
+                 100.0 * h[6] / std::max<unsigned long long>(h[7], 1));
   }
   return PS_OK;
 }
@@ -1265,7 +1268,6 @@ ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
   }
   if (c->h_cnt_cap < n_stages) {
     if (c->h_cnt) cudaFreeHost(c->h_cnt);
-  if (c->h_sbflag) cudaFreeHost(c->h_sbflag);
     c->h_cnt = nullptr;
     PS_CUDA(cudaHostAlloc(&c->h_cnt, (size_t)n_stages * sizeof(unsigned long long),
                           cudaHostAllocMapped | cudaHostAllocPortable));
@@ -1822,6 +1824,19 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
 // ============================================================================
 // C ABI
 // ============================================================================
+namespace {
+// Every entry point starts from a clean runtime error state: the launch
+// wrappers report errors through cudaGetLastError(), so an error an earlier
+// call left pending (one whose status was deliberately ignored, e.g. an
+// elapsed-time query) must not surface as a failure of this one.
+// PS_DEBUG_STALE=1 names the entry point that found one (diagnostics).
+void clear_stale(const char* fn) {
+  static const bool dbg = std::getenv("PS_DEBUG_STALE") != nullptr;
+  const cudaError_t e = cudaGetLastError();
+  if (dbg && e != cudaSuccess) std::fprintf(stderr, "[ps] pending CUDA error at entry of %s: %s\n", fn, cudaGetErrorString(e));
+}
+}  // namespace
+
 extern "C" {
 
 int ps_abi_version(void) { return PS_ABI_VERSION; }
@@ -1904,16 +1919,19 @@ static ps_status shard_move(ps_ctx* c, int64_t N, int32_t precision, int32_t P, 
 
 ps_status ps_shard_pack(ps_ctx* c, int64_t n_signals, int32_t precision, int32_t shard_count, int32_t shard_index,
                         const void* matrix, void* packed, void* stream) {
+  clear_stale(__func__);
   return shard_move(c, n_signals, precision, shard_count, shard_index, matrix, packed, true, 0, stream);
 }
 
 ps_status ps_shard_unpack(ps_ctx* c, int64_t n_signals, int32_t precision, int32_t shard_count, int32_t shard_index,
                           const void* packed, void* matrix, int32_t mirror, void* stream) {
+  clear_stale(__func__);
   return shard_move(c, n_signals, precision, shard_count, shard_index, packed, matrix, false, mirror, stream);
 }
 
 ps_status ps_reduce_partials(ps_ctx* c, const void* parts, int32_t n_parts, int64_t part_stride, int64_t n,
                              double divisor, int32_t dtype, void* out, void* stream) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   if (!parts || !out) return fail(PS_E_INVALID, "NULL buffer");
   if (n_parts < 1 || n < 0 || part_stride < n) return fail(PS_E_INVALID, "need n_parts >= 1 and part_stride >= n");
@@ -1929,6 +1947,7 @@ ps_status ps_reduce_partials(ps_ctx* c, const void* parts, int32_t n_parts, int6
 const char* ps_last_error(void) { return g_last_error.c_str(); }
 
 ps_status ps_ctx_create(int device, ps_ctx** out) {
+  clear_stale(__func__);
   if (!out) return fail(PS_E_INVALID, "out is NULL");
   *out = nullptr;
   int ndev = 0;
@@ -1953,6 +1972,7 @@ ps_status ps_ctx_create(int device, ps_ctx** out) {
 }
 
 ps_status ps_ctx_destroy(ps_ctx* c) {
+  clear_stale(__func__);
   if (!c) return PS_OK;
   cudaSetDevice(c->device);
   for (auto& kv : c->plans) cufftDestroy(kv.second);
@@ -1971,11 +1991,13 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
   for (cudaStream_t s : {c->s_in, c->s_comp, c->s_ref, c->s_out})
     if (s) cudaStreamDestroy(s);
   if (c->h_cnt) cudaFreeHost(c->h_cnt);
+  if (c->h_sbflag) cudaFreeHost(c->h_sbflag);
   delete c;
   return PS_OK;
 }
 
 ps_status ps_ctx_set_timing(ps_ctx* c, int enable) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   c->timing = enable != 0;
   return PS_OK;
@@ -2085,6 +2107,7 @@ ps_status plv_family_locked(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res)
 extern "C" {
 
 ps_status ps_plv_family(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   std::lock_guard<std::mutex> lock(c->mu);
   return plv_family_locked(c, a, res);
@@ -2109,6 +2132,7 @@ int64_t ps_welch_bins(int64_t W, double lo, double hi, int64_t* first_bin) {
 // PLV-family epilogue reads as COH / ICOH / coherency -> mean (trial-mean
 // machinery) or max (band_max) over the band's bins.
 ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_plv_result* res) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   if (!w) return fail(PS_E_INVALID, "welch config is NULL");
   std::lock_guard<std::mutex> lock(c->mu);
@@ -2232,6 +2256,7 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
 
 ps_status ps_plv_family_staged(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, int32_t n_stages,
                                const int64_t* stage_cols, void* const* ready_events) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   std::lock_guard<std::mutex> lock(c->mu);
   Call k;
@@ -2542,14 +2567,17 @@ ps_status host_output_call(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res, 
 extern "C" {
 
 ps_status ps_plv_family_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  clear_stale(__func__);
   return host_output_call(c, a, res, /*dev_input=*/false);
 }
 
 ps_status ps_plv_family_to_host(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res) {
+  clear_stale(__func__);
   return host_output_call(c, a, res, /*dev_input=*/true);
 }
 
 ps_status ps_analytic_signal(ps_ctx* c, const ps_plv_args* a0, void* out) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   if (!out) return fail(PS_E_INVALID, "out is NULL");
   std::lock_guard<std::mutex> lock(c->mu);
@@ -2582,6 +2610,7 @@ ps_status ps_analytic_signal(ps_ctx* c, const ps_plv_args* a0, void* out) {
 }
 
 ps_status ps_filter_two_pass(ps_ctx* c, const ps_plv_args* a0, void* out) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   if (!out) return fail(PS_E_INVALID, "out is NULL");
   if (!a0 || !a0->fir) return fail(PS_E_INVALID, "args->fir is required");
@@ -2610,6 +2639,7 @@ ps_status ps_filter_two_pass(ps_ctx* c, const ps_plv_args* a0, void* out) {
 }
 
 ps_status ps_normalize_phasors(ps_ctx* c, const ps_plv_args* a, void* out, uint8_t* mask_out) {
+  clear_stale(__func__);
   if (!c) return fail(PS_E_INVALID, "ctx is NULL");
   if (!out) return fail(PS_E_INVALID, "out is NULL");
   std::lock_guard<std::mutex> lock(c->mu);

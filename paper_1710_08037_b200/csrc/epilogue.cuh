@@ -113,6 +113,13 @@ __device__ __forceinline__ long long effective_T(const GramParams& p, int u0, in
   return tot;
 }
 
+// Trial-mean scaling at the last round of a slot: split (fp32) outputs are
+// multiplied by the fp32 reciprocal 1 / R on every path that forms a mean
+// (interior and general epilogues, trial-group reduce), so any two paths
+// that sum the same terms produce bit-identical means; FP64 divides.
+__device__ __forceinline__ float mean_scale(float acc, int div) { return acc * (1.0f / (float)div); }
+__device__ __forceinline__ double mean_scale(double acc, int div) { return acc / (double)div; }
+
 // Accumulating store of one metric value into slot `base` at (i, j); the
 // mirror (j, i) is written at the last round of the slot (negated for the
 // antisymmetric signed imaginary part).
@@ -121,7 +128,7 @@ __device__ __forceinline__ void emit(S* base, long long N, int i, int j, S v, bo
                                      bool anti, bool mirror) {
   const long long idx = (long long)i * N + j;
   S acc = first ? v : base[idx] + v;
-  if (last && div != 1) acc = acc / S(div);
+  if (last && div != 1) acc = mean_scale(acc, div);
   base[idx] = acc;
   if (mirror && last && i != j) base[(long long)j * N + i] = anti ? -acc : acc;
 }
@@ -167,7 +174,8 @@ __device__ __forceinline__ void emit4_all(const GramParams& p, long long slot, i
     float4 a = make_float4(prev[q].x + v[0], prev[q].y + v[1], prev[q].z + v[2], prev[q].w + v[3]);
     if (last && p.mean_div != 1) {
       const float d = (float)p.mean_div;
-      a = make_float4(a.x / d, a.y / d, a.z / d, a.w / d);
+      const float rd = 1.0f / d;
+      a = make_float4(a.x * rd, a.y * rd, a.z * rd, a.w * rd);
     }
     float* base = outs[q] + off;
     if (!(p.debug_flags & 8)) *reinterpret_cast<float4*>(base + (long long)i * N + j0) = a;
@@ -187,35 +195,89 @@ __device__ __forceinline__ void st_v8(float* p, const float (&v)[8]) {
                "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
                : "memory");
 }
-// Eight consecutive columns j0..j0+7 of row i in the FIRST round of their
-// slot (plain stores, nothing to accumulate), all strictly above the diagonal
-// and inside (N % 8 == 0, j0 % 8 == 0): one 32-byte store per metric for the
-// direct part (a full sector per lane), coalesced mirror stores.
-__device__ __forceinline__ void emit8_first(const GramParams& p, long long slot, int i, int j0,
-                                            const PairMetrics<float> (&m)[8], bool last) {
+// Interior warp blocks (every pair strictly above the diagonal and inside,
+// no masks or K7 counts): the split metrics of one pair plus the quantities
+// the ill-conditioning test reuses (one MUFU.RSQ of 1 - Re^2 serves both the
+// ciPLV denominator and the test).  Same arithmetic as pair_metrics<float, true>.
+struct InteriorPair {
+  float plv, aim, ci, cre, cim;  // aim = iPLV
+  float are, d, rd;              // |Re|, 1 - Re^2, rsqrt(1 - Re^2) (for the test)
+};
+
+__device__ __forceinline__ InteriorPair interior_pair(float gre, float gim, float inv_t) {
+  InteriorPair m;
+  m.cre = gre * inv_t;
+  m.cim = gim * inv_t;
+  m.are = fabsf(m.cre);
+  m.aim = fabsf(m.cim);
+  const float ss = m.cre * m.cre + m.cim * m.cim;
+  const float plv = ss * rsqrtf(fmaxf(ss, 1e-30f));
+  m.plv = plv > 1.0f ? 1.0f : plv;
+  m.d = (1.0f - m.are) * (1.0f + m.are);
+  m.rd = rsqrtf(m.d);
+  const float ci = m.d > 0.0f ? m.aim * m.rd : 0.0f;
+  m.ci = ci > 1.0f ? 1.0f : ci;
+  return m;
+}
+
+
+// Eight consecutive columns of one row in the FIRST round of their slot
+// (plain stores, nothing to accumulate; N % 8 == 0): element offsets od of
+// the direct entry (i, j0) and om of the mirror entry (j0, i).  One 32-byte
+// store per metric for the direct part (a full sector per lane), mirror
+// stores coalesced across the warp's lanes (consecutive i), their addresses
+// stepped by one row (N) per column.  rdiv = 1 / trial-mean divisor at the
+// last round of a slot (else 1).  PLV / iPLV / ciPLV only: the signed Re / Im
+// outputs (rarely requested) go through emit_signed_round, outside the hot
+// loop, so the loop body stays small enough for the instruction cache.
+__device__ __forceinline__ void emit8_interior(const GramParams& p, long long od, long long om,
+                                               const InteriorPair (&m)[8], bool direct, bool mirror, float rdiv) {
   const long long N = p.N;
-  const long long off = slot * N * N;
-  float* outs[5] = {static_cast<float*>(p.out_plv), static_cast<float*>(p.out_iplv),
-                    static_cast<float*>(p.out_ciplv), static_cast<float*>(p.out_cre),
-                    static_cast<float*>(p.out_cim)};
 #pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    if (!outs[q]) continue;
-    float* base = outs[q] + off;
+  for (int q = 0; q < 3; ++q) {
+    float* o = static_cast<float*>(q == 0 ? p.out_plv : q == 1 ? p.out_iplv : p.out_ciplv);
+    if (!o) continue;
     float a[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      a[e] = q == 0 ? m[e].plv : q == 1 ? m[e].iplv : q == 2 ? m[e].ciplv : q == 3 ? m[e].cre : m[e].cim;
-    if (last && p.mean_div != 1) {
-      const float d = (float)p.mean_div;
+    for (int e = 0; e < 8; ++e) a[e] = (q == 0 ? m[e].plv : q == 1 ? m[e].aim : m[e].ci) * rdiv;
+    if (direct) st_v8(o + od, a);
+    if (mirror) {
+      float* mp = o + om;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) a[e] = a[e] / d;
+      for (int e = 0; e < 8; ++e, mp += N) *mp = a[e];
     }
-    if (!(p.debug_flags & 8)) st_v8(base + (long long)i * N + j0, a);
-    if (last && !p.upper_only && !(p.debug_flags & 4)) {
-      const float s = q == 4 ? -1.f : 1.f;
+  }
+}
+
+// Four consecutive columns of one row (N % 4 == 0), any round: one 16-byte
+// read-modify-write per metric for the direct part, all reads issued before
+// any write so their latencies overlap; mirror writes (last round) as in
+// emit8_interior.
+__device__ __forceinline__ void emit4_interior(const GramParams& p, long long od, long long om,
+                                               const InteriorPair (&m)[4], bool first, bool direct, bool mirror,
+                                               float rdiv) {
+  const long long N = p.N;
+  float* outs[3] = {static_cast<float*>(p.out_plv), static_cast<float*>(p.out_iplv),
+                    static_cast<float*>(p.out_ciplv)};
+  float4 prev[3];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) base[(long long)(j0 + e) * N + i] = s * a[e];
+  for (int q = 0; q < 3; ++q) {
+    prev[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (outs[q] && !first) prev[q] = *reinterpret_cast<const float4*>(outs[q] + od);
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    if (!outs[q]) continue;
+    auto val = [&](int e) { return q == 0 ? m[e].plv : q == 1 ? m[e].aim : m[e].ci; };
+    const float4 a = make_float4((prev[q].x + val(0)) * rdiv, (prev[q].y + val(1)) * rdiv,
+                                 (prev[q].z + val(2)) * rdiv, (prev[q].w + val(3)) * rdiv);
+    if (direct) *reinterpret_cast<float4*>(outs[q] + od) = a;
+    if (mirror) {
+      float* mp = outs[q] + om;
+      mp[0] = a.x;
+      mp[N] = a.y;
+      mp[2 * N] = a.z;
+      mp[3 * N] = a.w;
     }
   }
 }

@@ -222,6 +222,138 @@ __device__ __forceinline__ void store_sums(const float (&s)[H], uint32_t taddr) 
   }
 }
 
+// Signed Re / Im outputs (cre, cim) of one interior warp slice: a second pass
+// over the TMEM columns, only when requested.  inv(j) = 1 / T_ij.
+template <int BN, int HALF, typename InvF>
+__device__ __forceinline__ void emit_signed_round(const GramParams& p, uint32_t ta, int jb, long long od, long long om,
+                                                  InvF inv, bool first, bool direct, bool mirror, float rdiv) {
+  const long long N = p.N;
+#pragma unroll 1
+  for (int g = 0; g < HALF; g += 4) {
+    uint32_t vre[4], vim[4];
+    ptx::tmem_ld_32x32b_x4(ta + g, vre);
+    ptx::tmem_ld_32x32b_x4(ta + BN + g, vim);
+    ptx::tmem_wait_ld();
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      float* o = static_cast<float*>(q == 0 ? p.out_cre : p.out_cim);
+      if (!o) continue;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float v = __uint_as_float(q == 0 ? vre[e] : vim[e]) * inv(jb + g + e);
+        const long long d = od + g + e;
+        const float a = ((first ? 0.0f : o[d]) + v) * rdiv;
+        if (direct) o[d] = a;
+        if (mirror) o[om + (long long)(g + e) * N] = q == 1 ? -a : a;
+      }
+    }
+  }
+}
+
+// Interior warp block of one finished round (every pair of the warp's 32
+// rows x HALF columns strictly above the diagonal and inside; N % 4 == 0).
+// Kept compact for the instruction cache: MASKED (per-pair counts from the K7
+// Gram, p.cnt) is a template parameter, so the common unmasked loop carries
+// no count code, and the ill-conditioned pairs of a column group are queued
+// for refinement after the group from a bit mask (one copy of the queue code).
+template <int BN, int HALF, bool MASKED>
+__device__ __forceinline__ void emit_interior(const GramParams& p, const RoundInfo ri, uint32_t ta, int i, int jb,
+                                           float inv_t) {
+  unsigned illc = 0, nind = 0;
+  // ill-conditioning test of the general path, 1e-6 (|cim| are / d + 1) >
+  // tol sqrt(d), multiplied through by d / 1e-6 (d > 0): no division
+  const float kt = p.illcond_tol * 1e6f;
+  const float tol = p.illcond_tol;
+  auto inv_at = [&](int j) -> float {
+    if (!MASKED) return inv_t;
+    const long long cs = p.pool ? (long long)(ri.u0 / p.R) : (long long)ri.u0;
+    const int te = p.cnt[cs * (long long)p.N * p.N + (long long)i * p.N + j];  // i < j
+    if (te <= 0) {
+      atomicOr(&p.status->flags, FLAG_EMPTY_WINDOW);
+      return 0.0f;
+    }
+    return __frcp_rn(static_cast<float>(te));  // == 1.0f / te (correctly rounded)
+  };
+  // flags of one column group -> counters / refinement queue
+  auto flush = [&](unsigned fl, int j0, const InteriorPair* m) {
+    while (fl) {
+      const int e = __ffs(fl) - 1;
+      fl &= fl - 1;
+      ++illc;
+      if (p.refine) {
+        const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
+        if (k < (unsigned long long)p.refine_cap) {
+          RefineEntry en;
+          en.slot = (int)ri.slot;
+          en.i = i;
+          en.j = j0 + e;
+          en.u0 = ri.u0;
+          en.nu = ri.nu;
+          en.approx = m[e].ci;
+          p.refine[k] = en;
+        }
+      }
+    }
+  };
+  // Element offsets of this warp slice's first direct entry (i, jb) and
+  // first mirror entry (jb, i) in the slot, computed once per round: the
+  // per-group addresses are 64-bit adds (the mirror column walks rows by N)
+  const long long N = p.N;
+  const long long soff = ri.slot * N * N;
+  const long long od = soff + (long long)i * N + jb;
+  const long long om = soff + (long long)jb * N + i;
+  const bool mirror = ri.last && !p.upper_only && !(p.debug_flags & 4);
+  const bool direct = !(p.debug_flags & 8);
+  // trial mean: the last round of a slot scales by 1 / R (a reciprocal
+  // multiply keeps the division's slow path out of the emission loops)
+  const float rdiv = (ri.last && p.mean_div != 1) ? 1.0f / (float)p.mean_div : 1.0f;
+  if (ri.first && (p.N & 7) == 0) {
+    // first round of the slot: 8 columns per step, one 32-byte direct store
+    // per metric (a full sector per lane) and lane-coalesced mirror stores
+#pragma unroll 1
+    for (int g = 0; g < HALF; g += 8) {
+      uint32_t vre[8], vim[8];
+      ptx::tmem_ld_32x32b_x4(ta + g, *reinterpret_cast<uint32_t(*)[4]>(&vre[0]));
+      ptx::tmem_ld_32x32b_x4(ta + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vre[4]));
+      ptx::tmem_ld_32x32b_x4(ta + BN + g, *reinterpret_cast<uint32_t(*)[4]>(&vim[0]));
+      ptx::tmem_ld_32x32b_x4(ta + BN + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vim[4]));
+      ptx::tmem_wait_ld();
+      InteriorPair m8[8];
+      unsigned fl = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const InteriorPair& m = m8[e] = interior_pair(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(jb + g + e));
+        nind += (m.d <= 0.0f && m.aim > tol) ? 1u : 0u;
+        fl |= (m.d > 0.0f && m.aim * m.are + m.d > kt * m.d * m.d * m.rd) ? (1u << e) : 0u;
+      }
+      if (fl) flush(fl, jb + g, m8);
+      emit8_interior(p, od + g, om + (long long)g * N, m8, direct, mirror, rdiv);
+    }
+  } else {
+#pragma unroll 1
+    for (int g = 0; g < HALF; g += 4) {
+      uint32_t vre[4], vim[4];
+      ptx::tmem_ld_32x32b_x4(ta + g, vre);
+      ptx::tmem_ld_32x32b_x4(ta + BN + g, vim);
+      ptx::tmem_wait_ld();
+      InteriorPair m4[4];
+      unsigned fl = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const InteriorPair& m = m4[e] = interior_pair(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(jb + g + e));
+        nind += (m.d <= 0.0f && m.aim > tol) ? 1u : 0u;
+        fl |= (m.d > 0.0f && m.aim * m.are + m.d > kt * m.d * m.d * m.rd) ? (1u << e) : 0u;
+      }
+      if (fl) flush(fl, jb + g, m4);
+      emit4_interior(p, od + g, om + (long long)g * N, m4, ri.first, direct, mirror, rdiv);
+    }
+  }
+  if (p.out_cre || p.out_cim)
+    emit_signed_round<BN, HALF>(p, ta, jb, od, om, inv_at, ri.first, direct, mirror, rdiv);
+  if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
+  if (nind) atomicAdd(&p.status->n_indeterminate, (unsigned long long)nind);
+}
+
 // PLV-family epilogue of one finished round for row i and this warp's
 // HALF-column slice; sums are read back 4 columns at a time from TMEM.
 template <int BN, int HALF>
@@ -253,88 +385,8 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
     return 1.0f / static_cast<float>(te);
   };
   if (interior) {
-    // ill-conditioning test of the general path, 1e-6 (|cim| are / d + 1) >
-    // tol sqrt(d), multiplied through by d / 1e-6 (d > 0): no division
-    const float kt = p.illcond_tol * 1e6f;
-    auto illcond = [&](const PairMetrics<float>& m, int j) {
-      const float are = fabsf(m.cre);
-      const float d = (1.0f - are) * (1.0f + are);
-      if (d <= 0.0f && m.iplv > p.illcond_tol) ++nind;
-      if (d > 0.0f && m.iplv * are + d > kt * d * d * rsqrtf(d)) {
-        ++illc;
-        if (p.refine) {
-          const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
-          if (k < (unsigned long long)p.refine_cap) {
-            RefineEntry en;
-            en.slot = (int)ri.slot;
-            en.i = i;
-            en.j = j;
-            en.u0 = ri.u0;
-            en.nu = ri.nu;
-            en.approx = m.ciplv;
-            p.refine[k] = en;
-          }
-        }
-      }
-    };
-    if (ri.first && (p.N & 7) == 0) {
-      // first round of the slot: 8 columns per step, 32-byte direct stores
-#pragma unroll 1
-      for (int g = 0; g < HALF; g += 8) {
-        uint32_t vre[8], vim[8];
-        ptx::tmem_ld_32x32b_x4(ta + g, *reinterpret_cast<uint32_t(*)[4]>(&vre[0]));
-        ptx::tmem_ld_32x32b_x4(ta + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vre[4]));
-        ptx::tmem_ld_32x32b_x4(ta + BN + g, *reinterpret_cast<uint32_t(*)[4]>(&vim[0]));
-        ptx::tmem_ld_32x32b_x4(ta + BN + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vim[4]));
-        ptx::tmem_wait_ld();
-        const int j0 = jb + g;
-        PairMetrics<float> m8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          m8[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(j0 + e));
-          illcond(m8[e], j0 + e);
-        }
-        emit8_first(p, ri.slot, i, j0, m8, ri.last);
-      }
-      if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
-      if (nind) atomicAdd(&p.status->n_indeterminate, (unsigned long long)nind);
-      return;
-    }
-#pragma unroll 1
-    for (int g = 0; g < HALF; g += 4) {
-      uint32_t vre[4], vim[4];
-      ptx::tmem_ld_32x32b_x4(ta + g, vre);
-      ptx::tmem_ld_32x32b_x4(ta + BN + g, vim);
-      ptx::tmem_wait_ld();
-      const int j0 = jb + g;
-      PairMetrics<float> m4[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        m4[e] = pair_metrics<float, true>(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(j0 + e));
-        const float are = fabsf(m4[e].cre);
-        const float d = (1.0f - are) * (1.0f + are);
-        if (d <= 0.0f && m4[e].iplv > p.illcond_tol) ++nind;
-        if (d > 0.0f && m4[e].iplv * are + d > kt * d * d * rsqrtf(d)) {
-          ++illc;
-          if (p.refine) {
-            const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
-            if (k < (unsigned long long)p.refine_cap) {
-              RefineEntry en;
-              en.slot = (int)ri.slot;
-              en.i = i;
-              en.j = j0 + e;
-              en.u0 = ri.u0;
-              en.nu = ri.nu;
-              en.approx = m4[e].ciplv;
-              p.refine[k] = en;
-            }
-          }
-        }
-      }
-      emit4_all(p, ri.slot, i, j0, m4, ri.first, ri.last);
-    }
-    if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
-    if (nind) atomicAdd(&p.status->n_indeterminate, (unsigned long long)nind);
+    if (any_masked) emit_interior<BN, HALF, true>(p, ri, ta, i, jb, inv_t);
+    else emit_interior<BN, HALF, false>(p, ri, ta, i, jb, inv_t);
     return;
   }
 #pragma unroll 1
@@ -695,6 +747,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float sre[H], sim[H];
 #pragma unroll
     for (int k = 0; k < H; ++k) sre[k] = sim[k] = 0.0f;
+    long long e_wait = 0, e_emit = 0;  // PS_GRAM_PROF: cycles blocked on tfull / emitting
+    const long long e_t0 = p.prof ? clock64() : 0;
     for (int it = grp; it < p.n_items; it += ngrp) {
       const Item w = p.items[it];
       const int r0 = p.pool ? 0 : w.g * p.Rg;
@@ -721,7 +775,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               }
             }
           }
-          ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
+          if (p.prof) ptx::mbar_wait_prof(&tfull[buf], uses[buf] & 1u, &e_wait);
+          else ptx::mbar_wait(&tfull[buf], uses[buf] & 1u, tflag);
           ptx::tc_fence_after();
           const uint32_t ta = tmem + lane_base + (uint32_t)buf * G::BUF + (uint32_t)(h * H);
           // single-chunk rounds (short K: over_trials, coherence, T <= 128):
@@ -767,7 +822,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
               store_sums<H>(sim, ta + BN);
               ptx::tmem_wait_st();
             }
+            const long long t_em = p.prof ? clock64() : 0;
             if (!(p.debug_flags & 1)) emit_round<BN, H>(p, w, r, r0, r1, ta, i, h, any_masked);
+            if (p.prof) e_emit += clock64() - t_em;
 #pragma unroll
             for (int k = 0; k < H; ++k) sre[k] = sim[k] = 0.0f;  // sums dead across the emission
           }
@@ -792,6 +849,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
       }
+    }
+    if (p.prof && lane == 0) {
+      atomicAdd(&p.prof[5], (unsigned long long)e_wait);
+      atomicAdd(&p.prof[6], (unsigned long long)e_emit);
+      atomicAdd(&p.prof[7], (unsigned long long)(clock64() - e_t0));
     }
   }
 

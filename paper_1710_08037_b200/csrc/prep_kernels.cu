@@ -371,15 +371,16 @@ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
   for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(v[4 * k1 + 0], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
 }
 
-// One radix-16 Stockham pass for sub-transform size NS (1, 16, 256): the
-// thread's v[] holds x[j + 256 r] in natural order; twiddle, DFT16, and (if
-// STORE) scatter to buf.  Without STORE the result stays in v[d16(r)].
-template <bool INV, int NS, bool STORE>
-__device__ __forceinline__ void stockham_pass(float2 (&v)[16], float2* buf, const float2* tw) {
-  const int j = threadIdx.x;
-  const int k = j % NS;
+// Radix-16 Stockham passes.  Every pass takes v[r] = x[j + 256 r] (natural
+// order, j = threadIdx.x), twiddles, runs the DFT16 and leaves output r in
+// v[d16(r)]; store16 scatters it for the next pass and load16 gathers the next
+// pass's inputs.  All shared-memory accesses of a pass are a per-thread base
+// plus a compile-time offset: pad(idx + r NS) = pad(idx) + r (NS + NS / 16)
+// when NS % 16 == 0, or NS == 1 and idx % 16 == 0.
+template <bool INV, int NS>
+__device__ __forceinline__ void twiddle16(float2 (&v)[16], const float2* tw) {
   if (NS > 1) {
-    const float2* t = tw + (NS == 16 ? kTw16 : kTw256) + k;
+    const float2* t = tw + (NS == 16 ? kTw16 : kTw256) + (threadIdx.x % NS);
 #pragma unroll
     for (int r = 1; r < 16; ++r) {
       float2 w = t[(r - 1) * NS];
@@ -387,22 +388,107 @@ __device__ __forceinline__ void stockham_pass(float2 (&v)[16], float2* buf, cons
       v[r] = cmul(v[r], w);
     }
   }
-  dft16<INV>(v);
-  if (STORE) {
-    const int idx = (j / NS) * NS * 16 + k;
-    __syncthreads();  // every thread has read its inputs of this pass
+}
+
+template <int NS>
+__device__ __forceinline__ void store16(const float2 (&v)[16], float2* buf) {
+  const int j = threadIdx.x;
+  const int base = kFftPad((j / NS) * NS * 16 + j % NS);
+  constexpr int step = NS + NS / 16;
+  __syncthreads();  // every thread has read its inputs of this pass
 #pragma unroll
-    for (int r = 0; r < 16; ++r) buf[kFftPad(idx + r * NS)] = v[d16(r)];
-    __syncthreads();
-  }
+  for (int r = 0; r < 16; ++r) buf[base + r * step] = v[d16(r)];
+  __syncthreads();
 }
 
 __device__ __forceinline__ void load16(float2 (&v)[16], const float2* buf) {
+  const int base = kFftPad(threadIdx.x);
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = buf[kFftPad(threadIdx.x + r * kFftThreads)];
+  for (int r = 0; r < 16; ++r) v[r] = buf[base + r * (kFftThreads + kFftThreads / 16)];
 }
 
-__global__ void __launch_bounds__(kFftThreads, 2) hilbert_fused4096_kernel(
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
+// L2 prefetch of `bytes` (multiple of 16, 16-byte aligned) at p (TMA bulk,
+// no registers or shared memory involved)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// 2^(1 - e) with m = m' 2^e, m' in [0.5, 1) (frexpf convention), clamped to
+// [2^-126, 2^126]: scales m into [1, 2).  0 / non-finite m -> 2 (e = 0).
+// Exponent-field arithmetic; denormal m clamps to 2^126 as frexpf would.
+__device__ __forceinline__ float pow2_scale(float m) {
+  int e = 0;
+  if (m > 0.f && m <= FLT_MAX) e = (int)((__float_as_uint(m) >> 23) & 0xffu) - 126;
+  const int s = min(126, max(-126, 1 - e));
+  return __uint_as_float((uint32_t)(127 + s) << 23);
+}
+
+template <bool INV, int NS>
+__device__ __forceinline__ void fft_pass(float2 (&v)[16], const float2* tw) {
+  twiddle16<INV, NS>(v, tw);
+  dft16<INV>(v);
+}
+
+// Normalises 4 consecutive samples (re = x * scale, im = H) into the four
+// fp16 split planes at o (plane stride ps) -- and, with GS, the Gauss-Gram
+// planes S = Zr + Zi, D = Zr - Zi (hi / lo) from the rounded split values,
+// the arithmetic of gauss_planes_kernel; returns their min / max |a|.
+template <bool GS>
+__device__ __forceinline__ void normalize4_split(const float (&re)[4], const float (&im)[4], __half* o,
+                                                 long long ps, float& lo2, float& hi2) {
+  float zr[4], zi[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float a2 = re[k] * re[k] + im[k] * im[k];
+    // |a|^2 clamped to FLT_MIN: a zero sample gives z = 0 (0 * finite); a
+    // sample this small is below the amplitude floor of its row, which the
+    // exact fixup then masks from H (its row min trips the pre-check)
+    const float inv = rsqrtf(fmaxf(a2, FLT_MIN));
+    zr[k] = re[k] * inv;
+    zi[k] = im[k] * inv;
+    lo2 = fminf(lo2, a2);
+    hi2 = fmax_nan(hi2, a2);  // NaN-propagating: a non-finite sample surfaces in the row max
+  }
+  // packed conversions (F2FP / HADD2.F32): the same round-to-nearest
+  // values as per-element __float2half_rn, half the instructions
+  uint32_t w[GS ? 8 : 4][2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const __half2 rh = __floats2half2_rn(zr[2 * q], zr[2 * q + 1]);
+    const __half2 ih = __floats2half2_rn(zi[2 * q], zi[2 * q + 1]);
+    const float2 rf = __half22float2(rh), jf = __half22float2(ih);
+    const __half2 rl = __floats2half2_rn(zr[2 * q] - rf.x, zr[2 * q + 1] - rf.y);
+    const __half2 il = __floats2half2_rn(zi[2 * q] - jf.x, zi[2 * q + 1] - jf.y);
+    w[0][q] = *reinterpret_cast<const uint32_t*>(&rh);
+    w[1][q] = *reinterpret_cast<const uint32_t*>(&rl);
+    w[2][q] = *reinterpret_cast<const uint32_t*>(&ih);
+    w[3][q] = *reinterpret_cast<const uint32_t*>(&il);
+    if (GS) {
+      const float2 rlf = __half22float2(rl), ilf = __half22float2(il);
+      const float ar = rf.x + rlf.x, br = rf.y + rlf.y;  // rounded Zr of the two samples
+      const float ai = jf.x + ilf.x, bi = jf.y + ilf.y;  // rounded Zi
+      const float s0 = ar + ai, s1 = br + bi, d0 = ar - ai, d1 = br - bi;
+      const __half2 sh = __floats2half2_rn(s0, s1), dh = __floats2half2_rn(d0, d1);
+      const float2 shf = __half22float2(sh), dhf = __half22float2(dh);
+      const __half2 sl = __floats2half2_rn(s0 - shf.x, s1 - shf.y), dl = __floats2half2_rn(d0 - dhf.x, d1 - dhf.y);
+      w[4][q] = *reinterpret_cast<const uint32_t*>(&sh);
+      w[5][q] = *reinterpret_cast<const uint32_t*>(&sl);
+      w[6][q] = *reinterpret_cast<const uint32_t*>(&dh);
+      w[7][q] = *reinterpret_cast<const uint32_t*>(&dl);
+    }
+  }
+#pragma unroll
+  for (int pl = 0; pl < (GS ? 8 : 4); ++pl) *reinterpret_cast<uint2*>(o + pl * ps) = make_uint2(w[pl][0], w[pl][1]);
+}
+
+template <bool GS>
+__global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
     SrcDesc src, long long row0, long long nrows, __half* out, int pitch, long long ps, unsigned long long* rowmin,
     unsigned long long* rowmax, float* hbuf, double amp_floor, DevStatus* st) {
   extern __shared__ float2 fsm[];
@@ -425,15 +511,24 @@ __global__ void __launch_bounds__(kFftThreads, 2) hilbert_fused4096_kernel(
     tw[m] = make_float2(c, s);
   }
   __shared__ float red[4][kFftThreads / 32];
+  __shared__ int need_flags[2];
   __syncthreads();
+  const int j = threadIdx.x;
   const long long npairs = (nrows + 1) / 2;
   for (long long pr = blockIdx.x; pr < npairs; pr += gridDim.x) {
     const long long ra = row0 + 2 * pr, rb = ra + 1;
     const bool hasb = 2 * pr + 1 < nrows;
     const long long oa = row_offset(src, ra), ob = hasb ? row_offset(src, rb) : 0;
     const float* x = static_cast<const float*>(src.ptr);  // s_samp == 1 (hilbert_fused_supported)
-    const float* xpa = x + oa + threadIdx.x;
-    const float* xpb = x + ob + threadIdx.x;
+    const float* xpa = x + oa + j;
+    const float* xpb = x + ob + j;
+    if (j == 0 && pr + gridDim.x < npairs) {
+      // the CTA's next pair into L2 while this one computes: its first loads
+      // (a full DRAM round trip ahead of the first barrier) then hit L2
+      const long long nra = row0 + 2 * (pr + gridDim.x);
+      bulk_prefetch_l2(x + row_offset(src, nra), kFftT * sizeof(float));
+      if (2 * (pr + gridDim.x) + 1 < nrows) bulk_prefetch_l2(x + row_offset(src, nra + 1), kFftT * sizeof(float));
+    }
     float2 v[16];
     float ma = 0.f, mb = 0.f;
 #pragma unroll
@@ -451,9 +546,9 @@ __global__ void __launch_bounds__(kFftThreads, 2) hilbert_fused4096_kernel(
       ma = fmaxf(ma, __shfl_xor_sync(0xffffffffu, ma, o));
       mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
     }
-    if ((threadIdx.x & 31) == 0) {
-      red[0][threadIdx.x >> 5] = ma;
-      red[1][threadIdx.x >> 5] = mb;
+    if ((j & 31) == 0) {
+      red[0][j >> 5] = ma;
+      red[1][j >> 5] = mb;
     }
     __syncthreads();
 #pragma unroll
@@ -461,133 +556,125 @@ __global__ void __launch_bounds__(kFftThreads, 2) hilbert_fused4096_kernel(
       ma = fmaxf(ma, red[0][w]);
       mb = fmaxf(mb, red[1][w]);
     }
-    int ea = 0, eb = 0;
-    if (ma > 0.f && ma <= FLT_MAX) frexpf(ma, &ea);
-    if (mb > 0.f && mb <= FLT_MAX) frexpf(mb, &eb);
-    const float sa = ldexpf(1.0f, min(126, max(-126, 1 - ea)));
-    const float sb = ldexpf(1.0f, min(126, max(-126, 1 - eb)));
+    const float sa = pow2_scale(ma), sb = pow2_scale(mb);
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
       v[q].x *= sa;
       v[q].y *= sb;
     }
-    // forward FFT
-    stockham_pass<false, 1, true>(v, buf, tw);
+    // forward FFT; the last pass leaves X[j + 256 r] in v[d16(r)]
+    fft_pass<false, 1>(v, tw);
+    store16<1>(v, buf);
     load16(v, buf);
-    stockham_pass<false, 16, true>(v, buf, tw);
+    fft_pass<false, 16>(v, tw);
+    store16<16>(v, buf);
     load16(v, buf);
-    stockham_pass<false, 256, true>(v, buf, tw);
-    // Hilbert multiplier on the natural-order spectrum, folded into the load:
-    // -i for 0 < k < T/2, +i for T/2 < k < T, 0 at DC and Nyquist; 1/T scale
-    const float inv_t = 1.0f / (float)kFftT;
+    fft_pass<false, 256>(v, tw);
+    // Hilbert multiplier -i sgn(k) in registers: k = j + 256 r is already the
+    // inverse's first-pass input index of this thread (no shared-memory round
+    // trip).  -i for 0 < k < T/2, +i for T/2 < k < T, 0 at DC and Nyquist.
+    // The inverse's 1/T is folded into the epilogue (x scaled by T instead:
+    // exact, power of two).
+    float2 u[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      const int kk = threadIdx.x + r * kFftThreads;
-      const float2 z = buf[kFftPad(kk)];
-      float2 y;
-      if (kk == 0 || kk == kFftT / 2) y = make_float2(0.f, 0.f);
-      else if (kk < kFftT / 2) y = make_float2(z.y * inv_t, -z.x * inv_t);   // -i z
-      else y = make_float2(-z.y * inv_t, z.x * inv_t);                        // +i z
-      v[r] = y;
+      const float2 z = v[d16(r)];
+      u[r] = r < 8 ? make_float2(z.y, -z.x) : make_float2(-z.y, z.x);
     }
-    // inverse FFT; the last pass leaves H_a + i H_b at t = j + 256 r in v[d16(r)]
-    stockham_pass<true, 1, true>(v, buf, tw);
-    load16(v, buf);
-    stockham_pass<true, 16, true>(v, buf, tw);
-    load16(v, buf);
-    stockham_pass<true, 256, true>(v, buf, tw);
+    if (j == 0) {
+      u[0] = make_float2(0.f, 0.f);
+      u[8] = make_float2(0.f, 0.f);
+    }
+    // inverse FFT -> T (H_a sa + i H_b sb) at t in natural order in buf
+    fft_pass<true, 1>(u, tw);
+    store16<1>(u, buf);
+    load16(u, buf);
+    fft_pass<true, 16>(u, tw);
+    store16<16>(u, buf);
+    load16(u, buf);
+    fft_pass<true, 256>(u, tw);
+    store16<256>(u, buf);
     // normalise both rows from (x, H in smem): 4 consecutive samples per
-    // thread and step (16-byte x loads, 8-byte plane stores), row min / max
+    // thread and step (16-byte x loads -- L2 hits, software-pipelined one
+    // step ahead -- and 8-byte plane stores); row min / max of |a|^2
+    const float soa = sa * (float)kFftT, sob = sb * (float)kFftT;
     float amin_a = FLT_MAX, amax_a = 0.f, amin_b = FLT_MAX, amax_b = 0.f;
-    bool bad = false;
+    const float2* hb = buf + kFftPad(4 * j);
+    __half* opa = out + ra * pitch + 4 * j;
+    __half* opb = out + rb * pitch + 4 * j;
+    const float4* xa4 = reinterpret_cast<const float4*>(x + oa) + j;
+    const float4* xb4 = reinterpret_cast<const float4*>(x + ob) + j;
+    float4 na = xa4[0], nb = hasb ? xb4[0] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
     for (int g = 0; g < kFftT / (4 * kFftThreads); ++g) {
-      const int t0 = 4 * (threadIdx.x + g * kFftThreads);
+      const int off = g * 4 * kFftThreads;  // samples
+      const float4 ca = na, cb = nb;
+      if (g + 1 < kFftT / (4 * kFftThreads)) {
+        na = xa4[(g + 1) * kFftThreads];
+        if (hasb) nb = xb4[(g + 1) * kFftThreads];
+      }
       float2 h[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) h[k] = buf[kFftPad(t0 + k)];
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        if (s == 1 && !hasb) continue;
-        const float4 x4 = *reinterpret_cast<const float4*>(x + (s == 0 ? oa : ob) + t0);
-        const float sc = s == 0 ? sa : sb;
-        const float re[4] = {x4.x * sc, x4.y * sc, x4.z * sc, x4.w * sc};
-        __half rh[4], rlo[4], ih[4], ilo[4];
-        float lo = FLT_MAX, hi = 0.f;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float im = s == 0 ? h[k].x : h[k].y;
-          const float a2 = re[k] * re[k] + im * im;
-          const float inv = a2 > 0.0f ? rsqrtf(a2) : 0.0f;
-          const float a = a2 * inv;
-          const float zr = re[k] * inv, zi = im * inv;
-          rh[k] = __float2half_rn(zr);
-          ih[k] = __float2half_rn(zi);
-          rlo[k] = __float2half_rn(zr - __half2float(rh[k]));
-          ilo[k] = __float2half_rn(zi - __half2float(ih[k]));
-          if (!(a <= FLT_MAX)) bad = true;
-          lo = fminf(lo, a);
-          hi = fmaxf(hi, a);
-        }
-        __half* o = out + (s == 0 ? ra : rb) * pitch + t0;
-        *reinterpret_cast<uint2*>(o) = make_uint2(pack_half2(rh[0], rh[1]), pack_half2(rh[2], rh[3]));
-        *reinterpret_cast<uint2*>(o + ps) = make_uint2(pack_half2(rlo[0], rlo[1]), pack_half2(rlo[2], rlo[3]));
-        *reinterpret_cast<uint2*>(o + 2 * ps) = make_uint2(pack_half2(ih[0], ih[1]), pack_half2(ih[2], ih[3]));
-        *reinterpret_cast<uint2*>(o + 3 * ps) = make_uint2(pack_half2(ilo[0], ilo[1]), pack_half2(ilo[2], ilo[3]));
-        if (s == 0) {
-          amin_a = fminf(amin_a, lo);
-          amax_a = fmaxf(amax_a, hi);
-        } else {
-          amin_b = fminf(amin_b, lo);
-          amax_b = fmaxf(amax_b, hi);
-        }
+      for (int k = 0; k < 4; ++k) h[k] = hb[kFftPad(off) + k];
+      {
+        const float re[4] = {ca.x * soa, ca.y * soa, ca.z * soa, ca.w * soa};
+        const float im[4] = {h[0].x, h[1].x, h[2].x, h[3].x};
+        normalize4_split<GS>(re, im, opa + off, ps, amin_a, amax_a);
+      }
+      if (hasb) {
+        const float re[4] = {cb.x * sob, cb.y * sob, cb.z * sob, cb.w * sob};
+        const float im[4] = {h[0].y, h[1].y, h[2].y, h[3].y};
+        normalize4_split<GS>(re, im, opb + off, ps, amin_b, amax_b);
       }
     }
-    if (bad) atomicOr(&st->flags, FLAG_NONFINITE);
     // block min / max of both rows (the CTA owns them: plain stores)
     float vals[4] = {amin_a, amax_a, amin_b, amax_b};
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       vals[0] = fminf(vals[0], __shfl_xor_sync(0xffffffffu, vals[0], o));
-      vals[1] = fmaxf(vals[1], __shfl_xor_sync(0xffffffffu, vals[1], o));
+      vals[1] = fmax_nan(vals[1], __shfl_xor_sync(0xffffffffu, vals[1], o));
       vals[2] = fminf(vals[2], __shfl_xor_sync(0xffffffffu, vals[2], o));
-      vals[3] = fmaxf(vals[3], __shfl_xor_sync(0xffffffffu, vals[3], o));
+      vals[3] = fmax_nan(vals[3], __shfl_xor_sync(0xffffffffu, vals[3], o));
     }
-    if ((threadIdx.x & 31) == 0)
+    if ((j & 31) == 0)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) red[q][threadIdx.x >> 5] = vals[q];
+      for (int q = 0; q < 4; ++q) red[q][j >> 5] = vals[q];
     __syncthreads();
-    __shared__ int need_flags[2];
-    if (threadIdx.x == 0) {
+    if (j == 0) {
       for (int w = 1; w < kFftThreads / 32; ++w) {
         vals[0] = fminf(vals[0], red[0][w]);
-        vals[1] = fmaxf(vals[1], red[1][w]);
+        vals[1] = fmax_nan(vals[1], red[1][w]);
         vals[2] = fminf(vals[2], red[2][w]);
-        vals[3] = fmaxf(vals[3], red[3][w]);
+        vals[3] = fmax_nan(vals[3], red[3][w]);
       }
+      // a non-finite |a| anywhere in a row leaves its max non-finite (NaN
+      // propagates, inf is the max)
+      if (!(vals[1] <= FLT_MAX) || (hasb && !(vals[3] <= FLT_MAX))) atomicOr(&st->flags, FLAG_NONFINITE);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) vals[q] = sqrtf(vals[q]);  // |a|^2 -> |a|
       // back to input units (exact: powers of two); the fixup decides on
       // the min / max ratio, which the scaling leaves unchanged
-      rowmin[ra] = key_of((double)vals[0] / sa);
-      rowmax[ra] = key_of((double)vals[1] / sa);
+      rowmin[ra] = key_of((double)vals[0] / soa);
+      rowmax[ra] = key_of((double)vals[1] / soa);
       need_flags[0] = (vals[0] == 0.0f) || ((double)vals[0] < amp_floor * (double)vals[1] * (1.0 + 1e-5));
       need_flags[1] = 0;
       if (hasb) {
-        rowmin[rb] = key_of((double)vals[2] / sb);
-        rowmax[rb] = key_of((double)vals[3] / sb);
+        rowmin[rb] = key_of((double)vals[2] / sob);
+        rowmax[rb] = key_of((double)vals[3] / sob);
         need_flags[1] = (vals[2] == 0.0f) || ((double)vals[2] < amp_floor * (double)vals[3] * (1.0 + 1e-5));
       }
     }
     __syncthreads();
     // rare: keep H (input units) of a row the exact-median fixup will inspect
     if (need_flags[0] || need_flags[1]) {
-      const float ua = 1.0f / sa, ub = 1.0f / sb;
-      for (int t = threadIdx.x; t < kFftT; t += kFftThreads) {
+      const float ua = 1.0f / soa, ub = 1.0f / sob;
+      for (int t = j; t < kFftT; t += kFftThreads) {
         const float2 hv = buf[kFftPad(t)];
         if (need_flags[0]) hbuf[(ra - src.h_row0) * src.h_ld + t] = hv.x * ua;
         if (need_flags[1]) hbuf[(rb - src.h_row0) * src.h_ld + t] = hv.y * ub;
       }
     }
-    __syncthreads();
+    // the next pair's first store16 synchronises before overwriting buf
   }
 }
 
@@ -892,7 +979,8 @@ __global__ void analytic_out_kernel(SrcDesc src, long long row0, long long nrows
   }
 }
 
-// out_m[i] = sum_g ws_m[g][i] / R  (deterministic fixed-order trial-group sum)
+// out_m[i] = sum_g ws_m[g][i] / R  (deterministic fixed-order trial-group sum; fp32:
+// times the fp32 reciprocal, as every split-path mean)
 template <typename S>
 __global__ void group_reduce_kernel(const S* ws, int G, long long slot_elems, long long elems, int R,
                                     S* out, long long upper_n) {
@@ -904,7 +992,7 @@ __global__ void group_reduce_kernel(const S* ws, int G, long long slot_elems, lo
     const S* p = ws + (b * G) * slot_elems + i;
     S acc = p[0];
     for (int g = 1; g < G; ++g) acc += p[g * slot_elems];
-    out[e] = acc / S(R);
+    out[e] = sizeof(S) == 4 ? acc * (S(1) / S(R)) : acc / S(R);  // = epilogue.cuh mean_scale
   }
 }
 
@@ -1280,28 +1368,44 @@ bool hilbert_fused_supported(const SrcDesc& src, int fmt, int cdouble, int pitch
          aligned;
 }
 
-cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long nrows, void* out, int pitch,
-                                 long long plane_stride, unsigned long long* rowstat, long long rows_total,
-                                 double amp_floor, DevStatus* status, cudaStream_t st) {
-  if (nrows <= 0) return cudaSuccess;
+template <bool GS>
+cudaError_t launch_hilbert_fused_t(const SrcDesc& src, long long row0, long long nrows, __half* out, int pitch,
+                                   long long plane_stride, unsigned long long* rowstat, long long rows_total,
+                                   double amp_floor, DevStatus* status, cudaStream_t st) {
   // the attribute is per device: set it on every launch (cheap), so a process
   // driving several GPUs gets it on each
-  cudaError_t e = cudaFuncSetAttribute(hilbert_fused4096_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(hilbert_fused4096_kernel<GS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        kFftSmemBytes);
   if (e != cudaSuccess) return e;
   int dev = 0, n_sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hilbert_fused4096_kernel, kFftThreads, kFftSmemBytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, hilbert_fused4096_kernel<GS>, kFftThreads,
+                                                    kFftSmemBytes);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
   const long long npairs = (nrows + 1) / 2;
   const long long cap = (long long)per_sm * n_sms;
   const unsigned grid = (unsigned)(npairs < cap ? npairs : cap);
-  hilbert_fused4096_kernel<<<grid, kFftThreads, kFftSmemBytes, st>>>(
-      src, row0, nrows, static_cast<__half*>(out), pitch, plane_stride, rowstat, rowstat + rows_total,
+  hilbert_fused4096_kernel<GS><<<grid, kFftThreads, kFftSmemBytes, st>>>(
+      src, row0, nrows, out, pitch, plane_stride, rowstat, rowstat + rows_total,
       static_cast<float*>(const_cast<void*>(src.hbuf)), amp_floor, status);
   return cudaGetLastError();
+}
+
+// With src.gauss_planes the kernel also writes the Gauss-Gram S / D planes
+// (planes 4..7); *gauss_done reports it.
+cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long nrows, void* out, int pitch,
+                                 long long plane_stride, unsigned long long* rowstat, long long rows_total,
+                                 double amp_floor, DevStatus* status, cudaStream_t st, int* gauss_done) {
+  if (gauss_done) *gauss_done = src.gauss_planes ? 1 : 0;
+  if (nrows <= 0) return cudaSuccess;
+  __half* o = static_cast<__half*>(out);
+  return src.gauss_planes
+             ? launch_hilbert_fused_t<true>(src, row0, nrows, o, pitch, plane_stride, rowstat, rows_total, amp_floor,
+                                            status, st)
+             : launch_hilbert_fused_t<false>(src, row0, nrows, o, pitch, plane_stride, rowstat, rows_total,
+                                             amp_floor, status, st);
 }
 
 // Gauss-Gram operand planes: S = Zr + Zi and D = Zr - Zi from the split

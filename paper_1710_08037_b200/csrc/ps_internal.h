@@ -146,10 +146,11 @@ cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows
                              cudaStream_t st);
 // Fused Hilbert + normalise (real fp32 rows, T = 4096, split planes): writes
 // planes and row min/max; H lands in src.hbuf only for rows the fixup inspects.
+// With src.gauss_planes it also writes the Gauss-Gram S / D planes (*gauss_done = 1).
 bool hilbert_fused_supported(const SrcDesc& src, int fmt, int cdouble, int pitch);
 cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long nrows, void* out, int pitch,
                                  long long plane_stride, unsigned long long* rowstat, long long rows_total,
-                                 double amp_floor, DevStatus* status, cudaStream_t st);
+                                 double amp_floor, DevStatus* status, cudaStream_t st, int* gauss_done);
 // Band-pass front end (two-pass FIR evaluated spectrally on length Lf)
 cudaError_t launch_reflect_pad(const SrcDesc& src, long long row0, long long nrows, long long pad, long long L,
                                long long Lf, void* xp, int dst_double, cudaStream_t st);

@@ -327,3 +327,22 @@ def test_host_trial_group_pipeline_small_shapes():
                          timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert float(out.stdout.strip().splitlines()[-1]) <= 2e-6
+
+
+def test_host_pipelined_growing_stage_counts_reuse_context():
+    # Regression: a streamed host call that needs more pipeline stages than any
+    # earlier call on the same context regrows the per-stage counters; the
+    # sub-block flag buffer (mapped pinned memory) must survive that -- it was
+    # freed there without being reset (later calls then wrote their flags
+    # into freed memory or freed it twice).  Small -> large -> small -> large
+    # again, each bit-identical to the device path.
+    import torch
+
+    rng = np.random.default_rng(91)
+    for N in (3072, 9216, 3328, 12288):
+        z = np.exp(1j * rng.uniform(0, 2 * np.pi, (N, 64))).astype(np.complex64)
+        host = C.plv_family(z, input_kind="phasor", layout="upper")
+        dev = C.plv_family(torch.from_numpy(z).cuda(), input_kind="phasor", layout="upper")
+        iu = np.triu_indices(N)
+        for m in ("plv", "iplv", "ciplv"):
+            assert np.array_equal(host[m].values[iu], dev[m].values.cpu().numpy()[iu]), (N, m)
