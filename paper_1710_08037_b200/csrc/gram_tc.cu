@@ -274,11 +274,17 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
     }
     return __frcp_rn(static_cast<float>(te));  // == 1.0f / te (correctly rounded)
   };
-  // flags of one column group -> counters / refinement queue
-  auto flush = [&](unsigned fl, int j0, const InteriorPair* m) {
+  // flags of one column group -> counters / refinement queue.  The group's
+  // values are selected with compile-time indices (a runtime-indexed array
+  // would live in local memory: every group would spill it)
+  auto flush = [&](unsigned fl, int j0, const auto& m) {
+    constexpr int n = sizeof(m) / sizeof(m[0]);
     while (fl) {
       const int e = __ffs(fl) - 1;
       fl &= fl - 1;
+      float ci = m[0].ci;
+#pragma unroll
+      for (int q = 1; q < n; ++q) ci = (e == q) ? m[q].ci : ci;
       ++illc;
       if (p.refine) {
         const unsigned long long k = atomicAdd(&p.status->n_illcond, 1ull);
@@ -289,7 +295,7 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
           en.j = j0 + e;
           en.u0 = ri.u0;
           en.nu = ri.nu;
-          en.approx = m[e].ci;
+          en.approx = ci;
           p.refine[k] = en;
         }
       }
