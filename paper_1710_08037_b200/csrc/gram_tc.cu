@@ -319,10 +319,8 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
 #pragma unroll 1
     for (int g = 0; g < HALF; g += 8) {
       uint32_t vre[8], vim[8];
-      ptx::tmem_ld_32x32b_x4(ta + g, *reinterpret_cast<uint32_t(*)[4]>(&vre[0]));
-      ptx::tmem_ld_32x32b_x4(ta + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vre[4]));
-      ptx::tmem_ld_32x32b_x4(ta + BN + g, *reinterpret_cast<uint32_t(*)[4]>(&vim[0]));
-      ptx::tmem_ld_32x32b_x4(ta + BN + g + 4, *reinterpret_cast<uint32_t(*)[4]>(&vim[4]));
+      ptx::tmem_ld_32x32b_x8(ta + g, vre);
+      ptx::tmem_ld_32x32b_x8(ta + BN + g, vim);
       ptx::tmem_wait_ld();
       InteriorPair m8[8];
       unsigned fl = 0;
@@ -619,6 +617,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == 1) {
     // ===================== MMA issuer (rank 0) =====================
     if (rank == 0) {  // whole warp: uniform descriptors, one elected lane issues
+      // PS_DEBUG_EPI & 128: the 4-product K step as 12 separately elected
+      // UMMAs (the previous issue form; experiments)
+      const bool mma_split_issue = (p.debug_flags & 128) != 0;
       constexpr uint32_t idesc_pos = ptx::make_idesc_f16(G::UMMA_M, BN, false);
       constexpr uint32_t idesc_neg = ptx::make_idesc_f16(G::UMMA_M, BN, true);
       int stage = 0;
@@ -694,6 +695,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 ptx::mma_f16_ss_warp<CG>(d_k3, aIh, bDh, idesc_pos, acc0);
                 ptx::mma_f16_ss_warp<CG>(d_k3, aIh, bDl, idesc_pos, 1u);
                 ptx::mma_f16_ss_warp<CG>(d_k3, aIl, bDh, idesc_pos, 1u);
+              } else if (!mma_split_issue) {
+                // one elected block per K step (12 UMMAs, see mma_4prod_step_warp)
+                const uint32_t alo = (uint32_t)dA + (uint32_t)ko, blo = (uint32_t)dB + (uint32_t)ko;
+                const uint32_t av[4] = {alo, alo + (G::A_PLANE >> 4), alo + 2 * (G::A_PLANE >> 4),
+                                        alo + 3 * (G::A_PLANE >> 4)};
+                const uint32_t bv[4] = {blo, blo + (G::B_PLANE >> 4), blo + 2 * (G::B_PLANE >> 4),
+                                        blo + 3 * (G::B_PLANE >> 4)};
+                ptx::mma_4prod_step_warp<CG>(d_re, d_im, av, bv, (uint32_t)(dA >> 32), idesc_pos, idesc_neg, acc0);
               } else {
                 // Re = Zr Zr' + Zi Zi'
                 ptx::mma_f16_ss_warp<CG>(d_re, aRh, bRh, idesc_pos, acc0);

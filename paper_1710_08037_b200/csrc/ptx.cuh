@@ -209,6 +209,45 @@ __device__ __forceinline__ void mma_f16_ss_warp(uint32_t d_tmem, uint64_t a_desc
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// One K = 16 step of the 4-product split Gram as a single warp-collective
+// block: one elect.sync for all 12 UMMAs; the descriptors are the stage's
+// 32-bit start-address words (lo, per plane) paired with the common high
+// word in registers (mov.b64), so per UMMA only the MMA itself issues.
+//   Re += Rh.Rh' + Rh.Rl' + Rl.Rh' + Ih.Ih' + Ih.Il' + Il.Ih'
+//   Im += Ih.Rh' + Ih.Rl' + Il.Rh' - Rh.Ih' - Rh.Il' - Rl.Ih'
+// a[0..3] / b[0..3] = {Rh, Rl, Ih, Il} low words; acc = 0 starts both sums.
+template <int CG>
+__device__ __forceinline__ void mma_4prod_step_warp(uint32_t d_re, uint32_t d_im, const uint32_t (&a)[4],
+                                                    const uint32_t (&b)[4], uint32_t hi, uint32_t ipos,
+                                                    uint32_t ineg, uint32_t acc) {
+#define PS_MMA4(CGS)                                                                                 \
+  asm volatile(                                                                                        \
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 ar, al, ai, aj, br, bl, bi, bj;\n\t"                   \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                              \
+      "setp.ne.b32 p, %13, 0;\n\tsetp.eq.b32 t, %13, %13;\n\t"                                       \
+      "mov.b64 ar, {%2, %10};\n\tmov.b64 al, {%3, %10};\n\tmov.b64 ai, {%4, %10};\n\t"             \
+      "mov.b64 aj, {%5, %10};\n\tmov.b64 br, {%6, %10};\n\tmov.b64 bl, {%7, %10};\n\t"             \
+      "mov.b64 bi, {%8, %10};\n\tmov.b64 bj, {%9, %10};\n\t"                                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ar, br, %11, p;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ar, bl, %11, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], al, br, %11, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ai, bi, %11, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ai, bj, %11, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], aj, bi, %11, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], ai, br, %11, p;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], ai, bl, %11, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], aj, br, %11, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], ar, bi, %12, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], ar, bj, %12, t;\n\t"                         \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], al, bi, %12, t;\n\t}"                        \
+      ::"r"(d_re), "r"(d_im), "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), \
+      "r"(b[3]), "r"(hi), "r"(ipos), "r"(ineg), "r"(acc)                                              \
+      : "memory")
+  if (CG == 1) PS_MMA4("1");
+  else PS_MMA4("2");
+#undef PS_MMA4
+}
+
 // kind::f8f6f4 (E4M3 A / B, fp32 D; the instruction descriptor's format
 // fields are 0 for E4M3 exactly as for F16, so make_idesc_f16 applies): the
 // K7 mask-count Gram's 0 / 1 indicator operands, K = 32 per instruction
@@ -316,6 +355,12 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&v)
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld_32x32b_x8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
