@@ -63,3 +63,17 @@ def test_downsample_errors_and_aliasing_warning():
         S.downsample(np.cos(0.05 * np.pi * np.arange(4000))[None, :], 10)  # band-limited: silent
     with pytest.warns(errors.AliasingWarning):
         S.downsample(np.random.default_rng(0).standard_normal((2, 4000)), 10)
+
+
+def test_reference_module_names_resolve():
+    # reference code importing the simulator / bench modules finds them
+    import numpy as np
+    from phasesync import bench, chaossim
+
+    z = bench.make_surrogate(5, 40, 2, seed=1)
+    assert z.data.shape == (5, 40, 2) and np.allclose(np.abs(z.data), 1.0, atol=1e-12)
+    assert np.array_equal(bench.make_surrogate(5, 40, 2, seed=1).data, z.data)
+    with pytest.raises(NotImplementedError, match="SPEC.md:281-377"):
+        chaossim.integrate_coupled(None)
+    with pytest.raises(NotImplementedError, match="SPEC.md:379-433"):
+        bench.run_benchmark(None)
