@@ -117,6 +117,11 @@ static_assert(2 * BUF_COLS <= TMEM_COLS, "two Re+Im buffers must fit TMEM");
 static_assert(BK % 16 == 0 && BK * 2 <= 128, "BK must be a multiple of 16 within one swizzle row");
 static_assert(HALF % 16 == 0, "epilogue loads 16 columns at a time");
 
+__device__ __forceinline__ Item load_item(const Item* items, int i) {
+  const int4 v = __ldg(reinterpret_cast<const int4*>(items + i));
+  return Item{v.x, v.y, v.z, v.w};
+}
+
 template <int H>
 __device__ __forceinline__ void add_chunk(float (&s)[H], uint32_t taddr) {
   uint32_t v[16];
@@ -535,8 +540,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       };
       long long e = 0;  // K blocks issued by this producer
       bool pace = true;  // cleared after a pacing timeout (counters are still published)
+      // next item loaded one iteration ahead (its latency off the per-item path)
+      Item w_next = grp < p.n_items ? load_item(p.items, grp) : Item{0, 0, 0, 0};
       for (int it = grp; it < p.n_items; it += ngrp) {
-        const Item w = p.items[it];
+        const Item w = w_next;
+        if (it + ngrp < p.n_items) w_next = load_item(p.items, it + ngrp);
         const int r0 = p.pool ? 0 : w.g * p.Rg;
         const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
         // (debug_flags & 16: every item streams panel 0 -- operands L2-resident,
@@ -628,8 +636,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       int buf = 0;
       long long w_full = 0, w_tempty = 0;
       const long long m_t0 = clock64();
+      // next item loaded one iteration ahead (its latency off the per-item path)
+      Item w_next = grp < p.n_items ? load_item(p.items, grp) : Item{0, 0, 0, 0};
       for (int it = grp; it < p.n_items; it += ngrp) {
-        const Item w = p.items[it];
+        const Item w = w_next;
+        if (it + ngrp < p.n_items) w_next = load_item(p.items, it + ngrp);
         const int r0 = p.pool ? 0 : w.g * p.Rg;
         const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
         for (int r = r0; r < r1; ++r) {
@@ -764,8 +775,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int k = 0; k < H; ++k) sre[k] = sim[k] = 0.0f;
     long long e_wait = 0, e_emit = 0;  // PS_GRAM_PROF: cycles blocked on tfull / emitting
     const long long e_t0 = p.prof ? clock64() : 0;
+    // next item loaded one iteration ahead (its latency off the per-item path)
+    Item w_next = grp < p.n_items ? load_item(p.items, grp) : Item{0, 0, 0, 0};
     for (int it = grp; it < p.n_items; it += ngrp) {
-      const Item w = p.items[it];
+      const Item w = w_next;
+      if (it + ngrp < p.n_items) w_next = load_item(p.items, it + ngrp);
       const int r0 = p.pool ? 0 : w.g * p.Rg;
       const int r1 = p.pool ? p.R : min(p.R, r0 + p.Rg);
       const int i = w.I * G::UMMA_M + (int)rank * BMC + il;
