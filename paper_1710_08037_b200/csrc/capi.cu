@@ -934,6 +934,9 @@ ps_status plan_call(ps_ctx* c, const ps_plv_args* a, Call& k, const std::vector<
     p.kc_blocks = unsafe ? want : std::min(want, kc_max);
   }
   p.upper_only = a->out_layout == PS_LAYOUT_UPPER ? 1 : 0;
+  // trial-group partial sums are written as upper triangles; the group reduce
+  // produces the mirror (half the slot stores and reduce reads)
+  p.slot_upper = (p.upper_only || k.slot_mode == 2) ? 1 : 0;
   static const int dbg = [] {
     const char* s = std::getenv("PS_DEBUG_EPI");
     return s ? std::atoi(s) : 0;
@@ -2072,8 +2075,8 @@ ps_status plv_family_locked(ps_ctx* c, const ps_plv_args* a, ps_plv_result* res)
                  k.stage_off.empty() ? 0 : k.stage_off.back());
   }
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, k.reduce_div, g.split ? 0 : 1, st,
-                                    a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, (int)g.N, (int)g.B, 5, k.outs, k.reduce_div, g.split ? 0 : 1, st,
+                                a->out_layout == PS_LAYOUT_UPPER ? 1 : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
   ps_status s = read_status(c, st);
@@ -2217,8 +2220,8 @@ ps_status ps_coherence(ps_ctx* c, const ps_plv_args* a, const ps_welch* w, ps_pl
   PS_TRY(plan_call(c, &at, k, {}, /*force_g1=*/false, st));
   PS_TRY(launch_stage(c, k, 0, st));
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, gt.B * k.nn, k.reduce_div, gt.split ? 0 : 1, st,
-                                    a->out_layout == PS_LAYOUT_UPPER ? g.N : 0));
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, (int)gt.N, (int)gt.B, 5, k.outs, k.reduce_div, gt.split ? 0 : 1, st,
+                                a->out_layout == PS_LAYOUT_UPPER ? 1 : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
   if (c->timing) PS_CUDA(cudaEventRecord(c->ev[2], st));
@@ -2439,8 +2442,8 @@ ps_status host_unit_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long lon
     if (trace) trace->rec(sc, "gram", s);
   }
   if (k.slot_mode == 2) {
-    PS_CUDA(launch_group_reduce(c->gws.p, k.G, k.nn, 5, k.outs, g.B * k.nn, k.reduce_div, g.split ? 0 : 1, sc,
-                                upper ? g.N : 0));
+    PS_CUDA(launch_group_reduce(c->gws.p, k.G, (int)g.N, (int)g.B, 5, k.outs, k.reduce_div, g.split ? 0 : 1, sc,
+                                upper ? 1 : 0));
     for (int m = 0; m < 5; ++m) c->launches += k.outs[m] ? 1 : 0;
   }
   ps_status st = read_status(c, sc);

@@ -138,12 +138,12 @@ __device__ __forceinline__ void emit_all(const GramParams& p, long long slot, in
                                          const PairMetrics<S>& m, bool first, bool last) {
   const long long off = slot * (long long)p.N * p.N;
   const long long N = p.N;
-  if (p.out_plv) emit<S>(static_cast<S*>(p.out_plv) + off, N, i, j, m.plv, first, last, p.mean_div, false, !p.upper_only);
-  if (p.out_iplv) emit<S>(static_cast<S*>(p.out_iplv) + off, N, i, j, m.iplv, first, last, p.mean_div, false, !p.upper_only);
+  if (p.out_plv) emit<S>(static_cast<S*>(p.out_plv) + off, N, i, j, m.plv, first, last, p.mean_div, false, !p.slot_upper);
+  if (p.out_iplv) emit<S>(static_cast<S*>(p.out_iplv) + off, N, i, j, m.iplv, first, last, p.mean_div, false, !p.slot_upper);
   if (p.out_ciplv)
-    emit<S>(static_cast<S*>(p.out_ciplv) + off, N, i, j, m.ciplv, first, last, p.mean_div, false, !p.upper_only);
-  if (p.out_cre) emit<S>(static_cast<S*>(p.out_cre) + off, N, i, j, m.cre, first, last, p.mean_div, false, !p.upper_only);
-  if (p.out_cim) emit<S>(static_cast<S*>(p.out_cim) + off, N, i, j, m.cim, first, last, p.mean_div, true, !p.upper_only);
+    emit<S>(static_cast<S*>(p.out_ciplv) + off, N, i, j, m.ciplv, first, last, p.mean_div, false, !p.slot_upper);
+  if (p.out_cre) emit<S>(static_cast<S*>(p.out_cre) + off, N, i, j, m.cre, first, last, p.mean_div, false, !p.slot_upper);
+  if (p.out_cim) emit<S>(static_cast<S*>(p.out_cim) + off, N, i, j, m.cim, first, last, p.mean_div, true, !p.slot_upper);
 }
 
 // Four consecutive columns j0..j0+3 of row i, all strictly above the diagonal
@@ -179,7 +179,7 @@ __device__ __forceinline__ void emit4_all(const GramParams& p, long long slot, i
     }
     float* base = outs[q] + off;
     if (!(p.debug_flags & 8)) *reinterpret_cast<float4*>(base + (long long)i * N + j0) = a;
-    if (last && !p.upper_only && !(p.debug_flags & 4)) {
+    if (last && !p.slot_upper && !(p.debug_flags & 4)) {
       const float s = q == 4 ? -1.f : 1.f;
       base[(long long)(j0 + 0) * N + i] = s * a.x;
       base[(long long)(j0 + 1) * N + i] = s * a.y;

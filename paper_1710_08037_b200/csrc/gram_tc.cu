@@ -313,7 +313,7 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
   const long long soff = ri.slot * N * N;
   const long long od = soff + (long long)i * N + jb;
   const long long om = soff + (long long)jb * N + i;
-  const bool mirror = ri.last && !p.upper_only && !(p.debug_flags & 4);
+  const bool mirror = ri.last && !p.slot_upper && !(p.debug_flags & 4);
   const bool direct = !(p.debug_flags & 8);
   // trial mean: the last round of a slot scales by 1 / R (a reciprocal
   // multiply keeps the division's slow path out of the emission loops)

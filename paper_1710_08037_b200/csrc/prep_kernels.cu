@@ -1639,19 +1639,79 @@ cudaError_t launch_indicator_plane(const void* planes, long long plane_stride, i
   return cudaGetLastError();
 }
 
-cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs, void* const* outs,
-                                long long elems_per_out, int R, int is_double, cudaStream_t st, long long upper_n) {
-  // ws holds n_outputs consecutive blocks of [B][G][slot_elems]
-  const int g = grid_for(elems_per_out, 256);
-  const long long ws_block = elems_per_out * G;
+// Full layout from upper-triangle slots: one 32 x 32 tile (I <= J) per block;
+// the block sums its upper entries over the G slots (coalesced rows), writes
+// them, and writes the mirror tile (J, I) from shared memory so those stores
+// are coalesced too.  Sum order per entry as group_reduce_kernel (g = 0 ..
+// G-1), so both triangles equal what mirrored slots would give.
+template <typename S>
+__global__ void __launch_bounds__(256) group_reduce_sym_kernel(const S* __restrict__ ws, int G, int N, int nt, int R,
+                                                               S* __restrict__ out, bool anti) {
+  __shared__ S tile[32][33];
+  // blockIdx.x -> (I, J), I <= J, row-major over the upper tile triangle
+  int t = blockIdx.x, I = 0;
+  while (t >= nt - I) {
+    t -= nt - I;
+    ++I;
+  }
+  const int J = I + t;
+  const long long nn = (long long)N * N;
+  const S* wb = ws + (long long)blockIdx.y * G * nn;
+  S* ob = out + (long long)blockIdx.y * nn;
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int j = J * 32 + tx;
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = ty + 8 * rr, i = I * 32 + r;
+    if (i < N && j < N && (I < J || r <= tx)) {
+      const S* p = wb + (long long)i * N + j;
+      S acc = p[0];
+      for (int g = 1; g < G; ++g) acc += p[g * nn];
+      acc = sizeof(S) == 4 ? acc * (S(1) / S(R)) : acc / S(R);  // = epilogue.cuh mean_scale
+      ob[(long long)i * N + j] = acc;
+      tile[r][tx] = acc;
+    }
+  }
+  __syncthreads();
+  const int ii = I * 32 + tx;  // output column of the mirror tile
+#pragma unroll
+  for (int rr = 0; rr < 4; ++rr) {
+    const int r = ty + 8 * rr, jj = J * 32 + r;  // output row
+    if (jj < N && ii < N && (I < J || tx < r)) {
+      const S v = tile[tx][r];
+      ob[(long long)jj * N + ii] = anti ? -v : v;
+    }
+  }
+}
+
+cudaError_t launch_group_reduce(const void* ws, int G, int N, int B, int n_outputs, void* const* outs, int R,
+                                int is_double, cudaStream_t st, int upper) {
+  // ws holds n_outputs consecutive blocks of [B][G][N*N]
+  const long long nn = (long long)N * N;
+  const long long elems = (long long)B * nn;
+  const long long ws_block = elems * G;
+  const int nt = (N + 31) / 32;
+  const long long tiles = (long long)nt * (nt + 1) / 2;
+  if (!upper && (tiles > 0x7fffffffLL || B > 65535)) return cudaErrorInvalidValue;
   for (int m = 0; m < n_outputs; ++m) {
     if (!outs[m]) continue;
-    if (is_double)
-      group_reduce_kernel<double><<<g, 256, 0, st>>>((const double*)ws + m * ws_block, G, slot_elems,
-                                                      elems_per_out, R, (double*)outs[m], upper_n);
-    else
-      group_reduce_kernel<float><<<g, 256, 0, st>>>((const float*)ws + m * ws_block, G, slot_elems,
-                                                     elems_per_out, R, (float*)outs[m], upper_n);
+    if (upper) {
+      const int g = grid_for(elems, 256);
+      if (is_double)
+        group_reduce_kernel<double><<<g, 256, 0, st>>>((const double*)ws + m * ws_block, G, nn, elems, R,
+                                                        (double*)outs[m], N);
+      else
+        group_reduce_kernel<float><<<g, 256, 0, st>>>((const float*)ws + m * ws_block, G, nn, elems, R,
+                                                       (float*)outs[m], N);
+    } else {
+      const dim3 grid((unsigned)tiles, (unsigned)B), block(32, 8);
+      if (is_double)
+        group_reduce_sym_kernel<double><<<grid, block, 0, st>>>((const double*)ws + m * ws_block, G, N, nt, R,
+                                                                 (double*)outs[m], m == 4);
+      else
+        group_reduce_sym_kernel<float><<<grid, block, 0, st>>>((const float*)ws + m * ws_block, G, N, nt, R,
+                                                                (float*)outs[m], m == 4);
+    }
   }
   return cudaGetLastError();
 }

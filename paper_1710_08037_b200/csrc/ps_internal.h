@@ -86,7 +86,9 @@ struct GramParams {
   int refine_cap;
   int kc_blocks;               // split kernel: K blocks per TMEM accumulation chunk (drain period)
   int debug_flags;             // experiments only (PS_DEBUG_EPI): 1 = skip the metric emission
-  int upper_only;              // PS_LAYOUT_UPPER: no mirror (j, i) writes
+  int upper_only;              // PS_LAYOUT_UPPER: the final outputs hold i <= j only (refinement skips mirrors)
+  int slot_upper;              // the Gram writes only i <= j of its output slots (no mirror (j, i) stores):
+                               // PS_LAYOUT_UPPER, and trial-group partial-sum slots, whose reduce mirrors
   // Producer lockstep (split kernel): every producer publishes each group of
   // lock_group issued K blocks in lock_cnt[group] and may not run more than
   // lock_lag groups ahead of the slowest producer, so the CTAs that share an
@@ -176,9 +178,12 @@ cudaError_t launch_analytic_out(const SrcDesc& src, long long row0, long long nr
 // Eq 8 (over trials): planes [P][B*R][N][Tp] -> [P][B*T][N][Rp] + masked-trial counts
 cudaError_t launch_transpose_trials(const void* src, long long sps, int Tp, void* dst, long long dps, int Rp, int B,
                                     int R, int N, int T, int split, int* maskcount_dst, cudaStream_t st);
-cudaError_t launch_group_reduce(const void* ws, int G, long long slot_elems, int n_outputs,
-                                void* const* outs, long long elems_per_out, int R,
-                                int is_double, cudaStream_t st, long long upper_n);
+// Trial-group reduce: out_m[b] = sum_g ws_m[b][g] scaled by 1 / R, from slots
+// holding only i <= j (GramParams::slot_upper); upper = 1 writes i <= j of the
+// outputs, upper = 0 both triangles (the mirror through shared-memory tiles,
+// negated for the antisymmetric signed Im output, m = 4).
+cudaError_t launch_group_reduce(const void* ws, int G, int N, int B, int n_outputs, void* const* outs, int R,
+                                int is_double, cudaStream_t st, int upper);
 // K7: per-pair observation counts from the unmasked-indicator plane (same
 // items / tiles / cluster layout as the split Gram; p.cnt receives the counts)
 cudaError_t launch_gram_count(const void* tmapA, const void* tmapB, const GramParams& p, int groups, cudaStream_t st);
