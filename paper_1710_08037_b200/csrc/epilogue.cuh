@@ -117,7 +117,13 @@ __device__ __forceinline__ long long effective_T(const GramParams& p, int u0, in
 // multiplied by the fp32 reciprocal 1 / R on every path that forms a mean
 // (interior and general epilogues, trial-group reduce), so any two paths
 // that sum the same terms produce bit-identical means; FP64 divides.
-__device__ __forceinline__ float mean_scale(float acc, int div) { return acc * (1.0f / (float)div); }
+// A sum equal to the divisor is an exact mean of 1 (every diagonal entry of
+// PLV / cre; SPEC.md:194 wants the self-pair PLV exactly 1) -- R * fl(1 / R)
+// alone can round below 1 (fp32: R = 41, 47, 55, ...).
+__device__ __forceinline__ float mean_scale(float acc, int div) {
+  const float d = (float)div;
+  return acc == d ? 1.0f : acc * (1.0f / d);
+}
 __device__ __forceinline__ double mean_scale(double acc, int div) { return acc / (double)div; }
 
 // Accumulating store of one metric value into slot `base` at (i, j); the
@@ -173,9 +179,8 @@ __device__ __forceinline__ void emit4_all(const GramParams& p, long long slot, i
       v[e] = q == 0 ? m[e].plv : q == 1 ? m[e].iplv : q == 2 ? m[e].ciplv : q == 3 ? m[e].cre : m[e].cim;
     float4 a = make_float4(prev[q].x + v[0], prev[q].y + v[1], prev[q].z + v[2], prev[q].w + v[3]);
     if (last && p.mean_div != 1) {
-      const float d = (float)p.mean_div;
-      const float rd = 1.0f / d;
-      a = make_float4(a.x * rd, a.y * rd, a.z * rd, a.w * rd);
+      const int d = p.mean_div;
+      a = make_float4(mean_scale(a.x, d), mean_scale(a.y, d), mean_scale(a.z, d), mean_scale(a.w, d));
     }
     float* base = outs[q] + off;
     if (!(p.debug_flags & 8)) *reinterpret_cast<float4*>(base + (long long)i * N + j0) = a;
@@ -226,12 +231,17 @@ __device__ __forceinline__ InteriorPair interior_pair(float gre, float gim, floa
 // the direct entry (i, j0) and om of the mirror entry (j0, i).  One 32-byte
 // store per metric for the direct part (a full sector per lane), mirror
 // stores coalesced across the warp's lanes (consecutive i), their addresses
-// stepped by one row (N) per column.  rdiv = 1 / trial-mean divisor at the
-// last round of a slot (else 1).  PLV / iPLV / ciPLV only: the signed Re / Im
-// outputs (rarely requested) go through emit_signed_round, outside the hot
-// loop, so the loop body stays small enough for the instruction cache.
+// stepped by one row (N) per column.  div = trial-mean divisor at the last
+// round of a slot (else 1; mean_scale).  PLV / iPLV / ciPLV only: the signed
+// Re / Im outputs (rarely requested) go through emit_signed_round, outside
+// the hot loop, so the loop body stays small enough for the instruction
+// cache.  DIAG (a warp block on the diagonal): column e of the group is this
+// lane's own column at e == d0; entries e < d0 lie below the diagonal (not
+// written), the mirror is written for e > d0 only.
+template <bool DIAG = false>
 __device__ __forceinline__ void emit8_interior(const GramParams& p, long long od, long long om,
-                                               const InteriorPair (&m)[8], bool direct, bool mirror, float rdiv) {
+                                               const InteriorPair (&m)[8], bool direct, bool mirror, int div,
+                                               int d0 = -1) {
   const long long N = p.N;
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
@@ -239,12 +249,24 @@ __device__ __forceinline__ void emit8_interior(const GramParams& p, long long od
     if (!o) continue;
     float a[8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) a[e] = (q == 0 ? m[e].plv : q == 1 ? m[e].aim : m[e].ci) * rdiv;
-    if (direct) st_v8(o + od, a);
+    for (int e = 0; e < 8; ++e) {
+      const float v = q == 0 ? m[e].plv : q == 1 ? m[e].aim : m[e].ci;
+      a[e] = div == 1 ? v : mean_scale(v, div);
+    }
+    if (direct) {
+      if (!DIAG || d0 <= 0) {
+        st_v8(o + od, a);
+      } else if (d0 < 8) {
+#pragma unroll
+        for (int e = 1; e < 8; ++e)
+          if (e >= d0) o[od + e] = a[e];
+      }
+    }
     if (mirror) {
       float* mp = o + om;
 #pragma unroll
-      for (int e = 0; e < 8; ++e, mp += N) *mp = a[e];
+      for (int e = 0; e < 8; ++e, mp += N)
+        if (!DIAG || e > d0) *mp = a[e];
     }
   }
 }
@@ -252,10 +274,12 @@ __device__ __forceinline__ void emit8_interior(const GramParams& p, long long od
 // Four consecutive columns of one row (N % 4 == 0), any round: one 16-byte
 // read-modify-write per metric for the direct part, all reads issued before
 // any write so their latencies overlap; mirror writes (last round) as in
-// emit8_interior.
+// emit8_interior.  DIAG as there (entries below the diagonal are read with
+// the row but never written).
+template <bool DIAG = false>
 __device__ __forceinline__ void emit4_interior(const GramParams& p, long long od, long long om,
                                                const InteriorPair (&m)[4], bool first, bool direct, bool mirror,
-                                               float rdiv) {
+                                               int div, int d0 = -1) {
   const long long N = p.N;
   float* outs[3] = {static_cast<float*>(p.out_plv), static_cast<float*>(p.out_iplv),
                     static_cast<float*>(p.out_ciplv)};
@@ -263,21 +287,29 @@ __device__ __forceinline__ void emit4_interior(const GramParams& p, long long od
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     prev[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (outs[q] && !first) prev[q] = *reinterpret_cast<const float4*>(outs[q] + od);
+    if (outs[q] && !first && (!DIAG || d0 < 4)) prev[q] = *reinterpret_cast<const float4*>(outs[q] + od);
   }
+  auto sc = [&](float x) { return div == 1 ? x : mean_scale(x, div); };
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     if (!outs[q]) continue;
     auto val = [&](int e) { return q == 0 ? m[e].plv : q == 1 ? m[e].aim : m[e].ci; };
-    const float4 a = make_float4((prev[q].x + val(0)) * rdiv, (prev[q].y + val(1)) * rdiv,
-                                 (prev[q].z + val(2)) * rdiv, (prev[q].w + val(3)) * rdiv);
-    if (direct) *reinterpret_cast<float4*>(outs[q] + od) = a;
+    const float a[4] = {sc(prev[q].x + val(0)), sc(prev[q].y + val(1)), sc(prev[q].z + val(2)),
+                        sc(prev[q].w + val(3))};
+    if (direct) {
+      if (!DIAG || d0 <= 0) {
+        *reinterpret_cast<float4*>(outs[q] + od) = make_float4(a[0], a[1], a[2], a[3]);
+      } else if (d0 < 4) {
+#pragma unroll
+        for (int e = 1; e < 4; ++e)
+          if (e >= d0) outs[q][od + e] = a[e];
+      }
+    }
     if (mirror) {
       float* mp = outs[q] + om;
-      mp[0] = a.x;
-      mp[N] = a.y;
-      mp[2 * N] = a.z;
-      mp[3 * N] = a.w;
+#pragma unroll
+      for (int e = 0; e < 4; ++e, mp += N)
+        if (!DIAG || e > d0) *mp = a[e];
     }
   }
 }

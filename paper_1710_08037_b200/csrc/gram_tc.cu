@@ -229,10 +229,11 @@ __device__ __forceinline__ void store_sums(const float (&s)[H], uint32_t taddr) 
 
 // Signed Re / Im outputs (cre, cim) of one interior warp slice: a second pass
 // over the TMEM columns, only when requested.  inv(j) = 1 / T_ij.
-template <int BN, int HALF, typename InvF>
+template <int BN, int HALF, bool DIAG, typename InvF>
 __device__ __forceinline__ void emit_signed_round(const GramParams& p, uint32_t ta, int jb, long long od, long long om,
-                                                  InvF inv, bool first, bool direct, bool mirror, float rdiv) {
+                                                  InvF inv, bool first, bool direct, bool mirror, int div) {
   const long long N = p.N;
+  const int l = threadIdx.x & 31;  // DIAG: this lane's own column in the block
 #pragma unroll 1
   for (int g = 0; g < HALF; g += 4) {
     uint32_t vre[4], vim[4];
@@ -245,11 +246,15 @@ __device__ __forceinline__ void emit_signed_round(const GramParams& p, uint32_t 
       if (!o) continue;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float v = __uint_as_float(q == 0 ? vre[e] : vim[e]) * inv(jb + g + e);
-        const long long d = od + g + e;
-        const float a = ((first ? 0.0f : o[d]) + v) * rdiv;
+        const int c = g + e;
+        if (DIAG && c < l) continue;  // below the diagonal
+        const float v = (DIAG && c == l) ? (q == 0 ? 1.0f : 0.0f)
+                                         : __uint_as_float(q == 0 ? vre[e] : vim[e]) * inv(jb + c);
+        const long long d = od + c;
+        const float s = (first ? 0.0f : o[d]) + v;
+        const float a = div == 1 ? s : mean_scale(s, div);
         if (direct) o[d] = a;
-        if (mirror) o[om + (long long)(g + e) * N] = q == 1 ? -a : a;
+        if (mirror && (!DIAG || c > l)) o[om + (long long)c * N] = q == 1 ? -a : a;
       }
     }
   }
@@ -261,16 +266,19 @@ __device__ __forceinline__ void emit_signed_round(const GramParams& p, uint32_t 
 // Gram, p.cnt) is a template parameter, so the common unmasked loop carries
 // no count code, and the ill-conditioned pairs of a column group are queued
 // for refinement after the group from a bit mask (one copy of the queue code).
-template <int BN, int HALF, bool MASKED>
+template <int BN, int HALF, bool MASKED, bool DIAG>
 __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundInfo ri, uint32_t ta, int i, int jb,
                                            float inv_t) {
+  // DIAG: the warp block sits on the diagonal (ib == jb): lane l's own column
+  // is c == l (exact diagonal metrics), columns c < l lie below it
+  const int l = threadIdx.x & 31;
   unsigned illc = 0, nind = 0;
   // ill-conditioning test of the general path, 1e-6 (|cim| are / d + 1) >
   // tol sqrt(d), multiplied through by d / 1e-6 (d > 0): no division
   const float kt = p.illcond_tol * 1e6f;
   const float tol = p.illcond_tol;
   auto inv_at = [&](int j) -> float {
-    if (!MASKED) return inv_t;
+    if (!MASKED || (DIAG && j <= i)) return inv_t;
     const long long cs = p.pool ? (long long)(ri.u0 / p.R) : (long long)ri.u0;
     const int te = p.cnt[cs * (long long)p.N * p.N + (long long)i * p.N + j];  // i < j
     if (te <= 0) {
@@ -315,9 +323,10 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
   const long long om = soff + (long long)jb * N + i;
   const bool mirror = ri.last && !p.slot_upper && !(p.debug_flags & 4);
   const bool direct = !(p.debug_flags & 8);
-  // trial mean: the last round of a slot scales by 1 / R (a reciprocal
-  // multiply keeps the division's slow path out of the emission loops)
-  const float rdiv = (ri.last && p.mean_div != 1) ? 1.0f / (float)p.mean_div : 1.0f;
+  // trial mean: the last round of a slot scales by 1 / R (mean_scale: a
+  // reciprocal multiply, exact for a mean of 1; no division slow path here)
+  const int div = (ri.last && p.mean_div != 1) ? p.mean_div : 1;
+  const InteriorPair dm = {1.0f, 0.0f, 0.0f, 1.0f, 0.0f, 1.0f, 0.0f, 0.0f};  // diagonal
   if (ri.first && (p.N & 7) == 0) {
     // first round of the slot: 8 columns per step, one 32-byte direct store
     // per metric (a full sector per lane) and lane-coalesced mirror stores
@@ -329,14 +338,17 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
       ptx::tmem_wait_ld();
       InteriorPair m8[8];
       unsigned fl = 0;
+      const int d0 = DIAG ? l - g : -1;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const InteriorPair& m = m8[e] = interior_pair(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(jb + g + e));
-        nind += (m.d <= 0.0f && m.aim > tol) ? 1u : 0u;
-        fl |= (m.d > 0.0f && m.aim * m.are + m.d > kt * m.d * m.d * m.rd) ? (1u << e) : 0u;
+        const bool up = !DIAG || e > d0;  // strictly above the diagonal
+        nind += (up && m.d <= 0.0f && m.aim > tol) ? 1u : 0u;
+        fl |= (up && m.d > 0.0f && m.aim * m.are + m.d > kt * m.d * m.d * m.rd) ? (1u << e) : 0u;
+        if (DIAG && e == d0) m8[e] = dm;
       }
       if (fl) flush(fl, jb + g, m8);
-      emit8_interior(p, od + g, om + (long long)g * N, m8, direct, mirror, rdiv);
+      emit8_interior<DIAG>(p, od + g, om + (long long)g * N, m8, direct, mirror, div, d0);
     }
   } else {
 #pragma unroll 1
@@ -347,18 +359,21 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
       ptx::tmem_wait_ld();
       InteriorPair m4[4];
       unsigned fl = 0;
+      const int d0 = DIAG ? l - g : -1;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const InteriorPair& m = m4[e] = interior_pair(__uint_as_float(vre[e]), __uint_as_float(vim[e]), inv_at(jb + g + e));
-        nind += (m.d <= 0.0f && m.aim > tol) ? 1u : 0u;
-        fl |= (m.d > 0.0f && m.aim * m.are + m.d > kt * m.d * m.d * m.rd) ? (1u << e) : 0u;
+        const bool up = !DIAG || e > d0;
+        nind += (up && m.d <= 0.0f && m.aim > tol) ? 1u : 0u;
+        fl |= (up && m.d > 0.0f && m.aim * m.are + m.d > kt * m.d * m.d * m.rd) ? (1u << e) : 0u;
+        if (DIAG && e == d0) m4[e] = dm;
       }
       if (fl) flush(fl, jb + g, m4);
-      emit4_interior(p, od + g, om + (long long)g * N, m4, ri.first, direct, mirror, rdiv);
+      if (!DIAG || d0 < 4) emit4_interior<DIAG>(p, od + g, om + (long long)g * N, m4, ri.first, direct, mirror, div, d0);
     }
   }
   if (p.out_cre || p.out_cim)
-    emit_signed_round<BN, HALF>(p, ta, jb, od, om, inv_at, ri.first, direct, mirror, rdiv);
+    emit_signed_round<BN, HALF, DIAG>(p, ta, jb, od, om, inv_at, ri.first, direct, mirror, div);
   if (illc && !p.refine) atomicAdd(&p.status->n_illcond, (unsigned long long)illc);
   if (nind) atomicAdd(&p.status->n_indeterminate, (unsigned long long)nind);
 }
@@ -394,8 +409,20 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
     return 1.0f / static_cast<float>(te);
   };
   if (interior) {
-    if (any_masked) emit_interior<BN, HALF, true>(p, ri, ta, i, jb, inv_t);
-    else emit_interior<BN, HALF, false>(p, ri, ta, i, jb, inv_t);
+    if (any_masked) emit_interior<BN, HALF, true, false>(p, ri, ta, i, jb, inv_t);
+    else emit_interior<BN, HALF, false, false>(p, ri, ta, i, jb, inv_t);
+    return;
+  }
+  // every row of the block below every column: no pair i <= j to emit
+  if (ib >= jb + HALF) return;
+  // diagonal warp block (ib == jb) inside the matrix: the interior loops with
+  // per-lane predicates (the general per-pair path below was measured to gate
+  // the whole pipeline in short-K regimes: it holds its tile's accumulator
+  // several times longer than an interior block, profiles/r02_session2/
+  // emission_experiments.md)
+  if (ib == jb && (!any_masked || p.cnt) && (p.N & 3) == 0 && jb + HALF <= p.N && !(p.debug_flags & 2048)) {
+    if (any_masked) emit_interior<BN, HALF, true, true>(p, ri, ta, i, jb, inv_t);
+    else emit_interior<BN, HALF, false, true>(p, ri, ta, i, jb, inv_t);
     return;
   }
 #pragma unroll 1

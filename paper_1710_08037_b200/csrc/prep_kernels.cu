@@ -992,7 +992,7 @@ __global__ void group_reduce_kernel(const S* ws, int G, long long slot_elems, lo
     const S* p = ws + (b * G) * slot_elems + i;
     S acc = p[0];
     for (int g = 1; g < G; ++g) acc += p[g * slot_elems];
-    out[e] = sizeof(S) == 4 ? acc * (S(1) / S(R)) : acc / S(R);  // = epilogue.cuh mean_scale
+    out[e] = sizeof(S) == 4 ? (acc == S(R) ? S(1) : acc * (S(1) / S(R))) : acc / S(R);  // = epilogue.cuh mean_scale
   }
 }
 
@@ -1667,7 +1667,7 @@ __global__ void __launch_bounds__(256) group_reduce_sym_kernel(const S* __restri
       const S* p = wb + (long long)i * N + j;
       S acc = p[0];
       for (int g = 1; g < G; ++g) acc += p[g * nn];
-      acc = sizeof(S) == 4 ? acc * (S(1) / S(R)) : acc / S(R);  // = epilogue.cuh mean_scale
+      acc = sizeof(S) == 4 ? (acc == S(R) ? S(1) : acc * (S(1) / S(R))) : acc / S(R);  // = epilogue.cuh mean_scale
       ob[(long long)i * N + j] = acc;
       tile[r][tx] = acc;
     }

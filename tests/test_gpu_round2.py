@@ -219,3 +219,86 @@ def test_concurrent_host_calls_one_context():
         t.join()
     torch.cuda.synchronize()
     assert not errs, errs
+
+
+@pytest.mark.parametrize("R,groups", [(41, None), (41, "1"), (47, "47")])
+def test_trial_mean_diagonal_exact_and_symmetric(R, groups, monkeypatch):
+    """Trial means over R trials where R * fl(1/R) != 1 in fp32: the self-pair
+    PLV stays exactly 1 and iPLV / ciPLV exactly 0, both
+    triangles are bit-identical mirrors, and the values match the oracle --
+    through the trial-group partial sums (upper-triangle slots + tiled
+    reduce) and through the single-group path (mean at the last round)."""
+    import subprocess
+    import sys
+
+    if groups is not None:
+        # PS_GROUPS is read once per process: run the check in a child
+        code = f"""
+import sys; sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
+import numpy as np, torch
+from oracle import plv_oracle as O
+from paper_1710_08037_b200 import connectivity as C
+z = O.make_surrogate(320, 64, {R}, seed=91)
+r = C.plv_family(torch.from_numpy(z).cuda(), input_kind="phasor")
+ref = O.plv_family(z, input_kind="phasor")
+for m in ("plv", "iplv", "ciplv"):
+    v = r[m].values[0].cpu().numpy() if r[m].values.dim() == 3 else r[m].values.cpu().numpy()
+    d = np.diag(v)
+    assert np.all(d == (1.0 if m == "plv" else 0.0)), (m, d[d != (1.0 if m == "plv" else 0.0)][:4])
+    assert np.array_equal(v, v.T), m
+    assert np.max(np.abs(v - ref[m])) <= 1e-5, m
+print("ok")
+"""
+        env = dict(__import__("os").environ, PS_GROUPS=groups)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+        return
+    import torch
+
+    z = O.make_surrogate(320, 64, R, seed=91)
+    r = C.plv_family(torch.from_numpy(z).cuda(), input_kind="phasor")
+    ref = O.plv_family(z, input_kind="phasor")
+    for m in METRICS:
+        v = r[m].values.cpu().numpy()
+        v = v[0] if v.ndim == 3 else v
+        want = 1.0 if m == "plv" else 0.0
+        assert np.all(np.diag(v) == want), m
+        assert np.array_equal(v, v.T), m
+        assert np.max(np.abs(v - ref[m])) <= 1e-5, m
+
+
+@pytest.mark.parametrize("N", [256, 260, 1032])
+def test_diagonal_blocks_fast_path_matches_general(N):
+    """Diagonal warp blocks take the predicated interior loops; the general
+    per-pair path (PS_DEBUG_EPI=2048 in a child process) must give the same
+    bits, per trial and for trial means, both layouts."""
+    import os
+    import subprocess
+    import sys
+
+    code = f"""
+import sys; sys.path.insert(0, {repr(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))})
+import numpy as np, torch
+from oracle import plv_oracle as O
+from paper_1710_08037_b200 import connectivity as C
+z = torch.from_numpy(O.make_surrogate({N}, 96, 3, seed=92)).cuda()
+out = []
+for red in ("none", "mean"):
+    for layout in ("full", "upper"):
+        r = C.plv_family(z, input_kind="phasor", trial_reduce=red, layout=layout,
+                         metrics=("plv", "iplv", "ciplv", "cre", "cim"))
+        out += [r[m].values.cpu().numpy() for m in ("plv", "iplv", "ciplv", "cre", "cim")]
+np.save(sys.argv[1], np.concatenate([o.reshape(-1) for o in out]))
+"""
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as td:
+        res = []
+        for flag in ("0", "2048"):
+            path = os.path.join(td, f"o{flag}.npy")
+            env = dict(os.environ, PS_DEBUG_EPI=flag)
+            out = subprocess.run([sys.executable, "-c", code, path], env=env, capture_output=True, text=True,
+                                 timeout=600)
+            assert out.returncode == 0, out.stderr[-2000:]
+            res.append(np.load(path))
+        assert np.array_equal(res[0], res[1])
