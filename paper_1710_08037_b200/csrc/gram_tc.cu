@@ -716,6 +716,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                     ptx::mma_f8_ss_warp<CG>(d_re, a8 + 2 * k8, b8 + 2 * k8, idesc_pos, (chunk_start && k8 == 0) ? 0u : 1u);
                 }
               } else if constexpr (GS) {
+               if (!mma_split_issue) {
+                // one elected block per K step (9 UMMAs, see mma_gauss_step_warp)
+                const uint32_t alo = (uint32_t)dA + (uint32_t)ko, blo = (uint32_t)dB + (uint32_t)ko;
+                constexpr uint32_t AP = G::A_PLANE >> 4, BP = G::B_PLANE >> 4;
+                const uint32_t av[6] = {alo, alo + AP, alo + 2 * AP, alo + 3 * AP, alo + 4 * AP, alo + 5 * AP};
+                const uint32_t bv[6] = {blo, blo + BP, blo + 2 * BP, blo + 3 * BP, blo + 4 * BP, blo + 5 * BP};
+                ptx::mma_gauss_step_warp<CG>(d_re, d_im, d_re + 2 * BN, av, bv, (uint32_t)(dA >> 32), idesc_pos,
+                                             idesc_neg, acc0);
+               } else {
                 const uint64_t aSh = dA + ko + 4 * (G::A_PLANE >> 4);
                 const uint64_t aSl = dA + ko + 5 * (G::A_PLANE >> 4);
                 const uint64_t bDh = dB + ko + 4 * (G::B_PLANE >> 4);
@@ -733,6 +742,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                 ptx::mma_f16_ss_warp<CG>(d_k3, aIh, bDh, idesc_pos, acc0);
                 ptx::mma_f16_ss_warp<CG>(d_k3, aIh, bDl, idesc_pos, 1u);
                 ptx::mma_f16_ss_warp<CG>(d_k3, aIl, bDh, idesc_pos, 1u);
+               }
               } else if (!mma_split_issue) {
                 // one elected block per K step (12 UMMAs, see mma_4prod_step_warp)
                 const uint32_t alo = (uint32_t)dA + (uint32_t)ko, blo = (uint32_t)dB + (uint32_t)ko;

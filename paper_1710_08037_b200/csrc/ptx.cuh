@@ -248,6 +248,43 @@ __device__ __forceinline__ void mma_4prod_step_warp(uint32_t d_re, uint32_t d_im
 #undef PS_MMA4
 }
 
+// One K = 16 step of the Gauss 3-product split Gram as a single
+// warp-collective block (see mma_4prod_step_warp):
+//   k1 += S_i Zr_j   (Sh.Rh' + Sh.Rl' + Sl.Rh')      -> d1
+//   k2 -= Zr_i S_j   (Rh.Sh' + Rh.Sl' + Rl.Sh')      -> d2 (negated A)
+//   k3 += Zi_i D_j   (Ih.Dh' + Ih.Dl' + Il.Dh')      -> d3
+// a = {Rh, Rl, Ih, Il, Sh, Sl} and b = {Rh, Rl, Sh, Sl, Dh, Dl} low words.
+template <int CG>
+__device__ __forceinline__ void mma_gauss_step_warp(uint32_t d1, uint32_t d2, uint32_t d3, const uint32_t (&a)[6],
+                                                    const uint32_t (&b)[6], uint32_t hi, uint32_t ipos,
+                                                    uint32_t ineg, uint32_t acc) {
+#define PS_MMAG(CGS)                                                                                 \
+  asm volatile(                                                                                        \
+      "{\n\t.reg .pred e, p, t;\n\t.reg .b64 arh, arl, aih, ail, ash, asl, brh, brl, bsh, bsl, bdh, bdl;\n\t" \
+      "elect.sync _|e, 0xffffffff;\n\t"                                                              \
+      "setp.ne.b32 p, %20, 0;\n\tsetp.eq.b32 t, %20, %20;\n\t"                                       \
+      "mov.b64 arh, {%3, %15};\n\tmov.b64 arl, {%4, %15};\n\tmov.b64 aih, {%5, %15};\n\t"          \
+      "mov.b64 ail, {%6, %15};\n\tmov.b64 ash, {%7, %15};\n\tmov.b64 asl, {%8, %15};\n\t"          \
+      "mov.b64 brh, {%9, %15};\n\tmov.b64 brl, {%10, %15};\n\tmov.b64 bsh, {%11, %15};\n\t"        \
+      "mov.b64 bsl, {%12, %15};\n\tmov.b64 bdh, {%13, %15};\n\tmov.b64 bdl, {%14, %15};\n\t"       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ash, brh, %16, p;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], ash, brl, %16, t;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%0], asl, brh, %16, t;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], arh, bsh, %17, p;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], arh, bsl, %17, t;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%1], arl, bsh, %17, t;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%2], aih, bdh, %16, p;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%2], aih, bdl, %16, t;\n\t"                       \
+      "@e tcgen05.mma.cta_group::" CGS ".kind::f16 [%2], ail, bdh, %16, t;\n\t}"                      \
+      ::"r"(d1), "r"(d2), "r"(d3), "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(b[0]), \
+      "r"(b[1]), "r"(b[2]), "r"(b[3]), "r"(b[4]), "r"(b[5]), "r"(hi), "r"(ipos), "r"(ineg), "r"(0u), "r"(0u), \
+      "r"(acc)                                                                                          \
+      : "memory")
+  if (CG == 1) PS_MMAG("1");
+  else PS_MMAG("2");
+#undef PS_MMAG
+}
+
 // kind::f8f6f4 (E4M3 A / B, fp32 D; the instruction descriptor's format
 // fields are 0 for E4M3 exactly as for F16, so make_idesc_f16 applies): the
 // K7 mask-count Gram's 0 / 1 indicator operands, K = 32 per instruction
