@@ -125,6 +125,9 @@ __device__ __forceinline__ float mean_scale(float acc, int div) {
   return acc == d ? 1.0f : acc * (1.0f / d);
 }
 __device__ __forceinline__ double mean_scale(double acc, int div) { return acc / (double)div; }
+// The same with fd = (float)div and rd = 1 / fd precomputed (fd = rd = 1: the
+// identity), branch-free for the emission loops.
+__device__ __forceinline__ float mean_scale_r(float acc, float fd, float rd) { return acc == fd ? 1.0f : acc * rd; }
 
 // Accumulating store of one metric value into slot `base` at (i, j); the
 // mirror (j, i) is written at the last round of the slot (negated for the
@@ -231,17 +234,17 @@ __device__ __forceinline__ InteriorPair interior_pair(float gre, float gim, floa
 // the direct entry (i, j0) and om of the mirror entry (j0, i).  One 32-byte
 // store per metric for the direct part (a full sector per lane), mirror
 // stores coalesced across the warp's lanes (consecutive i), their addresses
-// stepped by one row (N) per column.  div = trial-mean divisor at the last
-// round of a slot (else 1; mean_scale).  PLV / iPLV / ciPLV only: the signed
+// stepped by one row (N) per column.  fd / rd = the trial-mean divisor at
+// the last round of a slot and its reciprocal (else 1 / 1; mean_scale_r).  PLV / iPLV / ciPLV only: the signed
 // Re / Im outputs (rarely requested) go through emit_signed_round, outside
 // the hot loop, so the loop body stays small enough for the instruction
 // cache.  DIAG (a warp block on the diagonal): column e of the group is this
 // lane's own column at e == d0; entries e < d0 lie below the diagonal (not
 // written), the mirror is written for e > d0 only.
-template <bool DIAG = false>
+template <bool DIAG = false, bool SCALE = true>
 __device__ __forceinline__ void emit8_interior(const GramParams& p, long long od, long long om,
-                                               const InteriorPair (&m)[8], bool direct, bool mirror, int div,
-                                               int d0 = -1) {
+                                               const InteriorPair (&m)[8], bool direct, bool mirror, float fd,
+                                               float rd, int d0 = -1) {
   const long long N = p.N;
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
@@ -251,7 +254,7 @@ __device__ __forceinline__ void emit8_interior(const GramParams& p, long long od
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const float v = q == 0 ? m[e].plv : q == 1 ? m[e].aim : m[e].ci;
-      a[e] = div == 1 ? v : mean_scale(v, div);
+      a[e] = SCALE ? mean_scale_r(v, fd, rd) : v;
     }
     if (direct) {
       if (!DIAG || d0 <= 0) {
@@ -276,10 +279,10 @@ __device__ __forceinline__ void emit8_interior(const GramParams& p, long long od
 // any write so their latencies overlap; mirror writes (last round) as in
 // emit8_interior.  DIAG as there (entries below the diagonal are read with
 // the row but never written).
-template <bool DIAG = false>
+template <bool DIAG = false, bool SCALE = true>
 __device__ __forceinline__ void emit4_interior(const GramParams& p, long long od, long long om,
                                                const InteriorPair (&m)[4], bool first, bool direct, bool mirror,
-                                               int div, int d0 = -1) {
+                                               float fd, float rd, int d0 = -1) {
   const long long N = p.N;
   float* outs[3] = {static_cast<float*>(p.out_plv), static_cast<float*>(p.out_iplv),
                     static_cast<float*>(p.out_ciplv)};
@@ -289,7 +292,7 @@ __device__ __forceinline__ void emit4_interior(const GramParams& p, long long od
     prev[q] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (outs[q] && !first && (!DIAG || d0 < 4)) prev[q] = *reinterpret_cast<const float4*>(outs[q] + od);
   }
-  auto sc = [&](float x) { return div == 1 ? x : mean_scale(x, div); };
+  auto sc = [&](float x) { return SCALE ? mean_scale_r(x, fd, rd) : x; };
 #pragma unroll
   for (int q = 0; q < 3; ++q) {
     if (!outs[q]) continue;

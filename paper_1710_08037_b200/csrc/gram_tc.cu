@@ -266,7 +266,7 @@ __device__ __forceinline__ void emit_signed_round(const GramParams& p, uint32_t 
 // Gram, p.cnt) is a template parameter, so the common unmasked loop carries
 // no count code, and the ill-conditioned pairs of a column group are queued
 // for refinement after the group from a bit mask (one copy of the queue code).
-template <int BN, int HALF, bool MASKED, bool DIAG>
+template <int BN, int HALF, bool MASKED, bool DIAG, bool SCALE>
 __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundInfo ri, uint32_t ta, int i, int jb,
                                            float inv_t) {
   // DIAG: the warp block sits on the diagonal (ib == jb): lane l's own column
@@ -326,6 +326,7 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
   // trial mean: the last round of a slot scales by 1 / R (mean_scale: a
   // reciprocal multiply, exact for a mean of 1; no division slow path here)
   const int div = (ri.last && p.mean_div != 1) ? p.mean_div : 1;
+  const float fd = (float)div, rdv = 1.0f / fd;  // mean_scale_r operands (1, 1: identity)
   const InteriorPair dm = {1.0f, 0.0f, 0.0f, 1.0f, 0.0f, 1.0f, 0.0f, 0.0f};  // diagonal
   if (ri.first && (p.N & 7) == 0) {
     // first round of the slot: 8 columns per step, one 32-byte direct store
@@ -348,7 +349,7 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
         if (DIAG && e == d0) m8[e] = dm;
       }
       if (fl) flush(fl, jb + g, m8);
-      emit8_interior<DIAG>(p, od + g, om + (long long)g * N, m8, direct, mirror, div, d0);
+      emit8_interior<DIAG, SCALE>(p, od + g, om + (long long)g * N, m8, direct, mirror, fd, rdv, d0);
     }
   } else {
 #pragma unroll 1
@@ -369,7 +370,7 @@ __device__ __forceinline__ void emit_interior(const GramParams& p, const RoundIn
         if (DIAG && e == d0) m4[e] = dm;
       }
       if (fl) flush(fl, jb + g, m4);
-      if (!DIAG || d0 < 4) emit4_interior<DIAG>(p, od + g, om + (long long)g * N, m4, ri.first, direct, mirror, div, d0);
+      if (!DIAG || d0 < 4) emit4_interior<DIAG, SCALE>(p, od + g, om + (long long)g * N, m4, ri.first, direct, mirror, fd, rdv, d0);
     }
   }
   if (p.out_cre || p.out_cim)
@@ -408,9 +409,17 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
     }
     return 1.0f / static_cast<float>(te);
   };
+  // SCALE: the round that closes a trial mean divides (mean_scale); every
+  // other round stores its values as they are (no per-element select)
+  const bool scale = ri.last && p.mean_div != 1;
   if (interior) {
-    if (any_masked) emit_interior<BN, HALF, true, false>(p, ri, ta, i, jb, inv_t);
-    else emit_interior<BN, HALF, false, false>(p, ri, ta, i, jb, inv_t);
+    if (any_masked) {
+      if (scale) emit_interior<BN, HALF, true, false, true>(p, ri, ta, i, jb, inv_t);
+      else emit_interior<BN, HALF, true, false, false>(p, ri, ta, i, jb, inv_t);
+    } else {
+      if (scale) emit_interior<BN, HALF, false, false, true>(p, ri, ta, i, jb, inv_t);
+      else emit_interior<BN, HALF, false, false, false>(p, ri, ta, i, jb, inv_t);
+    }
     return;
   }
   // every row of the block below every column: no pair i <= j to emit
@@ -421,8 +430,13 @@ __device__ __forceinline__ void emit_round(const GramParams& p, const Item& w, i
   // several times longer than an interior block, profiles/r02_session2/
   // emission_experiments.md)
   if (ib == jb && (!any_masked || p.cnt) && (p.N & 3) == 0 && jb + HALF <= p.N && !(p.debug_flags & 2048)) {
-    if (any_masked) emit_interior<BN, HALF, true, true>(p, ri, ta, i, jb, inv_t);
-    else emit_interior<BN, HALF, false, true>(p, ri, ta, i, jb, inv_t);
+    if (any_masked) {
+      if (scale) emit_interior<BN, HALF, true, true, true>(p, ri, ta, i, jb, inv_t);
+      else emit_interior<BN, HALF, true, true, false>(p, ri, ta, i, jb, inv_t);
+    } else {
+      if (scale) emit_interior<BN, HALF, false, true, true>(p, ri, ta, i, jb, inv_t);
+      else emit_interior<BN, HALF, false, true, false>(p, ri, ta, i, jb, inv_t);
+    }
     return;
   }
 #pragma unroll 1
