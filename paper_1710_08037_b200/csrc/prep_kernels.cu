@@ -304,11 +304,15 @@ constexpr int kTw256 = 15 * 16;
 constexpr int kTwCount = kTw256 + 15 * 256;
 constexpr int kFftSmemBytes = (kFftPad(kFftT) + kTwCount) * 8;
 
+// Complex arithmetic on sm_100's packed FP32 pipe (FADD2 / FMUL2 / FFMA2 work
+// on an aligned register pair = one float2, with free per-operand swap
+// (.LO_HI), per-half negation and scalar broadcast): a complex add is one
+// instruction and a complex multiply two, half the scalar count.
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+  return __ffma2_rn(make_float2(-a.y, a.x), make_float2(b.y, b.y), __fmul2_rn(a, make_float2(b.x, b.x)));
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
 
 template <bool INV>
 __device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2& a3) {
@@ -357,9 +361,12 @@ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
       if (m == 4) {
         x = INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x);
       } else if (m == 2) {
-        x = INV ? make_float2((x.x - x.y) * c2, (x.x + x.y) * c2) : make_float2((x.x + x.y) * c2, (x.y - x.x) * c2);
+        // (1 -+ i) x c2 : x + (-+ i) x, one packed add and one packed multiply
+        x = __fmul2_rn(__fadd2_rn(x, INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x)), make_float2(c2, c2));
       } else if (m == 6) {
-        x = INV ? make_float2(-(x.x + x.y) * c2, (x.x - x.y) * c2) : make_float2((x.y - x.x) * c2, -(x.x + x.y) * c2);
+        // (-1 -+ i) x c2
+        x = __fmul2_rn(__fadd2_rn(make_float2(-x.x, -x.y), INV ? make_float2(-x.y, x.x) : make_float2(x.y, -x.x)),
+                       make_float2(c2, c2));
       } else {
         float2 tw = w16(m);
         if (INV) tw.y = -tw.y;
@@ -440,6 +447,9 @@ __device__ __forceinline__ void fft_pass(float2 (&v)[16], const float2* tw) {
 // planes S = Zr + Zi, D = Zr - Zi (hi / lo) from the rounded split values,
 // the arithmetic of gauss_planes_kernel; returns their min / max |a|.
 template <bool GS>
+__device__ __forceinline__ void emit4_split(const float (&zr)[4], const float (&zi)[4], __half* o, long long ps);
+
+template <bool GS>
 __device__ __forceinline__ void normalize4_split(const float (&re)[4], const float (&im)[4], __half* o,
                                                  long long ps, float& lo2, float& hi2) {
   float zr[4], zi[4];
@@ -455,6 +465,37 @@ __device__ __forceinline__ void normalize4_split(const float (&re)[4], const flo
     lo2 = fminf(lo2, a2);
     hi2 = fmax_nan(hi2, a2);  // NaN-propagating: a non-finite sample surfaces in the row max
   }
+  emit4_split<GS>(zr, zi, o, ps);
+}
+
+// The same for 4 consecutive samples of two rows at once, the rows riding the
+// two halves of the packed FP32 instructions: re[k] = (x_a, x_b) scaled,
+// h[k] = (H_a, H_b) as the packed inverse FFT left them.
+template <bool GS>
+__device__ __forceinline__ void normalize4_split_pair(const float2 (&re)[4], const float2 (&h)[4], __half* oa,
+                                                      __half* ob, bool hasb, long long ps, float& lo_a, float& hi_a,
+                                                      float& lo_b, float& hi_b) {
+  float zra[4], zia[4], zrb[4], zib[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 a2 = __ffma2_rn(re[k], re[k], __fmul2_rn(h[k], h[k]));
+    const float2 inv = make_float2(rsqrtf(fmaxf(a2.x, FLT_MIN)), rsqrtf(fmaxf(a2.y, FLT_MIN)));
+    const float2 zr = __fmul2_rn(re[k], inv), zi = __fmul2_rn(h[k], inv);
+    zra[k] = zr.x;
+    zrb[k] = zr.y;
+    zia[k] = zi.x;
+    zib[k] = zi.y;
+    lo_a = fminf(lo_a, a2.x);
+    hi_a = fmax_nan(hi_a, a2.x);
+    lo_b = fminf(lo_b, a2.y);
+    hi_b = fmax_nan(hi_b, a2.y);
+  }
+  emit4_split<GS>(zra, zia, oa, ps);
+  if (hasb) emit4_split<GS>(zrb, zib, ob, ps);
+}
+
+template <bool GS>
+__device__ __forceinline__ void emit4_split(const float (&zr)[4], const float (&zi)[4], __half* o, long long ps) {
   // packed conversions (F2FP / HADD2.F32): the same round-to-nearest
   // values as per-element __float2half_rn, half the instructions
   uint32_t w[GS ? 8 : 4][2];
@@ -558,10 +599,7 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
     }
     const float sa = pow2_scale(ma), sb = pow2_scale(mb);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      v[q].x *= sa;
-      v[q].y *= sb;
-    }
+    for (int q = 0; q < 16; ++q) v[q] = __fmul2_rn(v[q], make_float2(sa, sb));
     // forward FFT; the last pass leaves X[j + 256 r] in v[d16(r)]
     fft_pass<false, 1>(v, tw);
     store16<1>(v, buf);
@@ -616,16 +654,9 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
       float2 h[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) h[k] = hb[kFftPad(off) + k];
-      {
-        const float re[4] = {ca.x * soa, ca.y * soa, ca.z * soa, ca.w * soa};
-        const float im[4] = {h[0].x, h[1].x, h[2].x, h[3].x};
-        normalize4_split<GS>(re, im, opa + off, ps, amin_a, amax_a);
-      }
-      if (hasb) {
-        const float re[4] = {cb.x * sob, cb.y * sob, cb.z * sob, cb.w * sob};
-        const float im[4] = {h[0].y, h[1].y, h[2].y, h[3].y};
-        normalize4_split<GS>(re, im, opb + off, ps, amin_b, amax_b);
-      }
+      const float2 re[4] = {make_float2(ca.x * soa, cb.x * sob), make_float2(ca.y * soa, cb.y * sob),
+                            make_float2(ca.z * soa, cb.z * sob), make_float2(ca.w * soa, cb.w * sob)};
+      normalize4_split_pair<GS>(re, h, opa + off, opb + off, hasb, ps, amin_a, amax_a, amin_b, amax_b);
     }
     // block min / max of both rows (the CTA owns them: plain stores)
     float vals[4] = {amin_a, amax_a, amin_b, amax_b};
