@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
 // short-T, many-trial regime of config C4): one CTA per pair of rows, the two
 // rows packed as x_a + i x_b into one complex FFT (the Hilbert multiplier
 // -i sgn(k) is real-linear, so IFFT(h . FFT(x_a + i x_b)) = H{x_a} + i H{x_b}).
-// Radix-16 Stockham FFT in shared memory (3 passes each way, 256 threads x
+// In-place radix-16 FFT in shared memory (3 passes each way, 256 threads x
 // 16 values), the multiplier fused into the first inverse pass, and the
 // normalisation / fp16 hi-lo split / row min-max fused into the epilogue.
 // HBM traffic 12 B/sample (x in, planes out) versus ~40 B/sample for the
@@ -378,40 +378,56 @@ __device__ __forceinline__ void dft16(float2 (&v)[16]) {
   for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(v[4 * k1 + 0], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
 }
 
-// Radix-16 Stockham passes.  Every pass takes v[r] = x[j + 256 r] (natural
-// order, j = threadIdx.x), twiddles, runs the DFT16 and leaves output r in
-// v[d16(r)]; store16 scatters it for the next pass and load16 gathers the next
-// pass's inputs.  All shared-memory accesses of a pass are a per-thread base
-// plus a compile-time offset: pad(idx + r NS) = pad(idx) + r (NS + NS / 16)
-// when NS % 16 == 0, or NS == 1 and idx % 16 == 0.
-template <bool INV, int NS>
-__device__ __forceinline__ void twiddle16(float2 (&v)[16], const float2* tw) {
-  if (NS > 1) {
-    const float2* t = tw + (NS == 16 ? kTw16 : kTw256) + (threadIdx.x % NS);
-#pragma unroll
-    for (int r = 1; r < 16; ++r) {
-      float2 w = t[(r - 1) * NS];
-      if (INV) w.y = -w.y;
-      v[r] = cmul(v[r], w);
-    }
-  }
-}
-
-template <int NS>
-__device__ __forceinline__ void store16(const float2 (&v)[16], float2* buf) {
+// In-place radix-16 passes over the 4096-point buffer: decimation in frequency
+// forward (natural order in, digit-reversed out: frequency 256 k2 + 16 k1 + k0
+// at position 256 k0 + 16 k1 + k2), decimation in time inverse (digit-reversed
+// in, natural out).  Every thread reads and writes the SAME 16 positions in a
+// pass, so a pass needs no barrier between its loads and its stores, and the
+// exchanges between the stride-16 and stride-1 passes stay inside one aligned
+// group of 16 threads (a 256-point block): __syncwarp instead of a CTA barrier.
+// Position sets (pad(i) = i + i / 16; every access is a per-thread base plus
+// a compile-time offset):
+//   stride 256: pad(j + 256 r)          = pad(j) + 272 r
+//   stride 16 : pad(256 b + o + 16 r)   = 272 b + o + 17 r   (b = j / 16, o = j % 16)
+//   stride 1  : pad(16 j + r)           = 17 j + r
+// Twiddles multiply DFT16 output r (forward, after the butterfly) or input r
+// (inverse, before it) by W^(k r), k = j (stride 256, W_4096) or o (stride 16,
+// W_256), conjugated for the inverse.
+template <int STRIDE>
+__device__ __forceinline__ int pass_base() {
   const int j = threadIdx.x;
-  const int base = kFftPad((j / NS) * NS * 16 + j % NS);
-  constexpr int step = NS + NS / 16;
-  __syncthreads();  // every thread has read its inputs of this pass
-#pragma unroll
-  for (int r = 0; r < 16; ++r) buf[base + r * step] = v[d16(r)];
-  __syncthreads();
+  return STRIDE == 256 ? kFftPad(j) : STRIDE == 16 ? 272 * (j >> 4) + (j & 15) : 17 * j;
 }
-
-__device__ __forceinline__ void load16(float2 (&v)[16], const float2* buf) {
-  const int base = kFftPad(threadIdx.x);
+template <int STRIDE>
+__host__ __device__ constexpr int pass_step() {
+  return STRIDE == 256 ? 272 : STRIDE == 16 ? 17 : 1;
+}
+// v[r] = element r of this thread's set
+template <int STRIDE>
+__device__ __forceinline__ void load_set(float2 (&v)[16], const float2* buf) {
+  const float2* p = buf + pass_base<STRIDE>();
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = buf[base + r * (kFftThreads + kFftThreads / 16)];
+  for (int r = 0; r < 16; ++r) v[r] = p[r * pass_step<STRIDE>()];
+}
+// element r of the set = DFT16 output r (held in v[d16(r)])
+template <int STRIDE>
+__device__ __forceinline__ void store_set(const float2 (&v)[16], float2* buf) {
+  float2* p = buf + pass_base<STRIDE>();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) p[r * pass_step<STRIDE>()] = v[d16(r)];
+}
+// OUT: the DFT16 outputs (v[d16(r)]) are twiddled, else the inputs (v[r])
+template <bool INV, int STRIDE, bool OUT>
+__device__ __forceinline__ void twiddle16(float2 (&v)[16], const float2* tw) {
+  const float2* t = tw + (STRIDE == 16 ? kTw16 + (threadIdx.x & 15) : kTw256 + threadIdx.x);
+  constexpr int NS = STRIDE == 16 ? 16 : 256;
+#pragma unroll
+  for (int r = 1; r < 16; ++r) {
+    float2 w = t[(r - 1) * NS];
+    if (INV) w.y = -w.y;
+    float2& x = v[OUT ? d16(r) : r];
+    x = cmul(x, w);
+  }
 }
 
 __device__ __forceinline__ float fmax_nan(float a, float b) {
@@ -434,12 +450,6 @@ __device__ __forceinline__ float pow2_scale(float m) {
   if (m > 0.f && m <= FLT_MAX) e = (int)((__float_as_uint(m) >> 23) & 0xffu) - 126;
   const int s = min(126, max(-126, 1 - e));
   return __uint_as_float((uint32_t)(127 + s) << 23);
-}
-
-template <bool INV, int NS>
-__device__ __forceinline__ void fft_pass(float2 (&v)[16], const float2* tw) {
-  twiddle16<INV, NS>(v, tw);
-  dft16<INV>(v);
 }
 
 // Normalises 4 consecutive samples (re = x * scale, im = H) into the four
@@ -600,18 +610,24 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
     const float sa = pow2_scale(ma), sb = pow2_scale(mb);
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = __fmul2_rn(v[q], make_float2(sa, sb));
-    // forward FFT; the last pass leaves X[j + 256 r] in v[d16(r)]
-    fft_pass<false, 1>(v, tw);
-    store16<1>(v, buf);
-    load16(v, buf);
-    fft_pass<false, 16>(v, tw);
-    store16<16>(v, buf);
-    load16(v, buf);
-    fft_pass<false, 256>(v, tw);
-    // Hilbert multiplier -i sgn(k) in registers: k = j + 256 r is already the
-    // inverse's first-pass input index of this thread (no shared-memory round
-    // trip).  -i for 0 < k < T/2, +i for T/2 < k < T, 0 at DC and Nyquist.
-    // The inverse's 1/T is folded into the epilogue (x scaled by T instead:
+    // forward FFT, decimation in frequency.  buf is free: every thread of the
+    // previous pair passed that pair's last barrier after its last read.
+    dft16<false>(v);
+    twiddle16<false, 256, true>(v, tw);
+    store_set<256>(v, buf);
+    __syncthreads();
+    load_set<16>(v, buf);
+    dft16<false>(v);
+    twiddle16<false, 16, true>(v, tw);
+    store_set<16>(v, buf);
+    __syncwarp();
+    load_set<1>(v, buf);
+    dft16<false>(v);
+    // v[d16(r)] = X[256 r + 16 k1 + k0] with 16 k0 + k1 = j: the register index
+    // is the top digit of the frequency, so the Hilbert multiplier -i sgn(k)
+    // is -i for r < 8 and +i for r >= 8, with DC and Nyquist (0 there) in
+    // thread 0's r = 0 and r = 8.  The inverse's first pass runs on the same
+    // registers.  Its 1/T is folded into the epilogue (x scaled by T instead:
     // exact, power of two).
     float2 u[16];
 #pragma unroll
@@ -623,15 +639,21 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
       u[0] = make_float2(0.f, 0.f);
       u[8] = make_float2(0.f, 0.f);
     }
-    // inverse FFT -> T (H_a sa + i H_b sb) at t in natural order in buf
-    fft_pass<true, 1>(u, tw);
-    store16<1>(u, buf);
-    load16(u, buf);
-    fft_pass<true, 16>(u, tw);
-    store16<16>(u, buf);
-    load16(u, buf);
-    fft_pass<true, 256>(u, tw);
-    store16<256>(u, buf);
+    // inverse FFT, decimation in time -> T (H_a sa + i H_b sb) at t in natural
+    // order in buf
+    dft16<true>(u);
+    store_set<1>(u, buf);
+    __syncwarp();
+    load_set<16>(u, buf);
+    twiddle16<true, 16, false>(u, tw);
+    dft16<true>(u);
+    store_set<16>(u, buf);
+    __syncthreads();
+    load_set<256>(u, buf);
+    twiddle16<true, 256, false>(u, tw);
+    dft16<true>(u);
+    store_set<256>(u, buf);
+    __syncthreads();
     // normalise both rows from (x, H in smem): 4 consecutive samples per
     // thread and step (16-byte x loads -- L2 hits, software-pipelined one
     // step ahead -- and 8-byte plane stores); row min / max of |a|^2
@@ -705,7 +727,7 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
         if (need_flags[1]) hbuf[(rb - src.h_row0) * src.h_ld + t] = hv.y * ub;
       }
     }
-    // the next pair's first store16 synchronises before overwriting buf
+    // the next pair's first stores come after its row-max barrier
   }
 }
 
