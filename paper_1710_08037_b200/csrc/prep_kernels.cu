@@ -436,6 +436,17 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
   return d;
 }
 
+__device__ __forceinline__ float rsqrt_ftz(float a) {
+  float d;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(a));
+  return d;
+}
+__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 // L2 prefetch of `bytes` (multiple of 16, 16-byte aligned) at p (TMA bulk,
 // no registers or shared memory involved)
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
@@ -486,20 +497,25 @@ __device__ __forceinline__ void normalize4_split_pair(const float2 (&re)[4], con
                                                       __half* ob, bool hasb, long long ps, float& lo_a, float& hi_a,
                                                       float& lo_b, float& hi_b) {
   float zra[4], zia[4], zrb[4], zib[4];
+  float2 a2s[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     const float2 a2 = __ffma2_rn(re[k], re[k], __fmul2_rn(h[k], h[k]));
-    const float2 inv = make_float2(rsqrtf(fmaxf(a2.x, FLT_MIN)), rsqrtf(fmaxf(a2.y, FLT_MIN)));
+    // the argument is clamped to a normal number: the flush-to-zero form
+    // (one MUFU, no denormal pre-scaling) returns the same value
+    const float2 inv = make_float2(rsqrt_ftz(fmaxf(a2.x, FLT_MIN)), rsqrt_ftz(fmaxf(a2.y, FLT_MIN)));
     const float2 zr = __fmul2_rn(re[k], inv), zi = __fmul2_rn(h[k], inv);
     zra[k] = zr.x;
     zrb[k] = zr.y;
     zia[k] = zi.x;
     zib[k] = zi.y;
-    lo_a = fminf(lo_a, a2.x);
-    hi_a = fmax_nan(hi_a, a2.x);
-    lo_b = fminf(lo_b, a2.y);
-    hi_b = fmax_nan(hi_b, a2.y);
+    a2s[k] = a2;
   }
+  // 3-input min / max (FMNMX3): two instructions per row and statistic
+  lo_a = fminf(fminf(fminf(lo_a, a2s[0].x), a2s[1].x), fminf(a2s[2].x, a2s[3].x));
+  lo_b = fminf(fminf(fminf(lo_b, a2s[0].y), a2s[1].y), fminf(a2s[2].y, a2s[3].y));
+  hi_a = fmax3_nan(fmax3_nan(hi_a, a2s[0].x, a2s[1].x), a2s[2].x, a2s[3].x);
+  hi_b = fmax3_nan(fmax3_nan(hi_b, a2s[0].y, a2s[1].y), a2s[2].y, a2s[3].y);
   emit4_split<GS>(zra, zia, oa, ps);
   if (hasb) emit4_split<GS>(zrb, zib, ob, ps);
 }
@@ -665,7 +681,7 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
     const float4* xa4 = reinterpret_cast<const float4*>(x + oa) + j;
     const float4* xb4 = reinterpret_cast<const float4*>(x + ob) + j;
     float4 na = xa4[0], nb = hasb ? xb4[0] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 1
+#pragma unroll
     for (int g = 0; g < kFftT / (4 * kFftThreads); ++g) {
       const int off = g * 4 * kFftThreads;  // samples
       const float4 ca = na, cb = nb;
