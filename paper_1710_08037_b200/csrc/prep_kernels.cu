@@ -709,29 +709,33 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
 #pragma unroll
       for (int q = 0; q < 4; ++q) red[q][j >> 5] = vals[q];
     __syncthreads();
-    if (j == 0) {
+    // thread 0 closes row a, thread 32 (another warp) row b
+    if (j == 0 || j == 32) {
+      const int q0 = j == 0 ? 0 : 2;
+      float lo = red[q0][0], hi = red[q0 + 1][0];
       for (int w = 1; w < kFftThreads / 32; ++w) {
-        vals[0] = fminf(vals[0], red[0][w]);
-        vals[1] = fmax_nan(vals[1], red[1][w]);
-        vals[2] = fminf(vals[2], red[2][w]);
-        vals[3] = fmax_nan(vals[3], red[3][w]);
+        lo = fminf(lo, red[q0][w]);
+        hi = fmax_nan(hi, red[q0 + 1][w]);
       }
-      // a non-finite |a| anywhere in a row leaves its max non-finite (NaN
-      // propagates, inf is the max)
-      if (!(vals[1] <= FLT_MAX) || (hasb && !(vals[3] <= FLT_MAX))) atomicOr(&st->flags, FLAG_NONFINITE);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) vals[q] = sqrtf(vals[q]);  // |a|^2 -> |a|
-      // back to input units (exact: powers of two); the fixup decides on
-      // the min / max ratio, which the scaling leaves unchanged
-      rowmin[ra] = key_of((double)vals[0] / soa);
-      rowmax[ra] = key_of((double)vals[1] / soa);
-      need_flags[0] = (vals[0] == 0.0f) || ((double)vals[0] < amp_floor * (double)vals[1] * (1.0 + 1e-5));
-      need_flags[1] = 0;
-      if (hasb) {
-        rowmin[rb] = key_of((double)vals[2] / sob);
-        rowmax[rb] = key_of((double)vals[3] / sob);
-        need_flags[1] = (vals[2] == 0.0f) || ((double)vals[2] < amp_floor * (double)vals[3] * (1.0 + 1e-5));
+      int need = 0;
+      if (j == 0 || hasb) {
+        // a non-finite |a| anywhere in a row leaves its max non-finite (NaN
+        // propagates, inf is the max)
+        if (!(hi <= FLT_MAX)) atomicOr(&st->flags, FLAG_NONFINITE);
+        lo = sqrtf(lo);  // |a|^2 -> |a|
+        hi = sqrtf(hi);
+        // back to input units: 1 / (scale T) is a power of two, built from the
+        // exponent of the scale (exact; no double-precision division)
+        const float sc = j == 0 ? sa : sb;
+        const int e = (int)((__float_as_uint(sc) >> 23) & 0xffu) - 127 + 12;  // scale T = 2^e, T = 2^12
+        const double rs = __hiloint2double((1023 - e) << 20, 0);
+        const long long rr = j == 0 ? ra : rb;
+        rowmin[rr] = key_of((double)lo * rs);
+        rowmax[rr] = key_of((double)hi * rs);
+        // the fixup decides on the min / max ratio, which the scaling leaves unchanged
+        need = (lo == 0.0f) || ((double)lo < amp_floor * (double)hi * (1.0 + 1e-5));
       }
+      need_flags[j == 0 ? 0 : 1] = need;
     }
     __syncthreads();
     // rare: keep H (input units) of a row the exact-median fixup will inspect
