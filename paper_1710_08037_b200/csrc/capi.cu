@@ -261,7 +261,11 @@ ps_status get_plan(ps_ctx* c, int T, long long batch, long long idist, bool dbl,
   long long nb = T / 2 + 1;
   size_t ws = 0;
   cufftResult r;
-  if (dir == 0) {  // R2C / D2Z: input real rows of distance idist, output half spectra
+  if (dir == 2) {  // C2C / Z2Z of length T / 2: rows of distance idist (complex elements) -> dense rows
+    long long m[1] = {T / 2};
+    long long inembed[1] = {idist}, onembed[1] = {T / 2};
+    r = cufftMakePlanMany64(h, 1, m, inembed, 1, idist, onembed, 1, T / 2, dbl ? CUFFT_Z2Z : CUFFT_C2C, batch, &ws);
+  } else if (dir == 0) {  // R2C / D2Z: input real rows of distance idist, output half spectra
     long long inembed[1] = {idist}, onembed[1] = {nb};
     r = cufftMakePlanMany64(h, 1, n, inembed, 1, idist, onembed, 1, nb, dbl ? CUFFT_D2Z : CUFFT_R2C, batch, &ws);
   } else {         // C2R / Z2D: half spectra -> dense real rows of length T
@@ -275,6 +279,21 @@ ps_status get_plan(ps_ctx* c, int T, long long batch, long long idist, bool dbl,
   c->plans[k] = h;
   *out = h;
   return PS_OK;
+}
+
+// Which chain takes real rows of even length T.  For a power of two cuFFT's
+// R2C / C2R are single symmetric kernels (8 B/sample each: nothing to save,
+// `vector_fft_symm_r2c`); for any other length they run as a half-length
+// complex transform plus a split / merge pass, and the half-length complex
+// chain with the collapsed multiplier saves two of the five passes (C2,
+// T = 10000: 2.54 -> 1.95 ms; profiles/r02_session4/).  PS_HILBERT_CHAIN=r2c /
+// half forces one (A/B, tests of both).
+bool hilbert_half_chain(long long T) {
+  const char* s = std::getenv("PS_HILBERT_CHAIN");  // read per call: tests switch it
+  const int forced = (s && std::string(s) == "r2c") ? 0 : (s && std::string(s) == "half") ? 1 : -1;
+  if (T % 2 != 0 || T < 4) return false;
+  if (forced >= 0) return forced == 1;
+  return (T & (T - 1)) != 0;
 }
 
 long long hilbert_chunk_rows(const Geometry& g) {
@@ -314,6 +333,40 @@ ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cons
     c->launches++;
     in = c->xw.p;
     *copied = true;
+  }
+  if (hilbert_half_chain(g.T)) {
+    // Even T: the row re-read as T / 2 complex samples, one C2C each way and
+    // the collapsed multiplier in between (hilbert_halfspec_kernel): cuFFT's
+    // own R2C / C2R do the same half-length transforms plus a split / merge
+    // pass each, which with the -i sgn(k) pass made three passes of this one.
+    const long long M = g.T / 2;
+    const bool aligned = (reinterpret_cast<uintptr_t>(in) % (2 * es)) == 0 && idist % 2 == 0;
+    if (!aligned) {  // odd row distance or an unaligned base: pack (rows of distance T)
+      PS_TRY(ensure(c->xw, (size_t)nr * g.T * es));
+      PS_CUDA(launch_pack_real(src, row0, nr, c->xw.p, g.cdouble ? 1 : 0, st));
+      c->launches++;
+      in = c->xw.p;
+      idist = g.T;
+      *copied = true;
+    }
+    cufftHandle fw, iv;
+    PS_TRY(get_plan(c, (int)g.T, nr, idist / 2, g.cdouble, 2, &fw));
+    PS_TRY(get_plan(c, (int)g.T, nr, M, g.cdouble, 2, &iv));
+    PS_CUFFT(cufftSetStream(fw, st));
+    if (g.cdouble) {
+      PS_CUFFT(cufftExecZ2Z(fw, (cufftDoubleComplex*)const_cast<void*>(in), (cufftDoubleComplex*)c->spec.p, CUFFT_FORWARD));
+    } else {
+      PS_CUFFT(cufftExecC2C(fw, (cufftComplex*)const_cast<void*>(in), (cufftComplex*)c->spec.p, CUFFT_FORWARD));
+    }
+    PS_CUDA(launch_hilbert_halfspec(c->spec.p, nr, (int)g.T, g.cdouble ? 1 : 0, st));
+    c->launches++;
+    PS_CUFFT(cufftSetStream(iv, st));
+    if (g.cdouble) {
+      PS_CUFFT(cufftExecZ2Z(iv, (cufftDoubleComplex*)c->spec.p, (cufftDoubleComplex*)c->hbuf.p, CUFFT_INVERSE));
+    } else {
+      PS_CUFFT(cufftExecC2C(iv, (cufftComplex*)c->spec.p, (cufftComplex*)c->hbuf.p, CUFFT_INVERSE));
+    }
+    return PS_OK;
   }
   cufftHandle fwd, inv;
   PS_TRY(get_plan(c, (int)g.T, nr, idist, g.cdouble, 0, &fwd));

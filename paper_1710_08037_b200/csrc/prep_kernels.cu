@@ -1035,6 +1035,69 @@ __global__ void hilbert_spectrum_kernel(C* spec, long long nrows, int T) {
   }
 }
 
+// K2h: the Hilbert multiplier for real rows of EVEN length T transformed as
+// complex sequences of half the length (M = T / 2, z[n] = x[2n] + i x[2n+1],
+// i.e. the row itself re-read as complex).  With Z = FFT_M(z), the transform
+// of the even / odd samples is E_k = (Z_k + conj Z_{M-k}) / 2 and
+// O_k = (Z_k - conj Z_{M-k}) / 2i, the row's spectrum X_k = E_k + W_T^k O_k,
+// the Hilbert spectrum Y_k = -i X_k (0 < k < M), Y_0 = Y_M = 0, and the packed
+// output v[n] = H[2n] + i H[2n+1] has V_k = E'_k + i O'_k with
+// E'_k = (Y_k + conj Y_{M-k}) / 2, O'_k = (Y_k - conj Y_{M-k}) / (2 W_T^k).
+// Substituting, everything collapses to
+//   V_k = i sin(2 pi k / T) Z_k + cos(2 pi k / T) conj Z_{M-k}   (0 < k < M),  V_0 = 0,
+// so R2C's split pass, the -i sgn(k) pass and C2R's merge pass become this one
+// in-place pass between two C2C transforms of length M (8 instead of 24 bytes
+// per sample).  The 1/M of the unnormalised inverse is folded in.
+template <typename C>
+__global__ void __launch_bounds__(256) hilbert_halfspec_kernel(C* spec, long long nrows, int M) {
+  using S = decltype(spec->x);
+  const int per_row = M / 2 + 1;  // k = 0 .. M/2 handles (k, M - k)
+  const long long total = nrows * per_row;
+  const S inv = S(1) / S(M);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / per_row;
+    const int k = static_cast<int>(e % per_row);
+    C* z = spec + row * M;
+    if (k == 0) {
+      z[0].x = S(0);
+      z[0].y = S(0);
+      continue;
+    }
+    const int m = M - k;
+    S sn, cs;
+    if (sizeof(S) == 4) {
+      float sf, cf;
+      sincospif((float)k / (float)M, &sf, &cf);  // 2 pi k / T = pi k / M
+      sn = sf;
+      cs = cf;
+    } else {
+      double sd, cd;
+      sincospi((double)k / (double)M, &sd, &cd);
+      sn = sd;
+      cs = cd;
+    }
+    sn *= inv;
+    cs *= inv;
+    const C a = z[k];
+    if (m == k) {  // M even, k = M / 2: cos = 0
+      C v;
+      v.x = -sn * a.y;
+      v.y = sn * a.x;
+      z[k] = v;
+      continue;
+    }
+    const C b = z[m];
+    C vk, vm;
+    vk.x = cs * b.x - sn * a.y;
+    vk.y = sn * a.x - cs * b.y;
+    vm.x = -sn * b.y - cs * a.x;
+    vm.y = sn * b.x + cs * a.y;
+    z[k] = vk;
+    z[m] = vm;
+  }
+}
+
 // analytic output: out[rl][t] = (x, H) -- Re taken from x unchanged.
 template <typename IT, typename S>
 __global__ void analytic_out_kernel(SrcDesc src, long long row0, long long nrows, S* out) {
@@ -1431,6 +1494,14 @@ cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_d
   const int g = grid_for(nrows * (T / 2 + 1), 256);
   if (is_double) hilbert_spectrum_kernel<double2><<<g, 256, 0, st>>>((double2*)spec, nrows, T);
   else hilbert_spectrum_kernel<float2><<<g, 256, 0, st>>>((float2*)spec, nrows, T);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hilbert_halfspec(void* spec, long long nrows, int T, int is_double, cudaStream_t st) {
+  const int M = T / 2;
+  const int g = grid_for(nrows * (M / 2 + 1), 256);
+  if (is_double) hilbert_halfspec_kernel<double2><<<g, 256, 0, st>>>((double2*)spec, nrows, M);
+  else hilbert_halfspec_kernel<float2><<<g, 256, 0, st>>>((float2*)spec, nrows, M);
   return cudaGetLastError();
 }
 

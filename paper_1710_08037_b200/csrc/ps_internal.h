@@ -135,6 +135,9 @@ cudaError_t launch_scale_rows(void* y, long long nrows, long long L, long long l
                               int is_double, cudaStream_t st);
 cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_double,
                                     cudaStream_t st);
+// even T: the multiplier between two half-length complex transforms
+// ([nrows][T / 2] complex, in place; see hilbert_halfspec_kernel)
+cudaError_t launch_hilbert_halfspec(void* spec, long long nrows, int T, int is_double, cudaStream_t st);
 // fmt: 0 split fp16 planes, 1 f64 planes, 2 complex interleaved (compute type)
 // cdouble: compute in double although the source is float
 // *gauss_done (optional) = 1 when the Gauss planes 4..7 were written too

@@ -389,6 +389,41 @@ def test_real_input_lengths_unequal_scales(T):
     assert res["plv"].meta["n_masked_samples"] == int(m.sum())
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("T", [4, 6, 16, 250, 1000, 4098, 10000, 16384])
+def test_even_T_half_length_chain_matches_r2c_chain(T, dt, monkeypatch):
+    # even T: the row re-read as T / 2 complex samples, C2C -> collapsed
+    # multiplier (hilbert_halfspec_kernel) -> C2C, against the oracle and
+    # against cuFFT's R2C -> K2 -> C2R chain (PS_HILBERT_CHAIN forces one);
+    # rows of very different scale (the half-length transform never mixes rows),
+    # row distance > T (direct, unpacked input) and an odd row distance (packed)
+    import torch
+
+    rng = np.random.default_rng(T + 5)
+    for ld in (T, T + 2, T + 3):
+        buf = rng.standard_normal((6, ld)).astype(dt)
+        buf[1] *= 1e5
+        buf[4] *= 1e-5
+        x = buf[:, :T]
+        xd = torch.from_numpy(buf).cuda()[:, :T]  # device view, row distance ld
+        ar = O.analytic_signal(x.astype(np.float64), axis=1)
+        out = {}
+        for chain in ("half", "r2c"):
+            monkeypatch.setenv("PS_HILBERT_CHAIN", chain)
+            a = signalprep.analytic_signal(xd).data.cpu().numpy()
+            assert np.array_equal(a.real, x)  # Re(a) == x bit-exactly
+            rel = np.max(np.abs(a - ar), axis=1) / np.max(np.abs(ar), axis=1)
+            assert np.all(rel <= (1e-13 if dt is np.float64 else 2e-6)), (chain, ld, rel)
+            out[chain] = a
+        rel = np.max(np.abs(out["half"] - out["r2c"]), axis=1) / np.max(np.abs(ar), axis=1)
+        assert np.all(rel <= (1e-13 if dt is np.float64 else 2e-6)), (ld, rel)
+    monkeypatch.setenv("PS_HILBERT_CHAIN", "half")
+    xs = np.ascontiguousarray(rng.standard_normal((2, 7, T)).astype(dt)).transpose(1, 2, 0)
+    ref = O.plv_family(xs.astype(np.float64), input_kind="real")
+    prec = "split" if dt is np.float32 else "fp64"
+    check(C.plv_family(xs, input_kind="real", precision=prec), ref, prec, f"half chain T={T}")
+
+
 @pytest.mark.parametrize("prec,dt", [("split", np.float32), ("fp64", np.float64), ("fp64", np.float32)])
 @pytest.mark.parametrize("T", [1001, 2047])
 def test_odd_T_cufft_rows_of_unequal_scale(T, prec, dt):
