@@ -1251,7 +1251,7 @@ ps_status refine_range(ps_ctx* c, Call& k, unsigned long long lo, unsigned long 
       GramParams pr = k.p;
       pr.out_ciplv = k.outs[2];
       PS_CUDA(launch_refine_sorted(pr, static_cast<RefineEntry*>(c->refine.p) + lo, n, k.slot_mode == 2 ? k.G : 1, ib,
-                                   c->sortws.p, c->sortws.n, d_ent, d_exact, d_grp, single_round ? 1 : 0,
+                                   sb + 2 * ib, c->sortws.p, c->sortws.n, d_ent, d_exact, d_grp, single_round ? 1 : 0,
                                    k.trial_sum ? -(int)k.g.R : (int)k.g.R, st));
       c->launches += 8;
       PS_CUDA(cudaStreamSynchronize(st));

@@ -1051,50 +1051,49 @@ __global__ void hilbert_spectrum_kernel(C* spec, long long nrows, int T) {
 template <typename C>
 __global__ void __launch_bounds__(256) hilbert_halfspec_kernel(C* spec, long long nrows, int M) {
   using S = decltype(spec->x);
-  const int per_row = M / 2 + 1;  // k = 0 .. M/2 handles (k, M - k)
-  const long long total = nrows * per_row;
+  // blockIdx.x tiles k = 0 .. M/2 (thread k handles the bins k and M - k),
+  // blockIdx.y strides the rows: the twiddle is computed once per thread
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > M / 2) return;
+  const int m = M - k;
+  S sn, cs;
+  if (sizeof(S) == 4) {
+    float sf, cf;
+    sincospif((float)k / (float)M, &sf, &cf);  // 2 pi k / T = pi k / M
+    sn = sf;
+    cs = cf;
+  } else {
+    double sd, cd;
+    sincospi((double)k / (double)M, &sd, &cd);
+    sn = sd;
+    cs = cd;
+  }
   const S inv = S(1) / S(M);
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long row = e / per_row;
-    const int k = static_cast<int>(e % per_row);
+  sn *= inv;
+  cs *= inv;
+  for (long long row = blockIdx.y; row < nrows; row += gridDim.y) {
     C* z = spec + row * M;
     if (k == 0) {
-      z[0].x = S(0);
-      z[0].y = S(0);
-      continue;
-    }
-    const int m = M - k;
-    S sn, cs;
-    if (sizeof(S) == 4) {
-      float sf, cf;
-      sincospif((float)k / (float)M, &sf, &cf);  // 2 pi k / T = pi k / M
-      sn = sf;
-      cs = cf;
-    } else {
-      double sd, cd;
-      sincospi((double)k / (double)M, &sd, &cd);
-      sn = sd;
-      cs = cd;
-    }
-    sn *= inv;
-    cs *= inv;
-    const C a = z[k];
-    if (m == k) {  // M even, k = M / 2: cos = 0
+      C v;
+      v.x = S(0);
+      v.y = S(0);
+      z[0] = v;
+    } else if (m == k) {  // M even, k = M / 2: cos = 0
+      const C a = z[k];
       C v;
       v.x = -sn * a.y;
       v.y = sn * a.x;
       z[k] = v;
-      continue;
+    } else {
+      const C a = z[k], b = z[m];
+      C vk, vm;
+      vk.x = cs * b.x - sn * a.y;
+      vk.y = sn * a.x - cs * b.y;
+      vm.x = -sn * b.y - cs * a.x;
+      vm.y = sn * b.x + cs * a.y;
+      z[k] = vk;
+      z[m] = vm;
     }
-    const C b = z[m];
-    C vk, vm;
-    vk.x = cs * b.x - sn * a.y;
-    vk.y = sn * a.x - cs * b.y;
-    vm.x = -sn * b.y - cs * a.x;
-    vm.y = sn * b.x + cs * a.y;
-    z[k] = vk;
-    z[m] = vm;
   }
 }
 
@@ -1499,7 +1498,12 @@ cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_d
 
 cudaError_t launch_hilbert_halfspec(void* spec, long long nrows, int T, int is_double, cudaStream_t st) {
   const int M = T / 2;
-  const int g = grid_for(nrows * (M / 2 + 1), 256);
+  const int kb = (M / 2 + 1 + 255) / 256;
+  // enough row-strided blocks to fill the GPU a few times over; every thread
+  // keeps its twiddle across its rows
+  long long ry = (148LL * 16 + kb - 1) / kb;
+  ry = std::max(1LL, std::min(ry, std::min(nrows, 65535LL)));
+  const dim3 g((unsigned)kb, (unsigned)ry);
   if (is_double) hilbert_halfspec_kernel<double2><<<g, 256, 0, st>>>((double2*)spec, nrows, M);
   else hilbert_halfspec_kernel<float2><<<g, 256, 0, st>>>((float2*)spec, nrows, M);
   return cudaGetLastError();

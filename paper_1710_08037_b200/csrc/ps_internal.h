@@ -212,8 +212,8 @@ size_t refine_sort_ws_bytes(int n);
 // (flat output index, final ciPLV value) of queued refine entries (split outputs)
 cudaError_t launch_refine_pick(const RefineEntry* entries, int n, const float* out, long long N, long long* idx,
                                float* val, cudaStream_t st);
-cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, void* ws,
-                                 size_t ws_bytes, RefineEntry* sorted, double* exact, int* groups, int overwrite,
+cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, int key_bits,
+                                 void* ws, size_t ws_bytes, RefineEntry* sorted, double* exact, int* groups, int overwrite,
                                  int div, cudaStream_t st);
 
 // multi-GPU combine / gather (shard_kernels.cu)

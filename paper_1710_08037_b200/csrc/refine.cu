@@ -184,7 +184,8 @@ size_t refine_sort_ws_bytes(int n) {
   return (size_t)n * (4 * 2 + 4 * 3 + 8 * 2 + 1) + 10 * 256 + 256 + cubb;
 }
 
-cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, void* ws,
+cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int n, int slot_div, int ib, int key_bits,
+                                 void* ws,
                                  size_t ws_bytes, RefineEntry* sorted, double* exact, int* groups, int overwrite,
                                  int div, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
@@ -213,7 +214,8 @@ cudaError_t launch_refine_sorted(const GramParams& p, RefineEntry* entries, int 
   if (e != cudaSuccess) return e;
   refine_poskey_kernel<<<blocks, threads, 0, st>>>(entries, idx1, n, ib, kpos);
   cub_bytes = ws_bytes - used;
-  e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, kpos, kpos2, idx1, idx2, n, 0, 64, st);
+  // only the bits a (slot, i, j) key can occupy: 8-bit passes saved for small N
+  e = cub::DeviceRadixSort::SortPairs(cub_ws, cub_bytes, kpos, kpos2, idx1, idx2, n, 0, key_bits, st);
   if (e != cudaSuccess) return e;
   refine_gather_kernel<<<blocks, threads, 0, st>>>(entries, idx2, kpos2, n, sorted, flags);
   cub_bytes = ws_bytes - used;
