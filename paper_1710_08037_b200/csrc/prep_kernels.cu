@@ -1832,6 +1832,76 @@ __global__ void __launch_bounds__(256) group_reduce_sym_kernel(const S* __restri
   }
 }
 
+// The same for fp32 with N % 4 == 0: one row of the tile per thread group of
+// 8, 16-byte loads of the G slots and 16-byte stores of both triangles (a
+// quarter of the memory instructions; same sums in the same order).
+__global__ void __launch_bounds__(256) group_reduce_sym4_kernel(const float* __restrict__ ws, int G, int N, int nt,
+                                                                int R, float* __restrict__ out, bool anti) {
+  __shared__ float tile[32][33];
+  int t = blockIdx.x, I = 0;
+  while (t >= nt - I) {
+    t -= nt - I;
+    ++I;
+  }
+  const int J = I + t;
+  const long long nn = (long long)N * N;
+  const float* wb = ws + (long long)blockIdx.y * G * nn;
+  float* ob = out + (long long)blockIdx.y * nn;
+  const int c4 = (threadIdx.x & 7) * 4, r = threadIdx.x >> 3;  // 4 columns of row r
+  {
+    const int i = I * 32 + r, j = J * 32 + c4;
+    // a diagonal tile keeps column c of row r when r <= c: the float4 is
+    // loaded whole when any of its columns is kept (the slots hold finite
+    // values or zeros below the diagonal) and masked on the way out
+    if (i < N && j < N && (I < J || r <= c4 + 3)) {
+      const float4* p = reinterpret_cast<const float4*>(wb + (long long)i * N + j);
+      const long long step = nn / 4;
+      float4 acc = __ldg(p);
+      for (int g = 1; g < G; ++g) {
+        const float4 v = __ldg(p + g * step);
+        acc.x += v.x;
+        acc.y += v.y;
+        acc.z += v.z;
+        acc.w += v.w;
+      }
+      const float rR = 1.0f / (float)R, fR = (float)R;  // = epilogue.cuh mean_scale
+      acc.x = acc.x == fR ? 1.0f : acc.x * rR;
+      acc.y = acc.y == fR ? 1.0f : acc.y * rR;
+      acc.z = acc.z == fR ? 1.0f : acc.z * rR;
+      acc.w = acc.w == fR ? 1.0f : acc.w * rR;
+      tile[r][c4 + 0] = acc.x;
+      tile[r][c4 + 1] = acc.y;
+      tile[r][c4 + 2] = acc.z;
+      tile[r][c4 + 3] = acc.w;
+      float* o = ob + (long long)i * N + j;
+      if (I < J || r <= c4) {
+        *reinterpret_cast<float4*>(o) = acc;  // (N % 4 == 0: j + 3 < N)
+      } else {  // the diagonal crosses this float4: keep columns >= r
+        if (r <= c4 + 1) o[1] = acc.y;
+        if (r <= c4 + 2) o[2] = acc.z;
+        o[3] = acc.w;
+      }
+    }
+  }
+  __syncthreads();
+  {
+    // mirror tile (J, I): output row jj = J*32 + r, columns ii = I*32 + c4 ..
+    const int jj = J * 32 + r, ii = I * 32 + c4;
+    if (jj < N && ii < N && (I < J || c4 < r)) {
+      float4 v = make_float4(tile[c4][r], tile[c4 + 1][r], tile[c4 + 2][r], tile[c4 + 3][r]);
+      if (anti) v = make_float4(-v.x, -v.y, -v.z, -v.w);
+      float* o = ob + (long long)jj * N + ii;
+      if (I < J || c4 + 3 < r) {
+        *reinterpret_cast<float4*>(o) = v;
+      } else {  // diagonal tile: keep columns < r
+        o[0] = v.x;
+        if (c4 + 1 < r) o[1] = v.y;
+        if (c4 + 2 < r) o[2] = v.z;
+      }
+    }
+  }
+}
+
 cudaError_t launch_group_reduce(const void* ws, int G, int N, int B, int n_outputs, void* const* outs, int R,
                                 int is_double, cudaStream_t st, int upper) {
   // ws holds n_outputs consecutive blocks of [B][G][N*N]
@@ -1856,6 +1926,10 @@ cudaError_t launch_group_reduce(const void* ws, int G, int N, int B, int n_outpu
       if (is_double)
         group_reduce_sym_kernel<double><<<grid, block, 0, st>>>((const double*)ws + m * ws_block, G, N, nt, R,
                                                                  (double*)outs[m], m == 4);
+      else if (N % 4 == 0 && (reinterpret_cast<uintptr_t>(ws) & 15u) == 0 &&
+               (reinterpret_cast<uintptr_t>(outs[m]) & 15u) == 0)
+        group_reduce_sym4_kernel<<<grid, 256, 0, st>>>((const float*)ws + m * ws_block, G, N, nt, R,
+                                                       (float*)outs[m], m == 4);
       else
         group_reduce_sym_kernel<float><<<grid, block, 0, st>>>((const float*)ws + m * ws_block, G, N, nt, R,
                                                                 (float*)outs[m], m == 4);
