@@ -761,6 +761,7 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
 // |a| < floor*median or |a| == 0 are zeroed (masked).
 // ---------------------------------------------------------------------------
 constexpr int kFixThreads = 256;
+constexpr int kFixBatch = 32;  // rows pre-checked per CTA iteration
 
 template <typename IT, typename S, int KIND>
 __device__ double row_amp(const SrcDesc& src, long long roff, long long r, long long t) {
@@ -774,24 +775,37 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(SrcDesc src, long lo
                                                             void* out, int pitch, long long plane_stride,
                                                             const unsigned long long* rowmin,
                                                             const unsigned long long* rowmax, int* maskcount,
-                                                            double amp_floor, DevStatus* st) {
+                                                            double amp_floor, DevStatus* st, int batch) {
   __shared__ unsigned int hist[256];
   __shared__ unsigned long long sh_prefix;
   __shared__ long long sh_k;
   __shared__ unsigned long long red_u[kFixThreads / 32];
   __shared__ long long red_c[kFixThreads / 32];
+  __shared__ int need_list[kFixBatch];
+  __shared__ int n_need;
   const long long T = src.T;
-  for (long long rl = blockIdx.x; rl < nrows; rl += gridDim.x) {
-    const long long r = row0 + rl;
-    const double amin = val_of(rowmin[r]);
-    const double amax = val_of(rowmax[r]);
-    // (1 + 1e-5) margin: the vectorised normaliser's min/max come from a
-    // rsqrt-based |a| (a few ulp); the exact path below recomputes |a|.
-    const bool need = (amin == 0.0) || (amin < amp_floor * amax * (1.0 + 1e-5));
-    if (!need) {
-      if (threadIdx.x == 0) maskcount[r] = 0;
-      continue;
+  // Rows are pre-checked `batch` (<= kFixBatch) at a time, one row per lane of warp 0 (the
+  // common case -- no row needs the median -- is one pass of two loads per
+  // row instead of a CTA-wide iteration per row); the rows that fail the
+  // check are then taken one at a time by the whole CTA.
+  for (long long base = (long long)blockIdx.x * batch; base < nrows; base += (long long)gridDim.x * batch) {
+    if (threadIdx.x == 0) n_need = 0;
+    __syncthreads();
+    if (threadIdx.x < batch && base + threadIdx.x < nrows) {
+      const long long r = row0 + base + threadIdx.x;
+      const double amin = val_of(rowmin[r]);
+      const double amax = val_of(rowmax[r]);
+      // (1 + 1e-5) margin: the vectorised normaliser's min/max come from a
+      // rsqrt-based |a| (a few ulp); the exact path below recomputes |a|.
+      const bool need = (amin == 0.0) || (amin < amp_floor * amax * (1.0 + 1e-5));
+      if (!need) maskcount[r] = 0;
+      else need_list[atomicAdd(&n_need, 1)] = threadIdx.x;
     }
+    __syncthreads();
+    const int n_rows_needed = n_need;
+   for (int q = 0; q < n_rows_needed; ++q) {
+    const long long rl = base + need_list[q];
+    const long long r = row0 + rl;
     const long long roff = row_offset(src, r);
     // ---- radix select of the k-th smallest key -------------------------
     auto select_kth = [&](long long k) -> unsigned long long {
@@ -896,6 +910,7 @@ __global__ void __launch_bounds__(kFixThreads) fixup_kernel(SrcDesc src, long lo
       if (cnt == T) atomicOr(&st->flags, FLAG_ALL_MASKED);
     }
     __syncthreads();
+   }
   }
 }
 
@@ -1677,13 +1692,13 @@ cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long n
   do {                                                                                              \
     if (src.is_double)                                                                              \
       fixup_kernel<double, double, KIND, FMT><<<grid, kFixThreads, 0, st>>>(                        \
-          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status); \
+          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status, batch); \
     else if (cdouble)                                                                               \
       fixup_kernel<float, double, KIND, FMT><<<grid, kFixThreads, 0, st>>>(                         \
-          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status); \
+          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status, batch); \
     else                                                                                            \
       fixup_kernel<float, float, KIND, FMT><<<grid, kFixThreads, 0, st>>>(                          \
-          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status); \
+          src, row0, nrows, out, pitch, plane_stride, rowmin, rowmax, maskcount, amp_floor, status, batch); \
   } while (0)
 
 cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows, void* out, int fmt,
@@ -1691,7 +1706,11 @@ cudaError_t launch_fixup_fmt(const SrcDesc& src, long long row0, long long nrows
                              long long rows_total, int* maskcount, double amp_floor, DevStatus* status,
                              cudaStream_t st) {
   if (nrows <= 0) return cudaSuccess;
-  const unsigned grid = static_cast<unsigned>(nrows < 148 * 8 ? nrows : 148 * 8);
+  // rows per pre-check batch: as many as keep 148 * 8 CTAs busy when every
+  // row needs the exact pass, at most one per lane of a warp
+  const int batch = (int)std::max(1LL, std::min<long long>(kFixBatch, nrows / (148 * 8)));
+  const long long batches = (nrows + batch - 1) / batch;
+  const unsigned grid = static_cast<unsigned>(batches < 148 * 8 ? batches : 148 * 8);
   const unsigned long long* rowmin = rowstat;
   const unsigned long long* rowmax = rowstat + rows_total;
   if (src.kind == 2) {  // phasors: count the exact zeros (no median)
