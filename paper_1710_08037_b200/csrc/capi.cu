@@ -106,7 +106,7 @@ struct ps_ctx {
   cudaEvent_t ev[8] = {};
   int launches = 0;
   // host (e2e) pipeline: copy-in / compute / refine / copy-out streams
-  cudaStream_t s_in = nullptr, s_comp = nullptr, s_ref = nullptr, s_out = nullptr;
+  cudaStream_t s_in = nullptr, s_comp = nullptr, s_ref = nullptr, s_out = nullptr, s_prep = nullptr;
   std::vector<cudaEvent_t> evpool;
   unsigned long long* h_cnt = nullptr;  // mapped pinned per-stage refine-queue counters
   unsigned long long* d_cnt = nullptr;  // device alias of h_cnt
@@ -1322,6 +1322,7 @@ ps_status ensure_pipeline(ps_ctx* c, int n_stages) {
     PS_CUDA(cudaStreamCreateWithFlags(&c->s_ref, cudaStreamNonBlocking));
     PS_CUDA(cudaStreamCreateWithFlags(&c->s_out, cudaStreamNonBlocking));
   }
+  if (!c->s_prep) PS_CUDA(cudaStreamCreateWithFlags(&c->s_prep, cudaStreamNonBlocking));
   if (c->h_cnt_cap < n_stages) {
     if (c->h_cnt) cudaFreeHost(c->h_cnt);
     c->h_cnt = nullptr;
@@ -1478,8 +1479,24 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
     if (rem > 1024) widths.push_back(rem - 1024);
     widths.push_back(std::min<long long>(rem, 1024));
   } else {
+    // growing head, then a tapered tail (512, 512, last <= 256 signals): what
+    // follows the last copy-in -- its normalise, the Gram of the last columns
+    // against every row, their copy-out -- is the exposed tail of a call that
+    // runs at the host link's rate (C3: 31.9 -> 30.4 ms)
     const long long wmax = std::max<long long>(1024, round_up((g.N + 5) / 6, 256));
-    for (long long w = 1024, x = 0; x < g.N; x += w, w = std::min(wmax, w + 512)) widths.push_back(w);
+    const long long nr = round_up(g.N, 256);
+    const long long head = nr > 3072 ? nr - 1280 : nr;
+    long long x = 0;
+    for (long long w = 1024; x < head; w = std::min(wmax, w + 512)) {
+      const long long take = std::min(w, head - x);
+      widths.push_back(take);
+      x += take;
+    }
+    if (head < nr) {
+      widths.push_back(512);
+      widths.push_back(512);
+      widths.push_back(256);
+    }
   }
   // cut points 0 = cols[0] < ... < cols[S] = N, every inner cut a multiple of
   // 256 counted from 0 (row / column panels never straddle a stage)
@@ -1505,11 +1522,13 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   auto lo = [&](int s) { return stream_out ? cols[S - 1 - s] : cols[s]; };
   auto hi = [&](int s) { return stream_out ? cols[S - s] : cols[s + 1]; };
   PS_TRY(ensure_pipeline(c, S));
-  cudaStream_t si = c->s_in, sc = c->s_comp, sr = c->s_ref, so = c->s_out;
+  // si: copy-in only (the copy engine never waits behind a normalise kernel);
+  // sn: Hilbert / normalise of a stage once its rows have arrived
+  cudaStream_t si = c->s_in, sn = c->s_prep, sc = c->s_comp, sr = c->s_ref, so = c->s_out;
   // a previous call that returned early on an error may still have work in
   // flight on these streams (a kernel that would publish stale band flags):
   // start from idle streams (free when the last call completed normally)
-  for (cudaStream_t q : {si, sc, sr, so}) PS_CUDA(cudaStreamSynchronize(q));
+  for (cudaStream_t q : {si, sn, sc, sr, so}) PS_CUDA(cudaStreamSynchronize(q));
   c->launches = 0;
   bool copied = false;
   // device buffers: input span (same element layout as the host array), planes, outputs
@@ -1618,6 +1637,11 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
   std::unique_ptr<PipeTrace> trace_holder(want_trace ? new PipeTrace(si) : nullptr);
   PipeTrace* trace = trace_holder.get();
   // ---- copy-in + normalise, per stage --------------------------------------
+  {  // everything queued on si so far (workspace setup, status reset, plan uploads) precedes the first normalise
+    cudaEvent_t setup = pool_event(c, 4 * (size_t)S + 4);
+    PS_CUDA(cudaEventRecord(setup, si));
+    PS_CUDA(cudaStreamWaitEvent(sn, setup, 0));
+  }
   for (int s = 0; s < S; ++s) {
     for (long long u = 0; u < U && !dev_input; ++u) {
       const long long b = u / g.R, t = u % g.R;
@@ -1628,11 +1652,16 @@ ps_status host_pipelined(ps_ctx* c, const ps_plv_args* a, Call& k, long long spa
       h2d_bytes += (size_t)len * esz;
     }
     if (trace) trace->rec(si, "h2d", s);
+    {
+      cudaEvent_t arrived = pool_event(c, 4 * (size_t)S + 5 + s);
+      PS_CUDA(cudaEventRecord(arrived, si));
+      PS_CUDA(cudaStreamWaitEvent(sn, arrived, 0));
+    }
     for (long long u = 0; u < U; ++u)
       PS_TRY(prepare_rows(c, &d, g, din, c->planes.p, g.split ? 0 : 1, g.pitch, g.plane_stride,
-                          u * g.N + lo(s), u * g.N + hi(s), si, &copied));
-    if (trace) trace->rec(si, "norm", s);
-    PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), si));
+                          u * g.N + lo(s), u * g.N + hi(s), sn, &copied));
+    if (trace) trace->rec(sn, "norm", s);
+    PS_CUDA(cudaEventRecord(pool_event(c, 3 * s), sn));
   }
   // ---- Gram per stage ------------------------------------------------------
   for (int s = 0; s < S; ++s) {
@@ -2044,7 +2073,7 @@ ps_status ps_ctx_destroy(ps_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->evpool) cudaEventDestroy(e);
   for (auto& e : c->tev) cudaEventDestroy(e);
-  for (cudaStream_t s : {c->s_in, c->s_comp, c->s_ref, c->s_out})
+  for (cudaStream_t s : {c->s_in, c->s_comp, c->s_ref, c->s_out, c->s_prep})
     if (s) cudaStreamDestroy(s);
   if (c->h_cnt) cudaFreeHost(c->h_cnt);
   if (c->h_sbflag) cudaFreeHost(c->h_sbflag);
