@@ -324,7 +324,11 @@ ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cons
     c->launches++;
     in = c->xw.p;
     *h_scale = c->hscale.p;
-  } else if (fft_direct(a, g)) {
+  } else if (fft_direct(a, g) && a->stride_signal % 2 == 0 &&
+             (reinterpret_cast<uintptr_t>(static_cast<const char*>(src.ptr) + (size_t)row0 * a->stride_signal * es) %
+              (2 * es)) == 0) {
+    // (cuFFT wants real input rows aligned like its complex type: a view that
+    // starts an odd number of elements into its buffer is packed instead)
     in = static_cast<const char*>(src.ptr) + (size_t)row0 * a->stride_signal * es;
     idist = a->stride_signal;
   } else {
@@ -339,16 +343,7 @@ ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cons
     // the collapsed multiplier in between (hilbert_halfspec_kernel): cuFFT's
     // own R2C / C2R do the same half-length transforms plus a split / merge
     // pass each, which with the -i sgn(k) pass made three passes of this one.
-    const long long M = g.T / 2;
-    const bool aligned = (reinterpret_cast<uintptr_t>(in) % (2 * es)) == 0 && idist % 2 == 0;
-    if (!aligned) {  // odd row distance or an unaligned base: pack (rows of distance T)
-      PS_TRY(ensure(c->xw, (size_t)nr * g.T * es));
-      PS_CUDA(launch_pack_real(src, row0, nr, c->xw.p, g.cdouble ? 1 : 0, st));
-      c->launches++;
-      in = c->xw.p;
-      idist = g.T;
-      *copied = true;
-    }
+    const long long M = g.T / 2;  // (in is aligned and idist even: direct rows passed the check above, packed rows are dense)
     cufftHandle fw, iv;
     PS_TRY(get_plan(c, (int)g.T, nr, idist / 2, g.cdouble, 2, &fw));
     PS_TRY(get_plan(c, (int)g.T, nr, M, g.cdouble, 2, &iv));

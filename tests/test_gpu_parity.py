@@ -400,12 +400,13 @@ def test_even_T_half_length_chain_matches_r2c_chain(T, dt, monkeypatch):
     import torch
 
     rng = np.random.default_rng(T + 5)
-    for ld in (T, T + 2, T + 3):
+    for ld, c0 in ((T, 0), (T + 2, 0), (T + 3, 0), (T + 2, 1)):
+        # (T + 2, 1): even row distance but a base one element off the complex alignment (packed)
         buf = rng.standard_normal((6, ld)).astype(dt)
         buf[1] *= 1e5
         buf[4] *= 1e-5
-        x = buf[:, :T]
-        xd = torch.from_numpy(buf).cuda()[:, :T]  # device view, row distance ld
+        x = buf[:, c0:c0 + T]
+        xd = torch.from_numpy(buf).cuda()[:, c0:c0 + T]  # device view, row distance ld
         ar = O.analytic_signal(x.astype(np.float64), axis=1)
         out = {}
         for chain in ("half", "r2c"):
@@ -422,6 +423,34 @@ def test_even_T_half_length_chain_matches_r2c_chain(T, dt, monkeypatch):
     ref = O.plv_family(xs.astype(np.float64), input_kind="real")
     prec = "split" if dt is np.float32 else "fp64"
     check(C.plv_family(xs, input_kind="real", precision=prec), ref, prec, f"half chain T={T}")
+
+
+@pytest.mark.parametrize("kind,dt", [("real", np.float32), ("real", np.float64), ("analytic", np.complex64)])
+@pytest.mark.parametrize("T", [999, 1000, 2048, 4096])
+def test_views_starting_off_the_vector_alignment(T, kind, dt):
+    # device views that start 1 or 3 elements into their buffer: rows are not
+    # aligned for 16-byte loads, for cuFFT's R2C (complex-type alignment) or for
+    # re-reading a row as complex pairs -- every stage has to fall back to a
+    # packed copy or scalar loads (a direct cuFFT call on such rows fails with
+    # CUFFT_INVALID_VALUE)
+    import torch
+
+    rng = np.random.default_rng(T)
+    N = 9
+    for c0 in (1, 3):
+        buf = rng.standard_normal((N, T + 8))
+        if kind == "analytic":
+            buf = buf + 1j * rng.standard_normal((N, T + 8))
+        buf = buf.astype(dt)
+        x = buf[:, c0:c0 + T]
+        xd = torch.from_numpy(buf).cuda()[:, c0:c0 + T]
+        ref = O.plv_family(x[:, :, None].astype(np.complex128 if kind == "analytic" else np.float64), input_kind=kind)
+        for prec in ("split", "fp64"):
+            res = C.plv_family(xd[:, :, None], input_kind=kind, precision=prec)
+            tol = 1e-12 if (prec == "fp64" and dt is np.float64) else 1e-5
+            for m in ("plv", "iplv", "ciplv"):
+                err = float(np.max(np.abs(res[m].values.double().cpu().numpy() - ref[m])))
+                assert err <= tol, (T, kind, c0, prec, m, err)
 
 
 @pytest.mark.parametrize("prec,dt", [("split", np.float32), ("fp64", np.float64), ("fp64", np.float32)])
