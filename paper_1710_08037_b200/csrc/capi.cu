@@ -303,6 +303,33 @@ long long hilbert_chunk_rows(const Geometry& g) {
   return rc;
 }
 
+// H{x} of nr real rows of even length L at `in` (row distance idist reals,
+// even; base aligned like the complex type) into c->hbuf (dense rows of L):
+// C2C of length L / 2 -> collapsed multiplier -> C2C (hilbert_halfspec_kernel).
+// c->spec must hold nr * L / 2 complex values.
+ps_status hilbert_half_exec(ps_ctx* c, long long L, long long nr, const void* in, long long idist, bool dbl,
+                            cudaStream_t st) {
+  const long long M = L / 2;
+  cufftHandle fw, iv;
+  PS_TRY(get_plan(c, (int)L, nr, idist / 2, dbl, 2, &fw));
+  PS_TRY(get_plan(c, (int)L, nr, M, dbl, 2, &iv));
+  PS_CUFFT(cufftSetStream(fw, st));
+  if (dbl) {
+    PS_CUFFT(cufftExecZ2Z(fw, (cufftDoubleComplex*)const_cast<void*>(in), (cufftDoubleComplex*)c->spec.p, CUFFT_FORWARD));
+  } else {
+    PS_CUFFT(cufftExecC2C(fw, (cufftComplex*)const_cast<void*>(in), (cufftComplex*)c->spec.p, CUFFT_FORWARD));
+  }
+  PS_CUDA(launch_hilbert_halfspec(c->spec.p, nr, (int)L, dbl ? 1 : 0, st));
+  c->launches++;
+  PS_CUFFT(cufftSetStream(iv, st));
+  if (dbl) {
+    PS_CUFFT(cufftExecZ2Z(iv, (cufftDoubleComplex*)c->spec.p, (cufftDoubleComplex*)c->hbuf.p, CUFFT_INVERSE));
+  } else {
+    PS_CUFFT(cufftExecC2C(iv, (cufftComplex*)c->spec.p, (cufftComplex*)c->hbuf.p, CUFFT_INVERSE));
+  }
+  return PS_OK;
+}
+
 // Hilbert stage for rows [row0, row0+nr): leaves H{x} (compute type) in c->hbuf.
 // For odd T cuFFT's batched R2C transforms two rows as one complex sequence,
 // so a row's rounding error scales with its partner's magnitude: the rows are
@@ -343,25 +370,8 @@ ps_status hilbert_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, cons
     // the collapsed multiplier in between (hilbert_halfspec_kernel): cuFFT's
     // own R2C / C2R do the same half-length transforms plus a split / merge
     // pass each, which with the -i sgn(k) pass made three passes of this one.
-    const long long M = g.T / 2;  // (in is aligned and idist even: direct rows passed the check above, packed rows are dense)
-    cufftHandle fw, iv;
-    PS_TRY(get_plan(c, (int)g.T, nr, idist / 2, g.cdouble, 2, &fw));
-    PS_TRY(get_plan(c, (int)g.T, nr, M, g.cdouble, 2, &iv));
-    PS_CUFFT(cufftSetStream(fw, st));
-    if (g.cdouble) {
-      PS_CUFFT(cufftExecZ2Z(fw, (cufftDoubleComplex*)const_cast<void*>(in), (cufftDoubleComplex*)c->spec.p, CUFFT_FORWARD));
-    } else {
-      PS_CUFFT(cufftExecC2C(fw, (cufftComplex*)const_cast<void*>(in), (cufftComplex*)c->spec.p, CUFFT_FORWARD));
-    }
-    PS_CUDA(launch_hilbert_halfspec(c->spec.p, nr, (int)g.T, g.cdouble ? 1 : 0, st));
-    c->launches++;
-    PS_CUFFT(cufftSetStream(iv, st));
-    if (g.cdouble) {
-      PS_CUFFT(cufftExecZ2Z(iv, (cufftDoubleComplex*)c->spec.p, (cufftDoubleComplex*)c->hbuf.p, CUFFT_INVERSE));
-    } else {
-      PS_CUFFT(cufftExecC2C(iv, (cufftComplex*)c->spec.p, (cufftComplex*)c->hbuf.p, CUFFT_INVERSE));
-    }
-    return PS_OK;
+    // (in is aligned and idist even: direct rows passed the check above, packed rows are dense)
+    return hilbert_half_exec(c, g.T, nr, in, idist, g.cdouble, st);
   }
   cufftHandle fwd, inv;
   PS_TRY(get_plan(c, (int)g.T, nr, idist, g.cdouble, 0, &fwd));
@@ -484,7 +494,11 @@ ps_status bandpass_chunk(ps_ctx* c, const ps_plv_args* a, const Geometry& g, con
   PS_CUFFT(c2r(inv, c->xw.p));
   c->launches += 5;
   const bool odd = (f.L & 1) != 0;
-  if (hilbert) {  // analytic signal of the padded record (length L), before the trim
+  if (hilbert && hilbert_half_chain(f.L)) {
+    // even L that is not a power of two: the filtered records (row distance
+    // Lf, even) re-read as L / 2 complex samples (see hilbert_chunk)
+    PS_TRY(hilbert_half_exec(c, f.L, nr, c->xw.p, f.Lf, g.cdouble, st));
+  } else if (hilbert) {  // analytic signal of the padded record (length L), before the trim
     cufftHandle fl, il;
     PS_TRY(get_plan(c, (int)f.L, nr, f.Lf, g.cdouble, 0, &fl));
     PS_TRY(get_plan(c, (int)f.L, nr, f.L, g.cdouble, 1, &il));
