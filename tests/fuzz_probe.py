@@ -1,7 +1,7 @@
 """Randomised configurations through the public API against the CPU oracle
 (the checker): shapes, dtypes, memory layouts, trial reductions, layouts,
 zero stretches.  GPU box only.
-    python tools/fuzz_probe.py [n_cases] [seed]
+    python tests/fuzz_probe.py [n_cases] [seed]
 Prints one line per failing case and a summary; exit code 1 on any failure."""
 import os
 import sys
