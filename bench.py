@@ -449,6 +449,25 @@ def main():
                 "variant_ceiling": variant_peak, "frac_of_variant_ceiling": achieved / variant_peak,
                 "frac_of_bf16_peak": achieved / pk["bf16_tflops"] if not fp64 else None}
 
+    # ---- normalisation stage against the HBM roofline ----------------------
+    # algorithmic bytes per sample: the input sample in, the
+    # operand planes out (4 fp16 split planes, or re / im in f64); the Gauss
+    # form's S / D planes (8 more bytes) are listed apart
+    in_b = {"f32": 4, "f64": 8, "c64": 8, "c128": 16}.get(dt, 8)
+    out_b = 16 if fp64 else 8
+    n_samples = float(B) * R * N * T * (my_units / (B * R) if units else 1.0)
+    ms_norm = float(info["ms_normalize"])
+    norm_gbs = n_samples * (in_b + out_b) / (ms_norm / 1e3) / 1e9 if ms_norm > 0 else None
+    normalize_roofline = {"bound": "hbm", "achieved": norm_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                          "frac": norm_gbs / pk["hbm_gbs"] if norm_gbs else None,
+                          "bytes_per_sample": in_b + out_b,
+                          "gauss_plane_bytes_per_sample": 8 if variant == 1 else 0,
+                          "achieved_incl_gauss_planes": (norm_gbs * (in_b + out_b + (8 if variant == 1 else 0)) /
+                                                         (in_b + out_b)) if norm_gbs else None,
+                          "ms": ms_norm,
+                          "stage": ("Hilbert (cuFFT chain or fused radix-16 kernel) + normalise -> operand planes"
+                                    if kind == "real" else "normalise -> operand planes")}
+
     # ---- end to end through the public host API ----------------------------
     e2e = None
     if not args.no_e2e:
@@ -547,7 +566,8 @@ def main():
                 "scaling": "strong", "vs_baseline": None,
                 "dtype": "f16x3 split (fp32 accumulate, fp32 out)" if not fp64 else "f64",
                 "data": "synthetic (seeded numpy generator, SURVEY 8(d)); stands in for the paper's MEG data",
-                "config": cfg, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "config": cfg, "roofline": roofline, "normalize_roofline": normalize_roofline, "cpu_baseline": cpu,
+                "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks,
                 "stages_ms": {"normalize": float(info["ms_normalize"]), "gram": gram_avg,
                               "finish": float(info["ms_finish"])}}
