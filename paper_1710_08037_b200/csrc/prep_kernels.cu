@@ -752,6 +752,281 @@ __global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused4096_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// The same kernel for rows of T = 2048 or 1024 samples (NP = 4096 / T = 2 or 4
+// row pairs per CTA iteration, side by side in the 4096-point buffer).  Only
+// the outer pass changes: the stride-256 pass becomes NP independent radix-RQ
+// butterflies per thread (RQ = 16 / NP: 8 or 4, twiddles W_T^(j s)); the
+// stride-16 and stride-1 passes work inside 256-point blocks and do not care
+// which transform a block belongs to.  In pass C the register index is still
+// the top digit of the frequency (weight T / 16), so the Hilbert multiplier
+// keeps its r < 8 rule; DC and Nyquist of pair q sit in thread q * 256 / NP.
+// ---------------------------------------------------------------------------
+// 8-point DFT of v[b .. b + 7] in place; output k lands in v[b + d8(k)]
+__host__ __device__ constexpr int d8(int k) { return (k & 1) * 4 + (k >> 1); }
+template <bool INV>
+__device__ __forceinline__ void dft8(float2 (&v)[16], int b) {
+  const float c2 = 0.70710678118654752f;
+#pragma unroll
+  for (int n = 0; n < 4; ++n) {
+    const float2 a = v[b + n], c = v[b + n + 4];
+    v[b + n] = cadd(a, c);
+    float2 d = csub(a, c);
+    const float2 rot = INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);  // d * (-+ i)
+    if (n == 1) d = __fmul2_rn(__fadd2_rn(d, rot), make_float2(c2, c2));                            // W8^1
+    else if (n == 2) d = rot;                                                                       // W8^2
+    else if (n == 3) d = __fmul2_rn(__fadd2_rn(make_float2(-d.x, -d.y), rot), make_float2(c2, c2));  // W8^3
+    v[b + n + 4] = d;
+  }
+  dft4<INV>(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);  // X0 X2 X4 X6
+  dft4<INV>(v[b + 4], v[b + 5], v[b + 6], v[b + 7]);  // X1 X3 X5 X7
+}
+// radix-RQ butterfly of v[b .. b + RQ - 1]; output k in v[b + dq<RQ>(k)]
+template <int RQ>
+__host__ __device__ constexpr int dq(int k) { return RQ == 8 ? d8(k) : k; }
+template <bool INV, int RQ>
+__device__ __forceinline__ void dftq(float2 (&v)[16], int b) {
+  if (RQ == 8) dft8<INV>(v, b);
+  else dft4<INV>(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);
+}
+
+template <bool GS, int NP>
+__global__ void __launch_bounds__(kFftThreads, 3) hilbert_fused_short_kernel(
+    SrcDesc src, long long row0, long long nrows, __half* out, int pitch, long long ps, unsigned long long* rowmin,
+    unsigned long long* rowmax, float* hbuf, double amp_floor, DevStatus* st) {
+  constexpr int RQ = 16 / NP;        // radix of the outer pass
+  constexpr int TT = kFftT / NP;     // row length
+  constexpr int NR = 2 * NP;         // rows per CTA iteration
+  extern __shared__ float2 fsm[];
+  float2* buf = fsm;
+  float2* tw = fsm + kFftPad(kFftT);
+  // tw[kTw16 + (r-1) 16 + o] = W_256^(o r); tw[kTw256 + (s-1) 256 + j] = W_TT^(j s), s < RQ
+  for (int m = threadIdx.x; m < kTw256 + (RQ - 1) * 256; m += kFftThreads) {
+    int n, kk, r;
+    if (m < kTw256) {
+      n = 256;
+      r = 1 + m / 16;
+      kk = m % 16;
+    } else {
+      n = TT;
+      r = 1 + (m - kTw256) / 256;
+      kk = (m - kTw256) % 256;
+    }
+    float sn, cs;
+    sincospif(-2.0f * (float)((kk * r) % n) / (float)n, &sn, &cs);
+    tw[m] = make_float2(cs, sn);
+  }
+  __shared__ float red[2 * NR][kFftThreads / 32];
+  __shared__ int need_flags[NR];
+  __syncthreads();
+  const int j = threadIdx.x;
+  const float* x = static_cast<const float*>(src.ptr);  // s_samp == 1 (hilbert_fused_supported)
+  const long long ngroups = (nrows + NR - 1) / NR;
+  for (long long gr = blockIdx.x; gr < ngroups; gr += gridDim.x) {
+    long long rrow[NR], roff[NR];
+    bool has[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      has[i] = NR * gr + i < nrows;
+      rrow[i] = row0 + NR * gr + (has[i] ? i : 0);
+      roff[i] = row_offset(src, rrow[i]);
+    }
+    if (j < NR && gr + gridDim.x < ngroups && NR * (gr + gridDim.x) + j < nrows)
+      bulk_prefetch_l2(x + row_offset(src, row0 + NR * (gr + gridDim.x) + j), TT * sizeof(float));
+    // v[RQ q + r] = (x_a, x_b)[j + 256 r] of pair q
+    float2 v[16];
+    float mx[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) mx[i] = 0.f;
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) {
+        const float xa = has[2 * q] ? __ldg(x + roff[2 * q] + j + 256 * r) : 0.0f;
+        const float xb = has[2 * q + 1] ? __ldg(x + roff[2 * q + 1] + j + 256 * r) : 0.0f;
+        v[RQ * q + r] = make_float2(xa, xb);
+        mx[2 * q] = fmaxf(mx[2 * q], fabsf(xa));
+        mx[2 * q + 1] = fmaxf(mx[2 * q + 1], fabsf(xb));
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < NR; ++i) mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+    if ((j & 31) == 0)
+#pragma unroll
+      for (int i = 0; i < NR; ++i) red[i][j >> 5] = mx[i];
+    __syncthreads();
+    float sc[NR];  // per-row power-of-two scale (see the T = 4096 kernel)
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+#pragma unroll
+      for (int w = 0; w < kFftThreads / 32; ++w) mx[i] = fmaxf(mx[i], red[i][w]);
+      sc[i] = pow2_scale(mx[i]);
+    }
+#pragma unroll
+    for (int q = 0; q < NP; ++q)
+#pragma unroll
+      for (int r = 0; r < RQ; ++r) v[RQ * q + r] = __fmul2_rn(v[RQ * q + r], make_float2(sc[2 * q], sc[2 * q + 1]));
+    // outer pass (decimation in frequency): NP radix-RQ butterflies, output s
+    // of pair q times W_TT^(j s) to position 256 (RQ q + s) + j
+    {
+      const float2* t = tw + kTw256 + j;
+      float2* pb = buf + kFftPad(j);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+        dftq<false, RQ>(v, RQ * q);
+#pragma unroll
+        for (int sI = 0; sI < RQ; ++sI) {
+          float2 y = v[RQ * q + dq<RQ>(sI)];
+          if (sI > 0) y = cmul(y, t[(sI - 1) * 256]);
+          pb[(RQ * q + sI) * 272] = y;
+        }
+      }
+    }
+    __syncthreads();
+    load_set<16>(v, buf);
+    dft16<false>(v);
+    twiddle16<false, 16, true>(v, tw);
+    store_set<16>(v, buf);
+    __syncwarp();
+    load_set<1>(v, buf);
+    dft16<false>(v);
+    float2 u[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const float2 z = v[d16(r)];
+      u[r] = r < 8 ? make_float2(z.y, -z.x) : make_float2(-z.y, z.x);
+    }
+    if (j % (256 / NP) == 0) {  // DC and Nyquist of pair j / (256 / NP)
+      u[0] = make_float2(0.f, 0.f);
+      u[8] = make_float2(0.f, 0.f);
+    }
+    dft16<true>(u);
+    store_set<1>(u, buf);
+    __syncwarp();
+    load_set<16>(u, buf);
+    twiddle16<true, 16, false>(u, tw);
+    dft16<true>(u);
+    store_set<16>(u, buf);
+    __syncthreads();
+    // outer pass of the inverse (decimation in time): input s of pair q from
+    // position 256 (RQ q + s) + j times conj W_TT^(j s); output r back in place
+    {
+      const float2* t = tw + kTw256 + j;
+      float2* pb = buf + kFftPad(j);
+#pragma unroll
+      for (int q = 0; q < NP; ++q) {
+#pragma unroll
+        for (int sI = 0; sI < RQ; ++sI) {
+          float2 y = pb[(RQ * q + sI) * 272];
+          if (sI > 0) {
+            float2 w = t[(sI - 1) * 256];
+            w.y = -w.y;
+            y = cmul(y, w);
+          }
+          u[RQ * q + sI] = y;
+        }
+        dftq<true, RQ>(u, RQ * q);
+      }
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int r = 0; r < RQ; ++r) pb[(RQ * q + r) * 272] = u[RQ * q + dq<RQ>(r)];
+    }
+    __syncthreads();
+    // epilogue: positions [1024 g, 1024 g + 1024) belong to pair q = 1024 g / TT
+    float so[NR], amin[NR], amax[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      so[i] = sc[i] * (float)TT;
+      amin[i] = FLT_MAX;
+      amax[i] = 0.f;
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      const int q = (1024 * g) / TT;
+      const int t0 = (1024 * g) % TT + 4 * j;  // sample within the row
+      const int ia = 2 * q, ib = 2 * q + 1;
+      if (!has[ia]) continue;  // (rows are dealt in order: pair q absent means nothing follows)
+      const float4 ca = *reinterpret_cast<const float4*>(x + roff[ia] + t0);
+      const float4 cb = has[ib] ? *reinterpret_cast<const float4*>(x + roff[ib] + t0) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float2* hb = buf + kFftPad(1024 * g + 4 * j);
+      float2 h[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) h[k] = hb[k];
+      const float2 re[4] = {make_float2(ca.x * so[ia], cb.x * so[ib]), make_float2(ca.y * so[ia], cb.y * so[ib]),
+                            make_float2(ca.z * so[ia], cb.z * so[ib]), make_float2(ca.w * so[ia], cb.w * so[ib])};
+      normalize4_split_pair<GS>(re, h, out + rrow[ia] * pitch + t0, out + rrow[ib] * pitch + t0, has[ib], ps,
+                                amin[ia], amax[ia], amin[ib], amax[ib]);
+    }
+    // row statistics: thread 32 i closes row i
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        amin[i] = fminf(amin[i], __shfl_xor_sync(0xffffffffu, amin[i], o));
+        amax[i] = fmax_nan(amax[i], __shfl_xor_sync(0xffffffffu, amax[i], o));
+      }
+    if ((j & 31) == 0)
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        red[2 * i][j >> 5] = amin[i];
+        red[2 * i + 1][j >> 5] = amax[i];
+      }
+    __syncthreads();
+    if ((j & 31) == 0 && (j >> 5) < NR) {
+      const int i = j >> 5;
+      float lo = red[2 * i][0], hi = red[2 * i + 1][0];
+      for (int w = 1; w < kFftThreads / 32; ++w) {
+        lo = fminf(lo, red[2 * i][w]);
+        hi = fmax_nan(hi, red[2 * i + 1][w]);
+      }
+      int need = 0;
+      bool present = false;
+      float scale = 1.f;
+      long long rr = 0;
+#pragma unroll
+      for (int i2 = 0; i2 < NR; ++i2)
+        if (i2 == i) {
+          present = has[i2];
+          scale = sc[i2];
+          rr = rrow[i2];
+        }
+      if (present) {
+        if (!(hi <= FLT_MAX)) atomicOr(&st->flags, FLAG_NONFINITE);
+        lo = sqrtf(lo);
+        hi = sqrtf(hi);
+        int lg = 0;
+        while ((1 << lg) < TT) ++lg;
+        const int e = (int)((__float_as_uint(scale) >> 23) & 0xffu) - 127 + lg;  // scale TT = 2^e
+        const double rs = __hiloint2double((1023 - e) << 20, 0);
+        rowmin[rr] = key_of((double)lo * rs);
+        rowmax[rr] = key_of((double)hi * rs);
+        need = (lo == 0.0f) || ((double)lo < amp_floor * (double)hi * (1.0 + 1e-5));
+      }
+      need_flags[i] = need;
+    }
+    __syncthreads();
+    // rare: keep H (input units) of a row the exact-median fixup will inspect
+    bool any_need = false;
+#pragma unroll
+    for (int i = 0; i < NR; ++i) any_need = any_need || need_flags[i] != 0;
+    if (any_need) {
+#pragma unroll
+      for (int i = 0; i < NR; ++i) {
+        if (!need_flags[i]) continue;
+        const float un = 1.0f / so[i];
+        const int q = i / 2;
+        for (int t = j; t < TT; t += kFftThreads) {
+          const float2 hv = buf[kFftPad(q * TT + t)];
+          hbuf[(rrow[i] - src.h_row0) * src.h_ld + t] = ((i & 1) ? hv.y : hv.x) * un;
+        }
+      }
+    }
+    // the next group's first stores come after its row-max barrier
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Exact amplitude-floor fixup.  For each row: if the cheap
 // bound min|a| >= floor * max|a| holds, no sample can fall below
 // floor * median and the row is untouched (the common case: Rayleigh
@@ -1527,8 +1802,30 @@ cudaError_t launch_hilbert_halfspec(void* spec, long long nrows, int T, int is_d
 bool hilbert_fused_supported(const SrcDesc& src, int fmt, int cdouble, int pitch) {
   const bool aligned = (reinterpret_cast<uintptr_t>(src.ptr) & 15u) == 0 && src.s_samp == 1 && src.s_sig % 4 == 0 &&
                        (src.R == 1 || src.s_trial % 4 == 0) && (src.B == 1 || src.s_band % 4 == 0);
-  return src.kind == 0 && !src.is_double && !cdouble && fmt == OUT_SPLIT && src.T == kFftT && pitch == kFftT &&
-         aligned;
+  const bool len_ok = (src.T == kFftT || src.T == kFftT / 2 || src.T == kFftT / 4) && pitch == src.T;
+  return src.kind == 0 && !src.is_double && !cdouble && fmt == OUT_SPLIT && len_ok && aligned;
+}
+
+template <bool GS, int NP>
+cudaError_t launch_hilbert_fused_short_t(const SrcDesc& src, long long row0, long long nrows, __half* out, int pitch,
+                                         long long plane_stride, unsigned long long* rowstat, long long rows_total,
+                                         double amp_floor, DevStatus* status, cudaStream_t st) {
+  auto kern = hilbert_fused_short_kernel<GS, NP>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kFftSmemBytes);
+  if (e != cudaSuccess) return e;
+  int dev = 0, n_sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kFftThreads, kFftSmemBytes);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  const long long groups = (nrows + 2 * NP - 1) / (2 * NP);
+  const long long cap = (long long)per_sm * n_sms;
+  const unsigned grid = (unsigned)(groups < cap ? groups : cap);
+  kern<<<grid, kFftThreads, kFftSmemBytes, st>>>(src, row0, nrows, out, pitch, plane_stride, rowstat,
+                                                 rowstat + rows_total,
+                                                 static_cast<float*>(const_cast<void*>(src.hbuf)), amp_floor, status);
+  return cudaGetLastError();
 }
 
 template <bool GS>
@@ -1564,6 +1861,16 @@ cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long n
   if (gauss_done) *gauss_done = src.gauss_planes ? 1 : 0;
   if (nrows <= 0) return cudaSuccess;
   __half* o = static_cast<__half*>(out);
+  if (src.T == kFftT / 2)
+    return src.gauss_planes ? launch_hilbert_fused_short_t<true, 2>(src, row0, nrows, o, pitch, plane_stride, rowstat,
+                                                                    rows_total, amp_floor, status, st)
+                            : launch_hilbert_fused_short_t<false, 2>(src, row0, nrows, o, pitch, plane_stride, rowstat,
+                                                                     rows_total, amp_floor, status, st);
+  if (src.T == kFftT / 4)
+    return src.gauss_planes ? launch_hilbert_fused_short_t<true, 4>(src, row0, nrows, o, pitch, plane_stride, rowstat,
+                                                                    rows_total, amp_floor, status, st)
+                            : launch_hilbert_fused_short_t<false, 4>(src, row0, nrows, o, pitch, plane_stride, rowstat,
+                                                                     rows_total, amp_floor, status, st);
   return src.gauss_planes
              ? launch_hilbert_fused_t<true>(src, row0, nrows, o, pitch, plane_stride, rowstat, rows_total, amp_floor,
                                             status, st)

@@ -372,7 +372,7 @@ def test_fused_hilbert_t4096_bands():
     assert not res["plv"].meta["input_copied"]
 
 
-@pytest.mark.parametrize("T", [16, 30, 250, 1000, 2000, 2250, 4095, 4096, 10000, 12000])
+@pytest.mark.parametrize("T", [16, 30, 250, 1000, 1024, 2000, 2048, 2250, 4095, 4096, 10000, 12000])
 def test_real_input_lengths_unequal_scales(T):
     # fp32 real rows, samples contiguous, odd and even T (4096: the fused
     # radix-16 kernel; others: the cuFFT chain, odd T with per-row scaling),
@@ -488,10 +488,12 @@ def test_bandpass_odd_padded_length_unequal_scales():
     check(res, O.plv_family(x, input_kind="real", fir=(f.taps, 300)), "fp64", "bandpass odd L")
 
 
-def test_fused_hilbert_mixed_row_scales():
-    # rows sharing one packed FFT differ by 1e10 in amplitude
+@pytest.mark.parametrize("T", [4096, 2048, 1024])
+def test_fused_hilbert_mixed_row_scales(T):
+    # rows sharing one packed FFT differ by 1e10 in amplitude (T = 2048 / 1024:
+    # 2 / 4 row pairs per CTA iteration, 9 rows leave a partial last group)
     rng = np.random.default_rng(41)
-    x = rng.standard_normal((9, 4096, 1)).astype(np.float32)
+    x = rng.standard_normal((9, T, 1)).astype(np.float32)
     x = np.ascontiguousarray(x[:, :, 0])[:, :, None]
     x[0] *= 1e6
     x[1] *= 1e-4
@@ -501,11 +503,13 @@ def test_fused_hilbert_mixed_row_scales():
     check(res, ref, "split", "fused hilbert mixed scales")
 
 
-def test_fused_hilbert_amplitude_floor_fixup():
+@pytest.mark.parametrize("T", [4096, 2048, 1024])
+def test_fused_hilbert_amplitude_floor_fixup(T):
     rng = np.random.default_rng(42)
-    x = rng.standard_normal((6, 4096)).astype(np.float32)
-    x[1, 1000:1400] = 0.0
+    x = rng.standard_normal((7, T)).astype(np.float32)
+    x[1, T // 4:T // 4 + T // 10] = 0.0
     x[4, 100:130] = 0.0
+    x[6, T - 40:] = 0.0
     x = x[:, :, None]
     ref = O.plv_family(x.astype(np.float64), input_kind="real", amp_floor=0.05)
     res = C.plv_family(x, input_kind="real", precision="split", amp_floor=0.05)
