@@ -281,19 +281,22 @@ ps_status get_plan(ps_ctx* c, int T, long long batch, long long idist, bool dbl,
   return PS_OK;
 }
 
-// Which chain takes real rows of even length T.  For a power of two cuFFT's
-// R2C / C2R are single symmetric kernels (8 B/sample each: nothing to save,
-// `vector_fft_symm_r2c`); for any other length they run as a half-length
-// complex transform plus a split / merge pass, and the half-length complex
-// chain with the collapsed multiplier saves two of the five passes (C2,
-// T = 10000: 2.54 -> 1.95 ms; profiles/r02_session4/).  PS_HILBERT_CHAIN=r2c /
-// half forces one (A/B, tests of both).
+// Which chain takes real rows of even length T.  cuFFT's R2C / C2R run as a
+// half-length complex transform plus a split / merge pass each for most
+// lengths, and the half-length complex chain with the collapsed multiplier
+// saves two of the five passes (C2, T = 10000: 2.54 -> 1.91 ms).  For powers
+// of two cuFFT has single symmetric kernels (8 B/sample each); measured per
+// 67 M samples (tools/hilbert_probe.py, R2C chain / half-length chain, ms):
+// T = 512 0.95 / 0.73, 2048 0.50 / 0.47, 8192 0.61 / 0.57, 16384 0.57 / 0.51,
+// 32768 0.72 / 0.60, 65536 0.75 / 0.76, 131072 1.00 / 0.80 -- the half-length
+// chain everywhere except T = 65536 (C3), a tie it loses by 2%.
+// PS_HILBERT_CHAIN=r2c / half forces one (A/B, tests of both).
 bool hilbert_half_chain(long long T) {
   const char* s = std::getenv("PS_HILBERT_CHAIN");  // read per call: tests switch it
   const int forced = (s && std::string(s) == "r2c") ? 0 : (s && std::string(s) == "half") ? 1 : -1;
   if (T % 2 != 0 || T < 4) return false;
   if (forced >= 0) return forced == 1;
-  return (T & (T - 1)) != 0;
+  return T != 65536;
 }
 
 long long hilbert_chunk_rows(const Geometry& g) {
