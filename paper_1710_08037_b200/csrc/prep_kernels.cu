@@ -171,6 +171,78 @@ __device__ __forceinline__ uint32_t pack_half2(__half a, __half b) {
   return (uint32_t)__half_as_ushort(a) | ((uint32_t)__half_as_ushort(b) << 16);
 }
 
+// 4 consecutive samples at t0 of row r (source offset roff): normalise, split,
+// store the planes; folds |a| into amin / amax and non-finite into bad.
+template <int KIND>
+__device__ __forceinline__ void normalize_vec4(const SrcDesc& src, long long r, long long roff, long long t0, float hs,
+                                               __half* out, long long obase, long long ps, float& amin, float& amax,
+                                               bool& bad) {
+    float re[4], im[4];
+    if (KIND == 0) {
+      const float4 x = *reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + roff + t0);
+      const float4 h = *reinterpret_cast<const float4*>(static_cast<const float*>(src.hbuf) +
+                                                        (r - src.h_row0) * src.h_ld + t0);
+      re[0] = x.x; re[1] = x.y; re[2] = x.z; re[3] = x.w;
+      im[0] = h.x * hs; im[1] = h.y * hs; im[2] = h.z * hs; im[3] = h.w * hs;
+    } else {
+      const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + 2 * (roff + t0));
+      const float4 a = p[0], b = p[1];
+      re[0] = a.x; im[0] = a.y; re[1] = a.z; im[1] = a.w;
+      re[2] = b.x; im[2] = b.y; re[3] = b.z; im[3] = b.w;
+    }
+    __half rh[4], rlo[4], ih[4], ilo[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // one MUFU.RSQ instead of sqrt + two IEEE divisions: z is rounded to
+      // the 22-bit hi/lo split anyway, and the row min/max only feed the
+      // conservative amplitude-floor pre-check (the fixup recomputes |a|
+      // exactly for any row it inspects)
+      const float a2 = re[k] * re[k] + im[k] * im[k];
+      const float inv = a2 > 0.0f ? rsqrtf(a2) : 0.0f;
+      const float a = a2 * inv;
+      float zr = 0.0f, zi = 0.0f;
+      if (KIND == 2) {
+        zr = re[k];
+        zi = im[k];
+      } else {
+        zr = re[k] * inv;
+        zi = im[k] * inv;
+      }
+      rh[k] = __float2half_rn(zr);
+      ih[k] = __float2half_rn(zi);
+      rlo[k] = __float2half_rn(zr - __half2float(rh[k]));
+      ilo[k] = __float2half_rn(zi - __half2float(ih[k]));
+      if (!(a <= FLT_MAX)) bad = true;
+      amin = fminf(amin, a);
+      amax = fmaxf(amax, a);
+    }
+    __half* o = out + obase + t0;
+    *reinterpret_cast<uint2*>(o) = make_uint2(pack_half2(rh[0], rh[1]), pack_half2(rh[2], rh[3]));
+    *reinterpret_cast<uint2*>(o + ps) = make_uint2(pack_half2(rlo[0], rlo[1]), pack_half2(rlo[2], rlo[3]));
+    *reinterpret_cast<uint2*>(o + 2 * ps) = make_uint2(pack_half2(ih[0], ih[1]), pack_half2(ih[2], ih[3]));
+    *reinterpret_cast<uint2*>(o + 3 * ps) = make_uint2(pack_half2(ilo[0], ilo[1]), pack_half2(ilo[2], ilo[3]));
+    if (src.gauss_planes) {
+      // Gauss-Gram operands S = Zr + Zi, D = Zr - Zi from the rounded split
+      // values -- the arithmetic of gauss_planes_kernel, fused here so the
+      // planes are not read back (16 B / sample saved)
+      __half sh[4], sl[4], dh[4], dl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float zr = __half2float(rh[k]) + __half2float(rlo[k]);
+        const float zi = __half2float(ih[k]) + __half2float(ilo[k]);
+        const float S = zr + zi, D = zr - zi;
+        sh[k] = __float2half_rn(S);
+        sl[k] = __float2half_rn(S - __half2float(sh[k]));
+        dh[k] = __float2half_rn(D);
+        dl[k] = __float2half_rn(D - __half2float(dh[k]));
+      }
+      *reinterpret_cast<uint2*>(o + 4 * ps) = make_uint2(pack_half2(sh[0], sh[1]), pack_half2(sh[2], sh[3]));
+      *reinterpret_cast<uint2*>(o + 5 * ps) = make_uint2(pack_half2(sl[0], sl[1]), pack_half2(sl[2], sl[3]));
+      *reinterpret_cast<uint2*>(o + 6 * ps) = make_uint2(pack_half2(dh[0], dh[1]), pack_half2(dh[2], dh[3]));
+      *reinterpret_cast<uint2*>(o + 7 * ps) = make_uint2(pack_half2(dl[0], dl[1]), pack_half2(dl[2], dl[3]));
+    }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src, long long row0, int chunks,
                                                                      __half* out, int pitch, long long ps,
@@ -189,70 +261,7 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
   for (int g = 0; g < kVecPer; ++g) {
     const long long t0 = (long long)ch * kVecSamplesPerBlock + ((long long)g * kNormThreads + threadIdx.x) * 4;
     if (t0 < T) {
-      float re[4], im[4];
-      if (KIND == 0) {
-        const float4 x = *reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + roff + t0);
-        const float4 h = *reinterpret_cast<const float4*>(static_cast<const float*>(src.hbuf) +
-                                                          (r - src.h_row0) * src.h_ld + t0);
-        re[0] = x.x; re[1] = x.y; re[2] = x.z; re[3] = x.w;
-        im[0] = h.x * hs; im[1] = h.y * hs; im[2] = h.z * hs; im[3] = h.w * hs;
-      } else {
-        const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(src.ptr) + 2 * (roff + t0));
-        const float4 a = p[0], b = p[1];
-        re[0] = a.x; im[0] = a.y; re[1] = a.z; im[1] = a.w;
-        re[2] = b.x; im[2] = b.y; re[3] = b.z; im[3] = b.w;
-      }
-      __half rh[4], rlo[4], ih[4], ilo[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        // one MUFU.RSQ instead of sqrt + two IEEE divisions: z is rounded to
-        // the 22-bit hi/lo split anyway, and the row min/max only feed the
-        // conservative amplitude-floor pre-check (the fixup recomputes |a|
-        // exactly for any row it inspects)
-        const float a2 = re[k] * re[k] + im[k] * im[k];
-        const float inv = a2 > 0.0f ? rsqrtf(a2) : 0.0f;
-        const float a = a2 * inv;
-        float zr = 0.0f, zi = 0.0f;
-        if (KIND == 2) {
-          zr = re[k];
-          zi = im[k];
-        } else {
-          zr = re[k] * inv;
-          zi = im[k] * inv;
-        }
-        rh[k] = __float2half_rn(zr);
-        ih[k] = __float2half_rn(zi);
-        rlo[k] = __float2half_rn(zr - __half2float(rh[k]));
-        ilo[k] = __float2half_rn(zi - __half2float(ih[k]));
-        if (!(a <= FLT_MAX)) bad = true;
-        amin = fminf(amin, a);
-        amax = fmaxf(amax, a);
-      }
-      __half* o = out + obase + t0;
-      *reinterpret_cast<uint2*>(o) = make_uint2(pack_half2(rh[0], rh[1]), pack_half2(rh[2], rh[3]));
-      *reinterpret_cast<uint2*>(o + ps) = make_uint2(pack_half2(rlo[0], rlo[1]), pack_half2(rlo[2], rlo[3]));
-      *reinterpret_cast<uint2*>(o + 2 * ps) = make_uint2(pack_half2(ih[0], ih[1]), pack_half2(ih[2], ih[3]));
-      *reinterpret_cast<uint2*>(o + 3 * ps) = make_uint2(pack_half2(ilo[0], ilo[1]), pack_half2(ilo[2], ilo[3]));
-      if (src.gauss_planes) {
-        // Gauss-Gram operands S = Zr + Zi, D = Zr - Zi from the rounded split
-        // values -- the arithmetic of gauss_planes_kernel, fused here so the
-        // planes are not read back (16 B / sample saved)
-        __half sh[4], sl[4], dh[4], dl[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const float zr = __half2float(rh[k]) + __half2float(rlo[k]);
-          const float zi = __half2float(ih[k]) + __half2float(ilo[k]);
-          const float S = zr + zi, D = zr - zi;
-          sh[k] = __float2half_rn(S);
-          sl[k] = __float2half_rn(S - __half2float(sh[k]));
-          dh[k] = __float2half_rn(D);
-          dl[k] = __float2half_rn(D - __half2float(dh[k]));
-        }
-        *reinterpret_cast<uint2*>(o + 4 * ps) = make_uint2(pack_half2(sh[0], sh[1]), pack_half2(sh[2], sh[3]));
-        *reinterpret_cast<uint2*>(o + 5 * ps) = make_uint2(pack_half2(sl[0], sl[1]), pack_half2(sl[2], sl[3]));
-        *reinterpret_cast<uint2*>(o + 6 * ps) = make_uint2(pack_half2(dh[0], dh[1]), pack_half2(dh[2], dh[3]));
-        *reinterpret_cast<uint2*>(o + 7 * ps) = make_uint2(pack_half2(dl[0], dl[1]), pack_half2(dl[2], dl[3]));
-      }
+      normalize_vec4<KIND>(src, r, roff, t0, hs, out, obase, ps, amin, amax, bad);
     } else if (t0 < pitch) {  // T % 4 == 0: the pitch pad is one 4-sample group
       __half* o = out + obase + t0;
       const uint2 z = make_uint2(0u, 0u);
@@ -279,6 +288,42 @@ __global__ void __launch_bounds__(kNormThreads) normalize_vec_kernel(SrcDesc src
     atomicMin(&rowmin[r], key_of((double)amin));
     atomicMax(&rowmax[r], key_of((double)amax));
   }
+}
+
+// The same for short rows (T % 128 == 0, T <= kVecSamplesPerBlock / 2): a block
+// takes kVecSamplesPerBlock / T whole rows instead of leaving most of its
+// threads idle on one (T = 256: 2.2x the time per sample of long rows).  A
+// warp's 32 x 4 samples lie in one row, so row min / max are a warp reduction
+// and one atomic pair per warp.
+template <int KIND>
+__global__ void __launch_bounds__(kNormThreads) normalize_vec_rows_kernel(SrcDesc src, long long row0, long long nrows,
+                                                                          int rpb, __half* out, int pitch,
+                                                                          long long ps, unsigned long long* rowmin,
+                                                                          unsigned long long* rowmax, DevStatus* st) {
+  const int T = (int)src.T;
+  bool bad = false;
+#pragma unroll
+  for (int g = 0; g < kVecPer; ++g) {
+    const int s4 = (g * kNormThreads + threadIdx.x) * 4;  // sample slot within the block's rows
+    const long long rl = (long long)blockIdx.x * rpb + s4 / T;
+    if (s4 / T < rpb && rl < nrows) {
+      const long long r = row0 + rl;
+      const long long t0 = s4 % T;
+      const float hs = (KIND == 0 && src.h_scale) ? static_cast<const float*>(src.h_scale)[r - src.h_row0] : 1.0f;
+      float amin = FLT_MAX, amax = 0.0f;
+      normalize_vec4<KIND>(src, r, row_offset(src, r), t0, hs, out, r * pitch, ps, amin, amax, bad);
+      // (whole warps take this branch together: 128 samples of one row)
+      for (int o = 16; o > 0; o >>= 1) {
+        amin = fminf(amin, __shfl_xor_sync(0xffffffffu, amin, o));
+        amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomicMin(&rowmin[r], key_of((double)amin));
+        atomicMax(&rowmax[r], key_of((double)amax));
+      }
+    }
+  }
+  if (bad) atomicOr(&st->flags, FLAG_NONFINITE);
 }
 
 // ---------------------------------------------------------------------------
@@ -1339,11 +1384,14 @@ __global__ void hilbert_spectrum_kernel(C* spec, long long nrows, int T) {
 // in-place pass between two C2C transforms of length M (8 instead of 24 bytes
 // per sample).  The 1/M of the unnormalised inverse is folded in.
 template <typename C>
-__global__ void __launch_bounds__(256) hilbert_halfspec_kernel(C* spec, long long nrows, int M) {
+__global__ void __launch_bounds__(256) hilbert_halfspec_kernel(C* spec, long long nrows, int M, int tpr) {
   using S = decltype(spec->x);
   // blockIdx.x tiles k = 0 .. M/2 (thread k handles the bins k and M - k),
-  // blockIdx.y strides the rows: the twiddle is computed once per thread
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  // blockIdx.y strides the rows: the twiddle is computed once per thread.
+  // Short rows (M/2 + 1 < 256): tpr (a power of two) threads per row and
+  // 256 / tpr rows per block, so few lanes idle.
+  const int k = blockIdx.x * tpr + (threadIdx.x & (tpr - 1));
+  const int rsub = threadIdx.x / tpr, rpb = 256 / tpr;
   if (k > M / 2) return;
   const int m = M - k;
   S sn, cs;
@@ -1361,7 +1409,7 @@ __global__ void __launch_bounds__(256) hilbert_halfspec_kernel(C* spec, long lon
   const S inv = S(1) / S(M);
   sn *= inv;
   cs *= inv;
-  for (long long row = blockIdx.y; row < nrows; row += gridDim.y) {
+  for (long long row = (long long)blockIdx.y * rpb + rsub; row < nrows; row += (long long)gridDim.y * rpb) {
     C* z = spec + row * M;
     if (k == 0) {
       C v;
@@ -1788,14 +1836,18 @@ cudaError_t launch_hilbert_spectrum(void* spec, long long nrows, int T, int is_d
 
 cudaError_t launch_hilbert_halfspec(void* spec, long long nrows, int T, int is_double, cudaStream_t st) {
   const int M = T / 2;
-  const int kb = (M / 2 + 1 + 255) / 256;
+  const int per_row = M / 2 + 1;
+  int tpr = 256;  // threads per row: the smallest power of two covering the row, at most 256
+  while (tpr / 2 >= per_row && tpr > 1) tpr /= 2;
+  const int rpb = 256 / tpr;
+  const int kb = (per_row + tpr - 1) / tpr;
   // enough row-strided blocks to fill the GPU a few times over; every thread
   // keeps its twiddle across its rows
   long long ry = (148LL * 16 + kb - 1) / kb;
-  ry = std::max(1LL, std::min(ry, std::min(nrows, 65535LL)));
+  ry = std::max(1LL, std::min(ry, std::min((nrows + rpb - 1) / rpb, 65535LL)));
   const dim3 g((unsigned)kb, (unsigned)ry);
-  if (is_double) hilbert_halfspec_kernel<double2><<<g, 256, 0, st>>>((double2*)spec, nrows, M);
-  else hilbert_halfspec_kernel<float2><<<g, 256, 0, st>>>((float2*)spec, nrows, M);
+  if (is_double) hilbert_halfspec_kernel<double2><<<g, 256, 0, st>>>((double2*)spec, nrows, M, tpr);
+  else hilbert_halfspec_kernel<float2><<<g, 256, 0, st>>>((float2*)spec, nrows, M, tpr);
   return cudaGetLastError();
 }
 
@@ -1958,6 +2010,20 @@ cudaError_t launch_normalize_fmt(const SrcDesc& src, long long row0, long long n
       unsigned long long* rmin = rowstat;
       unsigned long long* rmax = rowstat + rows_total;
       if (gauss_done) *gauss_done = src.gauss_planes ? 1 : 0;
+      if (src.T % 128 == 0 && src.T * 2 <= kVecSamplesPerBlock && pitch == src.T) {  // short rows: several per block
+        const int rpb = (int)(kVecSamplesPerBlock / src.T);
+        const long long blocks = (nrows + rpb - 1) / rpb;
+        if (src.kind == 0)
+          normalize_vec_rows_kernel<0><<<(unsigned)blocks, kNormThreads, 0, st>>>(src, row0, nrows, rpb, o, pitch,
+                                                                                plane_stride, rmin, rmax, status);
+        else if (src.kind == 1)
+          normalize_vec_rows_kernel<1><<<(unsigned)blocks, kNormThreads, 0, st>>>(src, row0, nrows, rpb, o, pitch,
+                                                                                plane_stride, rmin, rmax, status);
+        else
+          normalize_vec_rows_kernel<2><<<(unsigned)blocks, kNormThreads, 0, st>>>(src, row0, nrows, rpb, o, pitch,
+                                                                                plane_stride, rmin, rmax, status);
+        return cudaGetLastError();
+      }
       if (src.kind == 0)
         normalize_vec_kernel<0><<<(unsigned)vblk, kNormThreads, 0, st>>>(src, row0, vchunks, o, pitch, plane_stride,
                                                                          rmin, rmax, status);
