@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ps_internal.h"
 
@@ -827,10 +828,11 @@ __device__ __forceinline__ void dft8(float2 (&v)[16], int b) {
 }
 // radix-RQ butterfly of v[b .. b + RQ - 1]; output k in v[b + dq<RQ>(k)]
 template <int RQ>
-__host__ __device__ constexpr int dq(int k) { return RQ == 8 ? d8(k) : k; }
+__host__ __device__ constexpr int dq(int k) { return RQ == 16 ? d16(k) : RQ == 8 ? d8(k) : k; }
 template <bool INV, int RQ>
 __device__ __forceinline__ void dftq(float2 (&v)[16], int b) {
-  if (RQ == 8) dft8<INV>(v, b);
+  if (RQ == 16) dft16<INV>(v);
+  else if (RQ == 8) dft8<INV>(v, b);
   else dft4<INV>(v[b + 0], v[b + 1], v[b + 2], v[b + 3]);
 }
 
@@ -1913,6 +1915,12 @@ cudaError_t launch_hilbert_fused(const SrcDesc& src, long long row0, long long n
   if (gauss_done) *gauss_done = src.gauss_planes ? 1 : 0;
   if (nrows <= 0) return cudaSuccess;
   __half* o = static_cast<__half*>(out);
+  static const bool unified = std::getenv("PS_HILBERT_UNIFIED") != nullptr;  // experiment: NP = 1 of the short kernel
+  if (src.T == kFftT && unified)
+    return src.gauss_planes ? launch_hilbert_fused_short_t<true, 1>(src, row0, nrows, o, pitch, plane_stride, rowstat,
+                                                                    rows_total, amp_floor, status, st)
+                            : launch_hilbert_fused_short_t<false, 1>(src, row0, nrows, o, pitch, plane_stride, rowstat,
+                                                                     rows_total, amp_floor, status, st);
   if (src.T == kFftT / 2)
     return src.gauss_planes ? launch_hilbert_fused_short_t<true, 2>(src, row0, nrows, o, pitch, plane_stride, rowstat,
                                                                     rows_total, amp_floor, status, st)
